@@ -1,0 +1,176 @@
+"""Generate golden vectors by running the REAL reference (``lioncomm`` at
+/root/reference/pkg/src) on seeded inputs.  Run in the build container only:
+
+    python tests/golden/make_golden.py
+
+Writes tests/golden/golden_steps.npz and tests/golden/golden_collectives.npz.
+The reference is imported read-only (no bytecode written); nothing here runs
+on the GPU box.  Inputs are fp32-representable (generated as float32, then
+upcast to float64 for the reference), so the CUDA path, which keeps fp32
+state and computes in fp64, can be compared bit-for-bit with float32 of the
+reference's float64 outputs.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+sys.dont_write_bytecode = True
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, REPO)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from lioncomm.collectives import (allreduce_mean_f32,  # noqa: E402
+                                  compressed_allreduce_1bit, direct_allreduce,
+                                  run_ranks)
+from lioncomm.optimizer import (LionHyper, SyncPolicy, WorkerState,  # noqa: E402
+                                distributed_lion_step, maybe_sync_momentum)
+from lioncomm.quant import (QuantSpec, SignPolicy, apply_sign,  # noqa: E402
+                            lp_mean_norm, pack, quantize)
+from lioncomm.transport import InprocTransport  # noqa: E402
+
+from tests.golden.cases import COLLECTIVE_CASES, SIZES, STEP_CASES  # noqa: E402
+from oracle.lioncub_oracle import synth_rank_inputs  # noqa: E402
+
+
+def sign_words(s: np.ndarray) -> np.ndarray:
+    """pack(s,1,1).payload as little-endian uint32 (zero-padded to 4 B)."""
+    payload = pack(s.ravel(), 1, 1).payload
+    buf = payload + b"\x00" * ((-len(payload)) % 4)
+    return np.frombuffer(buf, dtype="<u4").copy()
+
+
+def run_step_case(case: dict, out: dict):
+    name = case["name"]
+    world = case["world"]
+    ranks = synth_rank_inputs(case["seed"], world, SIZES, case["kind"])
+    h = LionHyper(beta1=0.9, beta2=0.99, lr=case["lr"],
+                  weight_decay=case["wd"])
+    spec = None if case["bits"] is None else QuantSpec(bits=case["bits"], norm_p=1.0)
+    mask = None
+    if case.get("mask"):
+        mrng = np.random.default_rng(case["seed"] + 77)
+        mask = {case["mask"]: mrng.random(size=SIZES[case["mask"]]) < 0.8}
+    sync = None
+    if case.get("sync"):
+        period, layers = case["sync"]
+        sync = SyncPolicy(period=period,
+                          layers=layers if isinstance(layers, str) else frozenset(layers))
+    t = case["iteration"] + 1
+    policy = SignPolicy(mode=case["zero_mode"], iteration=t)
+
+    def fn(topo):
+        r = topo.rank
+        st = WorkerState(
+            params={k: v.astype(np.float64) for k, v in ranks[r]["theta"].items()},
+            momentum={k: v.astype(np.float64) for k, v in ranks[r]["m"].items()},
+            iteration=case["iteration"])
+        grads = {k: v.astype(np.float64) for k, v in ranks[r]["g"].items()}
+        metrics = {}
+        st2 = distributed_lion_step(st, grads, h, spec, topo, case["algo"],
+                                    mask=mask, zero_mode=case["zero_mode"],
+                                    metrics_out=metrics)
+        if sync is not None:
+            st2 = maybe_sync_momentum(st2, sync, topo)
+        return st2, metrics
+
+    res = run_ranks(world, fn, transport=InprocTransport(world))
+    p = f"{name}/"
+    for layer in SIZES:
+        out[p + f"in/theta/{layer}"] = ranks[0]["theta"][layer]
+        for r in range(world):
+            out[p + f"in/m/{r}/{layer}"] = ranks[r]["m"][layer]
+            out[p + f"in/g/{r}/{layer}"] = ranks[r]["g"][layer]
+        th0 = res[0][0].params[layer]
+        for r in range(world):
+            assert np.array_equal(res[r][0].params[layer], th0), "theta diverged"
+            out[p + f"out/m/{r}/{layer}"] = res[r][0].momentum[layer]
+        out[p + f"out/theta/{layer}"] = th0
+        out[p + f"out/sign/{layer}"] = np.asarray(
+            res[0][1]["vote_sign"][layer]).astype(np.int8)
+        out[p + f"out/ties/{layer}"] = np.int64(res[0][1]["ties"][layer])
+        for r in range(world):
+            c = res[r][1]["c_local"][layer]
+            if world <= 2:
+                out[p + f"out/c/{r}/{layer}"] = c
+            s = apply_sign(c, policy)
+            if np.all(np.abs(s) == 1):
+                out[p + f"out/words/{r}/{layer}"] = sign_words(s)
+            if spec is not None and spec.bits > 1:
+                out[p + f"out/q/{r}/{layer}"] = quantize(c.ravel(), spec).astype(np.int16)
+                out[p + f"out/norm/{r}/{layer}"] = np.float64(lp_mean_norm(c.ravel(), 1.0))
+    if mask is not None:
+        for k, v in mask.items():
+            out[p + f"in/mask/{k}"] = v
+
+
+def run_collective_case(case: dict, out: dict):
+    name = case["name"]
+    world, n, kind = case["world"], case["n"], case["kind"]
+    rng = np.random.default_rng(case["seed"])
+    p = f"{name}/"
+    if kind == "direct":
+        q_max = case["q_max"]
+        binary = case.get("binary", False)
+        if binary:
+            vecs = [rng.choice([-1, 1], size=n).astype(np.int64) for _ in range(world)]
+        else:
+            vecs = [rng.integers(-q_max, q_max + 1, size=n).astype(np.int64)
+                    for _ in range(world)]
+
+        def fn(topo):
+            return direct_allreduce(vecs[topo.rank], topo, q_max=q_max,
+                                    binary_signs=binary)
+    elif kind == "compressed":
+        vecs = [rng.normal(size=n).astype(np.float32).astype(np.float64)
+                for _ in range(world)]
+        policy = SignPolicy("alternating", iteration=case["t"])
+
+        def fn(topo):
+            return compressed_allreduce_1bit(vecs[topo.rank], topo, policy)
+    elif kind == "mean":
+        vecs = [rng.normal(size=n).astype(np.float32).astype(np.float64)
+                for _ in range(world)]
+
+        def fn(topo):
+            return allreduce_mean_f32(vecs[topo.rank], topo)
+    else:
+        raise ValueError(kind)
+    res = run_ranks(world, fn, transport=InprocTransport(world))
+    for r in range(world):
+        out[p + f"in/{r}"] = vecs[r]
+    if kind == "mean":
+        for r in range(1, world):
+            assert np.array_equal(res[r], res[0])
+        out[p + "out/values"] = res[0]
+    else:
+        for r in range(1, world):
+            assert np.array_equal(res[r].values, res[0].values)
+        out[p + "out/values"] = np.asarray(res[0].values)
+        out[p + "out/ties"] = np.int64(res[0].ties)
+
+
+def main():
+    steps: dict = {}
+    for case in STEP_CASES:
+        run_step_case(case, steps)
+    steps["meta"] = np.frombuffer(json.dumps(
+        {"cases": STEP_CASES, "sizes": {k: list(v) for k, v in SIZES.items()}}
+    ).encode(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(HERE, "golden_steps.npz"), **steps)
+    colls: dict = {}
+    for case in COLLECTIVE_CASES:
+        run_collective_case(case, colls)
+    colls["meta"] = np.frombuffer(json.dumps({"cases": COLLECTIVE_CASES}).encode(),
+                                  dtype=np.uint8)
+    np.savez_compressed(os.path.join(HERE, "golden_collectives.npz"), **colls)
+    print(f"{len(STEP_CASES)} step cases, {len(COLLECTIVE_CASES)} collective cases")
+
+
+if __name__ == "__main__":
+    main()

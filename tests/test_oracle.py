@@ -1,0 +1,150 @@
+"""Pin the CPU oracle against the reference's own golden vectors (CPU only).
+
+The fixtures were produced by the real reference (tests/golden/make_golden.py);
+the hand-written known answers below are the reference tests' own
+(pkg/tests/test_quant.py, test_collectives.py, test_optimizer.py).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import lioncub_oracle as O
+from tests import golden_io as G
+
+
+# ---- known-answer tests of the reference test-suite ------------------------
+
+def test_pack_golden_bytes():
+    # test_quant.py:164-173
+    assert O.pack_words(np.array([3, 12]), 4)[0] == 0xC3
+    assert O.pack_words(np.array([1, 0, 1, 1, 0, 0, 0, 0]), 1)[0] == 0x0D
+    assert O.pack_signs(np.array([-1, 1]))[0] == 0x02
+    v = np.arange(16)
+    assert O.unpack_words(O.pack_words(v, 4), 4, 16).tolist() == v.tolist()
+
+
+def test_quantize_known_answers():
+    # test_quant.py:38-44
+    assert O.quantize_l1(np.array([1.0, -1, 1, -1]), 4).tolist() == [4, -4, 4, -4]
+    assert O.quantize_l1(np.array([7.0, 1, 1, 1]), 4).tolist() == [7, 1, 1, 1]
+    assert not O.quantize_l1(np.zeros(5), 8).any()
+    rng = np.random.default_rng(1)
+    x = rng.laplace(size=257)
+    for c in (1e-6, 0.5, 3.0, 1e7):  # test_quant.py:60-65
+        assert np.array_equal(O.quantize_l1(c * x, 8), O.quantize_l1(x, 8))
+
+
+def test_norm_known_answers():
+    assert O.lp_mean_norm_l1(np.array([1, -1, 1, -1])) == 1.0
+    with pytest.raises(O.OracleConfigError):
+        O.lp_mean_norm_l1(np.array([]))
+
+
+def test_sign_policy():
+    # test_quant.py:143-160
+    assert O.apply_sign(np.array([2.5, -0.1, 0.0]), "exact-ternary", 0).tolist() == [1, -1, 0]
+    assert O.apply_sign(np.array([0.0]), "alternating", 3).tolist() == [1]
+    assert O.apply_sign(np.array([0.0]), "alternating", 4).tolist() == [-1]
+    assert O.apply_sign(np.array([-0.0, 0.0]), "alternating", 1).tolist() == [1, 1]
+
+
+def test_lane_bits():
+    # test_collectives.py:118-124
+    assert O.choose_lane_bits(8, 15) == 8
+    assert O.choose_lane_bits(125, 15) == 16
+    assert O.choose_lane_bits(2, 7) == 8
+    assert O.choose_lane_bits(125, 1, binary_signs=True) == 8
+    with pytest.raises(O.OracleCapacityError):
+        O.choose_lane_bits(10 ** 9, 127)
+
+
+def test_hand_lion_step():
+    # test_optimizer.py:25-31, :39-43
+    h = O.Hyper(0.9, 0.99, 0.1, 0.0)
+    nt, nm = O.lion_step({"w": np.array([0.0])}, {"w": np.array([0.0])},
+                         {"w": np.array([2.0])}, h)
+    assert nt["w"].tolist() == [-0.1]
+    assert nm["w"][0] == pytest.approx(0.02)
+    h = O.Hyper(0.9, 0.99, 0.1, 0.1)
+    nt, _ = O.lion_step({"w": np.array([1.0])}, {"w": np.array([0.0])},
+                        {"w": np.array([0.0])}, h)
+    assert nt["w"][0] == pytest.approx(0.99)
+
+
+def test_tie_parity_two_steps():
+    # test_optimizer.py:137-153: t=1 tie -> +1, t=2 tie -> -1
+    h = O.Hyper(0.9, 0.99, 0.5, 0.0)
+    th = [{"w": np.zeros(1)}, {"w": np.zeros(1)}]
+    m = [{"w": np.zeros(1)}, {"w": np.zeros(1)}]
+    g = [{"w": np.array([1.0])}, {"w": np.array([-1.0])}]
+    th, m, *_ = O.distributed_step(th, m, g, h, O.Spec(1), "compressed1bit", 0)
+    assert th[0]["w"].tolist() == [-0.5]
+    th, m, *_ = O.distributed_step(th, m, g, h, O.Spec(1), "compressed1bit", 1)
+    assert th[0]["w"].tolist() == [0.0]
+
+
+def test_pairwise_sum_is_numpy_order():
+    rng = np.random.default_rng(0)
+    for n in (1, 7, 8, 9, 127, 128, 129, 1000, 4099, 20000):
+        x = np.abs(rng.standard_cauchy(size=n)) * 10.0 ** rng.integers(-6, 6, size=n)
+        assert O.pairwise_sum(x) == float(np.sum(x))
+
+
+def test_mean_within_two_ulp_of_fsum():
+    # test_collectives.py:210-224
+    rng = np.random.default_rng(1)
+    vecs = [rng.normal(size=200) for _ in range(3)]
+    got = O.mean_f32(vecs).astype(np.float64)
+    oracle = O.fsum_mean(vecs)
+    ulp = np.spacing(np.abs(oracle).astype(np.float32)).astype(np.float64)
+    assert np.all(np.abs(got - oracle) <= 2 * ulp)
+
+
+# ---- golden vectors produced by running the reference ----------------------
+
+@pytest.mark.parametrize("name", [c["name"] for c in G.step_cases()])
+def test_oracle_matches_reference_step(name):
+    gc = G.step_case(name)
+    case = gc["case"]
+    world = case["world"]
+    h = O.Hyper(0.9, 0.99, case["lr"], case["wd"])
+    spec = None if case["bits"] is None else O.Spec(case["bits"])
+    thetas = [dict(gc["theta"]) for _ in range(world)]
+    nt, nm, sign, ties, cs, _ = O.distributed_step(
+        thetas, gc["m"], gc["g"], h, spec, case["algo"], case["iteration"],
+        zero_mode=case["zero_mode"], masks=gc["mask"])
+    if case.get("sync"):
+        period, layers = case["sync"]
+        nm = O.sync_momentum(nm, period, layers, case["iteration"] + 1)
+    t = case["iteration"] + 1
+    for k in gc["sizes"]:
+        assert np.array_equal(nt[0][k], gc["theta_out"][k]), k
+        assert np.array_equal(sign[k], gc["sign"][k]), k
+        assert ties[k] == gc["ties"][k], k
+        for r in range(world):
+            assert np.array_equal(nm[r][k], gc["m_out"][r][k]), (k, r)
+            if gc["c"][r][k] is not None:
+                assert np.array_equal(cs[r][k], gc["c"][r][k])
+            if gc["words"][r][k] is not None:
+                s = O.apply_sign(cs[r][k], case["zero_mode"], t)
+                assert np.array_equal(O.pack_signs(s), gc["words"][r][k])
+            if gc["q"][r][k] is not None:
+                assert np.array_equal(O.quantize_l1(cs[r][k], case["bits"]),
+                                      gc["q"][r][k].astype(np.int64))
+                assert O.lp_mean_norm_l1(cs[r][k]) == float(gc["norm"][r][k])
+
+
+@pytest.mark.parametrize("name", [c["name"] for c in G.collective_cases()])
+def test_oracle_matches_reference_collective(name):
+    gc = G.collective_case(name)
+    case = gc["case"]
+    if case["kind"] == "direct":
+        v = O.direct_sum(gc["inputs"], case["q_max"], case.get("binary", False))
+        assert np.array_equal(v.values, gc["values"])
+        assert v.ties == gc["ties"]
+    elif case["kind"] == "compressed":
+        v = O.vote_1bit(gc["inputs"], "alternating", case["t"])
+        assert np.array_equal(v.values, gc["values"])
+        assert v.ties == gc["ties"]
+    else:
+        assert np.array_equal(O.mean_f32(gc["inputs"]), gc["values"])
