@@ -1,0 +1,512 @@
+"""Benchmark of the B200 Lion Cub distributed optimizer step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                    [--workload NAME]
+
+N > 1 runs under torchrun (one process per GPU, NCCL over NVLink).  A "step"
+is one ``distributed_lion_step`` (+ ``maybe_sync_momentum`` where the
+workload syncs) over the workload's full synthetic parameter buffer, inputs
+resident in HBM.  Rank 0 prints ONE JSON line.
+
+Default workload = BASELINE.json configs[1]: the GPT-2-small-sized buffer
+(124,439,808 params in its 148 tensors) with the p-bit sum-of-signs vote
+(algo="direct", QuantSpec(bits=1)).  Every array (498 MB each) is larger
+than the 126 MB L2, so no L2 flush is needed between steps.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+# ---------------------------------------------------------------------------
+# Workloads (BASELINE.json configs)
+# ---------------------------------------------------------------------------
+
+def gpt2_small_layout() -> dict:
+    d, L, V, T = 768, 12, 50257, 1024
+    shapes = {"wte.weight": (V, d), "wpe.weight": (T, d),
+              "ln_f.weight": (d,), "ln_f.bias": (d,)}
+    for i in range(L):
+        p = f"h.{i}."
+        shapes.update({p + "ln_1.weight": (d,), p + "ln_1.bias": (d,),
+                       p + "attn.c_attn.weight": (d, 3 * d), p + "attn.c_attn.bias": (3 * d,),
+                       p + "attn.c_proj.weight": (d, d), p + "attn.c_proj.bias": (d,),
+                       p + "ln_2.weight": (d,), p + "ln_2.bias": (d,),
+                       p + "mlp.c_fc.weight": (d, 4 * d), p + "mlp.c_fc.bias": (4 * d,),
+                       p + "mlp.c_proj.weight": (4 * d, d), p + "mlp.c_proj.bias": (d,)})
+    return shapes
+
+
+def tinyllama_layout() -> dict:
+    d, ff, kv, L, V = 2048, 5632, 256, 22, 32000
+    shapes = {"model.embed_tokens.weight": (V, d), "model.norm.weight": (d,),
+              "lm_head.weight": (V, d)}
+    for i in range(L):
+        p = f"model.layers.{i}."
+        shapes.update({p + "self_attn.q_proj.weight": (d, d),
+                       p + "self_attn.k_proj.weight": (kv, d),
+                       p + "self_attn.v_proj.weight": (kv, d),
+                       p + "self_attn.o_proj.weight": (d, d),
+                       p + "mlp.gate_proj.weight": (ff, d), p + "mlp.up_proj.weight": (ff, d),
+                       p + "mlp.down_proj.weight": (d, ff),
+                       p + "input_layernorm.weight": (d,),
+                       p + "post_attention_layernorm.weight": (d,)})
+    return shapes
+
+
+WORKLOADS = {
+    # name: (layout fn, algo, bits, sync (period, layers) or None, description)
+    "gpt2s_sumsigns": (gpt2_small_layout, "direct", 1, None,
+                       "GPT-2-small-sized buffer, p-bit sum-of-signs vote (configs[1])"),
+    "c1_1bit_1m": (lambda: {"w": (1 << 20,)}, "compressed1bit", None, None,
+                   "1M-param flat buffer, 1-bit compressed vote (configs[0] at GPU scale)"),
+    "tinyllama_1bit_sync": (tinyllama_layout, "compressed1bit", None,
+                            (10, ("model.embed_tokens.weight", "lm_head.weight")),
+                            "TinyLlama-1.1B layout, 1-bit vote, embed/head momentum sync "
+                            "every 10 steps (configs[3])"),
+    "tinyllama_1bit": (tinyllama_layout, "compressed1bit", None, None,
+                       "TinyLlama-1.1B layout, 1-bit vote, no sync"),
+    "gpt2s_l1_5bit": (gpt2_small_layout, "direct", 5, None,
+                      "GPT-2-small-sized buffer, L1 5-bit p-bit vote (paper's 8-bit Lion Cub)"),
+    "gpt2s_ps": (gpt2_small_layout, "ps", None, None,
+                 "GPT-2-small-sized buffer, full-precision (ps) vote"),
+    "flat7b_1bit_sync": (lambda: {"w": (7_000_000_000,)}, "compressed1bit", None,
+                         (1, "all"), "7e9 flat buffer, 1-bit vote + all-layer sync (configs[4])"),
+}
+
+
+def numel(shapes: dict) -> int:
+    return sum(math.prod(s) for s in shapes.values())
+
+
+# ---------------------------------------------------------------------------
+# Algorithmic bytes
+# ---------------------------------------------------------------------------
+
+def kernel_bytes(name: str, n: int, P: int, F: int, kind: str) -> float:
+    """Algorithmic HBM bytes of ONE launch of our kernel on an n-param step."""
+    L = -(-max(-(-n // P), 1) // 1024) * 1024
+    if name == "lc_fused_local_step":
+        return 20.0 * n
+    if name == "lc_encode":
+        if kind == "f64":
+            return 12.0 * n + 8.0 * n
+        return 12.0 * n + n * F / 8.0
+    if name == "lc_apply_update":
+        return 8.0 * n + n / 8.0
+    if name == "lc_vote_bits":
+        return (P + 1) * L / 8.0
+    if name == "lc_fields_vote":
+        return L * F / 8.0 + L / 8.0
+    if name == "lc_f64_sum_vote":
+        return P * L * 8.0 + L / 8.0
+    if name == "lc_mean_f32":
+        return 0.0
+    return 0.0
+
+
+def step_roofline(n: int, P: int, F: int, kind: str, sync_frac: float,
+                  hbm_gbs: float, nvl_gbs: float = 770.0) -> dict:
+    """Whole-step lower bound: max(HBM bytes / HBM BW, NVLink bytes / link BW)."""
+    if P == 1:
+        hbm = 20.0 * n
+        nvl = 0.0
+    elif kind == "1bit":
+        hbm = 20.0 * n + 2 * n / 8.0
+        nvl = 2 * (P - 1) / P * n / 8.0
+    elif kind == "fields":
+        hbm = 20.0 * n + 2 * n * F / 8.0 + 2 * n / 8.0
+        nvl = (P - 1) / P * n * (F + 1) / 8.0
+    else:
+        hbm = 36.0 * n
+        nvl = (P - 1) / P * n * 8.0 + (P - 1) / P * n / 8.0
+    if sync_frac:
+        hbm += 16.0 * sync_frac * n
+        nvl += sync_frac * 2 * (P - 1) / P * 4.0 * n
+    t_h = hbm / (hbm_gbs * 1e9)
+    t_n = nvl / (nvl_gbs * 1e9)
+    return {"hbm_bytes": hbm, "nvlink_bytes": nvl, "t_hbm_ms": t_h * 1e3,
+            "t_nvlink_ms": t_n * 1e3, "bound": "hbm" if t_h >= t_n else "nvlink"}
+
+
+def measured_peaks() -> tuple[dict, str]:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return json.load(f), "measured"
+    except (OSError, ValueError):
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+def traffic_table() -> dict:
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+# ---------------------------------------------------------------------------
+# Clock sampling (NVML, every ~5 ms in a thread)
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x2: "applications_clocks_setting"}
+
+    def __init__(self, device_index: int):
+        self.samples = []
+        self.ok = False
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((time.perf_counter(), sm, rs))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def start(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self, t0: float, t1: float) -> dict:
+        win = [s for s in self.samples if t0 <= s[0] <= t1]
+        if not win:  # region shorter than the sampling period: nearest samples
+            win = sorted(self.samples, key=lambda s: abs(s[0] - (t0 + t1) / 2))[:3]
+        if not win:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        mask = 0
+        for s in win:
+            mask |= s[2]
+        reasons = sorted({v for k, v in self.REASONS.items() if mask & k})
+        return {"sm_mhz": statistics.median(s[1] for s in win),
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(win)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline / reference arm: the oracle port on the host cores
+# ---------------------------------------------------------------------------
+
+def cpu_reference(world: int, algo: str, bits, sample: int, budget_s: float,
+                  threads: int | None = None) -> dict:
+    """Time the reference algorithm (oracle restatement of
+    optimizer.distributed_lion_step, ranks simulated in one process) on a
+    bounded sample.  Element chunks run on a thread pool (numpy releases the
+    GIL), so ``cores`` threads work at once."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import numpy as np
+
+    from oracle import lioncub_oracle as O
+
+    cores = threads or len(os.sched_getaffinity(0))
+    ranks = O.synth_rank_inputs(0, world, {"w": (sample,)}, "laplace")
+    h = O.Hyper(0.9, 0.99, 1e-4, 0.0)
+    spec = None if bits is None else O.Spec(bits)
+    chunk = -(-sample // cores)
+    pieces = []
+    for a in range(0, sample, chunk):
+        b = min(sample, a + chunk)
+        pieces.append(([{"w": rk["theta"]["w"][a:b]} for rk in ranks],
+                       [{"w": rk["m"]["w"][a:b]} for rk in ranks],
+                       [{"w": rk["g"]["w"][a:b]} for rk in ranks]))
+
+    def one(piece):
+        th, m, g = piece
+        O.distributed_step(th, m, g, h, spec, algo, 0)
+
+    times = []
+    with ThreadPoolExecutor(max_workers=cores) as ex:
+        list(ex.map(one, pieces))  # warm
+        t_end = time.perf_counter() + budget_s
+        while True:
+            t0 = time.perf_counter()
+            list(ex.map(one, pieces))
+            times.append(time.perf_counter() - t0)
+            if time.perf_counter() > t_end and len(times) >= 2:
+                break
+    t = statistics.median(times)
+    return {"value": world * sample / t, "unit": "params/s", "cores": cores,
+            "kind": "port", "sec_per_step": t, "steps": len(times),
+            "sample": f"{sample}-param slice per rank x {world} simulated ranks "
+                      f"({algo}{'' if bits is None else f', bits={bits}'}), float64 numpy "
+                      f"port of optimizer.distributed_lion_step on {cores} host threads"}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    layout_fn, algo, bits, sync, desc = WORKLOADS[args.workload]
+    n = numel(layout_fn())
+    world = args.gpus
+    sample = min(n, args.ref_sample)
+    steps = []
+    ref = cpu_reference(world, algo, bits, sample, budget_s=0.0)
+    per = ref["sec_per_step"]
+    for _ in range(args.warmup + args.steps):
+        r = cpu_reference(world, algo, bits, sample, budget_s=0.0)
+        steps.append(r["sec_per_step"])
+    timed = steps[args.warmup:]
+    t = sum(timed) / len(timed)
+    value = world * sample / t
+    line = {"metric": METRIC, "value": value, "unit": "params/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": args.workload, "description": desc, "params": n,
+                       "algo": algo, "bits": bits, "world": world,
+                       "sample_params_per_rank": sample},
+            "cpu_baseline": {"value": value, "unit": "params/s", "cores": ref["cores"],
+                             "kind": "port", "sample": ref["sample"]},
+            "e2e": {"value": value, "unit": "params/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "note": f"first-call {per * 1e3:.1f} ms"}
+    print(json.dumps(line))
+    return 0
+
+
+METRIC = "Lion Cub step time (ms) & params/s at 1/2/4/8 B200, % of HBM/NVLink roofline"
+
+
+# ---------------------------------------------------------------------------
+# The B200 arm
+# ---------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="gpt2s_sumsigns", choices=sorted(WORKLOADS))
+    ap.add_argument("--ref-sample", type=int, default=1 << 22)
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2411_16462_b200 as lc
+    from paper_2411_16462_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if rank == 0:
+            print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    _lib.load()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        transport = lc.NcclTransport.init_process(rank, world, dev)
+    else:
+        transport = lc.LocalTransport(1, device=dev)
+    topo = lc.Topology(world_size=world, rank=rank, transport=transport)
+
+    layout_fn, algo, bits, sync, desc = WORKLOADS[args.workload]
+    shapes = layout_fn()
+    n = numel(shapes)
+    spec = None if bits is None else lc.QuantSpec(bits=bits, norm_p=1.0)
+    policy = None
+    sync_frac = 0.0
+    if sync is not None:
+        period, layers = sync
+        policy = lc.SyncPolicy(period=period, layers=layers if isinstance(layers, str)
+                               else frozenset(layers))
+        sel = n if layers == "all" else sum(math.prod(shapes[k]) for k in layers)
+        sync_frac = sel / n / period
+    h = lc.LionHyper(beta1=0.9, beta2=0.99, lr=1e-4, weight_decay=0.0)
+
+    # synthetic state: theta shared (seed 0), m and g per rank; g = base + noise
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(0)
+    st = lc.WorkerState.initial({"_": torch.zeros(1, device=dev)})  # placeholder
+    layout = lc.Layout(shapes)
+    theta = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
+    theta.normal_(generator=gen)
+    base = torch.empty_like(theta).exponential_(generator=gen)
+    base *= torch.where(torch.rand(theta.shape, generator=gen, device=dev) < 0.5, -1.0, 1.0)
+    gen.manual_seed(1000 + rank)
+    mom = torch.empty_like(theta).normal_(generator=gen).mul_(0.1)
+    noise = torch.empty_like(theta).exponential_(generator=gen)
+    noise *= torch.where(torch.rand(theta.shape, generator=gen, device=dev) < 0.5, -1.0, 1.0)
+    grad = base.add_(noise)
+    del noise
+    st = lc.WorkerState(params=layout.views(theta), momentum=layout.views(mom), iteration=0)
+    g = layout.views(grad)
+    stream = topo.stream
+    torch.cuda.synchronize()
+
+    def step(state):
+        state = lc.distributed_lion_step(state, g, h, spec, topo, algo)
+        if policy is not None:
+            state = lc.maybe_sync_momentum(state, policy, topo)
+        return state
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        st = step(st)
+    sampler = ClockSampler(local)
+    sampler.start()
+    # untimed soak so the clock sampler sees the part under load
+    soak_end = time.perf_counter() + 0.3
+    while time.perf_counter() < soak_end:
+        st = step(st)
+        torch.cuda.synchronize()
+    barrier()
+    _lib.phase_events = {}
+    l0 = _lib.launches
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(args.steps):
+        st = step(st)
+    e1.record(stream)
+    barrier()
+    w1 = time.perf_counter()
+    launches = _lib.launches - l0
+    phases = _lib.phase_events
+    _lib.phase_events = None
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    clocks = sampler.summary(w0, w1)
+    sampler.stop()
+
+    # per-kernel average durations over the timed region
+    kern = {}
+    for name, evs in phases.items():
+        d = [a.elapsed_time(b) for a, b in evs]
+        kern[name] = {"launches": len(d), "avg_ms": sum(d) / len(d), "total_ms": sum(d)}
+    dominant = max(kern, key=lambda k: kern[k]["total_ms"]) if kern else None
+
+    peaks, peak_src = measured_peaks()
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    P = world
+    if algo == "compressed1bit":
+        kind, F = "1bit", 1
+    elif bits is None:
+        kind, F = "f64", 64
+    else:
+        kind = "fields"
+        F = lc.field_bits(P, 1 if bits == 1 else 2 * ((1 << (bits - 1)) - 1))
+    roof = None
+    if dominant:
+        bpl = kernel_bytes(dominant, n, P, F, kind)
+        ach = bpl / (kern[dominant]["avg_ms"] * 1e-3) / 1e9
+        tt = traffic_table().get(f"{args.workload}/P{P}/{dominant}")
+        roof = {"kernel": dominant, "bound": "hbm", "achieved": ach, "peak": hbm_peak,
+                "unit": "GB/s", "frac": ach / hbm_peak, "traffic": tt,
+                "algorithmic_bytes_per_launch": bpl,
+                "avg_launch_ms": kern[dominant]["avg_ms"],
+                "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs" if peak_src ==
+                "measured" else "fallback 6650 GB/s (B200_PROFILING.md)"}
+    sr = step_roofline(n, P, F, kind, sync_frac, hbm_peak)
+    sr["frac"] = max(sr["t_hbm_ms"], sr["t_nvlink_ms"]) / ms
+
+    # end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        host_g = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        host_g.copy_(grad[:n].cpu())
+        host_t = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        barrier()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(args.steps):
+                g.flat[:n].copy_(host_g, non_blocking=True)
+                st = step(st)
+                host_t.copy_(st.params.flat[:n], non_blocking=True)
+        f1.record(stream)
+        barrier()
+        ems = f0.elapsed_time(f1) / args.steps
+        if world > 1:
+            t = torch.tensor([ems], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": P * n / (ems * 1e-3), "unit": "params/s", "ms_per_step": ems,
+               "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n,
+               "path": "pinned host grads -> distributed_lion_step -> pinned host theta"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_reference(1, algo, bits, min(n, args.ref_sample), args.cpu_budget)
+        cpu.pop("sec_per_step", None)
+        cpu.pop("steps", None)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": P * n / (ms * 1e-3), "unit": "params/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "fp32 state, f64 math",
+                "data": "synthetic (Laplace-correlated grads, runner.py:289-297 recipe)",
+                "config": {"workload": args.workload, "description": desc, "params": n,
+                           "tensors": len(shapes), "algo": algo, "bits": bits,
+                           "parallelism": f"dp{world}", "field_bits": F,
+                           "l2": "inputs larger than L2 (no flush needed)"},
+                "roofline": roof, "step_roofline": sr, "kernels": kern,
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clocks}
+        print(json.dumps(line))
+    if world > 1:
+        transport.close()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,228 @@
+/*
+ * lioncub.h — C ABI of the B200-native Lion Cub distributed optimizer step.
+ *
+ * Everything is plain pointers, sizes and scalars (no torch types).  Device
+ * pointers point into CUDA global memory of the calling thread's current
+ * device; `stream` is a cudaStream_t passed as void*.  Every entry point
+ * returns 0 (LC_OK) or a negative LC_E_* code; lc_last_error() gives the
+ * thread-local message.  Kernels are enqueued asynchronously on `stream`.
+ *
+ * The reference (lioncomm, pure numpy, /root/reference/pkg/src/lioncomm) has
+ * no native code; each entry point below names the reference function whose
+ * per-layer numpy computation it replaces (file:line).  The Python host side
+ * (paper_2411_16462_b200/optimizer.py, collectives.py) keeps the reference's
+ * API and calls these through ctypes; INTEGRATION.md shows the binding.
+ */
+#ifndef LIONCUB_H_
+#define LIONCUB_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define LIONCUB_ABI_VERSION 1
+
+enum {
+  LC_OK = 0,
+  LC_E_CONFIG = -1,     /* -> ConfigError      (errors.py:8)            */
+  LC_E_CAPACITY = -2,   /* -> CapacityError    (errors.py:12-16)        */
+  LC_E_COLLECTIVE = -3, /* -> CollectiveError  (errors.py:35-52)        */
+  LC_E_CUDA = -4,       /* CUDA runtime failure                          */
+  LC_E_ARG = -5         /* bad pointer / size / alignment                */
+};
+
+/* Device flag bits written by the kernels (checked by the host shim). */
+enum {
+  LC_FLAG_ZERO_SIGN = 1u << 0, /* exact zero on a path that cannot carry it
+                                  (collectives.py:264-267, :202-203)        */
+  LC_FLAG_NAN = 1u << 1,       /* NaN in c (reference: PackRangeError)      */
+  LC_FLAG_TIE_TERNARY = 1u << 2, /* tied 1-bit vote in exact-ternary mode
+                                    (collectives.py:290-293)               */
+  LC_FLAG_RANGE = 1u << 3      /* |q| > q_max / non-binary value
+                                  (collectives.py:202-208)                  */
+};
+
+/* Encodings produced by the fused interpolate pass (lc_encode). */
+enum {
+  LC_ENC_SIGN1 = 0,       /* 1-bit sign words (compressed1bit)            */
+  LC_ENC_SIGN_FIELDS = 1, /* (s+1)>>1 in F-bit fields (sum-of-signs)      */
+  LC_ENC_QUANT_FIELDS = 2,/* q+q_max in F-bit fields (L1 p-bit)           */
+  LC_ENC_F64 = 3          /* c as float64 (full-precision ps arm)         */
+};
+
+typedef struct lc_hyper {
+  double beta1, one_minus_beta1; /* 1-b1 computed on the host in f64 */
+  double beta2, one_minus_beta2;
+  double lr;                     /* eta_t = LionHyper.lr_at(t)        */
+  double weight_decay;
+} lc_hyper;
+
+/* Per-layer segment table of a flat buffer (layers in sorted-name order). */
+typedef struct lc_segments {
+  const int64_t* start; /* device, nseg+1 offsets (elements)               */
+  const double* scale;  /* device, nseg quant scales qmax/(2 M1) or NULL   */
+  int32_t nseg;
+  int32_t qmax;
+} lc_segments;
+
+int lc_abi_version(void);
+const char* lc_last_error(void);
+int lc_device_sm_count(int device);
+
+/* ---- K1: fused Lion interpolate + sign/quantize + pack + momentum EMA ----
+ * Replaces optimizer.py:199-201 (c, mask), :205 (m'), quant.py:273-279
+ * (apply_sign), quant.py:330-356 (pack width 1 / F-bit fields),
+ * quant.py:236-243 (finite-p quantize given the per-layer scale), and the
+ * offsetting of collectives.py:201-210.  Computes c and m' in float64 from
+ * fp32 g,m (no FMA contraction) and writes m' (fp32) in place.
+ *   fill: +1 / -1 = alternating zero fill (quant.py:151-153), 0 = ternary.
+ *   field_bits: 1 for SIGN1, F in {1,2,4,8,16,32} for *_FIELDS, 64 for F64.
+ *   out: uint32 words (ceil(n*F/32)) or double[n].
+ *   g, m must be 16-byte aligned. mask may be NULL (uint8 per element). */
+int lc_encode(const float* g, float* m, const uint8_t* mask, int64_t n,
+              const lc_hyper* h, int fill, int enc, int field_bits,
+              const lc_segments* segs, void* out, uint32_t* flags,
+              void* stream);
+
+/* ---- K4: owner-side 1-bit majority vote over P packed chunks ----
+ * Replaces collectives.py:288-293 (stack+sum, local ties, apply_sign).
+ * recv: [P][cw] words, chunk of element range starting at bit 0;
+ * n_valid: number of real elements in this chunk (pads excluded).
+ * voted: cw words. tie_bits (nullable): 1 where the tally is 0. */
+int lc_vote_bits(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid,
+                 int fill, uint32_t* voted, uint32_t* tie_bits,
+                 uint32_t* flags, void* stream);
+
+/* ---- K6: owner-side p-bit sums -> signed aggregate -> 1-bit vote ----
+ * Replaces collectives.py:241-249 (de-offset, ties) + :313-316
+ * (majority_sign).  sums: F-bit fields holding sum of stored values for
+ * n elements (n multiple of 32 words-worth is not required).
+ * offset: q_max (0 with binary=1 for sum-of-signs, signed = 2k-P).
+ * voted/nz/tie: 1-bit words; nz (nullable) marks non-zero aggregates
+ * (exact-ternary), values (nullable): signed aggregate as int64. */
+int lc_fields_vote(const uint32_t* sums, int64_t n, int32_t field_bits,
+                   int32_t P, int32_t offset, int32_t binary, int fill,
+                   uint32_t* voted, uint32_t* nz, uint32_t* tie_bits,
+                   int64_t* values, void* stream);
+
+/* ---- full-precision arm: P float64 rows (row stride `stride`) -> sum of
+ * the first `len` elements in the reference's rank order (flat,
+ * collectives.py:153-158, or binomial tree :96-109) -> sign words.
+ * values (nullable) receives the f64 sum. */
+int lc_f64_sum_vote(const double* recv, int32_t P, int64_t len, int64_t stride,
+                    int tree, int fill, uint32_t* voted, uint32_t* nz,
+                    uint32_t* tie_bits, double* values, void* stream);
+
+/* ---- K5: theta' = theta - eta*(s + wd*theta)  (optimizer.py:204) ----
+ * s = +1/-1 from sign bits; 0 where nz_bits (nullable) has a 0 bit. */
+int lc_apply_update(float* theta, int64_t n, const uint32_t* sign_bits,
+                    const uint32_t* nz_bits, double lr, double weight_decay,
+                    void* stream);
+
+/* ---- one-pass step for P == 1 (no exchange: the vote of one rank is its
+ * own aggregate): reads theta,m,g, writes theta',m' (20 B/param).
+ * mode: LC_LOCAL_BINARY  sign(c) with the fill BEFORE aggregation
+ *                        (compressed1bit, direct bits=1; a zero in
+ *                        exact-ternary mode sets LC_FLAG_ZERO_SIGN),
+ *       LC_LOCAL_PS      aggregate = c (ps, spec=None), ties = #(c==0),
+ *       LC_LOCAL_QUANT   aggregate = L1-quantized c (needs segs->scale).
+ * Optional metric outputs (nullable): sign_bits/nz_bits = applied sign,
+ * tie_bits = aggregate exactly zero. */
+enum { LC_LOCAL_BINARY = 0, LC_LOCAL_PS = 1, LC_LOCAL_QUANT = 2 };
+int lc_fused_local_step(float* theta, float* m, const float* g,
+                        const uint8_t* mask, int64_t n, const lc_hyper* h,
+                        int fill, int mode, const lc_segments* segs,
+                        uint32_t* sign_bits, uint32_t* nz_bits,
+                        uint32_t* tie_bits, uint32_t* flags, void* stream);
+
+/* ---- K7: momentum mean (collectives.py:336-340): f64 rank-ordered sum of P
+ * fp32 rows (row stride in elements), /P, one rounding to fp32. */
+int lc_mean_f32(const float* recv, int32_t P, int64_t len, int64_t stride,
+                float* out, void* stream);
+
+/* ---- L1 norm per segment, numpy-exact (quant.py:156-179, p=1):
+ * M1 = max|c| * (pairwise_sum(|c|/max) / n) with numpy's pairwise
+ * summation order reproduced exactly; c recomputed from g,m,mask.
+ * Writes per-segment norms and scale = qmax/(2 M1) (0 if M1 == 0),
+ * quant.py:236.  The plan holds the summation-tree schedule (device). */
+typedef struct lc_l1_plan_s* lc_l1_plan_t;
+int lc_l1_plan_create(lc_l1_plan_t* plan, const int64_t* seg_start_host,
+                      int32_t nseg);
+int lc_l1_plan_destroy(lc_l1_plan_t plan);
+int lc_l1_scales(lc_l1_plan_t plan, const float* g, const float* m,
+                 const uint8_t* mask, const lc_hyper* h, int32_t qmax,
+                 double* norms, double* scales, void* stream);
+
+/* ---- metrics / operator helpers ---- */
+/* c as float64 (metrics_out["c_local"], optimizer.py:209). */
+int lc_compute_c(const float* g, const float* m, const uint8_t* mask,
+                 int64_t n, const lc_hyper* h, double* c, void* stream);
+/* Per-segment popcount of bit words (ties per layer, optimizer.py:207). */
+int lc_count_bits_segmented(const uint32_t* bits, const int64_t* seg_start,
+                            int32_t nseg, int64_t* counts, void* stream);
+/* bits -> int8 +-1 (0 where nz bit is 0): vote_sign (optimizer.py:208). */
+int lc_bits_to_sign(const uint32_t* sign_bits, const uint32_t* nz_bits,
+                    int64_t n, int8_t* out, void* stream);
+/* int64 values -> F-bit fields of v+offset (binary: (v+1)>>1), range check
+ * into flags (collectives.py:201-210, quant.py:330-356). */
+int lc_pack_i64_fields(const int64_t* v, int64_t n, int32_t field_bits,
+                       int32_t offset, int32_t binary, uint32_t* out,
+                       uint32_t* flags, void* stream);
+/* F-bit fields of sums -> signed int64 aggregate (collectives.py:241-247). */
+int lc_fields_decode(const uint32_t* sums, int64_t n, int32_t field_bits,
+                     int32_t P, int32_t offset, int32_t binary, int64_t* out,
+                     void* stream);
+/* sign of a float64/float32 vector with fill -> 1-bit words (K1 without
+ * the Lion interpolation; compressed_allreduce_1bit on raw c). */
+int lc_sign_pack_f64(const double* c, int64_t n, int fill, uint32_t* out,
+                     uint32_t* flags, void* stream);
+/* Sum of P uint32 rows into out (the in-process transport's reduce). */
+int lc_sum_u32_rows(const uint32_t* const* rows, int32_t P, int64_t count,
+                    uint32_t* out, void* stream);
+
+/* ---- NCCL transport (one communicator per GPU rank) ----
+ * The reference's plugin boundary is Transport.send/recv (transport.py:32-45);
+ * on B200 the collective boundary is an NCCL communicator over NVLink. */
+typedef struct lc_comm_s* lc_comm_t;
+int lc_nccl_version(void);
+int lc_nccl_unique_id(uint8_t out[128]);
+int lc_comm_init_rank(lc_comm_t* comm, const uint8_t id[128], int32_t nranks,
+                      int32_t rank);
+int lc_comm_init_all(lc_comm_t* comms, int32_t ndev, const int32_t* devices);
+int lc_comm_destroy(lc_comm_t comm);
+int lc_comm_abort(lc_comm_t comm);
+/* LC_OK, or LC_E_COLLECTIVE if the communicator hit an asynchronous error. */
+int lc_comm_check(lc_comm_t comm);
+/* Equal-block all-to-all: block j of send goes to rank j, block i of recv
+ * comes from rank i (collectives.py:276-286 stage 1). */
+int lc_alltoall(lc_comm_t comm, const void* send, void* recv,
+                int64_t bytes_per_peer, void* stream);
+/* Variable all-to-all (host byte counts/displacements, P entries each). */
+int lc_alltoallv(lc_comm_t comm, const void* send, const int64_t* send_bytes,
+                 const int64_t* send_displ, void* recv,
+                 const int64_t* recv_bytes, const int64_t* recv_displ,
+                 void* stream);
+/* AllGather; in place when send == recv + rank*bytes (collectives.py:295-306). */
+int lc_allgather(lc_comm_t comm, const void* send, void* recv, int64_t bytes,
+                 void* stream);
+/* ReduceScatter(sum) on uint32 words of packed fields: carry-free because
+ * the capacity check bounds every field sum (collectives.py:196-199,226-231). */
+int lc_reduce_scatter_u32(lc_comm_t comm, const uint32_t* send, uint32_t* recv,
+                          int64_t count_per_rank, void* stream);
+int lc_allreduce_max_u32(lc_comm_t comm, const uint32_t* send, uint32_t* recv,
+                         int64_t count, void* stream);
+int lc_allreduce_sum_i64(lc_comm_t comm, const int64_t* send, int64_t* recv,
+                         int64_t count, void* stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* LIONCUB_H_ */

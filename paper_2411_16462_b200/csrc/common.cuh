@@ -1,0 +1,92 @@
+// Shared helpers for the Lion Cub sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "lioncub.h"
+
+namespace lc {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// Thread-local error message behind lc_last_error().
+std::string& err_msg();
+int set_err(int code, const char* fmt, ...);
+
+#define LC_CUDA_TRY(expr)                                                    \
+  do {                                                                       \
+    cudaError_t e_ = (expr);                                                 \
+    if (e_ != cudaSuccess)                                                   \
+      return ::lc::set_err(LC_E_CUDA, "%s: %s (%s:%d)", #expr,               \
+                           cudaGetErrorString(e_), __FILE__, __LINE__);      \
+  } while (0)
+
+#define LC_LAUNCH_CHECK() LC_CUDA_TRY(cudaPeekAtLastError())
+
+// SMs of the current device (cached per device).
+int sm_count();
+
+// Grid size for a grid-stride streaming kernel: enough resident CTAs to fill
+// every SM (occupancy-derived), never more than the work needs.
+template <typename K>
+int stream_grid(K kernel, int block, int64_t work_items, int items_per_cta) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0);
+  if (per_sm < 1) per_sm = 1;
+  int64_t need = (work_items + items_per_cta - 1) / items_per_cta;
+  int64_t cap = (int64_t)sm_count() * per_sm;
+  int64_t g = need < cap ? need : cap;
+  return g < 1 ? 1 : (int)g;
+}
+
+struct Hyp {
+  double b1, omb1, b2, omb2;
+};
+
+// c = beta1*m + (1-beta1)*g in float64, each product and the sum rounded
+// separately exactly like numpy (optimizer.py:199); no FMA contraction.
+__device__ __forceinline__ double lion_c(float m, float g, const Hyp& h) {
+  return __dadd_rn(__dmul_rn(h.b1, (double)m), __dmul_rn(h.omb1, (double)g));
+}
+
+// m' = beta2*m + (1-beta2)*g (optimizer.py:205), rounded once to fp32.
+__device__ __forceinline__ float lion_m(float m, float g, const Hyp& h) {
+  return __double2float_rn(
+      __dadd_rn(__dmul_rn(h.b2, (double)m), __dmul_rn(h.omb2, (double)g)));
+}
+
+// theta' = theta - eta*(s + wd*theta) (optimizer.py:204), float64 then fp32.
+__device__ __forceinline__ float lion_theta(float th, double s, double lr,
+                                            double wd) {
+  double t = (double)th;
+  return __double2float_rn(
+      __dsub_rn(t, __dmul_rn(lr, __dadd_rn(s, __dmul_rn(wd, t)))));
+}
+
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+  return __ldcs(p);
+}
+__device__ __forceinline__ void st_stream(float4* p, float4 v) {
+  __stcs(p, v);
+}
+
+// Index of the segment containing element e: start[s] <= e < start[s+1].
+__device__ __forceinline__ int seg_find(const int64_t* __restrict__ start,
+                                        int nseg, int64_t e) {
+  int lo = 0, hi = nseg - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (__ldg(start + mid) <= e)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+}  // namespace lc

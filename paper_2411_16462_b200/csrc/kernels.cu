@@ -1,0 +1,1030 @@
+// Lion Cub distributed-step kernels for B200 (sm_100a).
+//
+// All kernels stream fp32 state with 128-bit loads: one warp covers a tile of
+// 128 consecutive elements (lane l owns elements 4l..4l+3), so the 1-bit words
+// of a tile (bit b of word w = element 32w+b, quant.py:330-356 layout) are
+// assembled with three shuffle-ORs across the 8 lanes that share a word.
+// Math that decides a sign (c, the p-bit scale, the update) runs in float64
+// with every product/sum rounded separately (no FMA contraction) so results
+// equal the float64 numpy reference bit-for-bit; fp32 state is rounded once.
+#include "common.cuh"
+
+namespace lc {
+
+std::string& err_msg() {
+  static thread_local std::string s;
+  return s;
+}
+
+int set_err(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  err_msg() = buf;
+  return code;
+}
+
+int sm_count() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = v > 0 ? v : 148;
+  }
+  return cache[dev];
+}
+
+struct SegQ {
+  const int64_t* start;
+  const double* scale;
+  int nseg;
+  int qmax;
+};
+
+// Per-lane cache of the segment (layer) containing the current element.
+struct SegCursor {
+  int64_t lo = 0, hi = -1;
+  double scale = 0.0;
+  __device__ __forceinline__ double get(const SegQ& sq, int64_t e) {
+    if (e < lo || e >= hi) {
+      int s = seg_find(sq.start, sq.nseg, e);
+      lo = __ldg(sq.start + s);
+      hi = __ldg(sq.start + s + 1);
+      scale = __ldg(sq.scale + s);
+    }
+    return scale;
+  }
+};
+
+// q = clip(round_half_even(scale*c), +-qmax)   (quant.py:236-243)
+__device__ __forceinline__ int quant_l1(double c, double scale, int qmax) {
+  double r = rint(__dmul_rn(scale, c));
+  r = fmin(fmax(r, -(double)qmax), (double)qmax);
+  return (int)r;
+}
+
+// Pack 4 F-bit values per lane into the tile's words (element-major layout).
+template <int F>
+__device__ __forceinline__ void pack_store(uint32_t* __restrict__ out,
+                                           int64_t t, int lane,
+                                           const uint32_t st[4],
+                                           int64_t nwords, bool full) {
+  if constexpr (F <= 8) {
+    constexpr int LPW = 8 / F;  // lanes sharing one 32-bit word
+    uint32_t v = st[0] | (st[1] << F) | (st[2] << (2 * F)) | (st[3] << (3 * F));
+    v <<= (4 * F) * (lane % LPW);
+#pragma unroll
+    for (int s = 1; s < LPW; s <<= 1) v |= __shfl_xor_sync(kFull, v, s);
+    int64_t w = t * (4 * F) + lane / LPW;
+    if (lane % LPW == 0 && (full || w < nwords)) out[w] = v;
+  } else if constexpr (F == 16) {
+    uint32_t w0 = st[0] | (st[1] << 16), w1 = st[2] | (st[3] << 16);
+    int64_t w = t * 64 + 2 * lane;
+    if (full) {
+      *reinterpret_cast<uint2*>(out + w) = make_uint2(w0, w1);
+    } else {
+      if (w < nwords) out[w] = w0;
+      if (w + 1 < nwords) out[w + 1] = w1;
+    }
+  } else {
+    int64_t w = t * 128 + 4 * lane;
+    if (full) {
+      *reinterpret_cast<uint4*>(out + w) = make_uint4(st[0], st[1], st[2], st[3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (w + k < nwords) out[w + k] = st[k];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1: c, m', encode.  One warp per 128-element tile, U tiles in flight.
+// ---------------------------------------------------------------------------
+template <int ENC, int F, bool MASK, int U>
+__global__ void __launch_bounds__(256)
+k_encode(const float* __restrict__ g, float* __restrict__ m,
+         const uint8_t* __restrict__ mask, int64_t n, Hyp h, int fill, SegQ sq,
+         void* __restrict__ out, uint32_t* __restrict__ flags) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t ntiles = (n + 127) >> 7, nfull = n >> 7;
+  const int64_t nwords = (ENC == LC_ENC_F64) ? 0 : (n * F + 31) / 32;
+  const bool ternary = fill == 0;
+  const uint32_t fillbit = fill > 0 ? 1u : 0u;
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  float4* m4 = reinterpret_cast<float4*>(m);
+  uint32_t flag = 0;
+  SegCursor cur;
+
+  for (int64_t t0 = gw; t0 < ntiles; t0 += nw * U) {
+    float4 gv[U], mv[U];
+    uchar4 mk[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      int64_t t = t0 + u * nw;
+      if (t < nfull) {
+        gv[u] = ld_stream(g4 + t * 32 + lane);
+        mv[u] = ld_stream(m4 + t * 32 + lane);
+        if (MASK) mk[u] = *reinterpret_cast<const uchar4*>(mask + t * 128 + lane * 4);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t t = t0 + u * nw;
+      if (t >= ntiles) break;  // warp-uniform
+      const bool full = t < nfull;
+      const int64_t e0 = t * 128 + lane * 4;
+      float ge[4], me[4];
+      bool valid[4], keep[4];
+      if (full) {
+        ge[0] = gv[u].x; ge[1] = gv[u].y; ge[2] = gv[u].z; ge[3] = gv[u].w;
+        me[0] = mv[u].x; me[1] = mv[u].y; me[2] = mv[u].z; me[3] = mv[u].w;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) valid[k] = true;
+        if (MASK) {
+          keep[0] = mk[u].x; keep[1] = mk[u].y; keep[2] = mk[u].z; keep[3] = mk[u].w;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          valid[k] = e0 + k < n;
+          ge[k] = valid[k] ? g[e0 + k] : 0.f;
+          me[k] = valid[k] ? m[e0 + k] : 0.f;
+          keep[k] = MASK ? (valid[k] ? mask[e0 + k] != 0 : true) : true;
+        }
+      }
+      double c[4];
+      float mn[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        c[k] = lion_c(me[k], ge[k], h);
+        if (MASK && !keep[k]) c[k] = 0.0;  // np.where(mask, c, 0.0)
+        mn[k] = lion_m(me[k], ge[k], h);
+      }
+      if (full) {
+        st_stream(m4 + t * 32 + lane, make_float4(mn[0], mn[1], mn[2], mn[3]));
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (valid[k]) m[e0 + k] = mn[k];
+      }
+      if constexpr (ENC == LC_ENC_F64) {
+        double* o = reinterpret_cast<double*>(out);
+        if (full) {
+          __stcs(reinterpret_cast<double2*>(o + e0), make_double2(c[0], c[1]));
+          __stcs(reinterpret_cast<double2*>(o + e0 + 2), make_double2(c[2], c[3]));
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (valid[k]) o[e0 + k] = c[k];
+        }
+      } else {
+        uint32_t st[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (ENC == LC_ENC_QUANT_FIELDS) {
+            if (valid[k]) {
+              double sc = cur.get(sq, e0 + k);
+              st[k] = (uint32_t)(quant_l1(c[k], sc, sq.qmax) + sq.qmax);
+            } else {
+              st[k] = 0u;
+            }
+          } else {
+            uint32_t b;
+            if (c[k] > 0.0) {
+              b = 1u;
+            } else if (c[k] < 0.0) {
+              b = 0u;
+            } else if (c[k] == 0.0) {  // -0.0 included (np.sign(-0.0) == 0)
+              b = fillbit;
+              if (ternary && valid[k]) flag |= LC_FLAG_ZERO_SIGN;
+            } else {
+              b = 0u;
+              if (valid[k]) flag |= LC_FLAG_NAN;
+            }
+            // pad with +1 on the 1-bit wire like collectives.py:269-271
+            st[k] = valid[k] ? b : (ENC == LC_ENC_SIGN1 ? 1u : 0u);
+          }
+        }
+        pack_store<F>(reinterpret_cast<uint32_t*>(out), t, lane, st, nwords, full);
+      }
+    }
+  }
+  if (flag) atomicOr(flags, flag);
+}
+
+// ---------------------------------------------------------------------------
+// K5: theta update from (sign bits, optional nonzero bits).
+// ---------------------------------------------------------------------------
+template <bool NZ, int U>
+__global__ void __launch_bounds__(256)
+k_apply_update(float* __restrict__ theta, int64_t n,
+               const uint32_t* __restrict__ sb, const uint32_t* __restrict__ nzb,
+               double lr, double wd) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t ntiles = (n + 127) >> 7, nfull = n >> 7;
+  float4* th4 = reinterpret_cast<float4*>(theta);
+  for (int64_t t0 = gw; t0 < ntiles; t0 += nw * U) {
+    float4 tv[U];
+    uint32_t sw[U], zw[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      int64_t t = t0 + u * nw;
+      if (t < ntiles) {
+        sw[u] = __ldg(sb + t * 4 + (lane >> 3));
+        zw[u] = NZ ? __ldg(nzb + t * 4 + (lane >> 3)) : ~0u;
+        if (t < nfull) tv[u] = ld_stream(th4 + t * 32 + lane);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t t = t0 + u * nw;
+      if (t >= ntiles) break;
+      const int sh = 4 * (lane & 7);
+      const uint32_t sn = (sw[u] >> sh) & 0xF, zn = (zw[u] >> sh) & 0xF;
+      double s[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        s[k] = ((zn >> k) & 1) ? (((sn >> k) & 1) ? 1.0 : -1.0) : 0.0;
+      if (t < nfull) {
+        float4 v = tv[u];
+        v.x = lion_theta(v.x, s[0], lr, wd);
+        v.y = lion_theta(v.y, s[1], lr, wd);
+        v.z = lion_theta(v.z, s[2], lr, wd);
+        v.w = lion_theta(v.w, s[3], lr, wd);
+        st_stream(th4 + t * 32 + lane, v);
+      } else {
+        const int64_t e0 = t * 128 + lane * 4;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (e0 + k < n) theta[e0 + k] = lion_theta(theta[e0 + k], s[k], lr, wd);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fused single-rank step (P == 1): one pass, theta/m/g in, theta'/m' out.
+// ---------------------------------------------------------------------------
+template <int MODE, bool MASK, bool METRICS, int U>
+__global__ void __launch_bounds__(256)
+k_fused_local(float* __restrict__ theta, float* __restrict__ m,
+              const float* __restrict__ g, const uint8_t* __restrict__ mask,
+              int64_t n, Hyp h, double lr, double wd, int fill, SegQ sq,
+              uint32_t* __restrict__ sbits, uint32_t* __restrict__ nzbits,
+              uint32_t* __restrict__ tbits, uint32_t* __restrict__ flags) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t ntiles = (n + 127) >> 7, nfull = n >> 7;
+  const int64_t nwords = (n + 31) >> 5;
+  const bool ternary = fill == 0;
+  const double fillv = fill > 0 ? 1.0 : (fill < 0 ? -1.0 : 0.0);
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  float4* m4 = reinterpret_cast<float4*>(m);
+  float4* th4 = reinterpret_cast<float4*>(theta);
+  uint32_t flag = 0;
+  SegCursor cur;
+  for (int64_t t0 = gw; t0 < ntiles; t0 += nw * U) {
+    float4 gv[U], mv[U], tv[U];
+    uchar4 mk[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      int64_t t = t0 + u * nw;
+      if (t < nfull) {
+        gv[u] = ld_stream(g4 + t * 32 + lane);
+        mv[u] = ld_stream(m4 + t * 32 + lane);
+        tv[u] = ld_stream(th4 + t * 32 + lane);
+        if (MASK) mk[u] = *reinterpret_cast<const uchar4*>(mask + t * 128 + lane * 4);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t t = t0 + u * nw;
+      if (t >= ntiles) break;
+      const bool full = t < nfull;
+      const int64_t e0 = t * 128 + lane * 4;
+      float ge[4], me[4], te[4];
+      bool valid[4], keep[4];
+      if (full) {
+        ge[0] = gv[u].x; ge[1] = gv[u].y; ge[2] = gv[u].z; ge[3] = gv[u].w;
+        me[0] = mv[u].x; me[1] = mv[u].y; me[2] = mv[u].z; me[3] = mv[u].w;
+        te[0] = tv[u].x; te[1] = tv[u].y; te[2] = tv[u].z; te[3] = tv[u].w;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) valid[k] = true;
+        if (MASK) {
+          keep[0] = mk[u].x; keep[1] = mk[u].y; keep[2] = mk[u].z; keep[3] = mk[u].w;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          valid[k] = e0 + k < n;
+          ge[k] = valid[k] ? g[e0 + k] : 0.f;
+          me[k] = valid[k] ? m[e0 + k] : 0.f;
+          te[k] = valid[k] ? theta[e0 + k] : 0.f;
+          keep[k] = MASK ? (valid[k] ? mask[e0 + k] != 0 : true) : true;
+        }
+      }
+      float mn[4], tn[4];
+      uint32_t sbit[4], nzb[4], tb[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        double c = lion_c(me[k], ge[k], h);
+        if (MASK && !keep[k]) c = 0.0;
+        mn[k] = lion_m(me[k], ge[k], h);
+        double agg;  // the single-rank aggregate the vote signs
+        if (MODE == LC_LOCAL_QUANT) {
+          agg = valid[k] ? (double)quant_l1(c, cur.get(sq, e0 + k), sq.qmax) : 1.0;
+        } else {
+          agg = c;
+        }
+        double s;
+        bool zero = false;
+        if (agg > 0.0) {
+          s = 1.0;
+        } else if (agg < 0.0) {
+          s = -1.0;
+        } else if (agg == 0.0) {
+          zero = MODE != LC_LOCAL_BINARY;
+          if (MODE == LC_LOCAL_BINARY && ternary && valid[k]) flag |= LC_FLAG_ZERO_SIGN;
+          s = fillv;
+        } else {
+          s = -1.0;
+          if (valid[k]) flag |= LC_FLAG_NAN;
+        }
+        tn[k] = lion_theta(te[k], s, lr, wd);
+        sbit[k] = s > 0.0 ? 1u : 0u;
+        nzb[k] = s != 0.0 ? 1u : 0u;
+        tb[k] = (zero && valid[k]) ? 1u : 0u;
+      }
+      if (full) {
+        st_stream(m4 + t * 32 + lane, make_float4(mn[0], mn[1], mn[2], mn[3]));
+        st_stream(th4 + t * 32 + lane, make_float4(tn[0], tn[1], tn[2], tn[3]));
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (valid[k]) {
+            m[e0 + k] = mn[k];
+            theta[e0 + k] = tn[k];
+          }
+      }
+      if (METRICS) {
+        if (sbits) pack_store<1>(sbits, t, lane, sbit, nwords, full);
+        if (nzbits) pack_store<1>(nzbits, t, lane, nzb, nwords, full);
+        if (tbits) pack_store<1>(tbits, t, lane, tb, nwords, full);
+      }
+    }
+  }
+  if (flag) atomicOr(flags, flag);
+}
+
+// ---------------------------------------------------------------------------
+// K4: 1-bit majority over P packed chunks, bit-sliced counting.
+// ---------------------------------------------------------------------------
+template <int NP>
+__global__ void __launch_bounds__(256)
+k_vote_bits(const uint32_t* __restrict__ recv, int P, int64_t cw,
+            int64_t n_valid, int fill, uint32_t* __restrict__ voted,
+            uint32_t* __restrict__ tie, uint32_t* __restrict__ flags) {
+  const int T = P >> 1;
+  const uint32_t fillmask = fill > 0 ? ~0u : 0u;
+  uint32_t flag = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cw;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t planes[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) planes[p] = 0u;
+    for (int j = 0; j < P; ++j) {
+      uint32_t carry = __ldcs(recv + (int64_t)j * cw + i);
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        uint32_t t = planes[p] & carry;
+        planes[p] ^= carry;
+        carry = t;
+      }
+    }
+    uint32_t gt = 0u, eq = ~0u;
+#pragma unroll
+    for (int p = NP - 1; p >= 0; --p) {
+      uint32_t pl = planes[p];
+      if ((T >> p) & 1) {
+        eq &= pl;
+      } else {
+        gt |= eq & pl;
+        eq &= ~pl;
+      }
+    }
+    int64_t rem = n_valid - i * 32;
+    uint32_t vm = rem >= 32 ? ~0u : (rem <= 0 ? 0u : ((1u << rem) - 1u));
+    uint32_t v;
+    if (P & 1) {
+      v = gt;  // count > (P-1)/2 is a strict majority; no ties possible
+      eq = 0u;
+    } else {
+      v = gt | (eq & fillmask);
+      if (fill == 0 && (eq & vm)) flag |= LC_FLAG_TIE_TERNARY;
+    }
+    voted[i] = v;
+    if (tie) tie[i] = eq & vm;
+  }
+  if (flag) atomicOr(flags, flag);
+}
+
+// ---------------------------------------------------------------------------
+// K6: p-bit field sums -> signed aggregate -> sign words (+ ties, values).
+// Each lane reads one input word (E = 32/F elements); F lanes form a word.
+// ---------------------------------------------------------------------------
+template <int F>
+__global__ void __launch_bounds__(256)
+k_fields_vote(const uint32_t* __restrict__ sums, int64_t n, int P, int offset,
+              int binary, int fill, uint32_t* __restrict__ voted,
+              uint32_t* __restrict__ nz, uint32_t* __restrict__ tie,
+              int64_t* __restrict__ values) {
+  constexpr int E = 32 / F;
+  constexpr uint32_t FM = (F == 32) ? 0xffffffffu : ((1u << F) - 1u);
+  const int lane = threadIdx.x & 31;
+  const int64_t nin = (n * F + 31) / 32;
+  const int64_t nout = (n + 31) / 32;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nchunks = (nin + 31) / 32;
+  for (int64_t ch = gw; ch < nchunks; ch += nw) {
+    const int64_t i = ch * 32 + lane;
+    const uint32_t w = i < nin ? __ldcs(sums + i) : 0u;
+    uint32_t pos = 0u, zer = 0u, val = 0u;
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const int64_t e = i * E + k;
+      if (e < n) {
+        const int64_t cnt = (int64_t)((w >> (F * k)) & FM);
+        const int64_t s = binary ? 2 * cnt - P : cnt - (int64_t)P * offset;
+        pos |= (uint32_t)(s > 0) << k;
+        zer |= (uint32_t)(s == 0) << k;
+        val |= 1u << k;
+        if (values) values[e] = s;
+      }
+    }
+    const int shift = (int)(i % F) * E;
+    if (E < 32) {
+      pos <<= shift;
+      zer <<= shift;
+      val <<= shift;
+    }
+#pragma unroll
+    for (int s = 1; s < F; s <<= 1) {
+      pos |= __shfl_xor_sync(kFull, pos, s);
+      zer |= __shfl_xor_sync(kFull, zer, s);
+      val |= __shfl_xor_sync(kFull, val, s);
+    }
+    const int64_t o = i / F;
+    if ((lane % F) == 0 && o < nout) {
+      voted[o] = pos | (fill > 0 ? zer : 0u);
+      if (nz) nz[o] = ~zer & val;
+      if (tie) tie[o] = zer & val;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Full-precision arm: rank-ordered float64 sum (flat or binomial tree).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+k_f64_sum_vote(const double* __restrict__ recv, int P, int64_t len, int64_t stride, int tree,
+               int fill, uint32_t* __restrict__ voted, uint32_t* __restrict__ nz,
+               uint32_t* __restrict__ tie, double* __restrict__ values) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nwords = (len + 31) / 32;
+  for (int64_t w = gw; w < nwords; w += nw) {
+    const int64_t e = w * 32 + lane;
+    const bool valid = e < len;
+    double tot = 0.0;
+    if (valid) {
+      if (!tree) {
+        tot = recv[e];
+        for (int j = 1; j < P; ++j) tot = __dadd_rn(tot, recv[(int64_t)j * stride + e]);
+      } else {
+        double acc[64];
+        for (int j = 0; j < P; ++j) acc[j] = recv[(int64_t)j * stride + e];
+        for (int mk = 1; mk < P; mk <<= 1)
+          for (int r = 0; r + mk < P; r += 2 * mk) acc[r] = __dadd_rn(acc[r], acc[r + mk]);
+        tot = acc[0];
+      }
+      if (values) values[e] = tot;
+    }
+    const uint32_t pb = __ballot_sync(kFull, valid && tot > 0.0);
+    const uint32_t zb = __ballot_sync(kFull, valid && tot == 0.0);
+    const uint32_t vb = __ballot_sync(kFull, valid);
+    if (lane == 0) {
+      voted[w] = pb | (fill > 0 ? zb : 0u);
+      if (nz) nz[w] = ~zb & vb;
+      if (tie) tie[w] = zb;
+    }
+  }
+}
+
+// K7: momentum mean, float64 accumulation in rank order, one fp32 rounding.
+__global__ void __launch_bounds__(256)
+k_mean_f32(const float* __restrict__ recv, int P, int64_t len, int64_t stride,
+           float* __restrict__ out) {
+  const double dp = (double)P;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = (double)__ldcs(recv + i);
+    for (int j = 1; j < P; ++j) acc = __dadd_rn(acc, (double)__ldcs(recv + (int64_t)j * stride + i));
+    out[i] = __double2float_rn(__ddiv_rn(acc, dp));
+  }
+}
+
+__global__ void k_compute_c(const float* __restrict__ g, const float* __restrict__ m,
+                            const uint8_t* __restrict__ mask, int64_t n, Hyp h,
+                            double* __restrict__ c) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v = lion_c(m[i], g[i], h);
+    if (mask && !mask[i]) v = 0.0;
+    c[i] = v;
+  }
+}
+
+__global__ void k_count_bits_seg(const uint32_t* __restrict__ bits,
+                                 const int64_t* __restrict__ start, int nseg,
+                                 int64_t* __restrict__ counts) {
+  const int64_t n = start[nseg];
+  const int64_t nwords = (n + 31) / 32;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t b = bits[w];
+    int64_t e = w * 32;
+    int64_t end = e + 32 < n ? e + 32 : n;
+    if (end - e < 32) b &= (1u << (end - e)) - 1u;
+    if (!b) continue;
+    int s = seg_find(start, nseg, e);
+    while (e < end) {
+      int64_t se = start[s + 1];
+      int64_t hi = se < end ? se : end;
+      int lo_bit = (int)(e - w * 32), hi_bit = (int)(hi - w * 32);
+      uint32_t msk = (hi_bit >= 32 ? ~0u : ((1u << hi_bit) - 1u)) & ~((1u << lo_bit) - 1u);
+      int cnt = __popc(b & msk);
+      if (cnt) atomicAdd(reinterpret_cast<unsigned long long*>(counts + s),
+                         (unsigned long long)cnt);
+      e = hi;
+      ++s;
+    }
+  }
+}
+
+__global__ void k_bits_to_sign(const uint32_t* __restrict__ sb,
+                               const uint32_t* __restrict__ nzb, int64_t n,
+                               int8_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t bit = (sb[i >> 5] >> (i & 31)) & 1u;
+    int8_t v = bit ? 1 : -1;
+    if (nzb && !((nzb[i >> 5] >> (i & 31)) & 1u)) v = 0;
+    out[i] = v;
+  }
+}
+
+template <int F>
+__global__ void k_pack_i64(const int64_t* __restrict__ v, int64_t n, int offset,
+                           int binary, uint32_t* __restrict__ out,
+                           uint32_t* __restrict__ flags) {
+  constexpr int E = 32 / F;
+  const int64_t nwords = (n * F + 31) / 32;
+  const uint64_t lim = (F == 32) ? 0xffffffffull : ((1ull << F) - 1ull);
+  uint32_t flag = 0;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t word = 0;
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      int64_t e = w * E + k;
+      if (e < n) {
+        int64_t x = v[e];
+        int64_t st;
+        if (binary) {
+          if (x != 1 && x != -1) flag |= LC_FLAG_RANGE;
+          st = (x + 1) >> 1;
+        } else {
+          st = x + offset;
+        }
+        if (st < 0 || (uint64_t)st > lim) {
+          flag |= LC_FLAG_RANGE;
+          st = 0;
+        }
+        word |= (uint32_t)st << (F * k % 32);
+      }
+    }
+    out[w] = word;
+  }
+  if (flag) atomicOr(flags, flag);
+}
+
+template <int F>
+__global__ void k_fields_decode(const uint32_t* __restrict__ sums, int64_t n, int P,
+                                int offset, int binary, int64_t* __restrict__ out) {
+  constexpr int E = 32 / F;
+  constexpr uint32_t FM = (F == 32) ? 0xffffffffu : ((1u << F) - 1u);
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t cnt = (int64_t)((sums[e / E] >> (F * (int)(e % E))) & FM);
+    out[e] = binary ? 2 * cnt - P : cnt - (int64_t)P * offset;
+  }
+}
+
+__global__ void k_sign_pack_f64(const double* __restrict__ c, int64_t n, int fill,
+                                uint32_t* __restrict__ out, uint32_t* __restrict__ flags) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nwords = (n + 31) / 32;
+  uint32_t flag = 0;
+  for (int64_t w = gw; w < nwords; w += nw) {
+    int64_t e = w * 32 + lane;
+    bool valid = e < n;
+    double x = valid ? c[e] : 1.0;
+    bool bit;
+    if (x > 0.0) bit = true;
+    else if (x < 0.0) bit = false;
+    else if (x == 0.0) {
+      bit = fill > 0;
+      if (fill == 0) flag |= LC_FLAG_ZERO_SIGN;
+    } else {
+      bit = false;
+      flag |= LC_FLAG_NAN;
+    }
+    uint32_t b = __ballot_sync(kFull, bit || !valid);
+    if (lane == 0) out[w] = b;
+  }
+  if (flag) atomicOr(flags, flag);
+}
+
+struct Rows {
+  const uint32_t* p[64];
+};
+
+__global__ void k_sum_rows(Rows rows, int P, int64_t count, uint32_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t s = 0;
+    for (int j = 0; j < P; ++j) s += rows.p[j][i];
+    out[i] = s;
+  }
+}
+
+}  // namespace lc
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using namespace lc;
+
+namespace {
+
+constexpr int kBlock = 256;
+
+Hyp to_hyp(const lc_hyper* h) { return Hyp{h->beta1, h->one_minus_beta1, h->beta2, h->one_minus_beta2}; }
+
+SegQ to_segq(const lc_segments* s) {
+  SegQ q{nullptr, nullptr, 0, 0};
+  if (s) {
+    q.start = s->start;
+    q.scale = s->scale;
+    q.nseg = s->nseg;
+    q.qmax = s->qmax;
+  }
+  return q;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int generic_grid(int64_t n) {
+  int64_t b = (n + kBlock - 1) / kBlock;
+  int64_t cap = (int64_t)sm_count() * 8;
+  if (b > cap) b = cap;
+  return b < 1 ? 1 : (int)b;
+}
+
+template <int ENC, int F, bool MASK>
+int launch_encode(const float* g, float* m, const uint8_t* mask, int64_t n, Hyp h,
+                  int fill, SegQ sq, void* out, uint32_t* flags, cudaStream_t st) {
+  constexpr int U = 2;
+  auto kern = k_encode<ENC, F, MASK, U>;
+  int64_t ntiles = (n + 127) >> 7;
+  int grid = stream_grid(kern, kBlock, ntiles, (kBlock / 32) * U);
+  kern<<<grid, kBlock, 0, st>>>(g, m, mask, n, h, fill, sq, out, flags);
+  LC_LAUNCH_CHECK();
+  return LC_OK;
+}
+
+template <int ENC, int F>
+int dispatch_mask(const float* g, float* m, const uint8_t* mask, int64_t n, Hyp h,
+                  int fill, SegQ sq, void* out, uint32_t* flags, cudaStream_t st) {
+  if (mask) return launch_encode<ENC, F, true>(g, m, mask, n, h, fill, sq, out, flags, st);
+  return launch_encode<ENC, F, false>(g, m, mask, n, h, fill, sq, out, flags, st);
+}
+
+template <int ENC>
+int dispatch_fields(int F, const float* g, float* m, const uint8_t* mask, int64_t n,
+                    Hyp h, int fill, SegQ sq, void* out, uint32_t* flags,
+                    cudaStream_t st) {
+  switch (F) {
+    case 1: return dispatch_mask<ENC, 1>(g, m, mask, n, h, fill, sq, out, flags, st);
+    case 2: return dispatch_mask<ENC, 2>(g, m, mask, n, h, fill, sq, out, flags, st);
+    case 4: return dispatch_mask<ENC, 4>(g, m, mask, n, h, fill, sq, out, flags, st);
+    case 8: return dispatch_mask<ENC, 8>(g, m, mask, n, h, fill, sq, out, flags, st);
+    case 16: return dispatch_mask<ENC, 16>(g, m, mask, n, h, fill, sq, out, flags, st);
+    case 32: return dispatch_mask<ENC, 32>(g, m, mask, n, h, fill, sq, out, flags, st);
+    default: return set_err(LC_E_ARG, "field_bits must be 1,2,4,8,16,32 (got %d)", F);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int lc_abi_version(void) { return LIONCUB_ABI_VERSION; }
+
+const char* lc_last_error(void) { return err_msg().c_str(); }
+
+int lc_device_sm_count(int device) {
+  int v = 0;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
+    return set_err(LC_E_CUDA, "cudaDeviceGetAttribute failed");
+  return v;
+}
+
+int lc_encode(const float* g, float* m, const uint8_t* mask, int64_t n,
+              const lc_hyper* hp, int fill, int enc, int field_bits,
+              const lc_segments* segs, void* out, uint32_t* flags, void* stream) {
+  if (n < 0 || !hp || !flags) return set_err(LC_E_ARG, "lc_encode: bad arguments");
+  if (n == 0) return LC_OK;
+  if (!g || !m || !out) return set_err(LC_E_ARG, "lc_encode: null pointer");
+  if (!aligned16(g) || !aligned16(m)) return set_err(LC_E_ARG, "lc_encode: g/m must be 16-byte aligned");
+  Hyp h = to_hyp(hp);
+  SegQ sq = to_segq(segs);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  switch (enc) {
+    case LC_ENC_SIGN1:
+      return dispatch_mask<LC_ENC_SIGN1, 1>(g, m, mask, n, h, fill, sq, out, flags, st);
+    case LC_ENC_SIGN_FIELDS:
+      return dispatch_fields<LC_ENC_SIGN_FIELDS>(field_bits, g, m, mask, n, h, fill, sq, out, flags, st);
+    case LC_ENC_QUANT_FIELDS:
+      if (!segs || !segs->start || !segs->scale || segs->nseg < 1)
+        return set_err(LC_E_ARG, "lc_encode: quant needs a segment table with scales");
+      if (field_bits < 2) return set_err(LC_E_ARG, "lc_encode: quant fields need >= 2 bits");
+      return dispatch_fields<LC_ENC_QUANT_FIELDS>(field_bits, g, m, mask, n, h, fill, sq, out, flags, st);
+    case LC_ENC_F64:
+      return dispatch_mask<LC_ENC_F64, 1>(g, m, mask, n, h, fill, sq, out, flags, st);
+    default:
+      return set_err(LC_E_ARG, "lc_encode: unknown encoding %d", enc);
+  }
+}
+
+int lc_apply_update(float* theta, int64_t n, const uint32_t* sign_bits,
+                    const uint32_t* nz_bits, double lr, double wd, void* stream) {
+  if (n < 0) return set_err(LC_E_ARG, "lc_apply_update: n < 0");
+  if (n == 0) return LC_OK;
+  if (!theta || !sign_bits) return set_err(LC_E_ARG, "lc_apply_update: null pointer");
+  if (!aligned16(theta)) return set_err(LC_E_ARG, "lc_apply_update: theta must be 16-byte aligned");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  constexpr int U = 4;
+  int64_t ntiles = (n + 127) >> 7;
+  if (nz_bits) {
+    auto kern = k_apply_update<true, U>;
+    int grid = stream_grid(kern, kBlock, ntiles, (kBlock / 32) * U);
+    kern<<<grid, kBlock, 0, st>>>(theta, n, sign_bits, nz_bits, lr, wd);
+  } else {
+    auto kern = k_apply_update<false, U>;
+    int grid = stream_grid(kern, kBlock, ntiles, (kBlock / 32) * U);
+    kern<<<grid, kBlock, 0, st>>>(theta, n, sign_bits, nz_bits, lr, wd);
+  }
+  LC_LAUNCH_CHECK();
+  return LC_OK;
+}
+
+int lc_fused_local_step(float* theta, float* m, const float* g, const uint8_t* mask,
+                        int64_t n, const lc_hyper* hp, int fill, int mode,
+                        const lc_segments* segs, uint32_t* sign_bits,
+                        uint32_t* nz_bits, uint32_t* tie_bits, uint32_t* flags,
+                        void* stream) {
+  if (n < 0 || !hp || !flags) return set_err(LC_E_ARG, "lc_fused_local_step: bad arguments");
+  if (n == 0) return LC_OK;
+  if (!theta || !m || !g) return set_err(LC_E_ARG, "lc_fused_local_step: null pointer");
+  if (!aligned16(theta) || !aligned16(m) || !aligned16(g))
+    return set_err(LC_E_ARG, "lc_fused_local_step: theta/m/g must be 16-byte aligned");
+  if (mode == LC_LOCAL_QUANT && (!segs || !segs->scale || !segs->start))
+    return set_err(LC_E_ARG, "lc_fused_local_step: quant needs segment scales");
+  Hyp h = to_hyp(hp);
+  SegQ sq = to_segq(segs);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool metrics = sign_bits || nz_bits || tie_bits;
+  constexpr int U = 2;
+  const int64_t ntiles = (n + 127) >> 7;
+#define LC_FUSED(MODE, MASK, MET)                                                      \
+  do {                                                                                 \
+    auto kern = k_fused_local<MODE, MASK, MET, U>;                                     \
+    int grid = stream_grid(kern, kBlock, ntiles, (kBlock / 32) * U);                   \
+    kern<<<grid, kBlock, 0, st>>>(theta, m, g, mask, n, h, hp->lr, hp->weight_decay,   \
+                                  fill, sq, sign_bits, nz_bits, tie_bits, flags);      \
+  } while (0)
+#define LC_FUSED_M(MODE)                         \
+  do {                                           \
+    if (mask) {                                  \
+      if (metrics) LC_FUSED(MODE, true, true);   \
+      else LC_FUSED(MODE, true, false);          \
+    } else {                                     \
+      if (metrics) LC_FUSED(MODE, false, true);  \
+      else LC_FUSED(MODE, false, false);         \
+    }                                            \
+  } while (0)
+  switch (mode) {
+    case LC_LOCAL_BINARY: LC_FUSED_M(LC_LOCAL_BINARY); break;
+    case LC_LOCAL_PS: LC_FUSED_M(LC_LOCAL_PS); break;
+    case LC_LOCAL_QUANT: LC_FUSED_M(LC_LOCAL_QUANT); break;
+    default: return set_err(LC_E_ARG, "lc_fused_local_step: unknown mode %d", mode);
+  }
+#undef LC_FUSED_M
+#undef LC_FUSED
+  LC_LAUNCH_CHECK();
+  return LC_OK;
+}
+
+int lc_vote_bits(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid, int fill,
+                 uint32_t* voted, uint32_t* tie_bits, uint32_t* flags, void* stream) {
+  if (P < 1 || P > 255 || cw < 0 || !flags) return set_err(LC_E_ARG, "lc_vote_bits: P must be in [1,255]");
+  if (cw == 0) return LC_OK;
+  if (!recv || !voted) return set_err(LC_E_ARG, "lc_vote_bits: null pointer");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int grid = generic_grid(cw);
+#define LC_VOTE(NP) k_vote_bits<NP><<<grid, kBlock, 0, st>>>(recv, P, cw, n_valid, fill, voted, tie_bits, flags)
+  if (P <= 1) LC_VOTE(1);
+  else if (P <= 3) LC_VOTE(2);
+  else if (P <= 7) LC_VOTE(3);
+  else if (P <= 15) LC_VOTE(4);
+  else if (P <= 31) LC_VOTE(5);
+  else if (P <= 63) LC_VOTE(6);
+  else if (P <= 127) LC_VOTE(7);
+  else LC_VOTE(8);
+#undef LC_VOTE
+  LC_LAUNCH_CHECK();
+  return LC_OK;
+}
+
+int lc_fields_vote(const uint32_t* sums, int64_t n, int32_t F, int32_t P, int32_t offset,
+                   int32_t binary, int fill, uint32_t* voted, uint32_t* nz,
+                   uint32_t* tie_bits, int64_t* values, void* stream) {
+  if (n < 0 || P < 1) return set_err(LC_E_ARG, "lc_fields_vote: bad arguments");
+  if (n == 0) return LC_OK;
+  if (!sums || !voted) return set_err(LC_E_ARG, "lc_fields_vote: null pointer");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int64_t nin = (n * F + 31) / 32;
+  int grid = generic_grid(nin);
+#define LC_FV(FF) k_fields_vote<FF><<<grid, kBlock, 0, st>>>(sums, n, P, offset, binary, fill, voted, nz, tie_bits, values)
+  switch (F) {
+    case 1: LC_FV(1); break;
+    case 2: LC_FV(2); break;
+    case 4: LC_FV(4); break;
+    case 8: LC_FV(8); break;
+    case 16: LC_FV(16); break;
+    case 32: LC_FV(32); break;
+    default: return set_err(LC_E_ARG, "lc_fields_vote: field_bits %d", F);
+  }
+#undef LC_FV
+  LC_LAUNCH_CHECK();
+  return LC_OK;
+}
+
+int lc_f64_sum_vote(const double* recv, int32_t P, int64_t len, int64_t stride, int tree, int fill,
+                    uint32_t* voted, uint32_t* nz, uint32_t* tie_bits, double* values,
+                    void* stream) {
+  if (len < 0 || P < 1 || (tree && P > 64)) return set_err(LC_E_ARG, "lc_f64_sum_vote: bad arguments");
+  if (len == 0) return LC_OK;
+  if (!recv || !voted) return set_err(LC_E_ARG, "lc_f64_sum_vote: null pointer");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int grid = generic_grid(len);
+  k_f64_sum_vote<<<grid, kBlock, 0, st>>>(recv, P, len, stride, tree, fill, voted, nz, tie_bits, values);
+  LC_LAUNCH_CHECK();
+  return LC_OK;
+}
+
+int lc_mean_f32(const float* recv, int32_t P, int64_t len, int64_t stride, float* out,
+                void* stream) {
+  if (len < 0 || P < 1) return set_err(LC_E_ARG, "lc_mean_f32: bad arguments");
+  if (len == 0) return LC_OK;
+  if (!recv || !out) return set_err(LC_E_ARG, "lc_mean_f32: null pointer");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  k_mean_f32<<<generic_grid(len), kBlock, 0, st>>>(recv, P, len, stride, out);
+  LC_LAUNCH_CHECK();
+  return LC_OK;
+}
+
+int lc_compute_c(const float* g, const float* m, const uint8_t* mask, int64_t n,
+                 const lc_hyper* hp, double* c, void* stream) {
+  if (n < 0 || !hp) return set_err(LC_E_ARG, "lc_compute_c: bad arguments");
+  if (n == 0) return LC_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  k_compute_c<<<generic_grid(n), kBlock, 0, st>>>(g, m, mask, n, to_hyp(hp), c);
+  LC_LAUNCH_CHECK();
+  return LC_OK;
+}
+
+int lc_count_bits_segmented(const uint32_t* bits, const int64_t* seg_start, int32_t nseg,
+                            int64_t* counts, void* stream) {
+  if (nseg < 1 || !bits || !seg_start || !counts)
+    return set_err(LC_E_ARG, "lc_count_bits_segmented: bad arguments");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  LC_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int64_t) * nseg, st));
+  // total length lives on the device; size the grid generously
+  k_count_bits_seg<<<sm_count() * 4, kBlock, 0, st>>>(bits, seg_start, nseg, counts);
+  LC_LAUNCH_CHECK();
+  return LC_OK;
+}
+
+int lc_bits_to_sign(const uint32_t* sign_bits, const uint32_t* nz_bits, int64_t n,
+                    int8_t* out, void* stream) {
+  if (n < 0) return set_err(LC_E_ARG, "lc_bits_to_sign: n < 0");
+  if (n == 0) return LC_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  k_bits_to_sign<<<generic_grid(n), kBlock, 0, st>>>(sign_bits, nz_bits, n, out);
+  LC_LAUNCH_CHECK();
+  return LC_OK;
+}
+
+int lc_pack_i64_fields(const int64_t* v, int64_t n, int32_t F, int32_t offset,
+                       int32_t binary, uint32_t* out, uint32_t* flags, void* stream) {
+  if (n < 0 || !flags) return set_err(LC_E_ARG, "lc_pack_i64_fields: bad arguments");
+  if (n == 0) return LC_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int grid = generic_grid((n * F + 31) / 32);
+#define LC_PK(FF) k_pack_i64<FF><<<grid, kBlock, 0, st>>>(v, n, offset, binary, out, flags)
+  switch (F) {
+    case 1: LC_PK(1); break;
+    case 2: LC_PK(2); break;
+    case 4: LC_PK(4); break;
+    case 8: LC_PK(8); break;
+    case 16: LC_PK(16); break;
+    case 32: LC_PK(32); break;
+    default: return set_err(LC_E_ARG, "lc_pack_i64_fields: field_bits %d", F);
+  }
+#undef LC_PK
+  LC_LAUNCH_CHECK();
+  return LC_OK;
+}
+
+int lc_fields_decode(const uint32_t* sums, int64_t n, int32_t F, int32_t P, int32_t offset,
+                     int32_t binary, int64_t* out, void* stream) {
+  if (n < 0) return set_err(LC_E_ARG, "lc_fields_decode: n < 0");
+  if (n == 0) return LC_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int grid = generic_grid(n);
+#define LC_FD(FF) k_fields_decode<FF><<<grid, kBlock, 0, st>>>(sums, n, P, offset, binary, out)
+  switch (F) {
+    case 1: LC_FD(1); break;
+    case 2: LC_FD(2); break;
+    case 4: LC_FD(4); break;
+    case 8: LC_FD(8); break;
+    case 16: LC_FD(16); break;
+    case 32: LC_FD(32); break;
+    default: return set_err(LC_E_ARG, "lc_fields_decode: field_bits %d", F);
+  }
+#undef LC_FD
+  LC_LAUNCH_CHECK();
+  return LC_OK;
+}
+
+int lc_sign_pack_f64(const double* c, int64_t n, int fill, uint32_t* out, uint32_t* flags,
+                     void* stream) {
+  if (n < 0 || !flags) return set_err(LC_E_ARG, "lc_sign_pack_f64: bad arguments");
+  if (n == 0) return LC_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  k_sign_pack_f64<<<generic_grid(n), kBlock, 0, st>>>(c, n, fill, out, flags);
+  LC_LAUNCH_CHECK();
+  return LC_OK;
+}
+
+int lc_sum_u32_rows(const uint32_t* const* rows, int32_t P, int64_t count, uint32_t* out,
+                    void* stream) {
+  if (P < 1 || P > 64 || count < 0 || !rows || !out)
+    return set_err(LC_E_ARG, "lc_sum_u32_rows: bad arguments (P <= 64)");
+  if (count == 0) return LC_OK;
+  Rows r;
+  for (int j = 0; j < P; ++j) r.p[j] = rows[j];
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  k_sum_rows<<<generic_grid(count), kBlock, 0, st>>>(r, P, count, out);
+  LC_LAUNCH_CHECK();
+  return LC_OK;
+}
+
+}  // extern "C"

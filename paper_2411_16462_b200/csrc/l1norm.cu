@@ -1,0 +1,448 @@
+// numpy-exact per-layer L1 mean norm for the p-bit Lion Cub path.
+//
+// quant.py:156-179 computes M1 = max|c| * mean(|c|/max|c|).  np.mean sums
+// float64 with numpy's pairwise algorithm: blocks of <= 128 elements use 8
+// strided accumulators combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus a
+// sequential tail; larger blocks split at n/2 rounded down to a multiple of 8
+// (checked against np.sum in tests/test_oracle.py).  The summation tree
+// depends only on the layer length, so the plan precomputes it once:
+//   * the tree is cut into CTA work items of <= kItem elements;
+//   * every distinct work-item size gets a template (its <=128-element leaves
+//     and the level-ordered internal additions);
+//   * the additions above the work items run level by level in one CTA per
+//     layer.
+// Every addition happens in exactly numpy's order, so the norm and therefore
+// the quantized integers are bit-identical to the reference.
+#include <algorithm>
+#include <functional>
+#include <map>
+#include <vector>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int64_t kItem = 8192;  // elements per work-item CTA
+constexpr int kLeaf = 128;       // numpy PW_BLOCKSIZE
+constexpr int kThreads = 256;
+
+struct Op {
+  int dst, left, right, height;
+};
+
+struct Tmpl {
+  std::vector<int> leaf_rel, leaf_size;
+  std::vector<Op> ops;  // sorted by height
+  std::vector<int> lvl; // op index where each height starts (+ end)
+  int root = 0;         // slot of the root
+  int nslots = 0;
+};
+
+int64_t split_left(int64_t n) {
+  int64_t n2 = n / 2;
+  return n2 - (n2 % 8);
+}
+
+// Build a work-item template: leaves are slots [0, L), internals [L, ...).
+void build_tmpl(int64_t size, Tmpl& t) {
+  struct Node {
+    bool leaf;
+    int idx;
+    int height;
+  };
+  std::vector<Op> raw;  // internal ops with provisional internal indices
+  int nleaf = 0, nint = 0;
+  std::vector<int> lrel, lsize;
+  // recursive lambda
+  std::function<Node(int64_t, int64_t)> rec = [&](int64_t off, int64_t n) -> Node {
+    if (n <= kLeaf) {
+      lrel.push_back((int)off);
+      lsize.push_back((int)n);
+      return Node{true, nleaf++, 0};
+    }
+    int64_t n2 = split_left(n);
+    Node a = rec(off, n2);
+    Node b = rec(off + n2, n - n2);
+    Op op;
+    op.dst = nint++;
+    op.left = a.leaf ? a.idx : -(a.idx + 1);
+    op.right = b.leaf ? b.idx : -(b.idx + 1);
+    op.height = 1 + std::max(a.height, b.height);
+    raw.push_back(op);
+    return Node{false, op.dst, op.height};
+  };
+  Node root = rec(0, size);
+  t.leaf_rel = lrel;
+  t.leaf_size = lsize;
+  auto slot = [&](int v) { return v >= 0 ? v : nleaf + (-v - 1); };
+  t.ops.clear();
+  for (auto& o : raw) t.ops.push_back(Op{nleaf + o.dst, slot(o.left), slot(o.right), o.height});
+  std::stable_sort(t.ops.begin(), t.ops.end(),
+                   [](const Op& a, const Op& b) { return a.height < b.height; });
+  t.lvl.clear();
+  int h = 0;
+  for (size_t i = 0; i < t.ops.size(); ++i) {
+    while (h < t.ops[i].height) {
+      t.lvl.push_back((int)i);
+      ++h;
+    }
+  }
+  t.lvl.push_back((int)t.ops.size());
+  t.root = root.leaf ? root.idx : nleaf + root.idx;
+  t.nslots = nleaf + nint;
+}
+
+struct DevTmpl {
+  int leaf_begin, nleaf, op_begin, nlvl, lvl_begin, root, nslots, pad;
+};
+
+struct DevSeg {
+  int64_t start, n;
+  int op_begin, nlvl, lvl_begin, root;
+};
+
+}  // namespace
+
+struct lc_l1_plan_s {
+  int nseg = 0;
+  int64_t n_total = 0;
+  int n_items = 0, n_nodes = 0, max_slots = 0;
+  std::vector<int64_t> seg_start;
+  // device
+  int64_t* d_seg_start = nullptr;
+  DevSeg* d_seg = nullptr;
+  DevTmpl* d_tmpl = nullptr;
+  int* d_leaf_rel = nullptr;
+  int* d_leaf_size = nullptr;
+  int4* d_tops = nullptr;     // template ops (dst, left, right, -)
+  int* d_tlvl = nullptr;      // template level starts
+  int4* d_uops = nullptr;     // upper ops
+  int* d_ulvl = nullptr;      // upper level starts
+  int64_t* d_wi_off = nullptr;  // work-item absolute element offset
+  int* d_wi_meta = nullptr;     // (seg, tmpl, node) triples
+  double* d_nodes = nullptr;
+  unsigned long long* d_max = nullptr;
+};
+
+namespace {
+
+using lc::Hyp;
+
+// Per-segment max|c| as uint64 bit patterns (non-negative doubles order as
+// unsigned integers).  Each CTA walks a contiguous element range so it meets
+// few segments; per-lane maxima are merged in shared memory first.
+__global__ void __launch_bounds__(kThreads)
+k_l1_max(const float* __restrict__ g, const float* __restrict__ m,
+         const uint8_t* __restrict__ mask, const int64_t* __restrict__ start,
+         int nseg, int64_t n, int64_t per_cta, Hyp h,
+         unsigned long long* __restrict__ gmax) {
+  constexpr int kTab = 256;
+  __shared__ unsigned long long tab[kTab];
+  const int64_t lo = (int64_t)blockIdx.x * per_cta;
+  if (lo >= n) return;
+  const int64_t hi = min(n, lo + per_cta);
+  const int s_first = lc::seg_find(start, nseg, lo);
+  const int s_last = lc::seg_find(start, nseg, hi - 1);
+  const bool use_tab = (s_last - s_first) < kTab;
+  for (int i = threadIdx.x; i < kTab; i += blockDim.x) tab[i] = 0ull;
+  __syncthreads();
+  int seg = s_first;
+  int64_t seg_hi = start[seg + 1];
+  unsigned long long cur = 0ull;
+  auto flush = [&](int s, unsigned long long v) {
+    if (!v) return;
+    if (use_tab)
+      atomicMax(&tab[s - s_first], v);
+    else
+      atomicMax(&gmax[s], v);
+  };
+  for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
+    if (e >= seg_hi) {
+      flush(seg, cur);
+      cur = 0ull;
+      seg = lc::seg_find(start, nseg, e);
+      seg_hi = start[seg + 1];
+    }
+    double c = lc::lion_c(m[e], g[e], h);
+    if (mask && !mask[e]) c = 0.0;
+    unsigned long long b = (unsigned long long)__double_as_longlong(fabs(c));
+    cur = b > cur ? b : cur;
+  }
+  flush(seg, cur);
+  __syncthreads();
+  if (use_tab)
+    for (int i = threadIdx.x; i <= s_last - s_first; i += blockDim.x)
+      if (tab[i]) atomicMax(&gmax[s_first + i], tab[i]);
+}
+
+__device__ __forceinline__ double l1_v(const float* g, const float* m, const uint8_t* mask,
+                                       int64_t e, const Hyp& h, double mx) {
+  double c = lc::lion_c(m[e], g[e], h);
+  if (mask && !mask[e]) c = 0.0;
+  return __ddiv_rn(fabs(c), mx);  // (a / m) ** 1.0 == a / m
+}
+
+// One CTA per work item: leaves with 8 lanes each, then templated additions.
+__global__ void __launch_bounds__(kThreads)
+k_l1_items(const float* __restrict__ g, const float* __restrict__ m,
+           const uint8_t* __restrict__ mask, Hyp h,
+           const unsigned long long* __restrict__ gmax,
+           const int64_t* __restrict__ wi_off, const int* __restrict__ wi_meta,
+           const DevTmpl* __restrict__ tmpl, const int* __restrict__ leaf_rel,
+           const int* __restrict__ leaf_size, const int4* __restrict__ tops,
+           const int* __restrict__ tlvl, double* __restrict__ nodes) {
+  extern __shared__ double slots[];
+  const int item = blockIdx.x;
+  const int64_t base = wi_off[item];
+  const int seg = wi_meta[3 * item], ti = wi_meta[3 * item + 1], node = wi_meta[3 * item + 2];
+  const DevTmpl T = tmpl[ti];
+  const double mx = __longlong_as_double((long long)gmax[seg]);
+  if (mx == 0.0) {  // lp_mean_norm returns 0 before summing (quant.py:176-178)
+    if (threadIdx.x == 0) nodes[node] = 0.0;
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const int k = lane & 7;
+  const int group = threadIdx.x >> 3;
+  const int ngroups = blockDim.x >> 3;
+  for (int lf = group; lf < T.nleaf; lf += ngroups) {
+    const int rel = leaf_rel[T.leaf_begin + lf];
+    const int sz = leaf_size[T.leaf_begin + lf];
+    const int64_t e0 = base + rel;
+    const unsigned gm = 0xffu << (lane & 24);  // the 8 lanes of this leaf
+    double res;
+    if (sz < 8) {  // only a whole tiny layer: sequential from 0
+      res = 0.0;
+      if (k == 0)
+        for (int i = 0; i < sz; ++i) res = __dadd_rn(res, l1_v(g, m, mask, e0 + i, h, mx));
+    } else {
+      const int full = sz - (sz % 8);
+      double r = l1_v(g, m, mask, e0 + k, h, mx);
+      for (int i = 8; i < full; i += 8) r = __dadd_rn(r, l1_v(g, m, mask, e0 + i + k, h, mx));
+      // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)); IEEE addition is commutative
+      r = __dadd_rn(r, __shfl_xor_sync(gm, r, 1));
+      r = __dadd_rn(r, __shfl_xor_sync(gm, r, 2));
+      r = __dadd_rn(r, __shfl_xor_sync(gm, r, 4));
+      res = r;
+      if (k == 0)
+        for (int i = full; i < sz; ++i) res = __dadd_rn(res, l1_v(g, m, mask, e0 + i, h, mx));
+    }
+    if (k == 0) slots[lf] = res;
+  }
+  __syncthreads();
+  for (int lv = 0; lv < T.nlvl; ++lv) {
+    const int b = tlvl[T.lvl_begin + lv], e = tlvl[T.lvl_begin + lv + 1];
+    for (int o = b + threadIdx.x; o < e; o += blockDim.x) {
+      const int4 op = tops[T.op_begin + o];
+      slots[op.x] = __dadd_rn(slots[op.y], slots[op.z]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) nodes[node] = slots[T.root];
+}
+
+// One CTA per layer: additions above the work items, then M1 and the scale.
+__global__ void __launch_bounds__(kThreads)
+k_l1_upper(const DevSeg* __restrict__ segs, const int4* __restrict__ uops,
+           const int* __restrict__ ulvl, const unsigned long long* __restrict__ gmax,
+           double* __restrict__ nodes, int qmax, double* __restrict__ norms,
+           double* __restrict__ scales) {
+  const int s = blockIdx.x;
+  const DevSeg S = segs[s];
+  const double mx = __longlong_as_double((long long)gmax[s]);
+  if (mx != 0.0) {
+    for (int lv = 0; lv < S.nlvl; ++lv) {
+      const int b = ulvl[S.lvl_begin + lv], e = ulvl[S.lvl_begin + lv + 1];
+      for (int o = b + threadIdx.x; o < e; o += blockDim.x) {
+        const int4 op = uops[S.op_begin + o];
+        nodes[op.x] = __dadd_rn(nodes[op.y], nodes[op.z]);
+      }
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) {
+    double M = 0.0;
+    if (mx != 0.0) {
+      const double mean = __ddiv_rn(nodes[S.root], (double)S.n);  // np.mean
+      M = __dmul_rn(mx, mean);                                   // m * mean**(1/1)
+    }
+    norms[s] = M;
+    scales[s] = (M == 0.0 || qmax == 0) ? 0.0 : __ddiv_rn((double)qmax, __dmul_rn(2.0, M));
+  }
+}
+
+template <typename T>
+int upload(T** dst, const std::vector<T>& v) {
+  size_t bytes = std::max<size_t>(1, v.size()) * sizeof(T);
+  LC_CUDA_TRY(cudaMalloc(dst, bytes));
+  if (!v.empty()) LC_CUDA_TRY(cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return LC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lc_l1_plan_destroy(lc_l1_plan_t p) {
+  if (!p) return LC_OK;
+  cudaFree(p->d_seg_start);
+  cudaFree(p->d_seg);
+  cudaFree(p->d_tmpl);
+  cudaFree(p->d_leaf_rel);
+  cudaFree(p->d_leaf_size);
+  cudaFree(p->d_tops);
+  cudaFree(p->d_tlvl);
+  cudaFree(p->d_uops);
+  cudaFree(p->d_ulvl);
+  cudaFree(p->d_wi_off);
+  cudaFree(p->d_wi_meta);
+  cudaFree(p->d_nodes);
+  cudaFree(p->d_max);
+  delete p;
+  return LC_OK;
+}
+
+int lc_l1_plan_create(lc_l1_plan_t* out, const int64_t* seg_start, int32_t nseg) {
+  if (!out || !seg_start || nseg < 1) return lc::set_err(LC_E_ARG, "lc_l1_plan_create: bad arguments");
+  for (int s = 0; s < nseg; ++s) {
+    if (seg_start[s + 1] < seg_start[s]) return lc::set_err(LC_E_ARG, "segment offsets must be sorted");
+    if (seg_start[s + 1] == seg_start[s])
+      return lc::set_err(LC_E_CONFIG, "lp_mean_norm of an empty vector (segment %d)", s);
+  }
+  auto* p = new lc_l1_plan_s();
+  p->nseg = nseg;
+  p->seg_start.assign(seg_start, seg_start + nseg + 1);
+  p->n_total = seg_start[nseg];
+
+  std::map<int64_t, int> tmpl_of;
+  std::vector<Tmpl> tmpls;
+  std::vector<int64_t> wi_off;
+  std::vector<int> wi_meta;
+  std::vector<int4> uops;
+  std::vector<int> ulvl;
+  std::vector<DevSeg> dsegs;
+  int node_ctr = 0;
+
+  for (int s = 0; s < nseg; ++s) {
+    const int64_t s0 = seg_start[s], n = seg_start[s + 1] - seg_start[s];
+    std::vector<Op> ops;
+    struct R {
+      int node, height;
+    };
+    std::function<R(int64_t, int64_t)> rec = [&](int64_t off, int64_t len) -> R {
+      if (len <= kItem) {
+        auto it = tmpl_of.find(len);
+        int ti;
+        if (it == tmpl_of.end()) {
+          Tmpl t;
+          build_tmpl(len, t);
+          ti = (int)tmpls.size();
+          tmpls.push_back(std::move(t));
+          tmpl_of[len] = ti;
+        } else {
+          ti = it->second;
+        }
+        int node = node_ctr++;
+        wi_off.push_back(s0 + off);
+        wi_meta.push_back(s);
+        wi_meta.push_back(ti);
+        wi_meta.push_back(node);
+        return R{node, 0};
+      }
+      int64_t n2 = split_left(len);
+      R a = rec(off, n2);
+      R b = rec(off + n2, len - n2);
+      int node = node_ctr++;
+      int h = 1 + std::max(a.height, b.height);
+      ops.push_back(Op{node, a.node, b.node, h});
+      return R{node, h};
+    };
+    R root = rec(0, n);
+    std::stable_sort(ops.begin(), ops.end(), [](const Op& a, const Op& b) { return a.height < b.height; });
+    DevSeg ds;
+    ds.start = s0;
+    ds.n = n;
+    ds.op_begin = (int)uops.size();
+    ds.lvl_begin = (int)ulvl.size();
+    ds.root = root.node;
+    int h = 0;
+    for (size_t i = 0; i < ops.size(); ++i)
+      while (h < ops[i].height) {
+        ulvl.push_back((int)i);
+        ++h;
+      }
+    ulvl.push_back((int)ops.size());
+    ds.nlvl = h;
+    for (auto& o : ops) uops.push_back(make_int4(o.dst, o.left, o.right, o.height));
+    dsegs.push_back(ds);
+  }
+
+  std::vector<DevTmpl> dt;
+  std::vector<int> leaf_rel, leaf_size, tlvl;
+  std::vector<int4> tops;
+  for (auto& t : tmpls) {
+    DevTmpl d;
+    d.leaf_begin = (int)leaf_rel.size();
+    d.nleaf = (int)t.leaf_rel.size();
+    d.op_begin = (int)tops.size();
+    d.lvl_begin = (int)tlvl.size();
+    d.nlvl = (int)t.lvl.size() - 1;
+    d.root = t.root;
+    d.nslots = t.nslots;
+    d.pad = 0;
+    leaf_rel.insert(leaf_rel.end(), t.leaf_rel.begin(), t.leaf_rel.end());
+    leaf_size.insert(leaf_size.end(), t.leaf_size.begin(), t.leaf_size.end());
+    for (auto& o : t.ops) tops.push_back(make_int4(o.dst, o.left, o.right, o.height));
+    tlvl.insert(tlvl.end(), t.lvl.begin(), t.lvl.end());
+    p->max_slots = std::max(p->max_slots, t.nslots);
+    dt.push_back(d);
+  }
+  p->n_items = (int)wi_off.size();
+  p->n_nodes = node_ctr;
+  int rc = LC_OK;
+  if ((rc = upload(&p->d_seg_start, p->seg_start)) ||
+      (rc = upload(&p->d_seg, dsegs)) || (rc = upload(&p->d_tmpl, dt)) ||
+      (rc = upload(&p->d_leaf_rel, leaf_rel)) || (rc = upload(&p->d_leaf_size, leaf_size)) ||
+      (rc = upload(&p->d_tops, tops)) || (rc = upload(&p->d_tlvl, tlvl)) ||
+      (rc = upload(&p->d_uops, uops)) || (rc = upload(&p->d_ulvl, ulvl)) ||
+      (rc = upload(&p->d_wi_off, wi_off)) || (rc = upload(&p->d_wi_meta, wi_meta))) {
+    lc_l1_plan_destroy(p);
+    return rc;
+  }
+  if (cudaMalloc(&p->d_nodes, sizeof(double) * std::max(1, p->n_nodes)) != cudaSuccess ||
+      cudaMalloc(&p->d_max, sizeof(unsigned long long) * nseg) != cudaSuccess) {
+    lc_l1_plan_destroy(p);
+    return lc::set_err(LC_E_CUDA, "lc_l1_plan_create: cudaMalloc failed");
+  }
+  *out = p;
+  return LC_OK;
+}
+
+int lc_l1_scales(lc_l1_plan_t p, const float* g, const float* m, const uint8_t* mask,
+                 const lc_hyper* hp, int32_t qmax, double* norms, double* scales,
+                 void* stream) {
+  if (!p || !g || !m || !hp || !norms || !scales) return lc::set_err(LC_E_ARG, "lc_l1_scales: bad arguments");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Hyp h{hp->beta1, hp->one_minus_beta1, hp->beta2, hp->one_minus_beta2};
+  LC_CUDA_TRY(cudaMemsetAsync(p->d_max, 0, sizeof(unsigned long long) * p->nseg, st));
+  const int64_t n = p->n_total;
+  int64_t nct = (int64_t)lc::sm_count() * 8;
+  int64_t per = (n + nct - 1) / nct;
+  per = std::max<int64_t>(per, 4096);
+  int grid = (int)((n + per - 1) / per);
+  k_l1_max<<<grid, kThreads, 0, st>>>(g, m, mask, p->d_seg_start, p->nseg, n, per, h, p->d_max);
+  LC_LAUNCH_CHECK();
+  size_t smem = sizeof(double) * std::max(1, p->max_slots);
+  if (smem > 48 * 1024)
+    LC_CUDA_TRY(cudaFuncSetAttribute(k_l1_items, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_l1_items<<<p->n_items, kThreads, smem, st>>>(g, m, mask, h, p->d_max, p->d_wi_off, p->d_wi_meta,
+                                                 p->d_tmpl, p->d_leaf_rel, p->d_leaf_size, p->d_tops,
+                                                 p->d_tlvl, p->d_nodes);
+  LC_LAUNCH_CHECK();
+  k_l1_upper<<<p->nseg, kThreads, 0, st>>>(p->d_seg, p->d_uops, p->d_ulvl, p->d_max, p->d_nodes,
+                                           qmax, norms, scales);
+  LC_LAUNCH_CHECK();
+  return LC_OK;
+}
+
+}  // extern "C"

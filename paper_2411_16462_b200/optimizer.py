@@ -1,0 +1,553 @@
+"""Lion Cub optimizer step on B200 -- the drop-in for lioncomm.optimizer.
+
+Same names, constructor arguments and step semantics as the reference
+(lioncomm/optimizer.py:43-258): ``LionHyper``, ``WorkerState``,
+``SyncPolicy``, ``lion_step``, ``distributed_lion_step``,
+``maybe_sync_momentum``.  Differences are representation only:
+
+* ``ParamSet`` values are CUDA fp32 tensors.  ``WorkerState.initial`` lays
+  every layer (sorted-name order, like the reference's per-layer loop,
+  optimizer.py:195) out as a view into ONE flat buffer for theta and one for
+  m (``FlatParamSet``); the step then runs over the flat buffer with a
+  per-layer segment table, one kernel per phase instead of one numpy pass
+  per layer and operation.
+* The step DONATES its input state: theta and m are updated in place (the
+  returned ``WorkerState`` shares the buffers; the reference returns fresh
+  arrays).  This is what makes the step 20 bytes of HBM traffic per param.
+* Arithmetic: c, m', theta' and the p-bit scale are computed in float64 from
+  fp32 state exactly as numpy orders them, then rounded once to fp32, so a
+  step from fp32 state equals float32(reference step) bit-for-bit; votes,
+  packed words, p-bit sums and ties are bit-exact.
+
+Step pipelines (P = topo.world_size, n = params in the flat buffer):
+
+  P == 1           lc_fused_local_step: theta,m,g -> theta',m' in one pass.
+  compressed1bit   K1 sign-pack -> all-to-all -> K4 vote -> allgather -> K5
+  direct, bits=1   K1 sign fields -> reduce-scatter -> K6 -> allgather -> K5
+  direct, bits>=2  L1 norm (numpy-exact) -> K1 quant fields -> RS -> K6 -> AG -> K5
+  ps/ps_efficient  K1 c(f64) -> all-to-all -> rank-ordered f64 sum -> AG -> K5
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import hashlib
+import math
+from dataclasses import dataclass, replace
+from typing import Callable, Mapping, Union
+
+import torch
+
+from . import _lib
+from .collectives import (Topology, choose_lane_bits, field_bits, mean_into,
+                          owner_elems, owner_valid)
+from .errors import ConfigError
+from .quant import QuantSpec, SignPolicy
+
+LrSchedule = Union[float, Callable[[int], float]]
+VOTE_ALGOS = ("ps", "ps_efficient", "direct", "compressed1bit")
+
+
+# ---------------------------------------------------------------------------
+# Hyperparameters and policies (optimizer.py:43-103)
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class LionHyper:
+    beta1: float = 0.9
+    beta2: float = 0.99
+    lr: LrSchedule = 1e-4
+    weight_decay: float = 0.0
+
+    def __post_init__(self):
+        ok = 0.0 < self.beta1 < 1.0 and 0.0 < self.beta2 < 1.0
+        if not ok:
+            raise ConfigError("beta1 and beta2 must be strictly inside (0, 1)")
+        if self.weight_decay < 0:
+            raise ConfigError("weight_decay must be >= 0")
+
+    def lr_at(self, t: int) -> float:
+        eta = float(self.lr(t)) if callable(self.lr) else float(self.lr)
+        if not eta > 0:
+            raise ConfigError(f"learning rate must be positive, got {eta} at t={t}")
+        return eta
+
+    def c_struct(self, t: int) -> _lib.Hyper:
+        return _lib.Hyper(self.beta1, 1.0 - self.beta1, self.beta2, 1.0 - self.beta2,
+                          self.lr_at(t), self.weight_decay)
+
+
+@dataclass(frozen=True)
+class SyncPolicy:
+    period: int = 0
+    layers: Union[str, frozenset] = "all"
+
+    def __post_init__(self):
+        if self.period < 0:
+            raise ConfigError("period must be >= 0")
+        if isinstance(self.layers, str):
+            if self.layers not in ("all", "none"):
+                raise ConfigError('layers must be "all", "none", or a set of names')
+        else:
+            object.__setattr__(self, "layers", frozenset(self.layers))
+
+    def fires(self, t: int) -> bool:
+        return self.period > 0 and t % self.period == 0
+
+    def selects(self, layer: str) -> bool:
+        if isinstance(self.layers, str):
+            return self.layers == "all"
+        return layer in self.layers
+
+
+# ---------------------------------------------------------------------------
+# Flat device layout
+# ---------------------------------------------------------------------------
+
+class Layout:
+    """Sorted-name flat layout of a ParamSet: offsets/lengths per layer."""
+
+    def __init__(self, shapes: Mapping[str, tuple]):
+        self.names = sorted(shapes)
+        self.shapes = {k: tuple(shapes[k]) for k in self.names}
+        self.numel = {k: math.prod(self.shapes[k]) for k in self.names}
+        self.offset, off = {}, 0
+        for k in self.names:
+            self.offset[k] = off
+            off += self.numel[k]
+        self.n = off
+        self.seg_start = [self.offset[k] for k in self.names] + [self.n]
+        self.key = tuple((k, self.shapes[k]) for k in self.names)
+        self._dev = {}
+
+    def seg_start_dev(self, dev) -> torch.Tensor:
+        k = str(dev)
+        if k not in self._dev:
+            self._dev[k] = torch.tensor(self.seg_start, dtype=torch.int64, device=dev)
+        return self._dev[k]
+
+    def views(self, flat: torch.Tensor) -> "FlatParamSet":
+        return FlatParamSet(flat, self)
+
+    def runs(self, select) -> list:
+        """Maximal contiguous element ranges of the selected layers."""
+        out = []
+        for k in self.names:
+            if not select(k) or self.numel[k] == 0:
+                continue
+            a, b = self.offset[k], self.offset[k] + self.numel[k]
+            if out and out[-1][1] == a:
+                out[-1] = (out[-1][0], b)
+            else:
+                out.append((a, b))
+        return out
+
+
+class FlatParamSet(dict):
+    """``dict[name -> tensor]`` whose tensors are views of one flat fp32
+    CUDA buffer in sorted-name order (``.flat``, ``.layout``)."""
+
+    def __init__(self, flat: torch.Tensor, layout: Layout):
+        super().__init__()
+        self.flat = flat
+        self.layout = layout
+        for k in layout.names:
+            o = layout.offset[k]
+            super().__setitem__(k, flat[o:o + layout.numel[k]].view(layout.shapes[k]))
+        self.workspace = {}
+
+    @classmethod
+    def empty_like(cls, other: "FlatParamSet", zero: bool = True) -> "FlatParamSet":
+        flat = (torch.zeros_like if zero else torch.empty_like)(other.flat)
+        return cls(flat, other.layout)
+
+
+def _alloc_flat(layout: Layout, dev) -> torch.Tensor:
+    # 16-byte aligned by the caching allocator; pad the tail to a whole tile
+    return torch.zeros(max(layout.n, 1), dtype=torch.float32, device=dev)
+
+
+def _to_flat(ps: Mapping[str, torch.Tensor], layout: Layout, dev) -> FlatParamSet:
+    if isinstance(ps, FlatParamSet) and ps.layout.key == layout.key \
+            and ps.flat.device == dev and ps.flat.dtype == torch.float32:
+        return ps
+    flat = _alloc_flat(layout, dev)
+    for k in layout.names:
+        v = ps[k]
+        if not isinstance(v, torch.Tensor) or not v.is_cuda:
+            raise ConfigError(f"layer {k!r}: the CUDA path needs CUDA tensors "
+                              "(no CPU fallback)")
+        o = layout.offset[k]
+        flat[o:o + layout.numel[k]].copy_(v.reshape(-1))
+    return FlatParamSet(flat, layout)
+
+
+def _check_shapes(params: Mapping, grad: Mapping):
+    if set(params) != set(grad):
+        raise ConfigError(f"layer mismatch: {sorted(params)} vs {sorted(grad)}")
+    for name in params:
+        if tuple(params[name].shape) != tuple(grad[name].shape):
+            raise ConfigError(f"shape mismatch in layer {name!r}")
+
+
+@dataclass
+class WorkerState:
+    params: Mapping
+    momentum: Mapping
+    iteration: int = 0
+
+    @classmethod
+    def initial(cls, params: Mapping, device=None) -> "WorkerState":
+        """Flat fp32 copy of ``params`` on the device, zero momentum
+        (optimizer.py:69-72)."""
+        if not params or not all(isinstance(v, torch.Tensor) and v.is_cuda
+                                 for v in params.values()):
+            raise ConfigError("WorkerState.initial needs CUDA tensors (no CPU fallback)")
+        layout = Layout({k: tuple(v.shape) for k, v in params.items()})
+        dev = torch.device(device) if device is not None else \
+            next(iter(params.values())).device
+        th = _to_flat(params, layout, dev)
+        if th is params:  # never alias the caller's buffer
+            th = FlatParamSet(th.flat.clone(), layout)
+        return cls(params=th, momentum=FlatParamSet(_alloc_flat(layout, dev), layout),
+                   iteration=0)
+
+    def flat(self) -> tuple:
+        """(layout, theta FlatParamSet, momentum FlatParamSet) on device."""
+        p = self.params
+        layout = p.layout if isinstance(p, FlatParamSet) else \
+            Layout({k: tuple(v.shape) for k, v in p.items()})
+        dev = next(iter(p.values())).device
+        th = _to_flat(p, layout, dev)
+        m = _to_flat(self.momentum, layout, dev)
+        self.params, self.momentum = th, m
+        return layout, th, m
+
+    def new_grad_buffer(self) -> FlatParamSet:
+        """A zeroed gradient ParamSet in this state's flat layout (the fast
+        path: no gather before the step)."""
+        _, th, _ = self.flat()
+        return FlatParamSet.empty_like(th)
+
+
+def hash_params(params: Mapping) -> str:
+    """Stable digest for cross-rank checks (optimizer.py:34-40); fp32 bytes."""
+    h = hashlib.sha256()
+    for name in sorted(params):
+        h.update(name.encode())
+        h.update(params[name].detach().to(torch.float32).contiguous().cpu().numpy().tobytes())
+    return h.hexdigest()
+
+
+# ---------------------------------------------------------------------------
+# Step workspace (preallocated per layout x world x algorithm)
+# ---------------------------------------------------------------------------
+
+class _Workspace:
+    def __init__(self, layout: Layout, dev, P: int, kind: str, F: int, ternary: bool,
+                 metrics: bool):
+        n = layout.n
+        self.L = L = owner_elems(n, P)
+        self.cw = L // 32
+        self.F = F
+        z = lambda k, dt=torch.int32: torch.zeros(max(k, 1), dtype=dt, device=dev)  # noqa
+        self.flags = z(1)
+        if kind == "1bit":
+            self.send = z(P * self.cw)
+            self.recv = z(P * self.cw) if P > 1 else self.send
+        elif kind == "fields":
+            self.cwf = L * F // 32
+            self.send = z(P * self.cwf)
+            self.red = z(self.cwf)
+        elif kind == "f64":
+            self.send = z(P * L, torch.float64)
+            self.recv = z(P * L, torch.float64) if P > 1 else self.send
+        self.full = z(P * self.cw)
+        self.nz = z(P * self.cw) if ternary else None
+        self.ties = z(P * self.cw) if metrics else None
+        self.l1 = None
+        self.norms = self.scales = None
+
+
+def _workspace(th: FlatParamSet, P: int, kind: str, F: int, ternary: bool,
+               metrics: bool) -> _Workspace:
+    key = (P, kind, F, ternary, metrics)
+    ws = th.workspace.get(key)
+    if ws is None:
+        ws = _Workspace(th.layout, th.flat.device, P, kind, F, ternary, metrics)
+        th.workspace[key] = ws
+    return ws
+
+
+class _L1Plan:
+    """Owns the numpy-order summation schedule of a layout (csrc/l1norm.cu)."""
+
+    def __init__(self, layout: Layout):
+        arr = (C.c_int64 * len(layout.seg_start))(*layout.seg_start)
+        h = C.c_void_p()
+        _lib.check(_lib.load().lc_l1_plan_create(C.byref(h), arr, len(layout.names)),
+                   "lc_l1_plan_create")
+        self.handle = h.value
+
+    def __del__(self):
+        try:
+            if self.handle:
+                _lib.load().lc_l1_plan_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def _l1_scales(ws: _Workspace, layout: Layout, dev, g, m, mask, hyp, qmax, stream):
+    if ws.l1 is None:
+        ws.l1 = _L1Plan(layout)
+        ws.norms = torch.zeros(len(layout.names), dtype=torch.float64, device=dev)
+        ws.scales = torch.zeros(len(layout.names), dtype=torch.float64, device=dev)
+    _lib.call("lc_l1_scales", ws.l1.handle, g.data_ptr(), m.data_ptr(), _lib.ptr(mask),
+              C.byref(hyp), qmax, ws.norms.data_ptr(), ws.scales.data_ptr(), stream)
+    return _lib.Segments(layout.seg_start_dev(dev).data_ptr(), ws.scales.data_ptr(),
+                         len(layout.names), qmax)
+
+
+def _flat_mask(mask, layout: Layout, dev):
+    if mask is None:
+        return None
+    sel = [k for k in layout.names if k in mask]
+    if not sel:
+        return None
+    flat = torch.ones(max(layout.n, 1), dtype=torch.uint8, device=dev)
+    for k in sel:
+        mk = mask[k]
+        if not isinstance(mk, torch.Tensor):
+            import numpy as np
+            mk = torch.from_numpy(np.asarray(mk))
+        o = layout.offset[k]
+        flat[o:o + layout.numel[k]].copy_(mk.reshape(-1).to(torch.bool).to(torch.uint8))
+    return flat
+
+
+def _off(t: torch.Tensor, elems: int) -> int:
+    return t.data_ptr() + elems * t.element_size()
+
+
+def _raise_flags(bits: int, binary: bool):
+    if bits & (_lib.LC_FLAG_ZERO_SIGN | _lib.LC_FLAG_TIE_TERNARY):
+        if binary:
+            raise ConfigError("1-bit path cannot carry exact zeros; use the alternating policy")
+        raise ConfigError("binary_signs requires values in {-1, +1}")
+
+
+# ---------------------------------------------------------------------------
+# Steps
+# ---------------------------------------------------------------------------
+
+def lion_step(state: WorkerState, grad, h: LionHyper) -> WorkerState:
+    """Single-worker Lion (optimizer.py:114-131): exact-ternary sign, one
+    fused pass.  In place (donates ``state``)."""
+    _check_shapes(state.params, grad)
+    layout, th, m = state.flat()
+    dev = th.flat.device
+    g = _to_flat(grad, layout, dev)
+    t = state.iteration + 1
+    hyp = h.c_struct(t)
+    flags = torch.zeros(1, dtype=torch.int32, device=dev)
+    st = torch.cuda.current_stream(dev).cuda_stream
+    _lib.call("lc_fused_local_step", th.flat.data_ptr(), m.flat.data_ptr(), g.flat.data_ptr(),
+              None, layout.n, C.byref(hyp), 0, _lib.LC_LOCAL_PS, None, None, None, None,
+              flags.data_ptr(), st)
+    return WorkerState(params=th, momentum=m, iteration=t)
+
+
+def _validate(spec, algo):
+    if algo not in VOTE_ALGOS:
+        raise ConfigError(f"unknown vote algorithm {algo!r}")
+    if algo == "direct" and spec is None:
+        raise ConfigError("direct allreduce needs an integer QuantSpec")
+    if spec is not None and not spec.cuda_supported():
+        raise ConfigError(f"{spec} is not implemented on the CUDA path "
+                          "(finite norm_p=1 with nearest rounding, or bits=1)")
+
+
+def distributed_lion_step(state: WorkerState, grad_i, h: LionHyper,
+                          spec: QuantSpec | None, topo: Topology, algo: str,
+                          mask: Mapping | None = None, zero_mode: str = "alternating",
+                          rng=None, metrics_out: dict | None = None) -> WorkerState:
+    """One distributed Lion Cub step (optimizer.py:172-210) on this rank.
+
+    Every rank must call it in the same order with the same layout; the
+    input state is donated (updated in place).  ``metrics_out`` receives the
+    reference's per-layer "ties", "vote_sign" and "c_local" (costly: a host
+    sync and an f64 copy of c)."""
+    _validate(spec, algo)
+    _check_shapes(state.params, grad_i)
+    layout, th, m = state.flat()
+    dev = th.flat.device
+    P, r = topo.world_size, topo.rank
+    t = state.iteration + 1
+    policy = SignPolicy(mode=zero_mode, iteration=t)
+    fill = policy.kernel_fill()
+    ternary = fill == 0
+    hyp = h.c_struct(t)
+    eta, wd = hyp.lr, hyp.weight_decay
+    if algo == "compressed1bit":
+        kind, binary, qmax = "1bit", True, 0
+    elif spec is None:
+        kind, binary, qmax = "f64", False, 0
+    elif spec.bits == 1:
+        kind, binary, qmax = "fields", True, 1
+    else:
+        kind, binary, qmax = "fields", False, spec.qmax
+    F = 1
+    if kind == "fields":
+        # reference capacity rule first: CapacityError before any exchange
+        choose_lane_bits(P, qmax, binary_signs=binary)
+        F = field_bits(P, 1 if binary else 2 * qmax)
+    metrics = metrics_out is not None
+    n = layout.n
+    with torch.cuda.device(dev):
+        stream = topo.stream
+        s = stream.cuda_stream
+        with torch.cuda.stream(stream):
+            g = _to_flat(grad_i, layout, dev)
+            mflat = _flat_mask(mask, layout, dev)
+            ws = _workspace(th, P, kind if P > 1 else "local", F,
+                            ternary and kind != "1bit", metrics)
+            gen = topo.next_generation()
+            if metrics:
+                c_local = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+                _lib.call("lc_compute_c", g.flat.data_ptr(), m.flat.data_ptr(),
+                          _lib.ptr(mflat), n, C.byref(hyp), c_local.data_ptr(), s)
+            if ternary and binary:
+                _ternary_precheck(topo, gen, g, m, mflat, n, hyp, dev, s, kind)
+            segs = None
+            if kind == "fields" and not binary:
+                segs = _l1_scales(ws, layout, dev, g.flat, m.flat, mflat, hyp, qmax, s)
+            if P == 1:
+                mode = (_lib.LC_LOCAL_BINARY if binary else
+                        _lib.LC_LOCAL_QUANT if kind == "fields" else _lib.LC_LOCAL_PS)
+                _lib.call("lc_fused_local_step", th.flat.data_ptr(), m.flat.data_ptr(),
+                          g.flat.data_ptr(), _lib.ptr(mflat), n, C.byref(hyp), fill, mode,
+                          C.byref(segs) if segs is not None else None,
+                          ws.full.data_ptr() if metrics else None,
+                          ws.nz.data_ptr() if (metrics and ws.nz is not None) else None,
+                          _lib.ptr(ws.ties), ws.flags.data_ptr(), s)
+                nz = ws.nz if metrics else None
+            else:
+                nz = _exchange_and_vote(topo, gen, ws, kind, binary, F, qmax, fill, n,
+                                        g, m, mflat, hyp, segs, s,
+                                        tree=algo == "ps_efficient")
+                _lib.call("lc_apply_update", th.flat.data_ptr(), n, ws.full.data_ptr(),
+                          _lib.ptr(nz), eta, wd, s)
+            if metrics:
+                _fill_metrics(metrics_out, layout, dev, ws, nz, c_local, s)
+    return WorkerState(params=th, momentum=m, iteration=t)
+
+
+def _ternary_precheck(topo, gen, g, m, mflat, n, hyp, dev, s, kind):
+    """exact-ternary on a binary path: the reference raises ConfigError on any
+    zero sign before communicating (collectives.py:264-267, :202-203).  Check
+    on every rank before touching the state, then agree on the outcome."""
+    c = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+    _lib.call("lc_compute_c", g.flat.data_ptr(), m.flat.data_ptr(), _lib.ptr(mflat), n,
+              C.byref(hyp), c.data_ptr(), s)
+    L = owner_elems(n, topo.world_size)
+    words = torch.zeros(topo.world_size * L // 32, dtype=torch.int32, device=dev)
+    flags = torch.zeros(1, dtype=torch.int32, device=dev)
+    _lib.call("lc_sign_pack_f64", c.data_ptr(), n, 0, words.data_ptr(), flags.data_ptr(), s)
+    if kind == "1bit":
+        # the owner tally must not tie either (collectives.py:290-293)
+        P, r = topo.world_size, topo.rank
+        cw = L // 32
+        recv = words
+        if P > 1:
+            recv = torch.zeros_like(words)
+            topo.transport.alltoall(r, gen, words, recv, cw * 4)
+        voted = torch.zeros(cw, dtype=torch.int32, device=dev)
+        _lib.call("lc_vote_bits", recv.data_ptr(), P, cw, owner_valid(n, P, r), 0,
+                  voted.data_ptr(), None, flags.data_ptr(), s)
+    if topo.world_size > 1:
+        topo.transport.allreduce_max_u32(topo.rank, gen, flags)
+    _raise_flags(int(flags.item()), binary=kind == "1bit")
+
+
+def _exchange_and_vote(topo, gen, ws, kind, binary, F, qmax, fill, n, g, m, mflat, hyp,
+                       segs, s, tree=False):
+    """K1 encode -> exchange -> owner vote into ws.full (+nz) -> allgather."""
+    P, r = topo.world_size, topo.rank
+    tp = topo.transport
+    cw = ws.cw
+    nvalid = owner_valid(n, P, r)
+    tie_ptr = _off(ws.ties, r * cw) if ws.ties is not None else None
+    nz_ptr = _off(ws.nz, r * cw) if ws.nz is not None else None
+    hp = C.byref(hyp)
+    gp, mp, mk = g.flat.data_ptr(), m.flat.data_ptr(), _lib.ptr(mflat)
+    if kind == "1bit":
+        _lib.call("lc_encode", gp, mp, mk, n, hp, fill, _lib.LC_ENC_SIGN1, 1, None,
+                  ws.send.data_ptr(), ws.flags.data_ptr(), s)
+        tp.alltoall(r, gen, ws.send, ws.recv, cw * 4)
+        _lib.call("lc_vote_bits", ws.recv.data_ptr(), P, cw, nvalid, fill,
+                  _off(ws.full, r * cw), tie_ptr, ws.flags.data_ptr(), s)
+    elif kind == "fields":
+        enc = _lib.LC_ENC_SIGN_FIELDS if binary else _lib.LC_ENC_QUANT_FIELDS
+        _lib.call("lc_encode", gp, mp, mk, n, hp, fill, enc, F,
+                  C.byref(segs) if segs is not None else None, ws.send.data_ptr(),
+                  ws.flags.data_ptr(), s)
+        tp.reduce_scatter_u32(r, gen, ws.send, ws.red, ws.cwf)
+        _lib.call("lc_fields_vote", ws.red.data_ptr(), nvalid, F, P,
+                  0 if binary else qmax, int(binary), fill, _off(ws.full, r * cw),
+                  nz_ptr, tie_ptr, None, s)
+    else:  # f64 full precision
+        _lib.call("lc_encode", gp, mp, mk, n, hp, fill, _lib.LC_ENC_F64, 64, None,
+                  ws.send.data_ptr(), ws.flags.data_ptr(), s)
+        tp.alltoall(r, gen, ws.send, ws.recv, ws.L * 8)
+        _lib.call("lc_f64_sum_vote", ws.recv.data_ptr(), P, nvalid, ws.L,
+                  int(tree), fill, _off(ws.full, r * cw), nz_ptr, tie_ptr,
+                  None, s)
+    tp.allgather(r, gen, ws.full[r * cw:], ws.full, cw * 4)
+    if ws.nz is not None:
+        tp.allgather(r, gen, ws.nz[r * cw:], ws.nz, cw * 4)
+    if ws.ties is not None:
+        tp.allgather(r, gen, ws.ties[r * cw:], ws.ties, cw * 4)
+    return ws.nz
+
+
+def _fill_metrics(out: dict, layout: Layout, dev, ws, nz, c_local, s):
+    n = layout.n
+    counts = torch.zeros(len(layout.names), dtype=torch.int64, device=dev)
+    _lib.call("lc_count_bits_segmented", ws.ties.data_ptr(),
+              layout.seg_start_dev(dev).data_ptr(), len(layout.names),
+              counts.data_ptr(), s)
+    signs = torch.empty(max(n, 1), dtype=torch.int8, device=dev)
+    _lib.call("lc_bits_to_sign", ws.full.data_ptr(), _lib.ptr(nz), n, signs.data_ptr(), s)
+    signs = signs.long()
+    cl = counts.tolist()
+    for i, k in enumerate(layout.names):
+        o, c = layout.offset[k], layout.numel[k]
+        out.setdefault("ties", {})[k] = int(cl[i])
+        out.setdefault("vote_sign", {})[k] = signs[o:o + c].view(layout.shapes[k])
+        out.setdefault("c_local", {})[k] = c_local[o:o + c].view(layout.shapes[k])
+
+
+def maybe_sync_momentum(state: WorkerState, policy: SyncPolicy,
+                        topo: Topology) -> WorkerState:
+    """Average the selected layers' momentum across ranks at firing steps
+    (optimizer.py:244-258), bit-identical to allreduce_mean_f32.  No-op (no
+    communication) when the policy does not fire.  In place."""
+    if not policy.fires(state.iteration):
+        return state
+    layout, th, m = state.flat()
+    dev = m.flat.device
+    with torch.cuda.device(dev), torch.cuda.stream(topo.stream):
+        runs = layout.runs(policy.selects)
+        if topo.world_size > 1 and runs:
+            longest = max(b - a for a, b in runs)
+            s = -(-longest // topo.world_size)
+            key = ("sync", topo.world_size, s)
+            scratch = m.workspace.get(key)
+            if scratch is None:
+                scratch = torch.empty(topo.world_size * s, dtype=torch.float32, device=dev)
+                m.workspace[key] = scratch
+            for a, b in runs:
+                gen = topo.next_generation()
+                seg = m.flat[a:b]
+                mean_into(topo, gen, seg, seg, scratch)
+    return replace(state, params=th, momentum=m)

@@ -1,0 +1,321 @@
+"""Parity of the CUDA path with the reference (golden vectors produced by the
+real reference) and with the CPU oracle at larger sizes.  Needs a B200.
+
+Tolerances: packed words, votes, ties, p-bit sums, quantized ints and c
+(float64) are compared bit-for-bit.  theta' and m' are fp32 state: they must
+equal float32 of the reference's float64 result exactly (0 ulp), because the
+kernels compute the same float64 expression and round once.
+"""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import lioncub_oracle as O
+from tests import golden_io as G
+from tests.gpu_helpers import assert_f32_equal, run_step_case
+
+pytestmark = pytest.mark.gpu
+
+lc = pytest.importorskip("paper_2411_16462_b200")
+from paper_2411_16462_b200 import _lib  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    _lib.load()  # fail loudly if the extension is missing
+
+
+STEP_NAMES = [c["name"] for c in G.step_cases()]
+
+
+@pytest.mark.parametrize("name", STEP_NAMES)
+def test_step_matches_reference_golden(name):
+    gc = G.step_case(name)
+    case = gc["case"]
+    res = run_step_case(case, gc["theta"], gc["m"], gc["g"], mask=gc["mask"])
+    for r, (th, m, met, it) in enumerate(res):
+        assert it == case["iteration"] + 1
+        for k in gc["sizes"]:
+            assert_f32_equal(th[k], gc["theta_out"][k], f"{name} theta {k} r{r}")
+            assert_f32_equal(m[k], gc["m_out"][r][k], f"{name} m {k} r{r}")
+            assert np.array_equal(met["vote_sign"][k], gc["sign"][k]), (name, k)
+            assert met["ties"][k] == gc["ties"][k], (name, k, met["ties"][k])
+            if gc["c"][r][k] is not None:
+                assert np.array_equal(met["c_local"][k].view(np.int64),
+                                      gc["c"][r][k].view(np.int64)), (name, k)
+
+
+def _hyper(lr=1e-3, wd=0.0):
+    return _lib.Hyper(0.9, 1.0 - 0.9, 0.99, 1.0 - 0.99, lr, wd)
+
+
+@pytest.mark.parametrize("name", [c["name"] for c in G.step_cases()
+                                  if c["algo"] == "compressed1bit"])
+def test_packed_sign_words_bit_exact(name):
+    """K1's 1-bit words == pack(apply_sign(c), 1, 1).payload (quant.py:330-356)."""
+    gc = G.step_case(name)
+    case = gc["case"]
+    fill = 0 if case["zero_mode"] == "exact-ternary" else O.zero_fill(case["iteration"] + 1)
+    for r in range(case["world"]):
+        for k in gc["sizes"]:
+            ref = gc["words"][r][k]
+            if ref is None:
+                continue
+            g = torch.from_numpy(gc["g"][r][k]).cuda()
+            m = torch.from_numpy(gc["m"][r][k].copy()).cuda()
+            mask = None
+            if gc["mask"] is not None and k in gc["mask"]:
+                mask = torch.from_numpy(gc["mask"][k].astype(np.uint8)).cuda()
+            n = g.numel()
+            out = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
+            flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+            hyp = _hyper()
+            _lib.call("lc_encode", g.data_ptr(), m.data_ptr(), _lib.ptr(mask), n,
+                      C.byref(hyp), fill, _lib.LC_ENC_SIGN1, 1, None, out.data_ptr(),
+                      flags.data_ptr(), 0)
+            got = out.cpu().numpy().view(np.uint32)
+            nb = (n + 7) // 8  # reference payload bytes; compare the valid bits
+            gb = got.view(np.uint8)[:nb].copy()
+            rb = ref.view(np.uint8)[:nb].copy()
+            if n % 8:
+                keep = (1 << (n % 8)) - 1
+                gb[-1] &= keep
+                rb[-1] &= keep
+            assert np.array_equal(gb, rb), (name, k, r)
+
+
+@pytest.mark.parametrize("name", [c["name"] for c in G.step_cases()
+                                  if c["bits"] is not None and c["bits"] > 1])
+def test_l1_norm_and_quantized_ints_bit_exact(name):
+    """numpy-order L1 norm (quant.py:156-179) and q ints (quant.py:236-243)."""
+    gc = G.step_case(name)
+    case = gc["case"]
+    sizes = gc["sizes"]
+    names = sorted(sizes)
+    qmax = 2 ** (case["bits"] - 1) - 1
+    starts = [0]
+    for k in names:
+        starts.append(starts[-1] + int(np.prod(sizes[k])))
+    n = starts[-1]
+    arr = (C.c_int64 * len(starts))(*starts)
+    plan = C.c_void_p()
+    _lib.check(_lib.load().lc_l1_plan_create(C.byref(plan), arr, len(names)))
+    try:
+        for r in range(case["world"]):
+            g = torch.from_numpy(np.concatenate([gc["g"][r][k] for k in names])).cuda()
+            m = torch.from_numpy(np.concatenate([gc["m"][r][k] for k in names])).cuda()
+            mask = None
+            if gc["mask"] is not None:
+                mk = np.concatenate([gc["mask"].get(k, np.ones(sizes[k], bool))
+                                     for k in names]).astype(np.uint8)
+                mask = torch.from_numpy(mk).cuda()
+            norms = torch.zeros(len(names), dtype=torch.float64, device="cuda")
+            scales = torch.zeros_like(norms)
+            hyp = _hyper()
+            _lib.call("lc_l1_scales", plan.value, g.data_ptr(), m.data_ptr(), _lib.ptr(mask),
+                      C.byref(hyp), qmax, norms.data_ptr(), scales.data_ptr(), 0)
+            got_norms = norms.cpu().numpy()
+            for i, k in enumerate(names):
+                assert got_norms[i] == float(gc["norm"][r][k]), (name, k, r)
+            # quantize into 32-bit fields and compare ints
+            seg_start = torch.tensor(starts, dtype=torch.int64, device="cuda")
+            segs = _lib.Segments(seg_start.data_ptr(), scales.data_ptr(), len(names), qmax)
+            out = torch.zeros(n, dtype=torch.int32, device="cuda")
+            flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+            _lib.call("lc_encode", g.data_ptr(), m.clone().data_ptr(), _lib.ptr(mask), n,
+                      C.byref(hyp), 1, _lib.LC_ENC_QUANT_FIELDS, 32, C.byref(segs),
+                      out.data_ptr(), flags.data_ptr(), 0)
+            q = out.cpu().numpy().astype(np.int64) - qmax
+            ref = np.concatenate([gc["q"][r][k].astype(np.int64) for k in names])
+            assert np.array_equal(q, ref), (name, r)
+    finally:
+        _lib.load().lc_l1_plan_destroy(plan.value)
+
+
+@pytest.mark.parametrize("name", [c["name"] for c in G.collective_cases()])
+def test_collective_matches_reference_golden(name):
+    gc = G.collective_case(name)
+    case = gc["case"]
+    world = case["world"]
+
+    def fn(topo):
+        x = torch.from_numpy(np.asarray(gc["inputs"][topo.rank])).cuda()
+        if case["kind"] == "direct":
+            v = lc.direct_allreduce(x, topo, q_max=case["q_max"],
+                                    binary_signs=case.get("binary", False))
+            return v.values.cpu().numpy(), v.ties
+        if case["kind"] == "compressed":
+            v = lc.compressed_allreduce_1bit(x, topo, lc.SignPolicy("alternating", case["t"]))
+            return v.values.cpu().numpy(), v.ties
+        return lc.allreduce_mean_f32(x, topo).cpu().numpy(), None
+
+    for vals, ties in lc.run_ranks(world, fn):
+        if case["kind"] == "mean":
+            assert np.array_equal(vals.view(np.int32), gc["values"].view(np.int32))
+        else:
+            assert np.array_equal(vals, gc["values"])
+            assert ties == gc["ties"]
+
+
+# ---- larger sizes against the oracle ---------------------------------------
+
+BIG = {"emb": (40_000,), "h0.w": (300_017,), "h1.w": (262_144,), "norm": (1_000,)}
+
+
+@pytest.mark.parametrize("algo,bits,world,kind,zm", [
+    ("compressed1bit", None, 4, "laplace", "alternating"),
+    ("compressed1bit", None, 8, "ties", "alternating"),
+    ("direct", 1, 8, "laplace", "alternating"),
+    ("direct", 1, 3, "ties", "exact-ternary"),
+    ("direct", 5, 8, "outliers", "alternating"),
+    ("direct", 8, 4, "laplace", "exact-ternary"),
+    ("ps", None, 4, "cancel", "exact-ternary"),
+    ("ps_efficient", None, 8, "laplace", "alternating"),
+    ("compressed1bit", None, 1, "laplace", "alternating"),
+    ("direct", 5, 1, "outliers", "alternating"),
+])
+def test_step_matches_oracle_large(algo, bits, world, kind, zm):
+    ranks = O.synth_rank_inputs(7, world, BIG, kind)
+    h = O.Hyper(0.9, 0.99, 1e-4, 0.1)
+    spec = None if bits is None else O.Spec(bits)
+    it = 2
+    nt, nm, sign, ties, _, _ = O.distributed_step(
+        [rk["theta"] for rk in ranks], [rk["m"] for rk in ranks], [rk["g"] for rk in ranks],
+        h, spec, algo, it, zero_mode=zm)
+    case = dict(world=world, lr=1e-4, wd=0.1, bits=bits, algo=algo, iteration=it,
+                zero_mode=zm)
+    res = run_step_case(case, ranks[0]["theta"], [rk["m"] for rk in ranks],
+                        [rk["g"] for rk in ranks])
+    for r, (th, m, met, _) in enumerate(res):
+        for k in BIG:
+            assert_f32_equal(th[k], nt[0][k], f"theta {k}")
+            assert_f32_equal(m[k], nm[r][k], f"m {k}")
+            assert np.array_equal(met["vote_sign"][k], sign[k])
+            assert met["ties"][k] == ties[k]
+
+
+def test_momentum_sync_matches_oracle_large():
+    world = 8
+    ranks = O.synth_rank_inputs(3, world, BIG, "laplace")
+    h = O.Hyper(0.9, 0.99, 1e-4, 0.0)
+    _, nm, *_ = O.distributed_step([rk["theta"] for rk in ranks], [rk["m"] for rk in ranks],
+                                   [rk["g"] for rk in ranks], h, None, "compressed1bit", 9)
+    synced = O.sync_momentum(nm, 10, frozenset({"emb", "h1.w"}), 10)
+    case = dict(world=world, lr=1e-4, wd=0.0, bits=None, algo="compressed1bit",
+                iteration=9, zero_mode="alternating", sync=(10, ["emb", "h1.w"]))
+    res = run_step_case(case, ranks[0]["theta"], [rk["m"] for rk in ranks],
+                        [rk["g"] for rk in ranks], metrics=False)
+    for r, (_, m, _, _) in enumerate(res):
+        for k in BIG:
+            assert_f32_equal(m[k], synced[r][k], f"m {k} r{r}")
+
+
+# ---- reference error behaviour ---------------------------------------------
+
+def test_capacity_guard_before_any_communication():
+    tp = lc.LocalTransport(125)
+    topo = lc.Topology(world_size=125, rank=0, transport=tp)
+    with pytest.raises(lc.CapacityError):
+        lc.direct_allreduce(torch.zeros(4, dtype=torch.int64, device="cuda"), topo,
+                            q_max=15, lane_bits=8)
+    assert all(p is None for p in tp._posts)
+
+
+def test_step_capacity_error_propagates():
+    h = lc.LionHyper(beta1=0.9, beta2=0.99, lr=0.01)
+    topo = lc.Topology(world_size=10 ** 8, rank=0, transport=lc.LocalTransport(1))
+    st = lc.WorkerState.initial({"w": torch.zeros(2, device="cuda")})
+    with pytest.raises(lc.CapacityError):
+        lc.distributed_lion_step(st, {"w": torch.ones(2, device="cuda")}, h,
+                                 lc.QuantSpec(bits=8), topo, "direct")
+
+
+def test_direct_requires_spec_and_zero_rejection():
+    h = lc.LionHyper(beta1=0.9, beta2=0.99, lr=0.01)
+
+    def fn(topo):
+        st = lc.WorkerState.initial({"w": torch.zeros(2, device="cuda")})
+        return lc.distributed_lion_step(st, {"w": torch.ones(2, device="cuda")}, h,
+                                        None, topo, "direct")
+
+    with pytest.raises(lc.ConfigError):
+        lc.run_ranks(2, fn)
+
+    def zeros(topo):
+        return lc.compressed_allreduce_1bit(torch.zeros(3, device="cuda"), topo,
+                                            lc.SignPolicy("exact-ternary"))
+
+    with pytest.raises(lc.ConfigError):
+        lc.run_ranks(2, zeros)
+
+
+def test_timeout_names_missing_rank():
+    def fn(topo):
+        if topo.rank == 1:
+            return None
+        return lc.compressed_allreduce_1bit(torch.ones(8, device="cuda"), topo,
+                                            lc.SignPolicy("alternating", 1))
+
+    with pytest.raises(lc.CollectiveError) as e:
+        lc.run_ranks(2, fn, timeout=0.3)
+    assert "1" in str(e.value)
+
+
+def test_tie_parity_two_steps():
+    """test_optimizer.py:137-153: t=1 tie -> theta -= lr; t=2 -> cancels."""
+    h = lc.LionHyper(beta1=0.9, beta2=0.99, lr=0.5)
+    grads = [torch.tensor([1.0]), torch.tensor([-1.0])]
+
+    def fn(topo):
+        st = lc.WorkerState.initial({"w": torch.zeros(1, device="cuda")})
+        g = {"w": grads[topo.rank].cuda()}
+        st = lc.distributed_lion_step(st, g, h, lc.QuantSpec(bits=1), topo, "compressed1bit")
+        first = st.params["w"].cpu().tolist()
+        st = lc.distributed_lion_step(st, g, h, lc.QuantSpec(bits=1), topo, "compressed1bit")
+        return first, st.params["w"].cpu().tolist()
+
+    for first, second in lc.run_ranks(2, fn):
+        assert first == [-0.5]
+        assert second == [0.0]
+
+
+def test_tie_rates():
+    """test_collectives.py:174-186: C(P,P/2)/2^P."""
+    n = 100_000
+    for world, expect in ((4, 0.375), (8, 0.2734375)):
+        rng = np.random.default_rng(world)
+        cs = [torch.from_numpy(rng.choice([-1.0, 1.0], size=n)).cuda() for _ in range(world)]
+
+        def fn(topo):
+            return lc.compressed_allreduce_1bit(cs[topo.rank], topo,
+                                                lc.SignPolicy("alternating", 1)).ties
+
+        assert abs(lc.run_ranks(world, fn)[0] / n - expect) < 0.01
+
+
+def test_lion_step_single_worker():
+    """test_optimizer.py:25-43."""
+    h = lc.LionHyper(beta1=0.9, beta2=0.99, lr=0.1)
+    st = lc.WorkerState.initial({"w": torch.zeros(1, device="cuda")})
+    st = lc.lion_step(st, {"w": torch.tensor([2.0], device="cuda")}, h)
+    assert st.params["w"].cpu().tolist() == [np.float32(-0.1)]
+    assert st.iteration == 1
+    h = lc.LionHyper(beta1=0.9, beta2=0.99, lr=0.1, weight_decay=0.1)
+    st = lc.WorkerState.initial({"w": torch.ones(1, device="cuda")})
+    st = lc.lion_step(st, {"w": torch.zeros(1, device="cuda")}, h)
+    assert st.params["w"].cpu().tolist() == [np.float32(0.99)]
+
+
+def test_cpu_tensors_fail_loudly():
+    h = lc.LionHyper()
+    with pytest.raises(lc.ConfigError):
+        lc.WorkerState.initial({"w": torch.zeros(3)})
+    st = lc.WorkerState.initial({"w": torch.zeros(3, device="cuda")})
+    topo = lc.Topology(1, 0, lc.LocalTransport(1))
+    with pytest.raises(lc.ConfigError):
+        lc.distributed_lion_step(st, {"w": torch.zeros(3)}, h, None, topo, "compressed1bit")
