@@ -222,50 +222,56 @@ class ClockSampler:
 # CPU baseline / reference arm: the oracle port on the host cores
 # ---------------------------------------------------------------------------
 
-def cpu_reference(world: int, algo: str, bits, sample: int, budget_s: float,
-                  threads: int | None = None) -> dict:
-    """Time the reference algorithm (oracle restatement of
+class CpuReference:
+    """The reference algorithm (the oracle's restatement of
     optimizer.distributed_lion_step, ranks simulated in one process) on a
-    bounded sample.  Element chunks run on a thread pool (numpy releases the
-    GIL), so ``cores`` threads work at once."""
-    from concurrent.futures import ThreadPoolExecutor
+    bounded sample, timed on the host cores.  Element chunks run on a thread
+    pool (numpy releases the GIL), so ``cores`` threads work at once."""
 
-    import numpy as np
+    def __init__(self, world: int, algo: str, bits, sample: int, threads: int | None = None):
+        from concurrent.futures import ThreadPoolExecutor
 
-    from oracle import lioncub_oracle as O
+        from oracle import lioncub_oracle as O
 
-    cores = threads or len(os.sched_getaffinity(0))
-    ranks = O.synth_rank_inputs(0, world, {"w": (sample,)}, "laplace")
-    h = O.Hyper(0.9, 0.99, 1e-4, 0.0)
-    spec = None if bits is None else O.Spec(bits)
-    chunk = -(-sample // cores)
-    pieces = []
-    for a in range(0, sample, chunk):
-        b = min(sample, a + chunk)
-        pieces.append(([{"w": rk["theta"]["w"][a:b]} for rk in ranks],
-                       [{"w": rk["m"]["w"][a:b]} for rk in ranks],
-                       [{"w": rk["g"]["w"][a:b]} for rk in ranks]))
+        self.O = O
+        self.world, self.algo, self.bits, self.sample = world, algo, bits, sample
+        self.cores = threads or len(os.sched_getaffinity(0))
+        ranks = O.synth_rank_inputs(0, world, {"w": (sample,)}, "laplace")
+        self.h = O.Hyper(0.9, 0.99, 1e-4, 0.0)
+        self.spec = None if bits is None else O.Spec(bits)
+        chunk = -(-sample // self.cores)
+        self.pieces = []
+        for a in range(0, sample, chunk):
+            b = min(sample, a + chunk)
+            self.pieces.append(([{"w": rk["theta"]["w"][a:b]} for rk in ranks],
+                                [{"w": rk["m"]["w"][a:b]} for rk in ranks],
+                                [{"w": rk["g"]["w"][a:b]} for rk in ranks]))
+        self.pool = ThreadPoolExecutor(max_workers=self.cores)
 
-    def one(piece):
+    def _one(self, piece):
         th, m, g = piece
-        O.distributed_step(th, m, g, h, spec, algo, 0)
+        self.O.distributed_step(th, m, g, self.h, self.spec, self.algo, 0)
 
-    times = []
-    with ThreadPoolExecutor(max_workers=cores) as ex:
-        list(ex.map(one, pieces))  # warm
+    def step(self) -> float:
+        t0 = time.perf_counter()
+        list(self.pool.map(self._one, self.pieces))
+        return time.perf_counter() - t0
+
+    def describe(self) -> str:
+        b = "" if self.bits is None else f", bits={self.bits}"
+        return (f"{self.sample}-param slice per rank x {self.world} simulated ranks "
+                f"({self.algo}{b}), float64 numpy port of optimizer.distributed_lion_step "
+                f"(oracle/lioncub_oracle.py) on {self.cores} host threads")
+
+    def timed(self, budget_s: float) -> dict:
+        self.step()
+        times = []
         t_end = time.perf_counter() + budget_s
-        while True:
-            t0 = time.perf_counter()
-            list(ex.map(one, pieces))
-            times.append(time.perf_counter() - t0)
-            if time.perf_counter() > t_end and len(times) >= 2:
-                break
-    t = statistics.median(times)
-    return {"value": world * sample / t, "unit": "params/s", "cores": cores,
-            "kind": "port", "sec_per_step": t, "steps": len(times),
-            "sample": f"{sample}-param slice per rank x {world} simulated ranks "
-                      f"({algo}{'' if bits is None else f', bits={bits}'}), float64 numpy "
-                      f"port of optimizer.distributed_lion_step on {cores} host threads"}
+        while not times or time.perf_counter() < t_end or len(times) < 2:
+            times.append(self.step())
+        t = statistics.median(times)
+        return {"value": self.world * self.sample / t, "unit": "params/s",
+                "cores": self.cores, "kind": "port", "sample": self.describe()}
 
 
 def run_reference_arm(args):
@@ -276,13 +282,10 @@ def run_reference_arm(args):
     n = numel(layout_fn())
     world = args.gpus
     sample = min(n, args.ref_sample)
-    steps = []
-    ref = cpu_reference(world, algo, bits, sample, budget_s=0.0)
-    per = ref["sec_per_step"]
-    for _ in range(args.warmup + args.steps):
-        r = cpu_reference(world, algo, bits, sample, budget_s=0.0)
-        steps.append(r["sec_per_step"])
-    timed = steps[args.warmup:]
+    ref = CpuReference(world, algo, bits, sample)
+    for _ in range(args.warmup):
+        ref.step()
+    timed = [ref.step() for _ in range(args.steps)]
     t = sum(timed) / len(timed)
     value = world * sample / t
     line = {"metric": METRIC, "value": value, "unit": "params/s", "n_gpus": world,
@@ -292,11 +295,10 @@ def run_reference_arm(args):
             "config": {"workload": args.workload, "description": desc, "params": n,
                        "algo": algo, "bits": bits, "world": world,
                        "sample_params_per_rank": sample},
-            "cpu_baseline": {"value": value, "unit": "params/s", "cores": ref["cores"],
-                             "kind": "port", "sample": ref["sample"]},
+            "cpu_baseline": {"value": value, "unit": "params/s", "cores": ref.cores,
+                             "kind": "port", "sample": ref.describe()},
             "e2e": {"value": value, "unit": "params/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0},
-            "note": f"first-call {per * 1e3:.1f} ms"}
+                    "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
 
@@ -484,9 +486,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_reference(1, algo, bits, min(n, args.ref_sample), args.cpu_budget)
-        cpu.pop("sec_per_step", None)
-        cpu.pop("steps", None)
+        cpu = CpuReference(1, algo, bits, min(n, args.ref_sample)).timed(args.cpu_budget)
 
     if rank == 0:
         line = {"metric": METRIC, "value": P * n / (ms * 1e-3), "unit": "params/s",
