@@ -43,8 +43,9 @@ enum {
   LC_FLAG_NAN = 1u << 1,       /* NaN in c (reference: PackRangeError)      */
   LC_FLAG_TIE_TERNARY = 1u << 2, /* tied 1-bit vote in exact-ternary mode
                                     (collectives.py:290-293)               */
-  LC_FLAG_RANGE = 1u << 3      /* |q| > q_max / non-binary value
+  LC_FLAG_RANGE = 1u << 3,     /* |q| > q_max / non-binary value
                                   (collectives.py:202-208)                  */
+  LC_FLAG_BARRIER_TIMEOUT = 1u << 4 /* a peer never reached lc_barrier     */
 };
 
 /* Encodings produced by the fused interpolate pass (lc_encode). */
@@ -74,6 +75,9 @@ int lc_abi_version(void);
 const char* lc_last_error(void);
 int lc_device_sm_count(int device);
 
+/* Maximum entries of a destination / peer table (blocks of a packed vector). */
+#define LC_MAX_BLOCKS 64
+
 /* ---- K1: fused Lion interpolate + sign/quantize + pack + momentum EMA ----
  * Replaces optimizer.py:199-201 (c, mask), :205 (m'), quant.py:273-279
  * (apply_sign), quant.py:330-356 (pack width 1 / F-bit fields),
@@ -82,41 +86,56 @@ int lc_device_sm_count(int device);
  * fp32 g,m (no FMA contraction) and writes m' (fp32) in place.
  *   fill: +1 / -1 = alternating zero fill (quant.py:151-153), 0 = ternary.
  *   field_bits: 1 for SIGN1, F in {1,2,4,8,16,32} for *_FIELDS, 64 for F64.
- *   out: uint32 words (ceil(n*F/32)) or double[n].
+ *   dst[j], j < nblocks: where block j (elements [j*L, (j+1)*L)) of the
+ *     packed vector goes -- uint32 words (L*F/32 per block) or doubles.
+ *     A local send buffer ([P][L*F/32] for an NCCL exchange) or, for the
+ *     NVLink path, the owner GPU's receive slot (peer pointer), so the
+ *     all-to-all happens inside the kernel.  L is a multiple of 1024.
  *   g, m must be 16-byte aligned. mask may be NULL (uint8 per element). */
 int lc_encode(const float* g, float* m, const uint8_t* mask, int64_t n,
               const lc_hyper* h, int fill, int enc, int field_bits,
-              const lc_segments* segs, void* out, uint32_t* flags,
-              void* stream);
+              const lc_segments* segs, void* const* dst, int32_t nblocks,
+              int64_t L, uint32_t* flags, void* stream);
+
+/* Output tables of the owner-side vote kernels: voted/nz/tie_bits are host
+ * arrays of `nout` word pointers; the owner's block is written to every one
+ * (nout = 1: local gather buffer before an NCCL allgather; nout = P: every
+ * rank's gather buffer over NVLink, i.e. the allgather inside the kernel).
+ * nz / tie_bits may be NULL.  nz marks non-zero aggregates (exact-ternary),
+ * tie_bits marks aggregates that are exactly 0 (VoteResult.ties). */
 
 /* ---- K4: owner-side 1-bit majority vote over P packed chunks ----
  * Replaces collectives.py:288-293 (stack+sum, local ties, apply_sign).
- * recv: [P][cw] words, chunk of element range starting at bit 0;
- * n_valid: number of real elements in this chunk (pads excluded).
- * voted: cw words. tie_bits (nullable): 1 where the tally is 0. */
+ * recv: [P][cw] words (cw % 4 == 0); n_valid: real elements in the chunk.
+ * sum_mode 0 = compressed1bit (exact-ternary tie -> LC_FLAG_TIE_TERNARY);
+ * sum_mode 1 = sum-of-signs (the tally is the exact p-bit sum 2k-P,
+ * collectives.py:241-248; a zero sum is a zero update in exact-ternary). */
 int lc_vote_bits(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid,
-                 int fill, uint32_t* voted, uint32_t* tie_bits,
-                 uint32_t* flags, void* stream);
+                 int fill, int sum_mode, void* const* voted, void* const* nz,
+                 void* const* tie_bits, int32_t nout, uint32_t* flags,
+                 void* stream);
 
 /* ---- K6: owner-side p-bit sums -> signed aggregate -> 1-bit vote ----
  * Replaces collectives.py:241-249 (de-offset, ties) + :313-316
- * (majority_sign).  sums: F-bit fields holding sum of stored values for
- * n elements (n multiple of 32 words-worth is not required).
+ * (majority_sign).  sums: `rows` rows (stride row_stride words) of F-bit
+ * fields whose word-wise sum is the field sum over ranks (rows = 1 after an
+ * NCCL reduce-scatter, rows = P when peers wrote over NVLink).
  * offset: q_max (0 with binary=1 for sum-of-signs, signed = 2k-P).
- * voted/nz/tie: 1-bit words; nz (nullable) marks non-zero aggregates
- * (exact-ternary), values (nullable): signed aggregate as int64. */
-int lc_fields_vote(const uint32_t* sums, int64_t n, int32_t field_bits,
-                   int32_t P, int32_t offset, int32_t binary, int fill,
-                   uint32_t* voted, uint32_t* nz, uint32_t* tie_bits,
-                   int64_t* values, void* stream);
+ * values (nullable): signed aggregate as int64 (VoteResult.values). */
+int lc_fields_vote(const uint32_t* sums, int32_t rows, int64_t row_stride,
+                   int64_t n, int32_t field_bits, int32_t P, int32_t offset,
+                   int32_t binary, int fill, void* const* voted, void* const* nz,
+                   void* const* tie_bits, int32_t nout, int64_t* values,
+                   void* stream);
 
 /* ---- full-precision arm: P float64 rows (row stride `stride`) -> sum of
  * the first `len` elements in the reference's rank order (flat,
  * collectives.py:153-158, or binomial tree :96-109) -> sign words.
- * values (nullable) receives the f64 sum. */
+ * values (nullable) receives the f64 sum.  nout <= 32. */
 int lc_f64_sum_vote(const double* recv, int32_t P, int64_t len, int64_t stride,
-                    int tree, int fill, uint32_t* voted, uint32_t* nz,
-                    uint32_t* tie_bits, double* values, void* stream);
+                    int tree, int fill, void* const* voted, void* const* nz,
+                    void* const* tie_bits, int32_t nout, double* values,
+                    void* stream);
 
 /* ---- K5: theta' = theta - eta*(s + wd*theta)  (optimizer.py:204) ----
  * s = +1/-1 from sign bits; 0 where nz_bits (nullable) has a 0 bit. */
@@ -218,6 +237,29 @@ int lc_allreduce_max_u32(lc_comm_t comm, const uint32_t* send, uint32_t* recv,
                          int64_t count, void* stream);
 int lc_allreduce_sum_i64(lc_comm_t comm, const int64_t* send, int64_t* recv,
                          int64_t count, void* stream);
+
+/* ---- NVLink peer memory (symmetric buffers) ----
+ * lc_sym_alloc: cudaMalloc'ed, zeroed buffer + its 64-byte IPC handle;
+ * lc_sym_open maps a peer process's handle (lc_sym_close unmaps).  With one
+ * thread per GPU, lc_enable_peer_access makes raw peer pointers usable. */
+int lc_sym_alloc(int64_t bytes, void** ptr, uint8_t handle[64]);
+int lc_sym_free(void* ptr);
+int lc_sym_open(const uint8_t handle[64], void** ptr);
+int lc_sym_close(void* ptr);
+int lc_enable_peer_access(int32_t device, int32_t peer);
+/* Stream-ordered cross-GPU barrier: publish `epoch` into slot `rank` of every
+ * peer's flag array (peer_flags[j] = rank j's uint64[P] array), then wait
+ * until all P slots of my_flags reach it.  Sets LC_FLAG_BARRIER_TIMEOUT in
+ * *err after timeout_s instead of hanging (-> CollectiveError). */
+int lc_barrier(void* const* peer_flags, int32_t P, int32_t rank, uint64_t* my_flags,
+               uint64_t epoch, double timeout_s, uint32_t* err, void* stream);
+/* Momentum sync over peer memory (collectives.py:319-344): push block j of a
+ * fp32 vector (blocks of s) to dst[j]; the owner then averages its P rows in
+ * float64 rank order and stores the fp32 mean to every out[k]. */
+int lc_push_blocks_f32(const float* src, int64_t len, int64_t s, void* const* dst,
+                       int32_t P, void* stream);
+int lc_mean_bcast_f32(const float* recv, int32_t P, int64_t cnt, int64_t s,
+                      void* const* out, int32_t nout, void* stream);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -27,6 +27,9 @@ LC_FLAG_ZERO_SIGN = 1
 LC_FLAG_NAN = 2
 LC_FLAG_TIE_TERNARY = 4
 LC_FLAG_RANGE = 8
+LC_FLAG_BARRIER_TIMEOUT = 16
+
+LC_MAX_BLOCKS = 64
 
 LC_ENC_SIGN1 = 0
 LC_ENC_SIGN_FIELDS = 1
@@ -60,10 +63,10 @@ SIGNATURES = {
     "lc_abi_version": (INT, []),
     "lc_last_error": (C.c_char_p, []),
     "lc_device_sm_count": (INT, [INT]),
-    "lc_encode": (INT, [P, P, P, I64, P, INT, INT, INT, P, P, P, P]),
-    "lc_vote_bits": (INT, [P, I32, I64, I64, INT, P, P, P, P]),
-    "lc_fields_vote": (INT, [P, I64, I32, I32, I32, I32, INT, P, P, P, P, P]),
-    "lc_f64_sum_vote": (INT, [P, I32, I64, I64, INT, INT, P, P, P, P, P]),
+    "lc_encode": (INT, [P, P, P, I64, P, INT, INT, INT, P, P, I32, I64, P, P]),
+    "lc_vote_bits": (INT, [P, I32, I64, I64, INT, INT, P, P, P, I32, P, P]),
+    "lc_fields_vote": (INT, [P, I32, I64, I64, I32, I32, I32, I32, INT, P, P, P, I32, P, P]),
+    "lc_f64_sum_vote": (INT, [P, I32, I64, I64, INT, INT, P, P, P, I32, P, P]),
     "lc_apply_update": (INT, [P, I64, P, P, D, D, P]),
     "lc_fused_local_step": (INT, [P, P, P, P, I64, P, INT, INT, P, P, P, P, P, P]),
     "lc_mean_f32": (INT, [P, I32, I64, I64, P, P]),
@@ -90,6 +93,14 @@ SIGNATURES = {
     "lc_reduce_scatter_u32": (INT, [P, P, P, I64, P]),
     "lc_allreduce_max_u32": (INT, [P, P, P, I64, P]),
     "lc_allreduce_sum_i64": (INT, [P, P, P, I64, P]),
+    "lc_sym_alloc": (INT, [I64, P, P]),
+    "lc_sym_free": (INT, [P]),
+    "lc_sym_open": (INT, [P, P]),
+    "lc_sym_close": (INT, [P]),
+    "lc_enable_peer_access": (INT, [I32, I32]),
+    "lc_barrier": (INT, [P, I32, I32, P, C.c_uint64, D, P, P]),
+    "lc_push_blocks_f32": (INT, [P, I64, I64, P, I32, P]),
+    "lc_mean_bcast_f32": (INT, [P, I32, I64, I64, P, I32, P]),
 }
 
 _lock = threading.Lock()
@@ -140,6 +151,7 @@ def check(rc: int, what: str = "", rank=None, generation=None):
 # Entry points that enqueue one of OUR kernels (for launch accounting).
 KERNEL_CALLS = frozenset({
     "lc_encode", "lc_vote_bits", "lc_fields_vote", "lc_f64_sum_vote",
+    "lc_barrier", "lc_push_blocks_f32", "lc_mean_bcast_f32",
     "lc_apply_update", "lc_fused_local_step", "lc_mean_f32", "lc_compute_c",
     "lc_count_bits_segmented", "lc_bits_to_sign", "lc_pack_i64_fields",
     "lc_fields_decode", "lc_sign_pack_f64", "lc_sum_u32_rows"})
@@ -174,6 +186,16 @@ def call(name: str, *args, what: str | None = None):
     else:
         launches += KERNELS_PER_CALL.get(name, 0)
     return rc
+
+
+def table(ptrs) -> C.Array | None:
+    """Host array of device pointers (a destination / output table)."""
+    if ptrs is None:
+        return None
+    ptrs = list(ptrs)
+    if len(ptrs) > LC_MAX_BLOCKS:
+        raise ConfigError(f"at most {LC_MAX_BLOCKS} blocks per table")
+    return (C.c_void_p * len(ptrs))(*ptrs)
 
 
 def ptr(t) -> int | None:

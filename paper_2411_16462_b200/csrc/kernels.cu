@@ -46,6 +46,12 @@ struct SegQ {
   int qmax;
 };
 
+// Destination table: block j of a packed vector goes to p[j] (local send
+// buffer, or the owner GPU's receive slot over NVLink).
+struct Dst {
+  void* p[LC_MAX_BLOCKS];
+};
+
 // Per-lane cache of the segment (layer) containing the current element.
 struct SegCursor {
   int64_t lo = 0, hi = -1;
@@ -104,18 +110,23 @@ __device__ __forceinline__ void pack_store(uint32_t* __restrict__ out,
 }
 
 // ---------------------------------------------------------------------------
-// K1: c, m', encode.  One warp per 128-element tile, U tiles in flight.
+// K1: c, m', encode.  A warp owns a 1024-element super-tile (8 sub-tiles of
+// 128); its 32*F packed words are staged in shared memory and leave as
+// 128-byte coalesced stores to the block's destination, which is either a
+// local send buffer or the owner GPU's receive slot over NVLink (Dst table:
+// block j = elements [j*L, (j+1)*L) goes to dst.p[j]).
 // ---------------------------------------------------------------------------
-template <int ENC, int F, bool MASK, int U>
+template <int ENC, int F, bool MASK>
 __global__ void __launch_bounds__(256)
 k_encode(const float* __restrict__ g, float* __restrict__ m,
          const uint8_t* __restrict__ mask, int64_t n, Hyp h, int fill, SegQ sq,
-         void* __restrict__ out, uint32_t* __restrict__ flags) {
-  const int lane = threadIdx.x & 31;
+         Dst dst, int64_t L, uint32_t* __restrict__ flags) {
+  constexpr int WPS = (ENC == LC_ENC_F64) ? 1 : 32 * F;  // words per super-tile
+  __shared__ __align__(16) uint32_t stage[8][WPS];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t ntiles = (n + 127) >> 7, nfull = n >> 7;
-  const int64_t nwords = (ENC == LC_ENC_F64) ? 0 : (n * F + 31) / 32;
+  const int64_t nsup = (n + 1023) >> 10;
   const bool ternary = fill == 0;
   const uint32_t fillbit = fill > 0 ? 1u : 0u;
   const float4* g4 = reinterpret_cast<const float4*>(g);
@@ -123,98 +134,131 @@ k_encode(const float* __restrict__ g, float* __restrict__ m,
   uint32_t flag = 0;
   SegCursor cur;
 
-  for (int64_t t0 = gw; t0 < ntiles; t0 += nw * U) {
-    float4 gv[U], mv[U];
-    uchar4 mk[U];
+  for (int64_t sidx = gw; sidx < nsup; sidx += nw) {
+    const int64_t ebase = sidx << 10;
+    const int j = (int)(ebase / L);
+    const int64_t boff = ebase - (int64_t)j * L;  // element offset inside block j
+#pragma unroll 1
+    for (int k0 = 0; k0 < 8; k0 += 2) {
+      float4 gv[2], mv[2];
+      uchar4 mk[2];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      int64_t t = t0 + u * nw;
-      if (t < nfull) {
-        gv[u] = ld_stream(g4 + t * 32 + lane);
-        mv[u] = ld_stream(m4 + t * 32 + lane);
-        if (MASK) mk[u] = *reinterpret_cast<const uchar4*>(mask + t * 128 + lane * 4);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t t = t0 + u * nw;
-      if (t >= ntiles) break;  // warp-uniform
-      const bool full = t < nfull;
-      const int64_t e0 = t * 128 + lane * 4;
-      float ge[4], me[4];
-      bool valid[4], keep[4];
-      if (full) {
-        ge[0] = gv[u].x; ge[1] = gv[u].y; ge[2] = gv[u].z; ge[3] = gv[u].w;
-        me[0] = mv[u].x; me[1] = mv[u].y; me[2] = mv[u].z; me[3] = mv[u].w;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) valid[k] = true;
-        if (MASK) {
-          keep[0] = mk[u].x; keep[1] = mk[u].y; keep[2] = mk[u].z; keep[3] = mk[u].w;
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          valid[k] = e0 + k < n;
-          ge[k] = valid[k] ? g[e0 + k] : 0.f;
-          me[k] = valid[k] ? m[e0 + k] : 0.f;
-          keep[k] = MASK ? (valid[k] ? mask[e0 + k] != 0 : true) : true;
+      for (int u = 0; u < 2; ++u) {
+        const int64_t t = (ebase >> 7) + k0 + u;  // 128-element tile index
+        if ((t + 1) * 128 <= n) {
+          gv[u] = ld_stream(g4 + t * 32 + lane);
+          mv[u] = ld_stream(m4 + t * 32 + lane);
+          if (MASK) mk[u] = *reinterpret_cast<const uchar4*>(mask + t * 128 + lane * 4);
         }
       }
-      double c[4];
-      float mn[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        c[k] = lion_c(me[k], ge[k], h);
-        if (MASK && !keep[k]) c[k] = 0.0;  // np.where(mask, c, 0.0)
-        mn[k] = lion_m(me[k], ge[k], h);
-      }
-      if (full) {
-        st_stream(m4 + t * 32 + lane, make_float4(mn[0], mn[1], mn[2], mn[3]));
-      } else {
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (valid[k]) m[e0 + k] = mn[k];
-      }
-      if constexpr (ENC == LC_ENC_F64) {
-        double* o = reinterpret_cast<double*>(out);
+      for (int u = 0; u < 2; ++u) {
+        const int k = k0 + u;
+        const int64_t t = (ebase >> 7) + k;
+        const int64_t e0 = t * 128 + lane * 4;
+        if (t * 128 >= n) {  // whole sub-tile past the end (warp-uniform)
+          if (ENC != LC_ENC_F64)
+            for (int w = lane; w < 4 * F; w += 32) stage[wib][k * 4 * F + w] = 0u;
+          continue;
+        }
+        const bool full = (t + 1) * 128 <= n;
+        float ge[4], me[4];
+        bool valid[4], keep[4];
         if (full) {
-          __stcs(reinterpret_cast<double2*>(o + e0), make_double2(c[0], c[1]));
-          __stcs(reinterpret_cast<double2*>(o + e0 + 2), make_double2(c[2], c[3]));
+          ge[0] = gv[u].x; ge[1] = gv[u].y; ge[2] = gv[u].z; ge[3] = gv[u].w;
+          me[0] = mv[u].x; me[1] = mv[u].y; me[2] = mv[u].z; me[3] = mv[u].w;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) valid[q] = true;
+          if (MASK) {
+            keep[0] = mk[u].x; keep[1] = mk[u].y; keep[2] = mk[u].z; keep[3] = mk[u].w;
+          }
         } else {
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (valid[k]) o[e0 + k] = c[k];
-        }
-      } else {
-        uint32_t st[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if (ENC == LC_ENC_QUANT_FIELDS) {
-            if (valid[k]) {
-              double sc = cur.get(sq, e0 + k);
-              st[k] = (uint32_t)(quant_l1(c[k], sc, sq.qmax) + sq.qmax);
-            } else {
-              st[k] = 0u;
-            }
-          } else {
-            uint32_t b;
-            if (c[k] > 0.0) {
-              b = 1u;
-            } else if (c[k] < 0.0) {
-              b = 0u;
-            } else if (c[k] == 0.0) {  // -0.0 included (np.sign(-0.0) == 0)
-              b = fillbit;
-              if (ternary && valid[k]) flag |= LC_FLAG_ZERO_SIGN;
-            } else {
-              b = 0u;
-              if (valid[k]) flag |= LC_FLAG_NAN;
-            }
-            // pad with +1 on the 1-bit wire like collectives.py:269-271
-            st[k] = valid[k] ? b : (ENC == LC_ENC_SIGN1 ? 1u : 0u);
+          for (int q = 0; q < 4; ++q) {
+            valid[q] = e0 + q < n;
+            ge[q] = valid[q] ? g[e0 + q] : 0.f;
+            me[q] = valid[q] ? m[e0 + q] : 0.f;
+            keep[q] = MASK ? (valid[q] ? mask[e0 + q] != 0 : true) : true;
           }
         }
-        pack_store<F>(reinterpret_cast<uint32_t*>(out), t, lane, st, nwords, full);
+        double c[4];
+        float mn[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          c[q] = lion_c(me[q], ge[q], h);
+          if (MASK && !keep[q]) c[q] = 0.0;  // np.where(mask, c, 0.0)
+          mn[q] = lion_m(me[q], ge[q], h);
+        }
+        if (full) {
+          st_stream(m4 + t * 32 + lane, make_float4(mn[0], mn[1], mn[2], mn[3]));
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (valid[q]) m[e0 + q] = mn[q];
+        }
+        if constexpr (ENC == LC_ENC_F64) {
+          double* o = reinterpret_cast<double*>(dst.p[j]) + boff + k * 128 + lane * 4;
+          if (full) {
+            __stcs(reinterpret_cast<double2*>(o), make_double2(c[0], c[1]));
+            __stcs(reinterpret_cast<double2*>(o + 2), make_double2(c[2], c[3]));
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (valid[q]) o[q] = c[q];
+          }
+        } else {
+          uint32_t st[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (ENC == LC_ENC_QUANT_FIELDS) {
+              st[q] = valid[q] ? (uint32_t)(quant_l1(c[q], cur.get(sq, e0 + q), sq.qmax) + sq.qmax)
+                               : 0u;
+            } else {
+              uint32_t b;
+              if (c[q] > 0.0) {
+                b = 1u;
+              } else if (c[q] < 0.0) {
+                b = 0u;
+              } else if (c[q] == 0.0) {  // -0.0 included (np.sign(-0.0) == 0)
+                b = fillbit;
+                if (ternary && valid[q]) flag |= LC_FLAG_ZERO_SIGN;
+              } else {
+                b = 0u;
+                if (valid[q]) flag |= LC_FLAG_NAN;
+              }
+              // pad with +1 on the 1-bit wire like collectives.py:269-271
+              st[q] = valid[q] ? b : (ENC == LC_ENC_SIGN1 ? 1u : 0u);
+            }
+          }
+          uint32_t* sw = &stage[wib][k * 4 * F];
+          if constexpr (F <= 8) {
+            constexpr int LPW = 8 / F;  // lanes sharing one 32-bit word
+            uint32_t v = st[0] | (st[1] << F) | (st[2] << (2 * F)) | (st[3] << (3 * F));
+            v <<= (4 * F) * (lane % LPW);
+#pragma unroll
+            for (int sh = 1; sh < LPW; sh <<= 1) v |= __shfl_xor_sync(kFull, v, sh);
+            if (lane % LPW == 0) sw[lane / LPW] = v;
+          } else if constexpr (F == 16) {
+            sw[2 * lane] = st[0] | (st[1] << 16);
+            sw[2 * lane + 1] = st[2] | (st[3] << 16);
+          } else {
+            *reinterpret_cast<uint4*>(sw + 4 * lane) = make_uint4(st[0], st[1], st[2], st[3]);
+          }
+        }
       }
+    }
+    if constexpr (ENC != LC_ENC_F64) {
+      __syncwarp();
+      uint32_t* d = reinterpret_cast<uint32_t*>(dst.p[j]) + (boff >> 5) * F;
+      const int64_t rem = n - ebase;
+      const int nwv = rem >= 1024 ? WPS : (int)((rem * F + 31) / 32);
+      if (nwv == WPS && (WPS % 128) == 0) {
+        for (int w = lane * 4; w < WPS; w += 128)
+          *reinterpret_cast<uint4*>(d + w) = *reinterpret_cast<const uint4*>(&stage[wib][w]);
+      } else {
+        for (int w = lane; w < nwv; w += 32) d[w] = stage[wib][w];
+      }
+      __syncwarp();
     }
   }
   if (flag) atomicOr(flags, flag);
@@ -388,66 +432,107 @@ k_fused_local(float* __restrict__ theta, float* __restrict__ m,
 }
 
 // ---------------------------------------------------------------------------
-// K4: 1-bit majority over P packed chunks, bit-sliced counting.
+// K4: 1-bit majority over P packed chunks, bit-sliced counting.  Each thread
+// votes 4 words (uint4 loads of every rank's chunk) and writes the result to
+// `nout` destinations: the local gather buffer (NCCL path) or every rank's
+// gather buffer over NVLink (the allgather fused into the vote).
+//   sum_mode 0: compressed1bit -- a tie in exact-ternary mode is an error
+//               (collectives.py:290-293).
+//   sum_mode 1: sum-of-signs (direct, bits=1) -- the tally IS the p-bit sum
+//               2k-P; a zero sum gives a zero update in exact-ternary mode.
 // ---------------------------------------------------------------------------
+struct VoteOut {
+  Dst v, nz, tie;
+  int nout;
+};
+
+__device__ __forceinline__ void vote_store(const VoteOut& o, int64_t i, uint4 v, uint4 nz,
+                                           uint4 tie) {
+  for (int k = 0; k < o.nout; ++k) {
+    *reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(o.v.p[k]) + i) = v;
+    if (o.nz.p[0]) *reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(o.nz.p[k]) + i) = nz;
+    if (o.tie.p[0]) *reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(o.tie.p[k]) + i) = tie;
+  }
+}
+
+template <int NP>
+__device__ __forceinline__ void vote_word(uint32_t planes[NP], int P, int T, uint32_t fillmask,
+                                          uint32_t vm, int fill, int sum_mode, uint32_t& v,
+                                          uint32_t& nz, uint32_t& tie, uint32_t& flag) {
+  uint32_t gt = 0u, eq = ~0u;
+#pragma unroll
+  for (int p = NP - 1; p >= 0; --p) {
+    uint32_t pl = planes[p];
+    if ((T >> p) & 1) {
+      eq &= pl;
+    } else {
+      gt |= eq & pl;
+      eq &= ~pl;
+    }
+  }
+  if (P & 1) {  // count > (P-1)/2 is a strict majority; no ties possible
+    v = gt;
+    eq = 0u;
+  } else {
+    v = gt | (eq & fillmask);
+    if (fill == 0 && sum_mode == 0 && (eq & vm)) flag |= LC_FLAG_TIE_TERNARY;
+  }
+  tie = eq & vm;
+  nz = ~eq & vm;
+}
+
 template <int NP>
 __global__ void __launch_bounds__(256)
-k_vote_bits(const uint32_t* __restrict__ recv, int P, int64_t cw,
-            int64_t n_valid, int fill, uint32_t* __restrict__ voted,
-            uint32_t* __restrict__ tie, uint32_t* __restrict__ flags) {
+k_vote_bits(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_valid,
+            int fill, int sum_mode, VoteOut out, uint32_t* __restrict__ flags) {
   const int T = P >> 1;
   const uint32_t fillmask = fill > 0 ? ~0u : 0u;
   uint32_t flag = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cw;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t planes[NP];
+  const int64_t nq = cw >> 2;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t pl[4][NP];
 #pragma unroll
-    for (int p = 0; p < NP; ++p) planes[p] = 0u;
+    for (int w = 0; w < 4; ++w)
+#pragma unroll
+      for (int p = 0; p < NP; ++p) pl[w][p] = 0u;
     for (int j = 0; j < P; ++j) {
-      uint32_t carry = __ldcs(recv + (int64_t)j * cw + i);
+      uint4 x = __ldcs(reinterpret_cast<const uint4*>(recv + (int64_t)j * cw) + q);
+      uint32_t xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-      for (int p = 0; p < NP; ++p) {
-        uint32_t t = planes[p] & carry;
-        planes[p] ^= carry;
-        carry = t;
+      for (int w = 0; w < 4; ++w) {
+        uint32_t carry = xs[w];
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          uint32_t t = pl[w][p] & carry;
+          pl[w][p] ^= carry;
+          carry = t;
+        }
       }
     }
-    uint32_t gt = 0u, eq = ~0u;
+    uint32_t v[4], nz[4], tie[4];
 #pragma unroll
-    for (int p = NP - 1; p >= 0; --p) {
-      uint32_t pl = planes[p];
-      if ((T >> p) & 1) {
-        eq &= pl;
-      } else {
-        gt |= eq & pl;
-        eq &= ~pl;
-      }
+    for (int w = 0; w < 4; ++w) {
+      int64_t rem = n_valid - (4 * q + w) * 32;
+      uint32_t vm = rem >= 32 ? ~0u : (rem <= 0 ? 0u : ((1u << rem) - 1u));
+      vote_word<NP>(pl[w], P, T, fillmask, vm, fill, sum_mode, v[w], nz[w], tie[w], flag);
     }
-    int64_t rem = n_valid - i * 32;
-    uint32_t vm = rem >= 32 ? ~0u : (rem <= 0 ? 0u : ((1u << rem) - 1u));
-    uint32_t v;
-    if (P & 1) {
-      v = gt;  // count > (P-1)/2 is a strict majority; no ties possible
-      eq = 0u;
-    } else {
-      v = gt | (eq & fillmask);
-      if (fill == 0 && (eq & vm)) flag |= LC_FLAG_TIE_TERNARY;
-    }
-    voted[i] = v;
-    if (tie) tie[i] = eq & vm;
+    vote_store(out, 4 * q, make_uint4(v[0], v[1], v[2], v[3]),
+               make_uint4(nz[0], nz[1], nz[2], nz[3]), make_uint4(tie[0], tie[1], tie[2], tie[3]));
   }
   if (flag) atomicOr(flags, flag);
 }
 
 // ---------------------------------------------------------------------------
 // K6: p-bit field sums -> signed aggregate -> sign words (+ ties, values).
-// Each lane reads one input word (E = 32/F elements); F lanes form a word.
+// `rows` partial-sum rows of the owner block are added first (1 after an
+// NCCL reduce-scatter; P when peers wrote their fields over NVLink).  Each
+// lane reads one input word (E = 32/F elements); F lanes form a sign word.
 // ---------------------------------------------------------------------------
 template <int F>
 __global__ void __launch_bounds__(256)
-k_fields_vote(const uint32_t* __restrict__ sums, int64_t n, int P, int offset,
-              int binary, int fill, uint32_t* __restrict__ voted,
-              uint32_t* __restrict__ nz, uint32_t* __restrict__ tie,
+k_fields_vote(const uint32_t* __restrict__ sums, int rows, int64_t row_stride, int64_t n,
+              int P, int offset, int binary, int fill, VoteOut out,
               int64_t* __restrict__ values) {
   constexpr int E = 32 / F;
   constexpr uint32_t FM = (F == 32) ? 0xffffffffu : ((1u << F) - 1u);
@@ -459,7 +544,9 @@ k_fields_vote(const uint32_t* __restrict__ sums, int64_t n, int P, int offset,
   const int64_t nchunks = (nin + 31) / 32;
   for (int64_t ch = gw; ch < nchunks; ch += nw) {
     const int64_t i = ch * 32 + lane;
-    const uint32_t w = i < nin ? __ldcs(sums + i) : 0u;
+    uint32_t w = 0u;
+    if (i < nin)
+      for (int r = 0; r < rows; ++r) w += __ldcs(sums + (int64_t)r * row_stride + i);
     uint32_t pos = 0u, zer = 0u, val = 0u;
 #pragma unroll
     for (int k = 0; k < E; ++k) {
@@ -487,9 +574,12 @@ k_fields_vote(const uint32_t* __restrict__ sums, int64_t n, int P, int offset,
     }
     const int64_t o = i / F;
     if ((lane % F) == 0 && o < nout) {
-      voted[o] = pos | (fill > 0 ? zer : 0u);
-      if (nz) nz[o] = ~zer & val;
-      if (tie) tie[o] = zer & val;
+      const uint32_t v = pos | (fill > 0 ? zer : 0u);
+      for (int k = 0; k < out.nout; ++k) {
+        reinterpret_cast<uint32_t*>(out.v.p[k])[o] = v;
+        if (out.nz.p[0]) reinterpret_cast<uint32_t*>(out.nz.p[k])[o] = ~zer & val;
+        if (out.tie.p[0]) reinterpret_cast<uint32_t*>(out.tie.p[k])[o] = zer & val;
+      }
     }
   }
 }
@@ -499,8 +589,7 @@ k_fields_vote(const uint32_t* __restrict__ sums, int64_t n, int P, int offset,
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256)
 k_f64_sum_vote(const double* __restrict__ recv, int P, int64_t len, int64_t stride, int tree,
-               int fill, uint32_t* __restrict__ voted, uint32_t* __restrict__ nz,
-               uint32_t* __restrict__ tie, double* __restrict__ values) {
+               int fill, VoteOut out, double* __restrict__ values) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -525,10 +614,10 @@ k_f64_sum_vote(const double* __restrict__ recv, int P, int64_t len, int64_t stri
     const uint32_t pb = __ballot_sync(kFull, valid && tot > 0.0);
     const uint32_t zb = __ballot_sync(kFull, valid && tot == 0.0);
     const uint32_t vb = __ballot_sync(kFull, valid);
-    if (lane == 0) {
-      voted[w] = pb | (fill > 0 ? zb : 0u);
-      if (nz) nz[w] = ~zb & vb;
-      if (tie) tie[w] = zb;
+    if (lane < out.nout) {
+      reinterpret_cast<uint32_t*>(out.v.p[lane])[w] = pb | (fill > 0 ? zb : 0u);
+      if (out.nz.p[0]) reinterpret_cast<uint32_t*>(out.nz.p[lane])[w] = ~zb & vb;
+      if (out.tie.p[0]) reinterpret_cast<uint32_t*>(out.tie.p[lane])[w] = zb;
     }
   }
 }
@@ -718,36 +807,46 @@ int generic_grid(int64_t n) {
 
 template <int ENC, int F, bool MASK>
 int launch_encode(const float* g, float* m, const uint8_t* mask, int64_t n, Hyp h,
-                  int fill, SegQ sq, void* out, uint32_t* flags, cudaStream_t st) {
-  constexpr int U = 2;
-  auto kern = k_encode<ENC, F, MASK, U>;
-  int64_t ntiles = (n + 127) >> 7;
-  int grid = stream_grid(kern, kBlock, ntiles, (kBlock / 32) * U);
-  kern<<<grid, kBlock, 0, st>>>(g, m, mask, n, h, fill, sq, out, flags);
+                  int fill, SegQ sq, const Dst& dst, int64_t L, uint32_t* flags,
+                  cudaStream_t st) {
+  auto kern = k_encode<ENC, F, MASK>;
+  int64_t nsup = (n + 1023) >> 10;
+  int grid = stream_grid(kern, kBlock, nsup, kBlock / 32);
+  kern<<<grid, kBlock, 0, st>>>(g, m, mask, n, h, fill, sq, dst, L, flags);
   LC_LAUNCH_CHECK();
   return LC_OK;
 }
 
 template <int ENC, int F>
 int dispatch_mask(const float* g, float* m, const uint8_t* mask, int64_t n, Hyp h,
-                  int fill, SegQ sq, void* out, uint32_t* flags, cudaStream_t st) {
-  if (mask) return launch_encode<ENC, F, true>(g, m, mask, n, h, fill, sq, out, flags, st);
-  return launch_encode<ENC, F, false>(g, m, mask, n, h, fill, sq, out, flags, st);
+                  int fill, SegQ sq, const Dst& dst, int64_t L, uint32_t* flags,
+                  cudaStream_t st) {
+  if (mask) return launch_encode<ENC, F, true>(g, m, mask, n, h, fill, sq, dst, L, flags, st);
+  return launch_encode<ENC, F, false>(g, m, mask, n, h, fill, sq, dst, L, flags, st);
 }
 
 template <int ENC>
 int dispatch_fields(int F, const float* g, float* m, const uint8_t* mask, int64_t n,
-                    Hyp h, int fill, SegQ sq, void* out, uint32_t* flags,
+                    Hyp h, int fill, SegQ sq, const Dst& dst, int64_t L, uint32_t* flags,
                     cudaStream_t st) {
   switch (F) {
-    case 1: return dispatch_mask<ENC, 1>(g, m, mask, n, h, fill, sq, out, flags, st);
-    case 2: return dispatch_mask<ENC, 2>(g, m, mask, n, h, fill, sq, out, flags, st);
-    case 4: return dispatch_mask<ENC, 4>(g, m, mask, n, h, fill, sq, out, flags, st);
-    case 8: return dispatch_mask<ENC, 8>(g, m, mask, n, h, fill, sq, out, flags, st);
-    case 16: return dispatch_mask<ENC, 16>(g, m, mask, n, h, fill, sq, out, flags, st);
-    case 32: return dispatch_mask<ENC, 32>(g, m, mask, n, h, fill, sq, out, flags, st);
+    case 1: return dispatch_mask<ENC, 1>(g, m, mask, n, h, fill, sq, dst, L, flags, st);
+    case 2: return dispatch_mask<ENC, 2>(g, m, mask, n, h, fill, sq, dst, L, flags, st);
+    case 4: return dispatch_mask<ENC, 4>(g, m, mask, n, h, fill, sq, dst, L, flags, st);
+    case 8: return dispatch_mask<ENC, 8>(g, m, mask, n, h, fill, sq, dst, L, flags, st);
+    case 16: return dispatch_mask<ENC, 16>(g, m, mask, n, h, fill, sq, dst, L, flags, st);
+    case 32: return dispatch_mask<ENC, 32>(g, m, mask, n, h, fill, sq, dst, L, flags, st);
     default: return set_err(LC_E_ARG, "field_bits must be 1,2,4,8,16,32 (got %d)", F);
   }
+}
+
+// Build a Dst table from a host array of nd pointers (nd <= LC_MAX_BLOCKS).
+bool make_dst(Dst& d, void* const* ptrs, int nd) {
+  if (nd < 1 || nd > LC_MAX_BLOCKS || !ptrs) return false;
+  for (int i = 0; i < LC_MAX_BLOCKS; ++i) d.p[i] = i < nd ? ptrs[i] : nullptr;
+  for (int i = 0; i < nd; ++i)
+    if (!d.p[i]) return false;
+  return true;
 }
 
 }  // namespace
@@ -767,26 +866,31 @@ int lc_device_sm_count(int device) {
 
 int lc_encode(const float* g, float* m, const uint8_t* mask, int64_t n,
               const lc_hyper* hp, int fill, int enc, int field_bits,
-              const lc_segments* segs, void* out, uint32_t* flags, void* stream) {
+              const lc_segments* segs, void* const* dst, int32_t nblocks, int64_t L,
+              uint32_t* flags, void* stream) {
   if (n < 0 || !hp || !flags) return set_err(LC_E_ARG, "lc_encode: bad arguments");
   if (n == 0) return LC_OK;
-  if (!g || !m || !out) return set_err(LC_E_ARG, "lc_encode: null pointer");
+  if (!g || !m) return set_err(LC_E_ARG, "lc_encode: null pointer");
   if (!aligned16(g) || !aligned16(m)) return set_err(LC_E_ARG, "lc_encode: g/m must be 16-byte aligned");
+  if (L <= 0 || (L % 1024) != 0 || (int64_t)nblocks * L < n)
+    return set_err(LC_E_ARG, "lc_encode: block length must be a positive multiple of 1024 covering n");
+  Dst d;
+  if (!make_dst(d, dst, nblocks)) return set_err(LC_E_ARG, "lc_encode: bad destination table");
   Hyp h = to_hyp(hp);
   SegQ sq = to_segq(segs);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   switch (enc) {
     case LC_ENC_SIGN1:
-      return dispatch_mask<LC_ENC_SIGN1, 1>(g, m, mask, n, h, fill, sq, out, flags, st);
+      return dispatch_mask<LC_ENC_SIGN1, 1>(g, m, mask, n, h, fill, sq, d, L, flags, st);
     case LC_ENC_SIGN_FIELDS:
-      return dispatch_fields<LC_ENC_SIGN_FIELDS>(field_bits, g, m, mask, n, h, fill, sq, out, flags, st);
+      return dispatch_fields<LC_ENC_SIGN_FIELDS>(field_bits, g, m, mask, n, h, fill, sq, d, L, flags, st);
     case LC_ENC_QUANT_FIELDS:
       if (!segs || !segs->start || !segs->scale || segs->nseg < 1)
         return set_err(LC_E_ARG, "lc_encode: quant needs a segment table with scales");
       if (field_bits < 2) return set_err(LC_E_ARG, "lc_encode: quant fields need >= 2 bits");
-      return dispatch_fields<LC_ENC_QUANT_FIELDS>(field_bits, g, m, mask, n, h, fill, sq, out, flags, st);
+      return dispatch_fields<LC_ENC_QUANT_FIELDS>(field_bits, g, m, mask, n, h, fill, sq, d, L, flags, st);
     case LC_ENC_F64:
-      return dispatch_mask<LC_ENC_F64, 1>(g, m, mask, n, h, fill, sq, out, flags, st);
+      return dispatch_mask<LC_ENC_F64, 1>(g, m, mask, n, h, fill, sq, d, L, flags, st);
     default:
       return set_err(LC_E_ARG, "lc_encode: unknown encoding %d", enc);
   }
@@ -861,14 +965,27 @@ int lc_fused_local_step(float* theta, float* m, const float* g, const uint8_t* m
   return LC_OK;
 }
 
+bool make_out(VoteOut& o, void* const* v, void* const* nz, void* const* tie, int nout) {
+  if (!make_dst(o.v, v, nout)) return false;
+  o.nout = nout;
+  for (int i = 0; i < LC_MAX_BLOCKS; ++i) o.nz.p[i] = o.tie.p[i] = nullptr;
+  if (nz && !make_dst(o.nz, nz, nout)) return false;
+  if (tie && !make_dst(o.tie, tie, nout)) return false;
+  return true;
+}
+
 int lc_vote_bits(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid, int fill,
-                 uint32_t* voted, uint32_t* tie_bits, uint32_t* flags, void* stream) {
-  if (P < 1 || P > 255 || cw < 0 || !flags) return set_err(LC_E_ARG, "lc_vote_bits: P must be in [1,255]");
+                 int sum_mode, void* const* voted, void* const* nz, void* const* tie_bits,
+                 int32_t nout, uint32_t* flags, void* stream) {
+  if (P < 1 || P > 255 || cw < 0 || (cw % 4) != 0 || !flags)
+    return set_err(LC_E_ARG, "lc_vote_bits: P must be in [1,255], cw a multiple of 4");
   if (cw == 0) return LC_OK;
-  if (!recv || !voted) return set_err(LC_E_ARG, "lc_vote_bits: null pointer");
+  VoteOut o;
+  if (!recv || !make_out(o, voted, nz, tie_bits, nout))
+    return set_err(LC_E_ARG, "lc_vote_bits: bad pointers / output table");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  int grid = generic_grid(cw);
-#define LC_VOTE(NP) k_vote_bits<NP><<<grid, kBlock, 0, st>>>(recv, P, cw, n_valid, fill, voted, tie_bits, flags)
+  int grid = generic_grid(cw / 4);
+#define LC_VOTE(NP) k_vote_bits<NP><<<grid, kBlock, 0, st>>>(recv, P, cw, n_valid, fill, sum_mode, o, flags)
   if (P <= 1) LC_VOTE(1);
   else if (P <= 3) LC_VOTE(2);
   else if (P <= 7) LC_VOTE(3);
@@ -882,16 +999,19 @@ int lc_vote_bits(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid, i
   return LC_OK;
 }
 
-int lc_fields_vote(const uint32_t* sums, int64_t n, int32_t F, int32_t P, int32_t offset,
-                   int32_t binary, int fill, uint32_t* voted, uint32_t* nz,
-                   uint32_t* tie_bits, int64_t* values, void* stream) {
-  if (n < 0 || P < 1) return set_err(LC_E_ARG, "lc_fields_vote: bad arguments");
+int lc_fields_vote(const uint32_t* sums, int32_t rows, int64_t row_stride, int64_t n,
+                   int32_t F, int32_t P, int32_t offset, int32_t binary, int fill,
+                   void* const* voted, void* const* nz, void* const* tie_bits, int32_t nout,
+                   int64_t* values, void* stream) {
+  if (n < 0 || P < 1 || rows < 1) return set_err(LC_E_ARG, "lc_fields_vote: bad arguments");
   if (n == 0) return LC_OK;
-  if (!sums || !voted) return set_err(LC_E_ARG, "lc_fields_vote: null pointer");
+  VoteOut o;
+  if (!sums || !make_out(o, voted, nz, tie_bits, nout))
+    return set_err(LC_E_ARG, "lc_fields_vote: bad pointers / output table");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int64_t nin = (n * F + 31) / 32;
   int grid = generic_grid(nin);
-#define LC_FV(FF) k_fields_vote<FF><<<grid, kBlock, 0, st>>>(sums, n, P, offset, binary, fill, voted, nz, tie_bits, values)
+#define LC_FV(FF) k_fields_vote<FF><<<grid, kBlock, 0, st>>>(sums, rows, row_stride, n, P, offset, binary, fill, o, values)
   switch (F) {
     case 1: LC_FV(1); break;
     case 2: LC_FV(2); break;
@@ -907,14 +1027,17 @@ int lc_fields_vote(const uint32_t* sums, int64_t n, int32_t F, int32_t P, int32_
 }
 
 int lc_f64_sum_vote(const double* recv, int32_t P, int64_t len, int64_t stride, int tree, int fill,
-                    uint32_t* voted, uint32_t* nz, uint32_t* tie_bits, double* values,
-                    void* stream) {
-  if (len < 0 || P < 1 || (tree && P > 64)) return set_err(LC_E_ARG, "lc_f64_sum_vote: bad arguments");
+                    void* const* voted, void* const* nz, void* const* tie_bits, int32_t nout,
+                    double* values, void* stream) {
+  if (len < 0 || P < 1 || (tree && P > 64) || nout > 32)
+    return set_err(LC_E_ARG, "lc_f64_sum_vote: bad arguments");
   if (len == 0) return LC_OK;
-  if (!recv || !voted) return set_err(LC_E_ARG, "lc_f64_sum_vote: null pointer");
+  VoteOut o;
+  if (!recv || !make_out(o, voted, nz, tie_bits, nout))
+    return set_err(LC_E_ARG, "lc_f64_sum_vote: bad pointers / output table");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int grid = generic_grid(len);
-  k_f64_sum_vote<<<grid, kBlock, 0, st>>>(recv, P, len, stride, tree, fill, voted, nz, tie_bits, values);
+  k_f64_sum_vote<<<grid, kBlock, 0, st>>>(recv, P, len, stride, tree, fill, o, values);
   LC_LAUNCH_CHECK();
   return LC_OK;
 }

@@ -1,0 +1,182 @@
+// NVLink peer-memory exchange for the Lion Cub step.
+//
+// With every rank's receive / gather buffers mapped into every other rank's
+// address space (CUDA IPC for one process per GPU, peer access for one thread
+// per GPU), the exchange needs no collective library: the encode kernel
+// stores packed words straight into the owners' receive slots and the vote
+// kernels store voted words into every rank's gather buffer.  What remains is
+// ordering, provided by lc_barrier: a one-CTA kernel that publishes an epoch
+// to every peer with a system-scope release store and waits (acquire loads,
+// bounded by a timeout so a missing peer reports instead of hanging) until
+// every peer has published the same epoch.
+#include "common.cuh"
+
+namespace {
+
+struct Ptrs {
+  void* p[LC_MAX_BLOCKS];
+};
+
+__global__ void k_barrier(Ptrs peer_flags, uint64_t* __restrict__ my_flags, int P, int rank,
+                          unsigned long long epoch, long long timeout_cycles,
+                          uint32_t* __restrict__ err) {
+  const int j = threadIdx.x;
+  if (j < P) {
+    __threadfence_system();  // make this GPU's earlier peer stores visible first
+    uint64_t* slot = reinterpret_cast<uint64_t*>(peer_flags.p[j]) + rank;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(slot), "l"(epoch) : "memory");
+  }
+  __syncthreads();
+  if (j < P) {
+    const long long t0 = clock64();
+    while (true) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(my_flags + j) : "memory");
+      if (v >= epoch) break;
+      if (clock64() - t0 > timeout_cycles) {
+        atomicOr(err, (uint32_t)LC_FLAG_BARRIER_TIMEOUT);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+
+// dst[j][i] = src[j*s + i] for i < min(s, len - j*s): an owner-blocked
+// scatter of one fp32 vector to P destinations (peer receive slots).
+__global__ void __launch_bounds__(256)
+k_push_blocks(const float* __restrict__ src, int64_t len, int64_t s, Ptrs dst, int P) {
+  const int64_t total = len;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(e / s);
+    reinterpret_cast<float*>(dst.p[j])[e - (int64_t)j * s] = __ldcs(src + e);
+  }
+}
+
+// out[k][i] = fp32( (sum_j f64(recv[j][i])) / P ) for every destination k:
+// the reference's rank-ordered float64 mean (collectives.py:336-340), with
+// the broadcast (:344) fused as peer stores.
+__global__ void __launch_bounds__(256)
+k_mean_bcast(const float* __restrict__ recv, int P, int64_t cnt, int64_t s, Ptrs out, int nout) {
+  const double dp = (double)P;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = (double)__ldcs(recv + i);
+    for (int j = 1; j < P; ++j) acc = __dadd_rn(acc, (double)__ldcs(recv + (int64_t)j * s + i));
+    const float v = __double2float_rn(__ddiv_rn(acc, dp));
+    for (int k = 0; k < nout; ++k) reinterpret_cast<float*>(out.p[k])[i] = v;
+  }
+}
+
+bool make_ptrs(Ptrs& d, void* const* src, int n) {
+  if (n < 1 || n > LC_MAX_BLOCKS || !src) return false;
+  for (int i = 0; i < LC_MAX_BLOCKS; ++i) d.p[i] = i < n ? src[i] : nullptr;
+  for (int i = 0; i < n; ++i)
+    if (!d.p[i]) return false;
+  return true;
+}
+
+int grid_for(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  int64_t cap = (int64_t)lc::sm_count() * 8;
+  if (b > cap) b = cap;
+  return b < 1 ? 1 : (int)b;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lc_sym_alloc(int64_t bytes, void** ptr, uint8_t handle[64]) {
+  if (bytes <= 0 || !ptr || !handle) return lc::set_err(LC_E_ARG, "lc_sym_alloc: bad arguments");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
+  void* p = nullptr;
+  LC_CUDA_TRY(cudaMalloc(&p, bytes));
+  cudaError_t e = cudaMemset(p, 0, bytes);
+  cudaIpcMemHandle_t h;
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return lc::set_err(LC_E_CUDA, "lc_sym_alloc: %s", cudaGetErrorString(e));
+  }
+  memcpy(handle, &h, sizeof(h));
+  *ptr = p;
+  return LC_OK;
+}
+
+int lc_sym_free(void* ptr) {
+  if (ptr) LC_CUDA_TRY(cudaFree(ptr));
+  return LC_OK;
+}
+
+int lc_sym_open(const uint8_t handle[64], void** ptr) {
+  if (!handle || !ptr) return lc::set_err(LC_E_ARG, "lc_sym_open: bad arguments");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  LC_CUDA_TRY(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return LC_OK;
+}
+
+int lc_sym_close(void* ptr) {
+  if (ptr) LC_CUDA_TRY(cudaIpcCloseMemHandle(ptr));
+  return LC_OK;
+}
+
+int lc_enable_peer_access(int32_t device, int32_t peer) {
+  int can = 0;
+  LC_CUDA_TRY(cudaDeviceCanAccessPeer(&can, device, peer));
+  if (!can) return lc::set_err(LC_E_CONFIG, "device %d cannot access peer %d", device, peer);
+  int cur = 0;
+  LC_CUDA_TRY(cudaGetDevice(&cur));
+  LC_CUDA_TRY(cudaSetDevice(device));
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    e = cudaSuccess;
+  }
+  cudaSetDevice(cur);
+  if (e != cudaSuccess) return lc::set_err(LC_E_CUDA, "peer access %d->%d: %s", device, peer, cudaGetErrorString(e));
+  return LC_OK;
+}
+
+int lc_barrier(void* const* peer_flags, int32_t P, int32_t rank, uint64_t* my_flags,
+               uint64_t epoch, double timeout_s, uint32_t* err, void* stream) {
+  Ptrs pf;
+  if (P < 1 || P > 32 || rank < 0 || rank >= P || !my_flags || !err || !make_ptrs(pf, peer_flags, P))
+    return lc::set_err(LC_E_ARG, "lc_barrier: bad arguments");
+  int dev = 0, khz = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, dev);
+  if (khz <= 0) khz = 2000000;
+  long long cycles = (long long)(timeout_s * 1e3 * (double)khz);
+  k_barrier<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(pf, my_flags, P, rank,
+                                                                  epoch, cycles, err);
+  LC_LAUNCH_CHECK();
+  return LC_OK;
+}
+
+int lc_push_blocks_f32(const float* src, int64_t len, int64_t s, void* const* dst, int32_t P,
+                       void* stream) {
+  Ptrs d;
+  if (len < 0 || s <= 0 || (len + s - 1) / s > P || !make_ptrs(d, dst, P))
+    return lc::set_err(LC_E_ARG, "lc_push_blocks_f32: bad arguments");
+  if (len == 0) return LC_OK;
+  k_push_blocks<<<grid_for(len), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(src, len, s, d, P);
+  LC_LAUNCH_CHECK();
+  return LC_OK;
+}
+
+int lc_mean_bcast_f32(const float* recv, int32_t P, int64_t cnt, int64_t s, void* const* out,
+                      int32_t nout, void* stream) {
+  Ptrs o;
+  if (cnt < 0 || P < 1 || !recv || !make_ptrs(o, out, nout))
+    return lc::set_err(LC_E_ARG, "lc_mean_bcast_f32: bad arguments");
+  if (cnt == 0) return LC_OK;
+  k_mean_bcast<<<grid_for(cnt), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(recv, P, cnt, s, o, nout);
+  LC_LAUNCH_CHECK();
+  return LC_OK;
+}
+
+}  // extern "C"

@@ -41,7 +41,7 @@ import torch
 from . import _lib
 from .collectives import (Topology, choose_lane_bits, field_bits, mean_into,
                           owner_elems, owner_valid)
-from .errors import ConfigError
+from .errors import CollectiveError, ConfigError
 from .quant import QuantSpec, SignPolicy
 
 LrSchedule = Union[float, Callable[[int], float]]
@@ -240,41 +240,83 @@ def hash_params(params: Mapping) -> str:
 
 
 # ---------------------------------------------------------------------------
-# Step workspace (preallocated per layout x world x algorithm)
+# Step workspace (preallocated per layout x world x algorithm x exchange)
 # ---------------------------------------------------------------------------
 
+def _loc(x):
+    """Local tensor of a workspace buffer (SymBuffer or plain tensor)."""
+    return None if x is None else getattr(x, "local", x)
+
+
 class _Workspace:
-    def __init__(self, layout: Layout, dev, P: int, kind: str, F: int, ternary: bool,
+    """Buffers and pointer tables of one rank's step.
+
+    NCCL exchange: K1 writes owner blocks into a local send buffer, NCCL moves
+    them (all-to-all or reduce-scatter), the owner votes into its block of the
+    local gather buffer and NCCL allgathers it.
+    Peer-memory exchange (transport.p2p): receive/gather buffers are mapped on
+    every rank; K1 writes block j straight into rank j's receive slot and the
+    owner's vote kernel writes its voted block into every rank's gather
+    buffer -- the two collectives happen inside the kernels, ordered by two
+    device barriers."""
+
+    def __init__(self, layout: Layout, topo: Topology, kind: str, F: int, ternary: bool,
                  metrics: bool):
-        n = layout.n
+        n, P, r = layout.n, topo.world_size, topo.rank
+        dev = topo.device
+        tp = topo.transport
         self.L = L = owner_elems(n, P)
-        self.cw = L // 32
+        self.cw = cw = L // 32
         self.F = F
+        self.cwf = L * F // 32
+        self.p2p = p2p = P > 1 and tp.p2p
         z = lambda k, dt=torch.int32: torch.zeros(max(k, 1), dtype=dt, device=dev)  # noqa
         self.flags = z(1)
-        if kind == "1bit":
-            self.send = z(P * self.cw)
-            self.recv = z(P * self.cw) if P > 1 else self.send
-        elif kind == "fields":
-            self.cwf = L * F // 32
-            self.send = z(P * self.cwf)
-            self.red = z(self.cwf)
-        elif kind == "f64":
-            self.send = z(P * L, torch.float64)
-            self.recv = z(P * L, torch.float64) if P > 1 else self.send
-        self.full = z(P * self.cw)
-        self.nz = z(P * self.cw) if ternary else None
-        self.ties = z(P * self.cw) if metrics else None
         self.l1 = None
         self.norms = self.scales = None
+        if kind == "f64":
+            blk_bytes, rdt, rlen = L * 8, torch.float64, P * L
+        elif kind == "fields":
+            blk_bytes, rdt, rlen = self.cwf * 4, torch.int32, P * self.cwf
+        else:
+            blk_bytes, rdt, rlen = cw * 4, torch.int32, P * cw
+        if P == 1:
+            self.full, self.nz, self.ties = z(cw), (z(cw) if ternary else None), \
+                (z(cw) if metrics else None)
+            return
+        if p2p:
+            key = (layout.key, P, kind, F)
+            sym = lambda name, k, dt=torch.int32: tp.sym_buffer(r, key + (name,), k, dt)  # noqa
+            self.recv = sym("recv", rlen, rdt)
+            self.full = sym("full", P * cw)
+            self.nz = sym("nz", P * cw) if ternary else None
+            self.ties = sym("ties", P * cw) if metrics else None
+            self.dst = _lib.table([self.recv.peers[j] + r * blk_bytes for j in range(P)])
+            outs = lambda b: None if b is None else _lib.table(  # noqa: E731
+                [b.peers[j] + r * cw * 4 for j in range(P)])
+            self.vout, self.nzout, self.tout = outs(self.full), outs(self.nz), outs(self.ties)
+            self.nout = P
+        else:
+            self.send = torch.zeros(rlen, dtype=rdt, device=dev)
+            if kind == "fields":
+                self.red = z(self.cwf)
+            else:
+                self.recv = torch.zeros(rlen, dtype=rdt, device=dev)
+            self.full = z(P * cw)
+            self.nz = z(P * cw) if ternary else None
+            self.ties = z(P * cw) if metrics else None
+            self.dst = _lib.table([self.send.data_ptr() + j * blk_bytes for j in range(P)])
+            one = lambda t: None if t is None else _lib.table([_off(t, r * cw)])  # noqa
+            self.vout, self.nzout, self.tout = one(self.full), one(self.nz), one(self.ties)
+            self.nout = 1
 
 
-def _workspace(th: FlatParamSet, P: int, kind: str, F: int, ternary: bool,
+def _workspace(th: FlatParamSet, topo: Topology, kind: str, F: int, ternary: bool,
                metrics: bool) -> _Workspace:
-    key = (P, kind, F, ternary, metrics)
+    key = (id(topo.transport), topo.world_size, topo.rank, kind, F, ternary, metrics)
     ws = th.workspace.get(key)
     if ws is None:
-        ws = _Workspace(th.layout, th.flat.device, P, kind, F, ternary, metrics)
+        ws = _Workspace(th.layout, topo, kind, F, ternary, metrics)
         th.workspace[key] = ws
     return ws
 
@@ -381,13 +423,14 @@ def distributed_lion_step(state: WorkerState, grad_i, h: LionHyper,
     _check_shapes(state.params, grad_i)
     layout, th, m = state.flat()
     dev = th.flat.device
-    P, r = topo.world_size, topo.rank
+    P = topo.world_size
     t = state.iteration + 1
     policy = SignPolicy(mode=zero_mode, iteration=t)
     fill = policy.kernel_fill()
     ternary = fill == 0
     hyp = h.c_struct(t)
     eta, wd = hyp.lr, hyp.weight_decay
+    sum_mode = 0
     if algo == "compressed1bit":
         kind, binary, qmax = "1bit", True, 0
     elif spec is None:
@@ -401,6 +444,13 @@ def distributed_lion_step(state: WorkerState, grad_i, h: LionHyper,
         # reference capacity rule first: CapacityError before any exchange
         choose_lane_bits(P, qmax, binary_signs=binary)
         F = field_bits(P, 1 if binary else 2 * qmax)
+        if binary and P > 1 and topo.transport.p2p:
+            # sum-of-signs over peer memory: ship 1-bit signs; the owner's
+            # bit-sliced counter yields the same exact p-bit sums 2k-P
+            kind, F, sum_mode = "1bit", 1, 1
+    if P > 1 and topo.transport.poll_error(topo.rank):
+        raise CollectiveError("a peer never reached the step barrier",
+                              generation=topo.generation)
     metrics = metrics_out is not None
     n = layout.n
     with torch.cuda.device(dev):
@@ -409,15 +459,16 @@ def distributed_lion_step(state: WorkerState, grad_i, h: LionHyper,
         with torch.cuda.stream(stream):
             g = _to_flat(grad_i, layout, dev)
             mflat = _flat_mask(mask, layout, dev)
-            ws = _workspace(th, P, kind if P > 1 else "local", F,
-                            ternary and kind != "1bit", metrics)
+            ws = _workspace(th, topo, kind if P > 1 else "local", F,
+                            ternary and (kind != "1bit" or sum_mode == 1), metrics)
             gen = topo.next_generation()
             if metrics:
                 c_local = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
                 _lib.call("lc_compute_c", g.flat.data_ptr(), m.flat.data_ptr(),
                           _lib.ptr(mflat), n, C.byref(hyp), c_local.data_ptr(), s)
             if ternary and binary:
-                _ternary_precheck(topo, gen, g, m, mflat, n, hyp, dev, s, kind)
+                _ternary_precheck(topo, gen, g, m, mflat, n, hyp, dev, s,
+                                  "1bit" if algo == "compressed1bit" else "fields")
             segs = None
             if kind == "fields" and not binary:
                 segs = _l1_scales(ws, layout, dev, g.flat, m.flat, mflat, hyp, qmax, s)
@@ -427,15 +478,15 @@ def distributed_lion_step(state: WorkerState, grad_i, h: LionHyper,
                 _lib.call("lc_fused_local_step", th.flat.data_ptr(), m.flat.data_ptr(),
                           g.flat.data_ptr(), _lib.ptr(mflat), n, C.byref(hyp), fill, mode,
                           C.byref(segs) if segs is not None else None,
-                          ws.full.data_ptr() if metrics else None,
-                          ws.nz.data_ptr() if (metrics and ws.nz is not None) else None,
-                          _lib.ptr(ws.ties), ws.flags.data_ptr(), s)
-                nz = ws.nz if metrics else None
+                          _loc(ws.full).data_ptr() if metrics else None,
+                          _loc(ws.nz).data_ptr() if (metrics and ws.nz is not None) else None,
+                          _lib.ptr(_loc(ws.ties)), ws.flags.data_ptr(), s)
+                nz = _loc(ws.nz) if metrics else None
             else:
-                nz = _exchange_and_vote(topo, gen, ws, kind, binary, F, qmax, fill, n,
-                                        g, m, mflat, hyp, segs, s,
+                nz = _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill,
+                                        n, g, m, mflat, hyp, segs, s,
                                         tree=algo == "ps_efficient")
-                _lib.call("lc_apply_update", th.flat.data_ptr(), n, ws.full.data_ptr(),
+                _lib.call("lc_apply_update", th.flat.data_ptr(), n, _loc(ws.full).data_ptr(),
                           _lib.ptr(nz), eta, wd, s)
             if metrics:
                 _fill_metrics(metrics_out, layout, dev, ws, nz, c_local, s)
@@ -462,62 +513,74 @@ def _ternary_precheck(topo, gen, g, m, mflat, n, hyp, dev, s, kind):
             recv = torch.zeros_like(words)
             topo.transport.alltoall(r, gen, words, recv, cw * 4)
         voted = torch.zeros(cw, dtype=torch.int32, device=dev)
-        _lib.call("lc_vote_bits", recv.data_ptr(), P, cw, owner_valid(n, P, r), 0,
-                  voted.data_ptr(), None, flags.data_ptr(), s)
+        _lib.call("lc_vote_bits", recv.data_ptr(), P, cw, owner_valid(n, P, r), 0, 0,
+                  _lib.table([voted.data_ptr()]), None, None, 1, flags.data_ptr(), s)
     if topo.world_size > 1:
         topo.transport.allreduce_max_u32(topo.rank, gen, flags)
     _raise_flags(int(flags.item()), binary=kind == "1bit")
 
 
-def _exchange_and_vote(topo, gen, ws, kind, binary, F, qmax, fill, n, g, m, mflat, hyp,
-                       segs, s, tree=False):
-    """K1 encode -> exchange -> owner vote into ws.full (+nz) -> allgather."""
+def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, g, m, mflat,
+                       hyp, segs, s, tree=False):
+    """K1 encode -> exchange -> owner vote into the gather buffer (+nz, ties)."""
     P, r = topo.world_size, topo.rank
     tp = topo.transport
-    cw = ws.cw
+    cw, L = ws.cw, ws.L
     nvalid = owner_valid(n, P, r)
-    tie_ptr = _off(ws.ties, r * cw) if ws.ties is not None else None
-    nz_ptr = _off(ws.nz, r * cw) if ws.nz is not None else None
-    hp = C.byref(hyp)
     gp, mp, mk = g.flat.data_ptr(), m.flat.data_ptr(), _lib.ptr(mflat)
     if kind == "1bit":
-        _lib.call("lc_encode", gp, mp, mk, n, hp, fill, _lib.LC_ENC_SIGN1, 1, None,
-                  ws.send.data_ptr(), ws.flags.data_ptr(), s)
-        tp.alltoall(r, gen, ws.send, ws.recv, cw * 4)
-        _lib.call("lc_vote_bits", ws.recv.data_ptr(), P, cw, nvalid, fill,
-                  _off(ws.full, r * cw), tie_ptr, ws.flags.data_ptr(), s)
+        enc, fb = _lib.LC_ENC_SIGN1, 1
     elif kind == "fields":
-        enc = _lib.LC_ENC_SIGN_FIELDS if binary else _lib.LC_ENC_QUANT_FIELDS
-        _lib.call("lc_encode", gp, mp, mk, n, hp, fill, enc, F,
-                  C.byref(segs) if segs is not None else None, ws.send.data_ptr(),
-                  ws.flags.data_ptr(), s)
+        enc, fb = (_lib.LC_ENC_SIGN_FIELDS if binary else _lib.LC_ENC_QUANT_FIELDS), F
+    else:
+        enc, fb = _lib.LC_ENC_F64, 64
+    _lib.call("lc_encode", gp, mp, mk, n, C.byref(hyp), fill, enc, fb,
+              C.byref(segs) if segs is not None else None, ws.dst, P, L,
+              ws.flags.data_ptr(), s)
+    rows = 1
+    if ws.p2p:
+        tp.device_barrier(r, gen)          # every rank's blocks have landed
+        recv, rows = ws.recv.local, P
+    elif kind == "1bit":
+        tp.alltoall(r, gen, ws.send, ws.recv, cw * 4)
+        recv = ws.recv
+    elif kind == "fields":
         tp.reduce_scatter_u32(r, gen, ws.send, ws.red, ws.cwf)
-        _lib.call("lc_fields_vote", ws.red.data_ptr(), nvalid, F, P,
-                  0 if binary else qmax, int(binary), fill, _off(ws.full, r * cw),
-                  nz_ptr, tie_ptr, None, s)
-    else:  # f64 full precision
-        _lib.call("lc_encode", gp, mp, mk, n, hp, fill, _lib.LC_ENC_F64, 64, None,
-                  ws.send.data_ptr(), ws.flags.data_ptr(), s)
-        tp.alltoall(r, gen, ws.send, ws.recv, ws.L * 8)
-        _lib.call("lc_f64_sum_vote", ws.recv.data_ptr(), P, nvalid, ws.L,
-                  int(tree), fill, _off(ws.full, r * cw), nz_ptr, tie_ptr,
-                  None, s)
-    tp.allgather(r, gen, ws.full[r * cw:], ws.full, cw * 4)
-    if ws.nz is not None:
-        tp.allgather(r, gen, ws.nz[r * cw:], ws.nz, cw * 4)
-    if ws.ties is not None:
-        tp.allgather(r, gen, ws.ties[r * cw:], ws.ties, cw * 4)
-    return ws.nz
+        recv = ws.red
+    else:
+        tp.alltoall(r, gen, ws.send, ws.recv, L * 8)
+        recv = ws.recv
+    if kind == "1bit":
+        _lib.call("lc_vote_bits", recv.data_ptr(), P, cw, nvalid, fill, sum_mode, ws.vout,
+                  ws.nzout, ws.tout, ws.nout, ws.flags.data_ptr(), s)
+    elif kind == "fields":
+        _lib.call("lc_fields_vote", recv.data_ptr(), rows, ws.cwf, nvalid, F, P,
+                  0 if binary else qmax, int(binary), fill, ws.vout, ws.nzout, ws.tout,
+                  ws.nout, None, s)
+    else:
+        _lib.call("lc_f64_sum_vote", recv.data_ptr(), P, nvalid, L, int(tree), fill, ws.vout,
+                  ws.nzout, ws.tout, ws.nout, None, s)
+    if ws.p2p:
+        tp.device_barrier(r, gen)          # every owner's voted block has landed
+    else:
+        full = ws.full
+        tp.allgather(r, gen, full[r * cw:], full, cw * 4)
+        if ws.nz is not None:
+            tp.allgather(r, gen, ws.nz[r * cw:], ws.nz, cw * 4)
+        if ws.ties is not None:
+            tp.allgather(r, gen, ws.ties[r * cw:], ws.ties, cw * 4)
+    return _loc(ws.nz)
 
 
 def _fill_metrics(out: dict, layout: Layout, dev, ws, nz, c_local, s):
     n = layout.n
     counts = torch.zeros(len(layout.names), dtype=torch.int64, device=dev)
-    _lib.call("lc_count_bits_segmented", ws.ties.data_ptr(),
+    _lib.call("lc_count_bits_segmented", _loc(ws.ties).data_ptr(),
               layout.seg_start_dev(dev).data_ptr(), len(layout.names),
               counts.data_ptr(), s)
     signs = torch.empty(max(n, 1), dtype=torch.int8, device=dev)
-    _lib.call("lc_bits_to_sign", ws.full.data_ptr(), _lib.ptr(nz), n, signs.data_ptr(), s)
+    _lib.call("lc_bits_to_sign", _loc(ws.full).data_ptr(), _lib.ptr(nz), n,
+              signs.data_ptr(), s)
     signs = signs.long()
     cl = counts.tolist()
     for i, k in enumerate(layout.names):
@@ -527,27 +590,67 @@ def _fill_metrics(out: dict, layout: Layout, dev, ws, nz, c_local, s):
         out.setdefault("c_local", {})[k] = c_local[o:o + c].view(layout.shapes[k])
 
 
+def _symmetric_momentum(m: FlatParamSet, topo: Topology) -> FlatParamSet:
+    """Re-home the momentum into a buffer mapped on every rank (once), so the
+    sync's owner can store the mean straight into every rank's m."""
+    if getattr(m, "sym", None) is not None:
+        return m
+    layout = m.layout
+    buf = topo.transport.sym_buffer(topo.rank, ("momentum", layout.key), max(layout.n, 1),
+                                    torch.float32)
+    buf.local.copy_(m.flat)
+    out = FlatParamSet(buf.local, layout)
+    out.sym = buf
+    out.workspace = m.workspace
+    return out
+
+
 def maybe_sync_momentum(state: WorkerState, policy: SyncPolicy,
                         topo: Topology) -> WorkerState:
     """Average the selected layers' momentum across ranks at firing steps
     (optimizer.py:244-258), bit-identical to allreduce_mean_f32.  No-op (no
-    communication) when the policy does not fire.  In place."""
+    communication) when the policy does not fire.  In place.
+
+    Peer-memory exchange: each rank stores block j of the selected range into
+    owner j's staging slot, the owner averages its P rows in float64 rank
+    order and stores the fp32 mean into every rank's momentum (two barriers).
+    NCCL exchange: all-to-all, owner mean, allgather (collectives.mean_into)."""
     if not policy.fires(state.iteration):
         return state
     layout, th, m = state.flat()
     dev = m.flat.device
+    P, r = topo.world_size, topo.rank
+    tp = topo.transport
     with torch.cuda.device(dev), torch.cuda.stream(topo.stream):
         runs = layout.runs(policy.selects)
-        if topo.world_size > 1 and runs:
+        if P > 1 and runs:
             longest = max(b - a for a, b in runs)
-            s = -(-longest // topo.world_size)
-            key = ("sync", topo.world_size, s)
-            scratch = m.workspace.get(key)
-            if scratch is None:
-                scratch = torch.empty(topo.world_size * s, dtype=torch.float32, device=dev)
-                m.workspace[key] = scratch
-            for a, b in runs:
-                gen = topo.next_generation()
-                seg = m.flat[a:b]
-                mean_into(topo, gen, seg, seg, scratch)
+            smax = -(-longest // P)
+            st = topo.stream.cuda_stream
+            if tp.p2p:
+                m = _symmetric_momentum(m, topo)
+                stage = tp.sym_buffer(r, ("sync_stage", P, smax), P * smax, torch.float32)
+                for a, b in runs:
+                    gen = topo.next_generation()
+                    ln = b - a
+                    sr = -(-ln // P)
+                    cnt = max(0, min(sr, ln - r * sr))
+                    _lib.call("lc_push_blocks_f32", _off(m.flat, a), ln, sr,
+                              _lib.table([stage.peers[j] + r * sr * 4 for j in range(P)]),
+                              P, st)
+                    tp.device_barrier(r, gen)
+                    _lib.call("lc_mean_bcast_f32", stage.local.data_ptr(), P, cnt, sr,
+                              _lib.table([m.sym.peers[j] + (a + r * sr) * 4
+                                          for j in range(P)]), P, st)
+                    tp.device_barrier(r, gen)
+            else:
+                key = ("sync", P, smax)
+                scratch = m.workspace.get(key)
+                if scratch is None:
+                    scratch = torch.empty(P * smax, dtype=torch.float32, device=dev)
+                    m.workspace[key] = scratch
+                for a, b in runs:
+                    gen = topo.next_generation()
+                    seg = m.flat[a:b]
+                    mean_into(topo, gen, seg, seg, scratch)
     return replace(state, params=th, momentum=m)

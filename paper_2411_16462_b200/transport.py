@@ -18,11 +18,20 @@ flags) -- so the packed words never leave HBM / NVLink:
   B200.
 
 Both raise ``CollectiveError`` naming a missing rank on timeout.
+
+Peer-memory mode (``transport.p2p``): buffers allocated with ``sym_buffer``
+are mapped on every rank (CUDA IPC between processes, peer access between
+threads), so the step's kernels store packed words directly into the owners'
+receive slots and voted words into every rank's gather buffer over NVLink;
+``device_barrier`` orders the phases.  ``LocalTransport`` simulates the same
+mode on one GPU (all ranks' buffers live on that GPU; the barrier is the host
+rendezvous, since the ranks share one stream).
 """
 
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 import time
 
@@ -34,6 +43,35 @@ from .errors import CollectiveError, ConfigError
 DEFAULT_TIMEOUT = 30.0
 
 
+class SymBuffer:
+    """A buffer mapped on every rank: ``local`` is this rank's tensor,
+    ``peers[j]`` the device address of rank j's buffer (usable here)."""
+
+    def __init__(self, local: torch.Tensor, peers: list, keep=None):
+        self.local = local
+        self.peers = peers
+        self._keep = keep
+
+    def peer(self, j: int, byte_offset: int = 0) -> int:
+        return self.peers[j] + byte_offset
+
+
+class _RawCuda:
+    """Expose a raw cudaMalloc'ed range to torch via __cuda_array_interface__."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (ptr, False), "version": 3,
+                                         "strides": None}
+
+
+def _wrap(ptr: int, numel: int, dtype, dev) -> torch.Tensor:
+    nbytes = numel * torch.empty((), dtype=dtype).element_size()
+    with torch.cuda.device(dev):
+        t = torch.as_tensor(_RawCuda(ptr, nbytes), device=dev)
+    return t.view(dtype)
+
+
 class DeviceTransport:
     """Collectives over device buffers for ranks 0..world_size-1.
 
@@ -42,6 +80,19 @@ class DeviceTransport:
     """
 
     world_size: int
+    p2p: bool = False
+
+    def sym_buffer(self, rank: int, key, numel: int, dtype) -> SymBuffer:
+        """Collective: a zeroed buffer mapped on every rank (p2p mode)."""
+        raise NotImplementedError
+
+    def device_barrier(self, rank: int, gen: int):
+        """Stream-ordered barrier across ranks (p2p mode)."""
+        raise NotImplementedError
+
+    def poll_error(self, rank: int) -> bool:
+        """True if an earlier device barrier timed out (no host sync)."""
+        return False
 
     def device(self, rank: int) -> torch.device:
         raise NotImplementedError
@@ -98,7 +149,8 @@ class _Rendezvous:
 class LocalTransport(DeviceTransport):
     """P simulated ranks on one GPU, one host thread per rank."""
 
-    def __init__(self, world_size: int, device=None, timeout: float = DEFAULT_TIMEOUT):
+    def __init__(self, world_size: int, device=None, timeout: float = DEFAULT_TIMEOUT,
+                 p2p: bool = True):
         if world_size < 1:
             raise ConfigError("world_size must be >= 1")
         if not torch.cuda.is_available():
@@ -107,8 +159,25 @@ class LocalTransport(DeviceTransport):
         self.dev = (torch.device(device) if device is not None
                     else torch.device("cuda", torch.cuda.current_device()))
         self.timeout = timeout
+        self.p2p = p2p
         self._posts = [None] * world_size
         self._rv = _Rendezvous(world_size)
+        self._sym = {}
+
+    def sym_buffer(self, rank, key, numel, dtype):
+        k = (rank, key)
+        if k not in self._sym:
+            t = torch.zeros(max(numel, 1), dtype=dtype, device=self.dev)
+            posts = self._exchange(rank, 0, "sym_buffer", t.data_ptr())
+            peers = list(posts)
+            self._done(rank, 0, "sym_buffer")
+            self._sym[k] = SymBuffer(t, peers)
+        return self._sym[k]
+
+    def device_barrier(self, rank, gen):
+        # all simulated ranks enqueue on the same stream: the host rendezvous
+        # orders every rank's earlier kernels before every later one
+        self._rv.wait(rank, gen, "barrier", self.timeout)
 
     def device(self, rank):
         return self.dev
@@ -188,10 +257,31 @@ class NcclTransport(DeviceTransport):
     drives (all of them for ``init_all``, one for ``init_process``).
     """
 
-    def __init__(self, world_size: int, comms: dict, devices: dict):
+    def __init__(self, world_size: int, comms: dict, devices: dict, group=None,
+                 threaded: bool = False, p2p: bool | None = None):
         self.world_size = world_size
         self._comms = comms
         self._devices = devices
+        self._group = group
+        self._threaded = threaded
+        self._rv = _Rendezvous(world_size) if threaded else None
+        self._posts = [None] * world_size
+        self._sym = {}
+        self._opened = []   # peer mappings to close
+        self._owned = []    # local cudaMalloc'ed buffers to free
+        self._epoch = {}
+        self._err = {}
+        self._err_host = {}
+        if p2p is None:
+            p2p = os.environ.get("LIONCUB_P2P", "1") != "0" and world_size > 1
+        self.p2p = bool(p2p)
+        if self.p2p and threaded:
+            lib = _lib.load()
+            devs = [devices[r].index for r in range(world_size)]
+            for a in devs:
+                for b in devs:
+                    if a != b:
+                        _lib.check(lib.lc_enable_peer_access(a, b), "enable peer access")
 
     @classmethod
     def init_all(cls, devices=None) -> "NcclTransport":
@@ -204,7 +294,7 @@ class NcclTransport(DeviceTransport):
         devs = (C.c_int32 * n)(*devices)
         _lib.check(lib.lc_comm_init_all(handles, n, devs), "ncclCommInitAll")
         return cls(n, {r: handles[r] for r in range(n)},
-                   {r: torch.device("cuda", devices[r]) for r in range(n)})
+                   {r: torch.device("cuda", devices[r]) for r in range(n)}, threaded=True)
 
     @classmethod
     def init_process(cls, rank: int, world_size: int, device=None,
@@ -225,13 +315,74 @@ class NcclTransport(DeviceTransport):
         with torch.cuda.device(dev):
             _lib.check(lib.lc_comm_init_rank(C.byref(handle), uid, world_size, rank),
                        "ncclCommInitRank", rank=rank)
-        return cls(world_size, {rank: handle.value}, {rank: dev})
+        return cls(world_size, {rank: handle.value}, {rank: dev}, group=group)
 
     def device(self, rank):
         return self._devices[rank]
 
     def stream(self, rank):
         return torch.cuda.current_stream(self._devices[rank])
+
+    # ---- peer memory -------------------------------------------------------
+    def sym_buffer(self, rank, key, numel, dtype):
+        k = (rank, key)
+        if k in self._sym:
+            return self._sym[k]
+        dev = self._devices[rank]
+        if self._threaded:
+            t = torch.zeros(max(numel, 1), dtype=dtype, device=dev)
+            self._posts[rank] = t.data_ptr()
+            self._rv.wait(rank, 0, "sym_buffer:post", DEFAULT_TIMEOUT)
+            peers = list(self._posts)
+            self._rv.wait(rank, 0, "sym_buffer:done", DEFAULT_TIMEOUT)
+            buf = SymBuffer(t, peers)
+        else:
+            import torch.distributed as dist
+            lib = _lib.load()
+            nbytes = max(numel, 1) * torch.empty((), dtype=dtype).element_size()
+            p = C.c_void_p()
+            h = (C.c_uint8 * 64)()
+            with torch.cuda.device(dev):
+                _lib.check(lib.lc_sym_alloc(nbytes, C.byref(p), h), "lc_sym_alloc", rank=rank)
+            self._owned.append(p.value)
+            handles = [None] * self.world_size
+            dist.all_gather_object(handles, bytes(h), group=self._group)
+            peers = []
+            for j, hb in enumerate(handles):
+                if j == rank:
+                    peers.append(p.value)
+                    continue
+                q = C.c_void_p()
+                with torch.cuda.device(dev):
+                    _lib.check(lib.lc_sym_open((C.c_uint8 * 64)(*hb), C.byref(q)),
+                               "lc_sym_open", rank=j)
+                self._opened.append((dev, q.value))
+                peers.append(q.value)
+            buf = SymBuffer(_wrap(p.value, max(numel, 1), dtype, dev), peers)
+        self._sym[k] = buf
+        return buf
+
+    def device_barrier(self, rank, gen):
+        flags = self.sym_buffer(rank, ("__barrier__",), self.world_size, torch.int64)
+        if rank not in self._err:
+            dev = self._devices[rank]
+            self._err[rank] = torch.zeros(1, dtype=torch.int32, device=dev)
+            self._err_host[rank] = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+            self._epoch[rank] = 0
+        self._epoch[rank] += 1
+        st = self.stream(rank).cuda_stream
+        _lib.call("lc_barrier", _lib.table(flags.peers), self.world_size, rank,
+                  flags.local.data_ptr(), self._epoch[rank], DEFAULT_TIMEOUT,
+                  self._err[rank].data_ptr(), st)
+
+    def poll_error(self, rank):
+        """Non-blocking: the barrier error flag as of the last poll; schedules
+        the next device->host copy of it."""
+        if rank not in self._err:
+            return False
+        seen = bool(self._err_host[rank].item())
+        self._err_host[rank].copy_(self._err[rank], non_blocking=True)
+        return seen
 
     def _c(self, rank):
         return self._comms[rank]
@@ -270,6 +421,19 @@ class NcclTransport(DeviceTransport):
 
     def close(self):
         lib = _lib.load()
+        torch.cuda.synchronize()
+        for dev, q in self._opened:
+            with torch.cuda.device(dev):
+                lib.lc_sym_close(q)
+        self._opened = []
+        self._sym = {}
+        if self._owned and not self._threaded:
+            import torch.distributed as dist
+            if dist.is_initialized():
+                dist.barrier(group=self._group)  # peers unmapped before we free
+        for p in self._owned:
+            lib.lc_sym_free(p)
+        self._owned = []
         for r, h in list(self._comms.items()):
             if h:
                 lib.lc_comm_destroy(h)

@@ -1,0 +1,127 @@
+"""Multi-GPU parity over NCCL (one process per GPU), checked against the CPU
+oracle.  Launched by tests/test_multigpu.py:
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/mgpu_parity.py
+
+Every rank builds the same seeded inputs for all P ranks, runs ITS step
+through the public API over an NcclTransport, and compares its outputs with
+the oracle's P-rank result (theta'/m' bit-exact to float32 of the reference,
+votes/ties exact).  Rank 0 prints a JSON summary; the exit code is non-zero
+on any mismatch.
+"""
+
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import paper_2411_16462_b200 as lc  # noqa: E402
+from oracle import lioncub_oracle as O  # noqa: E402
+from tests import golden_io as G  # noqa: E402
+
+SIZES = {"emb": (50_000,), "h0.w": (300_017,), "h1.w": (262_144,), "norm": (7,)}
+
+CONFIGS = [
+    ("compressed1bit", None, "laplace", "alternating", None),
+    ("compressed1bit", None, "ties", "alternating", None),
+    ("direct", 1, "laplace", "alternating", None),
+    ("direct", 1, "ties", "exact-ternary", None),
+    ("direct", 5, "outliers", "alternating", None),
+    ("direct", 8, "laplace", "exact-ternary", None),
+    ("ps", None, "cancel", "exact-ternary", None),
+    ("ps_efficient", None, "laplace", "alternating", None),
+    ("compressed1bit", None, "laplace", "alternating", (10, frozenset({"emb", "h1.w"}))),
+    ("direct", 1, "zeros", "alternating", (10, "all")),
+]
+
+
+def f32_eq(a, b):
+    a = np.asarray(a, dtype=np.float32)
+    b = np.asarray(b, dtype=np.float64).astype(np.float32)
+    return np.array_equal(a.view(np.int32), b.view(np.int32))
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    tp = lc.NcclTransport.init_process(rank, world, dev)
+    topo = lc.Topology(world_size=world, rank=rank, transport=tp)
+    fails = []
+    checked = 0
+    for ci, (algo, bits, kind, zm, sync) in enumerate(CONFIGS):
+        ranks = O.synth_rank_inputs(100 + ci, world, SIZES, kind)
+        h = O.Hyper(0.9, 0.99, 1e-4, 0.1)
+        it = 9
+        nt, nm, sign, ties, _, _ = O.distributed_step(
+            [r["theta"] for r in ranks], [r["m"] for r in ranks], [r["g"] for r in ranks],
+            h, None if bits is None else O.Spec(bits), algo, it, zero_mode=zm)
+        if sync is not None:
+            nm = O.sync_momentum(nm, sync[0], sync[1], it + 1)
+        mine = ranks[rank]
+        st = lc.WorkerState.initial({k: torch.from_numpy(v).to(dev)
+                                     for k, v in mine["theta"].items()})
+        for k, v in mine["m"].items():
+            st.momentum[k].copy_(torch.from_numpy(v))
+        st.iteration = it
+        g = st.new_grad_buffer()
+        for k, v in mine["g"].items():
+            g[k].copy_(torch.from_numpy(v))
+        met = {}
+        st = lc.distributed_lion_step(st, g, lc.LionHyper(0.9, 0.99, 1e-4, 0.1),
+                                      None if bits is None else lc.QuantSpec(bits=bits),
+                                      topo, algo, zero_mode=zm, metrics_out=met)
+        if sync is not None:
+            st = lc.maybe_sync_momentum(st, lc.SyncPolicy(period=sync[0], layers=sync[1]), topo)
+        torch.cuda.synchronize()
+        for k in SIZES:
+            checked += 1
+            if not f32_eq(st.params[k].cpu().numpy(), nt[rank][k]):
+                fails.append(f"{algo}/{bits}/{kind}/{zm}: theta {k}")
+            if not f32_eq(st.momentum[k].cpu().numpy(), nm[rank][k]):
+                fails.append(f"{algo}/{bits}/{kind}/{zm}: m {k}")
+            if not np.array_equal(met["vote_sign"][k].cpu().numpy(), sign[k]):
+                fails.append(f"{algo}/{bits}/{kind}/{zm}: sign {k}")
+            if met["ties"][k] != ties[k]:
+                fails.append(f"{algo}/{bits}/{kind}/{zm}: ties {k} {met['ties'][k]} != {ties[k]}")
+    # reference golden collectives at this world size
+    for c in G.collective_cases():
+        if c["world"] != world:
+            continue
+        gc = G.collective_case(c["name"])
+        x = torch.from_numpy(np.asarray(gc["inputs"][rank])).to(dev)
+        checked += 1
+        if c["kind"] == "direct":
+            v = lc.direct_allreduce(x, topo, q_max=c["q_max"], binary_signs=c.get("binary", False))
+            ok = np.array_equal(v.values.cpu().numpy(), gc["values"]) and v.ties == gc["ties"]
+        elif c["kind"] == "compressed":
+            v = lc.compressed_allreduce_1bit(x, topo, lc.SignPolicy("alternating", c["t"]))
+            ok = np.array_equal(v.values.cpu().numpy(), gc["values"]) and v.ties == gc["ties"]
+        else:
+            v = lc.allreduce_mean_f32(x, topo)
+            ok = np.array_equal(v.cpu().numpy().view(np.int32), gc["values"].view(np.int32))
+        if not ok:
+            fails.append(f"golden {c['name']}")
+    nfail = torch.tensor([len(fails)], device=dev)
+    dist.all_reduce(nfail)
+    if fails:
+        print(f"rank {rank} FAIL: {fails[:10]}", file=sys.stderr)
+    if rank == 0:
+        print(json.dumps({"world": world, "checked_per_rank": checked,
+                          "failures_all_ranks": int(nfail.item())}))
+    tp.close()
+    dist.destroy_process_group()
+    return 0 if int(nfail.item()) == 0 else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -33,11 +33,15 @@ def _need_gpu():
 STEP_NAMES = [c["name"] for c in G.step_cases()]
 
 
+@pytest.mark.parametrize("p2p", [True, False], ids=["peer-memory", "collectives"])
 @pytest.mark.parametrize("name", STEP_NAMES)
-def test_step_matches_reference_golden(name):
+def test_step_matches_reference_golden(name, p2p):
+    """Both exchange modes: kernels storing into peers' buffers (NVLink
+    path) and the collective path (NCCL path), simulated ranks on one GPU."""
     gc = G.step_case(name)
     case = gc["case"]
-    res = run_step_case(case, gc["theta"], gc["m"], gc["g"], mask=gc["mask"])
+    res = run_step_case(case, gc["theta"], gc["m"], gc["g"], mask=gc["mask"],
+                        transport=lc.LocalTransport(case["world"], p2p=p2p))
     for r, (th, m, met, it) in enumerate(res):
         assert it == case["iteration"] + 1
         for k in gc["sizes"]:
@@ -75,9 +79,10 @@ def test_packed_sign_words_bit_exact(name):
             out = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
             flags = torch.zeros(1, dtype=torch.int32, device="cuda")
             hyp = _hyper()
+            L = -(-n // 1024) * 1024
             _lib.call("lc_encode", g.data_ptr(), m.data_ptr(), _lib.ptr(mask), n,
-                      C.byref(hyp), fill, _lib.LC_ENC_SIGN1, 1, None, out.data_ptr(),
-                      flags.data_ptr(), 0)
+                      C.byref(hyp), fill, _lib.LC_ENC_SIGN1, 1, None,
+                      _lib.table([out.data_ptr()]), 1, L, flags.data_ptr(), 0)
             got = out.cpu().numpy().view(np.uint32)
             nb = (n + 7) // 8  # reference payload bytes; compare the valid bits
             gb = got.view(np.uint8)[:nb].copy()
@@ -129,7 +134,8 @@ def test_l1_norm_and_quantized_ints_bit_exact(name):
             flags = torch.zeros(1, dtype=torch.int32, device="cuda")
             _lib.call("lc_encode", g.data_ptr(), m.clone().data_ptr(), _lib.ptr(mask), n,
                       C.byref(hyp), 1, _lib.LC_ENC_QUANT_FIELDS, 32, C.byref(segs),
-                      out.data_ptr(), flags.data_ptr(), 0)
+                      _lib.table([out.data_ptr()]), 1, -(-n // 1024) * 1024,
+                      flags.data_ptr(), 0)
             q = out.cpu().numpy().astype(np.int64) - qmax
             ref = np.concatenate([gc["q"][r][k].astype(np.int64) for k in names])
             assert np.array_equal(q, ref), (name, r)
@@ -167,6 +173,7 @@ def test_collective_matches_reference_golden(name):
 BIG = {"emb": (40_000,), "h0.w": (300_017,), "h1.w": (262_144,), "norm": (1_000,)}
 
 
+@pytest.mark.parametrize("p2p", [True, False], ids=["peer-memory", "collectives"])
 @pytest.mark.parametrize("algo,bits,world,kind,zm", [
     ("compressed1bit", None, 4, "laplace", "alternating"),
     ("compressed1bit", None, 8, "ties", "alternating"),
@@ -179,7 +186,7 @@ BIG = {"emb": (40_000,), "h0.w": (300_017,), "h1.w": (262_144,), "norm": (1_000,
     ("compressed1bit", None, 1, "laplace", "alternating"),
     ("direct", 5, 1, "outliers", "alternating"),
 ])
-def test_step_matches_oracle_large(algo, bits, world, kind, zm):
+def test_step_matches_oracle_large(algo, bits, world, kind, zm, p2p):
     ranks = O.synth_rank_inputs(7, world, BIG, kind)
     h = O.Hyper(0.9, 0.99, 1e-4, 0.1)
     spec = None if bits is None else O.Spec(bits)
@@ -190,7 +197,8 @@ def test_step_matches_oracle_large(algo, bits, world, kind, zm):
     case = dict(world=world, lr=1e-4, wd=0.1, bits=bits, algo=algo, iteration=it,
                 zero_mode=zm)
     res = run_step_case(case, ranks[0]["theta"], [rk["m"] for rk in ranks],
-                        [rk["g"] for rk in ranks])
+                        [rk["g"] for rk in ranks],
+                        transport=lc.LocalTransport(world, p2p=p2p))
     for r, (th, m, met, _) in enumerate(res):
         for k in BIG:
             assert_f32_equal(th[k], nt[0][k], f"theta {k}")
@@ -199,7 +207,8 @@ def test_step_matches_oracle_large(algo, bits, world, kind, zm):
             assert met["ties"][k] == ties[k]
 
 
-def test_momentum_sync_matches_oracle_large():
+@pytest.mark.parametrize("p2p", [True, False], ids=["peer-memory", "collectives"])
+def test_momentum_sync_matches_oracle_large(p2p):
     world = 8
     ranks = O.synth_rank_inputs(3, world, BIG, "laplace")
     h = O.Hyper(0.9, 0.99, 1e-4, 0.0)
@@ -209,7 +218,8 @@ def test_momentum_sync_matches_oracle_large():
     case = dict(world=world, lr=1e-4, wd=0.0, bits=None, algo="compressed1bit",
                 iteration=9, zero_mode="alternating", sync=(10, ["emb", "h1.w"]))
     res = run_step_case(case, ranks[0]["theta"], [rk["m"] for rk in ranks],
-                        [rk["g"] for rk in ranks], metrics=False)
+                        [rk["g"] for rk in ranks], metrics=False,
+                        transport=lc.LocalTransport(world, p2p=p2p))
     for r, (_, m, _, _) in enumerate(res):
         for k in BIG:
             assert_f32_equal(m[k], synced[r][k], f"m {k} r{r}")

@@ -1,0 +1,78 @@
+"""Multi-GPU NCCL parity (needs >= 2 B200s; skipped otherwise)."""
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _ngpu():
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+@pytest.mark.parametrize("p2p", ["1", "0"], ids=["nvlink-peer-memory", "nccl"])
+@pytest.mark.parametrize("nproc", [2, 4, 8])
+def test_process_per_gpu_parity(nproc, p2p):
+    if _ngpu() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1",
+           f"--master-port={29600 + 2 * nproc + int(p2p)}",
+           os.path.join(ROOT, "tests", "mgpu_parity.py")]
+    env = dict(os.environ, LIONCUB_P2P=p2p)
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    assert '"failures_all_ranks": 0' in res.stdout
+
+
+@pytest.mark.parametrize("p2p", [True, False], ids=["nvlink-peer-memory", "nccl"])
+def test_thread_per_gpu_run_ranks(p2p):
+    """One process, one thread per GPU (ncclCommInitAll + peer access),
+    reference-style run_ranks: the vote collective and a full 1-bit step
+    with momentum sync equal the oracle on every rank."""
+    n = _ngpu()
+    if n < 2:
+        pytest.skip("needs 2 GPUs")
+    import paper_2411_16462_b200 as lc
+    from oracle import lioncub_oracle as O
+    from tests.gpu_helpers import assert_f32_equal, run_step_case
+    tp = lc.NcclTransport.init_all(list(range(n)))
+    tp.p2p = p2p
+    rng = np.random.default_rng(0)
+    cs = [rng.normal(size=100_003) for _ in range(n)]
+    expect = O.vote_1bit(cs, "alternating", 1)
+
+    def fn(topo):
+        x = torch.from_numpy(cs[topo.rank]).to(topo.device)
+        v = lc.compressed_allreduce_1bit(x, topo, lc.SignPolicy("alternating", 1))
+        return v.values.cpu().numpy(), v.ties
+
+    try:
+        for vals, ties in lc.run_ranks(n, fn, transport=tp):
+            assert np.array_equal(vals, expect.values)
+            assert ties == expect.ties
+        sizes = {"a": (70_001,), "b": (4_099,)}
+        ranks = O.synth_rank_inputs(5, n, sizes, "laplace")
+        h = O.Hyper(0.9, 0.99, 1e-3, 0.1)
+        nt, nm, sign, ties, _, _ = O.distributed_step(
+            [r["theta"] for r in ranks], [r["m"] for r in ranks], [r["g"] for r in ranks],
+            h, None, "compressed1bit", 9)
+        nm = O.sync_momentum(nm, 10, "all", 10)
+        case = dict(world=n, lr=1e-3, wd=0.1, bits=None, algo="compressed1bit",
+                    iteration=9, zero_mode="alternating", sync=(10, "all"))
+        res = run_step_case(case, ranks[0]["theta"], [r["m"] for r in ranks],
+                            [r["g"] for r in ranks], transport=tp)
+        for r, (th, m, met, _) in enumerate(res):
+            for k in sizes:
+                assert_f32_equal(th[k], nt[0][k], f"theta {k}")
+                assert_f32_equal(m[k], nm[r][k], f"m {k}")
+                assert met["ties"][k] == ties[k]
+    finally:
+        tp.close()
