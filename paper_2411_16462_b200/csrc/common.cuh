@@ -33,11 +33,25 @@ int sm_count();
 
 // Grid size for a grid-stride streaming kernel: enough resident CTAs to fill
 // every SM (occupancy-derived), never more than the work needs.
+// Resident CTAs per SM of `kernel` at `block` threads, cached per kernel and
+// device (the occupancy query is not free on the launch path).
+template <typename K>
+int resident_ctas(K kernel, int block) {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0);
+    cache[dev] = per_sm < 1 ? 1 : per_sm;
+  }
+  return cache[dev];
+}
+
 template <typename K>
 int stream_grid(K kernel, int block, int64_t work_items, int items_per_cta) {
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0);
-  if (per_sm < 1) per_sm = 1;
+  int per_sm = resident_ctas(kernel, block);
   int64_t need = (work_items + items_per_cta - 1) / items_per_cta;
   int64_t cap = (int64_t)sm_count() * per_sm;
   int64_t g = need < cap ? need : cap;

@@ -17,8 +17,14 @@ struct Ptrs {
   void* p[LC_MAX_BLOCKS];
 };
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void k_barrier(Ptrs peer_flags, uint64_t* __restrict__ my_flags, int P, int rank,
-                          unsigned long long epoch, long long timeout_cycles,
+                          unsigned long long epoch, unsigned long long timeout_ns,
                           uint32_t* __restrict__ err) {
   const int j = threadIdx.x;
   if (j < P) {
@@ -28,12 +34,12 @@ __global__ void k_barrier(Ptrs peer_flags, uint64_t* __restrict__ my_flags, int 
   }
   __syncthreads();
   if (j < P) {
-    const long long t0 = clock64();
+    const unsigned long long t0 = globaltimer_ns();
     while (true) {
       unsigned long long v;
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(my_flags + j) : "memory");
       if (v >= epoch) break;
-      if (clock64() - t0 > timeout_cycles) {
+      if (globaltimer_ns() - t0 > timeout_ns) {
         atomicOr(err, (uint32_t)LC_FLAG_BARRIER_TIMEOUT);
         break;
       }
@@ -146,13 +152,9 @@ int lc_barrier(void* const* peer_flags, int32_t P, int32_t rank, uint64_t* my_fl
   Ptrs pf;
   if (P < 1 || P > 32 || rank < 0 || rank >= P || !my_flags || !err || !make_ptrs(pf, peer_flags, P))
     return lc::set_err(LC_E_ARG, "lc_barrier: bad arguments");
-  int dev = 0, khz = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, dev);
-  if (khz <= 0) khz = 2000000;
-  long long cycles = (long long)(timeout_s * 1e3 * (double)khz);
+  const unsigned long long ns = (unsigned long long)(timeout_s * 1e9);
   k_barrier<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(pf, my_flags, P, rank,
-                                                                  epoch, cycles, err);
+                                                                  epoch, ns, err);
   LC_LAUNCH_CHECK();
   return LC_OK;
 }
