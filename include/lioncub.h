@@ -138,10 +138,14 @@ int lc_f64_sum_vote(const double* recv, int32_t P, int64_t len, int64_t stride,
                     void* stream);
 
 /* ---- K5: theta' = theta - eta*(s + wd*theta)  (optimizer.py:204) ----
- * s = +1/-1 from sign bits; 0 where nz_bits (nullable) has a 0 bit. */
-int lc_apply_update(float* theta, int64_t n, const uint32_t* sign_bits,
-                    const uint32_t* nz_bits, double lr, double weight_decay,
-                    void* stream);
+ * s = +1/-1 from the voted sign bits; 0 where nz_bits has a 0 bit.
+ * sign_bits / nz_bits (nullable) are tables of nsrc word arrays indexed by
+ * the GLOBAL word index; word w is read from table entry w / wpb -- the
+ * owner of that block.  nsrc = 1: local gather buffer; nsrc = P: each
+ * owner's vote output over NVLink (the allgather pulled inside K5). */
+int lc_apply_update(float* theta, int64_t n, void* const* sign_bits,
+                    void* const* nz_bits, int32_t nsrc, int64_t wpb, double lr,
+                    double weight_decay, void* stream);
 
 /* ---- one-pass step for P == 1 (no exchange: the vote of one rank is its
  * own aggregate): reads theta,m,g, writes theta',m' (20 B/param).

@@ -67,7 +67,7 @@ SIGNATURES = {
     "lc_vote_bits": (INT, [P, I32, I64, I64, INT, INT, P, P, P, I32, P, P]),
     "lc_fields_vote": (INT, [P, I32, I64, I64, I32, I32, I32, I32, INT, P, P, P, I32, P, P]),
     "lc_f64_sum_vote": (INT, [P, I32, I64, I64, INT, INT, P, P, P, I32, P, P]),
-    "lc_apply_update": (INT, [P, I64, P, P, D, D, P]),
+    "lc_apply_update": (INT, [P, I64, P, P, I32, I64, D, D, P]),
     "lc_fused_local_step": (INT, [P, P, P, P, I64, P, INT, INT, P, P, P, P, P, P]),
     "lc_mean_f32": (INT, [P, I32, I64, I64, P, P]),
     "lc_l1_plan_create": (INT, [P, P, I32]),

@@ -116,134 +116,147 @@ __device__ __forceinline__ void pack_store(uint32_t* __restrict__ out,
 // local send buffer or the owner GPU's receive slot over NVLink (Dst table:
 // block j = elements [j*L, (j+1)*L) goes to dst.p[j]).
 // ---------------------------------------------------------------------------
+// Encode 4 consecutive elements of one lane: c and m' in float64, m' back as
+// fp32, and the stored value of each element (sign bit / field).  VALID is
+// false only for the last, partial sub-tile.
+template <int ENC, bool MASK>
+__device__ __forceinline__ void encode4(const float ge[4], const float me[4], const bool keep[4],
+                                        const bool valid[4], const Hyp& h, uint32_t fillbit,
+                                        uint32_t zflag, const SegQ& sq, SegCursor& cur,
+                                        int64_t e0, double c[4], float mn[4], uint32_t st[4],
+                                        uint32_t& flag) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    c[q] = lion_c(me[q], ge[q], h);
+    if (MASK && !keep[q]) c[q] = 0.0;  // np.where(mask, c, 0.0)
+    mn[q] = lion_m(me[q], ge[q], h);
+    if constexpr (ENC == LC_ENC_QUANT_FIELDS) {
+      st[q] = valid[q] ? (uint32_t)(quant_l1(c[q], cur.get(sq, e0 + q), sq.qmax) + sq.qmax) : 0u;
+    } else if constexpr (ENC != LC_ENC_F64) {
+      // sign with the zero fill; -0.0 == 0 (np.sign(-0.0) == 0); NaN -> 0
+      const bool pos = c[q] > 0.0, zero = c[q] == 0.0;
+      const uint32_t b = (uint32_t)pos | ((uint32_t)zero & fillbit);
+      if (zero && valid[q]) flag |= zflag;
+      // pad with +1 on the 1-bit wire like collectives.py:269-271
+      st[q] = valid[q] ? b : (ENC == LC_ENC_SIGN1 ? 1u : 0u);
+    }
+  }
+}
+
+// Place one sub-tile's stored values (lane holds elements 4l..4l+3) into the
+// warp's staged words for that sub-tile.
+template <int F>
+__device__ __forceinline__ void stage_subtile(uint32_t* sw, int lane, const uint32_t st[4]) {
+  if constexpr (F <= 8) {
+    constexpr int LPW = 8 / F;  // lanes sharing one 32-bit word
+    uint32_t v = st[0] | (st[1] << F) | (st[2] << (2 * F)) | (st[3] << (3 * F));
+    v <<= (4 * F) * (lane % LPW);
+#pragma unroll
+    for (int sh = 1; sh < LPW; sh <<= 1) v |= __shfl_xor_sync(kFull, v, sh);
+    if (lane % LPW == 0) sw[lane / LPW] = v;
+  } else if constexpr (F == 16) {
+    sw[2 * lane] = st[0] | (st[1] << 16);
+    sw[2 * lane + 1] = st[2] | (st[3] << 16);
+  } else {
+    *reinterpret_cast<uint4*>(sw + 4 * lane) = make_uint4(st[0], st[1], st[2], st[3]);
+  }
+}
+
 template <int ENC, int F, bool MASK>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
 k_encode(const float* __restrict__ g, float* __restrict__ m,
          const uint8_t* __restrict__ mask, int64_t n, Hyp h, int fill, SegQ sq,
          Dst dst, int64_t L, uint32_t* __restrict__ flags) {
   constexpr int WPS = (ENC == LC_ENC_F64) ? 1 : 32 * F;  // words per super-tile
+  constexpr int KU = 4;  // sub-tiles whose loads are in flight together
   __shared__ __align__(16) uint32_t stage[8][WPS];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t nsup = (n + 1023) >> 10;
-  const bool ternary = fill == 0;
   const uint32_t fillbit = fill > 0 ? 1u : 0u;
+  const uint32_t zflag = fill == 0 ? (uint32_t)LC_FLAG_ZERO_SIGN : 0u;
   const float4* g4 = reinterpret_cast<const float4*>(g);
   float4* m4 = reinterpret_cast<float4*>(m);
   uint32_t flag = 0;
   SegCursor cur;
+  const bool valid_all[4] = {true, true, true, true};
 
   for (int64_t sidx = gw; sidx < nsup; sidx += nw) {
     const int64_t ebase = sidx << 10;
     const int j = (int)(ebase / L);
     const int64_t boff = ebase - (int64_t)j * L;  // element offset inside block j
+    if (ebase + 1024 <= n) {
+      // ---- fast path: a full super-tile, no per-element bounds ----
+      const float4* gp = g4 + (ebase >> 2) + lane;
+      float4* mp = m4 + (ebase >> 2) + lane;
 #pragma unroll 1
-    for (int k0 = 0; k0 < 8; k0 += 2) {
-      float4 gv[2], mv[2];
-      uchar4 mk[2];
+      for (int k0 = 0; k0 < 8; k0 += KU) {
+        float4 gv[KU], mv[KU];
+        uchar4 mk[KU];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int64_t t = (ebase >> 7) + k0 + u;  // 128-element tile index
-        if ((t + 1) * 128 <= n) {
-          gv[u] = ld_stream(g4 + t * 32 + lane);
-          mv[u] = ld_stream(m4 + t * 32 + lane);
-          if (MASK) mk[u] = *reinterpret_cast<const uchar4*>(mask + t * 128 + lane * 4);
+        for (int u = 0; u < KU; ++u) {
+          gv[u] = ld_stream(gp + (k0 + u) * 32);
+          mv[u] = ld_stream(mp + (k0 + u) * 32);
+          if (MASK) mk[u] = *reinterpret_cast<const uchar4*>(mask + ebase + (k0 + u) * 128 + lane * 4);
+        }
+#pragma unroll
+        for (int u = 0; u < KU; ++u) {
+          const int k = k0 + u;
+          const float ge[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
+          const float me[4] = {mv[u].x, mv[u].y, mv[u].z, mv[u].w};
+          bool keep[4] = {true, true, true, true};
+          if (MASK) {
+            keep[0] = mk[u].x; keep[1] = mk[u].y; keep[2] = mk[u].z; keep[3] = mk[u].w;
+          }
+          double c[4];
+          float mn[4];
+          uint32_t st[4];
+          encode4<ENC, MASK>(ge, me, keep, valid_all, h, fillbit, zflag, sq, cur,
+                             ebase + k * 128 + lane * 4, c, mn, st, flag);
+          st_stream(mp + k * 32, make_float4(mn[0], mn[1], mn[2], mn[3]));
+          if constexpr (ENC == LC_ENC_F64) {
+            double* o = reinterpret_cast<double*>(dst.p[j]) + boff + k * 128 + lane * 4;
+            __stcs(reinterpret_cast<double2*>(o), make_double2(c[0], c[1]));
+            __stcs(reinterpret_cast<double2*>(o + 2), make_double2(c[2], c[3]));
+          } else {
+            stage_subtile<F>(&stage[wib][k * 4 * F], lane, st);
+          }
         }
       }
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int k = k0 + u;
-        const int64_t t = (ebase >> 7) + k;
-        const int64_t e0 = t * 128 + lane * 4;
-        if (t * 128 >= n) {  // whole sub-tile past the end (warp-uniform)
+    } else {
+      // ---- tail super-tile: per-element bounds ----
+#pragma unroll 1
+      for (int k = 0; k < 8; ++k) {
+        const int64_t e0 = ebase + k * 128 + lane * 4;
+        if (ebase + k * 128 >= n) {  // whole sub-tile past the end (warp-uniform)
           if (ENC != LC_ENC_F64)
             for (int w = lane; w < 4 * F; w += 32) stage[wib][k * 4 * F + w] = 0u;
           continue;
         }
-        const bool full = (t + 1) * 128 <= n;
         float ge[4], me[4];
         bool valid[4], keep[4];
-        if (full) {
-          ge[0] = gv[u].x; ge[1] = gv[u].y; ge[2] = gv[u].z; ge[3] = gv[u].w;
-          me[0] = mv[u].x; me[1] = mv[u].y; me[2] = mv[u].z; me[3] = mv[u].w;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) valid[q] = true;
-          if (MASK) {
-            keep[0] = mk[u].x; keep[1] = mk[u].y; keep[2] = mk[u].z; keep[3] = mk[u].w;
-          }
-        } else {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            valid[q] = e0 + q < n;
-            ge[q] = valid[q] ? g[e0 + q] : 0.f;
-            me[q] = valid[q] ? m[e0 + q] : 0.f;
-            keep[q] = MASK ? (valid[q] ? mask[e0 + q] != 0 : true) : true;
-          }
+        for (int q = 0; q < 4; ++q) {
+          valid[q] = e0 + q < n;
+          ge[q] = valid[q] ? g[e0 + q] : 0.f;
+          me[q] = valid[q] ? m[e0 + q] : 0.f;
+          keep[q] = MASK ? (valid[q] ? mask[e0 + q] != 0 : true) : true;
         }
         double c[4];
         float mn[4];
+        uint32_t st[4];
+        encode4<ENC, MASK>(ge, me, keep, valid, h, fillbit, zflag, sq, cur, e0, c, mn, st, flag);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          c[q] = lion_c(me[q], ge[q], h);
-          if (MASK && !keep[q]) c[q] = 0.0;  // np.where(mask, c, 0.0)
-          mn[q] = lion_m(me[q], ge[q], h);
-        }
-        if (full) {
-          st_stream(m4 + t * 32 + lane, make_float4(mn[0], mn[1], mn[2], mn[3]));
-        } else {
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (valid[q]) m[e0 + q] = mn[q];
-        }
+        for (int q = 0; q < 4; ++q)
+          if (valid[q]) m[e0 + q] = mn[q];
         if constexpr (ENC == LC_ENC_F64) {
           double* o = reinterpret_cast<double*>(dst.p[j]) + boff + k * 128 + lane * 4;
-          if (full) {
-            __stcs(reinterpret_cast<double2*>(o), make_double2(c[0], c[1]));
-            __stcs(reinterpret_cast<double2*>(o + 2), make_double2(c[2], c[3]));
-          } else {
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              if (valid[q]) o[q] = c[q];
-          }
+          for (int q = 0; q < 4; ++q)
+            if (valid[q]) o[q] = c[q];
         } else {
-          uint32_t st[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if (ENC == LC_ENC_QUANT_FIELDS) {
-              st[q] = valid[q] ? (uint32_t)(quant_l1(c[q], cur.get(sq, e0 + q), sq.qmax) + sq.qmax)
-                               : 0u;
-            } else {
-              uint32_t b;
-              if (c[q] > 0.0) {
-                b = 1u;
-              } else if (c[q] < 0.0) {
-                b = 0u;
-              } else if (c[q] == 0.0) {  // -0.0 included (np.sign(-0.0) == 0)
-                b = fillbit;
-                if (ternary && valid[q]) flag |= LC_FLAG_ZERO_SIGN;
-              } else {
-                b = 0u;
-                if (valid[q]) flag |= LC_FLAG_NAN;
-              }
-              // pad with +1 on the 1-bit wire like collectives.py:269-271
-              st[q] = valid[q] ? b : (ENC == LC_ENC_SIGN1 ? 1u : 0u);
-            }
-          }
-          uint32_t* sw = &stage[wib][k * 4 * F];
-          if constexpr (F <= 8) {
-            constexpr int LPW = 8 / F;  // lanes sharing one 32-bit word
-            uint32_t v = st[0] | (st[1] << F) | (st[2] << (2 * F)) | (st[3] << (3 * F));
-            v <<= (4 * F) * (lane % LPW);
-#pragma unroll
-            for (int sh = 1; sh < LPW; sh <<= 1) v |= __shfl_xor_sync(kFull, v, sh);
-            if (lane % LPW == 0) sw[lane / LPW] = v;
-          } else if constexpr (F == 16) {
-            sw[2 * lane] = st[0] | (st[1] << 16);
-            sw[2 * lane + 1] = st[2] | (st[3] << 16);
-          } else {
-            *reinterpret_cast<uint4*>(sw + 4 * lane) = make_uint4(st[0], st[1], st[2], st[3]);
-          }
+          stage_subtile<F>(&stage[wib][k * 4 * F], lane, st);
         }
       }
     }
@@ -265,52 +278,66 @@ k_encode(const float* __restrict__ g, float* __restrict__ m,
 }
 
 // ---------------------------------------------------------------------------
-// K5: theta update from (sign bits, optional nonzero bits).
+// K5: theta update from (sign bits, optional nonzero bits).  A warp owns a
+// 1024-element super-tile: lane i fetches word i of its 32 voted words with
+// one coalesced 128-byte load from the word's owner -- the local gather
+// buffer, or the owner GPU's vote output over NVLink (src table indexed by
+// owner block, wpb words per block) -- then sub-tile k takes its 4 words by
+// shuffle.  theta streams with KU sub-tiles of float4 loads in flight.
 // ---------------------------------------------------------------------------
-template <bool NZ, int U>
-__global__ void __launch_bounds__(256)
-k_apply_update(float* __restrict__ theta, int64_t n,
-               const uint32_t* __restrict__ sb, const uint32_t* __restrict__ nzb,
+template <bool NZ>
+__global__ void __launch_bounds__(256, 3)
+k_apply_update(float* __restrict__ theta, int64_t n, Dst sb, Dst nzb, int64_t wpb,
                double lr, double wd) {
+  constexpr int KU = 4;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t ntiles = (n + 127) >> 7, nfull = n >> 7;
+  const int64_t nsup = (n + 1023) >> 10;
+  const int64_t nwords = (n + 31) >> 5;
   float4* th4 = reinterpret_cast<float4*>(theta);
-  for (int64_t t0 = gw; t0 < ntiles; t0 += nw * U) {
-    float4 tv[U];
-    uint32_t sw[U], zw[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      int64_t t = t0 + u * nw;
-      if (t < ntiles) {
-        sw[u] = __ldg(sb + t * 4 + (lane >> 3));
-        zw[u] = NZ ? __ldg(nzb + t * 4 + (lane >> 3)) : ~0u;
-        if (t < nfull) tv[u] = ld_stream(th4 + t * 32 + lane);
-      }
+  for (int64_t sidx = gw; sidx < nsup; sidx += nw) {
+    const int64_t w = sidx * 32 + lane;  // global word index of this lane
+    uint32_t myw = 0u, myz = ~0u;
+    if (w < nwords) {
+      const int j = (int)(w / wpb);
+      myw = __ldcs(reinterpret_cast<const uint32_t*>(sb.p[j]) + w);
+      if (NZ) myz = __ldcs(reinterpret_cast<const uint32_t*>(nzb.p[j]) + w);
     }
+#pragma unroll 1
+    for (int k0 = 0; k0 < 8; k0 += KU) {
+      float4 tv[KU];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t t = t0 + u * nw;
-      if (t >= ntiles) break;
-      const int sh = 4 * (lane & 7);
-      const uint32_t sn = (sw[u] >> sh) & 0xF, zn = (zw[u] >> sh) & 0xF;
-      double s[4];
+      for (int u = 0; u < KU; ++u) {
+        const int64_t t = sidx * 8 + k0 + u;
+        if ((t + 1) * 128 <= n) tv[u] = ld_stream(th4 + t * 32 + lane);
+      }
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        s[k] = ((zn >> k) & 1) ? (((sn >> k) & 1) ? 1.0 : -1.0) : 0.0;
-      if (t < nfull) {
-        float4 v = tv[u];
-        v.x = lion_theta(v.x, s[0], lr, wd);
-        v.y = lion_theta(v.y, s[1], lr, wd);
-        v.z = lion_theta(v.z, s[2], lr, wd);
-        v.w = lion_theta(v.w, s[3], lr, wd);
-        st_stream(th4 + t * 32 + lane, v);
-      } else {
-        const int64_t e0 = t * 128 + lane * 4;
+      for (int u = 0; u < KU; ++u) {
+        const int k = k0 + u;
+        const int64_t t = sidx * 8 + k;
+        const uint32_t sw = __shfl_sync(kFull, myw, 4 * k + (lane >> 3));
+        const uint32_t zw = NZ ? __shfl_sync(kFull, myz, 4 * k + (lane >> 3)) : ~0u;
+        if (t * 128 >= n) continue;  // warp-uniform
+        const int sh = 4 * (lane & 7);
+        const uint32_t sn = (sw >> sh) & 0xF, zn = (zw >> sh) & 0xF;
+        double sg[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (e0 + k < n) theta[e0 + k] = lion_theta(theta[e0 + k], s[k], lr, wd);
+        for (int q = 0; q < 4; ++q)
+          sg[q] = ((zn >> q) & 1) ? (((sn >> q) & 1) ? 1.0 : -1.0) : 0.0;
+        if ((t + 1) * 128 <= n) {
+          float4 v = tv[u];
+          v.x = lion_theta(v.x, sg[0], lr, wd);
+          v.y = lion_theta(v.y, sg[1], lr, wd);
+          v.z = lion_theta(v.z, sg[2], lr, wd);
+          v.w = lion_theta(v.w, sg[3], lr, wd);
+          st_stream(th4 + t * 32 + lane, v);
+        } else {
+          const int64_t e0 = t * 128 + lane * 4;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (e0 + q < n) theta[e0 + q] = lion_theta(theta[e0 + q], sg[q], lr, wd);
+        }
       }
     }
   }
@@ -896,23 +923,26 @@ int lc_encode(const float* g, float* m, const uint8_t* mask, int64_t n,
   }
 }
 
-int lc_apply_update(float* theta, int64_t n, const uint32_t* sign_bits,
-                    const uint32_t* nz_bits, double lr, double wd, void* stream) {
+int lc_apply_update(float* theta, int64_t n, void* const* sign_bits, void* const* nz_bits,
+                    int32_t nsrc, int64_t wpb, double lr, double wd, void* stream) {
   if (n < 0) return set_err(LC_E_ARG, "lc_apply_update: n < 0");
   if (n == 0) return LC_OK;
-  if (!theta || !sign_bits) return set_err(LC_E_ARG, "lc_apply_update: null pointer");
+  Dst sb, zb;
+  if (!theta || !make_dst(sb, sign_bits, nsrc) || (nz_bits && !make_dst(zb, nz_bits, nsrc)))
+    return set_err(LC_E_ARG, "lc_apply_update: bad pointers / source table");
+  if (wpb <= 0 || (int64_t)nsrc * wpb * 32 < n)
+    return set_err(LC_E_ARG, "lc_apply_update: source blocks do not cover n");
   if (!aligned16(theta)) return set_err(LC_E_ARG, "lc_apply_update: theta must be 16-byte aligned");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  constexpr int U = 4;
-  int64_t ntiles = (n + 127) >> 7;
+  const int64_t nsup = (n + 1023) >> 10;
   if (nz_bits) {
-    auto kern = k_apply_update<true, U>;
-    int grid = stream_grid(kern, kBlock, ntiles, (kBlock / 32) * U);
-    kern<<<grid, kBlock, 0, st>>>(theta, n, sign_bits, nz_bits, lr, wd);
+    auto kern = k_apply_update<true>;
+    int grid = stream_grid(kern, kBlock, nsup, kBlock / 32);
+    kern<<<grid, kBlock, 0, st>>>(theta, n, sb, zb, wpb, lr, wd);
   } else {
-    auto kern = k_apply_update<false, U>;
-    int grid = stream_grid(kern, kBlock, ntiles, (kBlock / 32) * U);
-    kern<<<grid, kBlock, 0, st>>>(theta, n, sign_bits, nz_bits, lr, wd);
+    auto kern = k_apply_update<false>;
+    int grid = stream_grid(kern, kBlock, nsup, kBlock / 32);
+    kern<<<grid, kBlock, 0, st>>>(theta, n, sb, sb, wpb, lr, wd);
   }
   LC_LAUNCH_CHECK();
   return LC_OK;

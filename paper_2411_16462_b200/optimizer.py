@@ -292,10 +292,23 @@ class _Workspace:
             self.nz = sym("nz", P * cw) if ternary else None
             self.ties = sym("ties", P * cw) if metrics else None
             self.dst = _lib.table([self.recv.peers[j] + r * blk_bytes for j in range(P)])
-            outs = lambda b: None if b is None else _lib.table(  # noqa: E731
-                [b.peers[j] + r * cw * 4 for j in range(P)])
+            if metrics:
+                # metrics need every block locally: owners push to all ranks
+                outs = lambda b: None if b is None else _lib.table(  # noqa: E731
+                    [b.peers[j] + r * cw * 4 for j in range(P)])
+                self.nout = P
+                self.src = _lib.table([self.full.local.data_ptr()])
+                self.nzsrc = None if self.nz is None else _lib.table([self.nz.local.data_ptr()])
+                self.nsrc, self.wpb = 1, P * cw
+            else:
+                # owners keep their block; K5 pulls each word from its owner
+                outs = lambda b: None if b is None else _lib.table(  # noqa: E731
+                    [b.local.data_ptr() + r * cw * 4])
+                self.nout = 1
+                self.src = _lib.table(self.full.peers)
+                self.nzsrc = None if self.nz is None else _lib.table(self.nz.peers)
+                self.nsrc, self.wpb = P, cw
             self.vout, self.nzout, self.tout = outs(self.full), outs(self.nz), outs(self.ties)
-            self.nout = P
         else:
             self.send = torch.zeros(rlen, dtype=rdt, device=dev)
             if kind == "fields":
@@ -309,6 +322,9 @@ class _Workspace:
             one = lambda t: None if t is None else _lib.table([_off(t, r * cw)])  # noqa
             self.vout, self.nzout, self.tout = one(self.full), one(self.nz), one(self.ties)
             self.nout = 1
+            self.src = _lib.table([self.full.data_ptr()])
+            self.nzsrc = None if self.nz is None else _lib.table([self.nz.data_ptr()])
+            self.nsrc, self.wpb = 1, P * cw
 
 
 def _workspace(th: FlatParamSet, topo: Topology, kind: str, F: int, ternary: bool,
@@ -486,8 +502,8 @@ def distributed_lion_step(state: WorkerState, grad_i, h: LionHyper,
                 nz = _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill,
                                         n, g, m, mflat, hyp, segs, s,
                                         tree=algo == "ps_efficient")
-                _lib.call("lc_apply_update", th.flat.data_ptr(), n, _loc(ws.full).data_ptr(),
-                          _lib.ptr(nz), eta, wd, s)
+                _lib.call("lc_apply_update", th.flat.data_ptr(), n, ws.src, ws.nzsrc,
+                          ws.nsrc, ws.wpb, eta, wd, s)
             if metrics:
                 _fill_metrics(metrics_out, layout, dev, ws, nz, c_local, s)
     return WorkerState(params=th, momentum=m, iteration=t)
