@@ -1,0 +1,176 @@
+"""CPU-only tests: the C ABI library loads and exports everything the header
+declares, the API's validation mirrors the reference, host-side planning,
+loud failure without CUDA, and the multi-process (gloo) host logic."""
+
+import os
+import re
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2411_16462_b200 as lc
+from paper_2411_16462_b200 import _lib
+from paper_2411_16462_b200.collectives import (_mean_blocks, owner_elems,
+                                               owner_valid)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    text = open(os.path.join(ROOT, "include", "lioncub.h")).read()
+    return set(re.findall(r"\b(lc_[a-z0-9_]+)\s*\(", text))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load()
+    declared = header_symbols()
+    assert len(declared) >= 40
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert declared == set(_lib.SIGNATURES), declared ^ set(_lib.SIGNATURES)
+    assert lib.lc_abi_version() == 1
+    assert lib.lc_nccl_version() >= 22800
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH],
+                         capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_error_codes_map_to_reference_exceptions():
+    with pytest.raises(lc.ConfigError):
+        _lib.check(_lib.LC_E_CONFIG, "x")
+    with pytest.raises(lc.CapacityError):
+        _lib.check(_lib.LC_E_CAPACITY, "x")
+    with pytest.raises(lc.CollectiveError):
+        _lib.check(_lib.LC_E_COLLECTIVE, "x")
+    with pytest.raises(lc.DeviceError):
+        _lib.check(_lib.LC_E_CUDA, "x")
+    # argument validation happens before any device work
+    rc = _lib.load().lc_vote_bits(None, 0, 4, 0, 1, 0, None, None, None, 1, None, None)
+    assert rc == _lib.LC_E_ARG and "P must be" in _lib.last_error()
+
+
+def test_config_validation_mirrors_reference():
+    # optimizer.py:50-60, :86-93; quant.py:119-125, :145-149
+    with pytest.raises(lc.ConfigError):
+        lc.LionHyper(beta1=1.0)
+    with pytest.raises(lc.ConfigError):
+        lc.LionHyper(weight_decay=-1)
+    with pytest.raises(lc.ConfigError):
+        lc.LionHyper(lr=0.0).lr_at(1)
+    assert lc.LionHyper(lr=lambda t: 1.0 / t).lr_at(4) == 0.25
+    with pytest.raises(lc.ConfigError):
+        lc.SyncPolicy(period=-1)
+    with pytest.raises(lc.ConfigError):
+        lc.SyncPolicy(layers="some")
+    p = lc.SyncPolicy(period=10, layers={"head"})
+    assert p.fires(10) and not p.fires(7) and p.selects("head") and not p.selects("x")
+    assert not lc.SyncPolicy(period=0).fires(10)
+    with pytest.raises(lc.ConfigError):
+        lc.QuantSpec(bits=0)
+    with pytest.raises(lc.ConfigError):
+        lc.QuantSpec(rounding="up")
+    assert lc.QuantSpec(bits=5).qmax == 15 and lc.QuantSpec(bits=1).qmax == 0
+    with pytest.raises(lc.ConfigError):
+        lc.SignPolicy(mode="x")
+    assert lc.SignPolicy("alternating", 3).zero_fill() == 1
+    assert lc.SignPolicy("alternating", 4).zero_fill() == -1
+    assert lc.SignPolicy("exact-ternary", 3).kernel_fill() == 0
+
+
+def test_lane_and_field_widths():
+    assert lc.choose_lane_bits(8, 15) == 8
+    assert lc.choose_lane_bits(125, 15) == 16
+    assert lc.choose_lane_bits(125, 1, binary_signs=True) == 8
+    with pytest.raises(lc.CapacityError):
+        lc.choose_lane_bits(10 ** 9, 127)
+    assert lc.field_bits(8, 1) == 4 and lc.field_bits(2, 1) == 2 and lc.field_bits(1, 1) == 1
+    assert lc.field_bits(8, 30) == 8 and lc.field_bits(4, 254) == 16
+
+
+@pytest.mark.parametrize("n", [1, 7, 1000, 1024, 4099, 124_439_808])
+@pytest.mark.parametrize("P", [1, 2, 3, 8])
+def test_owner_blocks_partition(n, P):
+    L = owner_elems(n, P)
+    assert L % 1024 == 0 and P * L >= n
+    assert sum(owner_valid(n, P, r) for r in range(P)) == n
+    s, counts = _mean_blocks(n, P)
+    assert sum(counts) == n and all(c <= s for c in counts)
+
+
+def test_layout_and_runs():
+    lay = lc.Layout({"b": (3,), "a": (2, 2), "c": (5,)})
+    assert lay.names == ["a", "b", "c"] and lay.n == 12
+    assert lay.seg_start == [0, 4, 7, 12]
+    assert lay.runs(lambda k: k in ("a", "b")) == [(0, 7)]
+    assert lay.runs(lambda k: k in ("a", "c")) == [(0, 4), (7, 12)]
+
+
+def test_product_path_fails_loudly_without_cuda():
+    with pytest.raises(lc.ConfigError):
+        lc.WorkerState.initial({"w": torch.zeros(3)})
+    with pytest.raises(lc.ConfigError):
+        lc.WorkerState.initial({"w": np.zeros(3)})
+
+
+def _gloo_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ok = True
+    for n in (1, 1000, 1_000_003, 124_439_808):
+        L = owner_elems(n, world)
+        mine = torch.tensor([rank * L, owner_valid(n, world, rank)], dtype=torch.int64)
+        got = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(got, mine)
+        # blocks are contiguous, disjoint and cover [0, n) exactly once
+        pos = 0
+        for start, cnt in (t.tolist() for t in got):
+            if cnt:
+                ok &= start == pos
+                pos += cnt
+        ok &= pos == n
+    # every rank derives the identical layout / segment table
+    lay = lc.Layout({"z": (5, 3), "a": (7,), "m": (1,)})
+    seg = torch.tensor(lay.seg_start)
+    seg0 = seg.clone()
+    dist.broadcast(seg0, 0)
+    ok &= bool(torch.equal(seg, seg0))
+    q.put((rank, ok))
+    dist.destroy_process_group()
+
+
+def test_gloo_two_rank_partition_plan():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29700 + os.getpid() % 200
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res
+
+
+def test_bench_reference_arm_under_torchrun_two_ranks():
+    """--impl reference under torchrun: rank 0 alone prints the JSON line,
+    the other rank exits 0 without work (bench contract)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node=2", "--master-addr=127.0.0.1",
+           f"--master-port={29900 + os.getpid() % 90}", "bench.py", "--impl", "reference",
+           "--gpus", "2", "--steps", "2", "--warmup", "3", "--ref-sample", "65536"]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    import json
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "port" and d["e2e"]["h2d_bytes_per_step"] == 0
