@@ -217,8 +217,8 @@ k_encode(const float* __restrict__ g, float* __restrict__ m,
           st_stream(mp + k * 32, make_float4(mn[0], mn[1], mn[2], mn[3]));
           if constexpr (ENC == LC_ENC_F64) {
             double* o = reinterpret_cast<double*>(dst.p[j]) + boff + k * 128 + lane * 4;
-            __stcs(reinterpret_cast<double2*>(o), make_double2(c[0], c[1]));
-            __stcs(reinterpret_cast<double2*>(o + 2), make_double2(c[2], c[3]));
+            *reinterpret_cast<double2*>(o) = make_double2(c[0], c[1]);
+            *reinterpret_cast<double2*>(o + 2) = make_double2(c[2], c[3]);
           } else {
             stage_subtile<F>(&stage[wib][k * 4 * F], lane, st);
           }
@@ -296,14 +296,23 @@ k_apply_update(float* __restrict__ theta, int64_t n, Dst sb, Dst nzb, int64_t wp
   const int64_t nsup = (n + 1023) >> 10;
   const int64_t nwords = (n + 31) >> 5;
   float4* th4 = reinterpret_cast<float4*>(theta);
-  for (int64_t sidx = gw; sidx < nsup; sidx += nw) {
-    const int64_t w = sidx * 32 + lane;  // global word index of this lane
-    uint32_t myw = 0u, myz = ~0u;
-    if (w < nwords) {
+  // voted words of super-tile sidx (lane i: word i), fetched one super-tile
+  // ahead so a remote owner's NVLink latency overlaps the theta stream
+  auto fetch = [&](int64_t sidx, uint32_t& sw_, uint32_t& zw_) {
+    const int64_t w = sidx * 32 + lane;
+    sw_ = 0u;
+    zw_ = ~0u;
+    if (sidx < nsup && w < nwords) {
       const int j = (int)(w / wpb);
-      myw = __ldcs(reinterpret_cast<const uint32_t*>(sb.p[j]) + w);
-      if (NZ) myz = __ldcs(reinterpret_cast<const uint32_t*>(nzb.p[j]) + w);
+      sw_ = __ldcs(reinterpret_cast<const uint32_t*>(sb.p[j]) + w);
+      if (NZ) zw_ = __ldcs(reinterpret_cast<const uint32_t*>(nzb.p[j]) + w);
     }
+  };
+  uint32_t nxw, nxz;
+  fetch(gw, nxw, nxz);
+  for (int64_t sidx = gw; sidx < nsup; sidx += nw) {
+    const uint32_t myw = nxw, myz = nxz;
+    fetch(sidx + nw, nxw, nxz);
 #pragma unroll 1
     for (int k0 = 0; k0 < 8; k0 += KU) {
       float4 tv[KU];

@@ -129,14 +129,16 @@ namespace {
 using lc::Hyp;
 
 // Per-segment max|c| as uint64 bit patterns (non-negative doubles order as
-// unsigned integers).  Each CTA walks a contiguous element range so it meets
-// few segments; per-lane maxima are merged in shared memory first.
+// unsigned integers).  Each CTA walks a contiguous, 16-byte aligned element
+// range (so it meets few segments) with 128-bit loads, 4 quads per thread in
+// flight; per-lane maxima are merged in shared memory first.
 __global__ void __launch_bounds__(kThreads)
 k_l1_max(const float* __restrict__ g, const float* __restrict__ m,
          const uint8_t* __restrict__ mask, const int64_t* __restrict__ start,
          int nseg, int64_t n, int64_t per_cta, Hyp h,
          unsigned long long* __restrict__ gmax) {
   constexpr int kTab = 256;
+  constexpr int QU = 4;
   __shared__ unsigned long long tab[kTab];
   const int64_t lo = (int64_t)blockIdx.x * per_cta;
   if (lo >= n) return;
@@ -146,29 +148,55 @@ k_l1_max(const float* __restrict__ g, const float* __restrict__ m,
   const bool use_tab = (s_last - s_first) < kTab;
   for (int i = threadIdx.x; i < kTab; i += blockDim.x) tab[i] = 0ull;
   __syncthreads();
-  int seg = s_first;
-  int64_t seg_hi = start[seg + 1];
+  int seg = -1;
+  int64_t seg_lo = 1, seg_hi = 0;
   unsigned long long cur = 0ull;
-  auto flush = [&](int s, unsigned long long v) {
-    if (!v) return;
+  auto flush = [&]() {
+    if (seg < 0 || !cur) return;
     if (use_tab)
-      atomicMax(&tab[s - s_first], v);
+      atomicMax(&tab[seg - s_first], cur);
     else
-      atomicMax(&gmax[s], v);
+      atomicMax(&gmax[seg], cur);
   };
-  for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
-    if (e >= seg_hi) {
-      flush(seg, cur);
+  auto take = [&](int64_t e, float gv, float mv) {
+    if (e < seg_lo || e >= seg_hi) {
+      flush();
       cur = 0ull;
       seg = lc::seg_find(start, nseg, e);
+      seg_lo = start[seg];
       seg_hi = start[seg + 1];
     }
-    double c = lc::lion_c(m[e], g[e], h);
+    double c = lc::lion_c(mv, gv, h);
     if (mask && !mask[e]) c = 0.0;
     unsigned long long b = (unsigned long long)__double_as_longlong(fabs(c));
     cur = b > cur ? b : cur;
+  };
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  const float4* m4 = reinterpret_cast<const float4*>(m);
+  const int64_t q_lo = lo >> 2, q_hi = hi >> 2;  // full quads of this range
+  for (int64_t q0 = q_lo + threadIdx.x; q0 < q_hi; q0 += (int64_t)QU * blockDim.x) {
+    float4 gv[QU], mv[QU];
+#pragma unroll
+    for (int u = 0; u < QU; ++u) {
+      const int64_t q = q0 + (int64_t)u * blockDim.x;
+      if (q < q_hi) {
+        gv[u] = __ldcs(g4 + q);
+        mv[u] = __ldcs(m4 + q);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < QU; ++u) {
+      const int64_t q = q0 + (int64_t)u * blockDim.x;
+      if (q < q_hi) {
+        take(4 * q, gv[u].x, mv[u].x);
+        take(4 * q + 1, gv[u].y, mv[u].y);
+        take(4 * q + 2, gv[u].z, mv[u].z);
+        take(4 * q + 3, gv[u].w, mv[u].w);
+      }
+    }
   }
-  flush(seg, cur);
+  for (int64_t e = (q_hi << 2) + threadIdx.x; e < hi; e += blockDim.x) take(e, g[e], m[e]);
+  flush();
   __syncthreads();
   if (use_tab)
     for (int i = threadIdx.x; i <= s_last - s_first; i += blockDim.x)
@@ -216,16 +244,36 @@ k_l1_items(const float* __restrict__ g, const float* __restrict__ m,
       if (k == 0)
         for (int i = 0; i < sz; ++i) res = __dadd_rn(res, l1_v(g, m, mask, e0 + i, h, mx));
     } else {
-      const int full = sz - (sz % 8);
-      double r = l1_v(g, m, mask, e0 + k, h, mx);
-      for (int i = 8; i < full; i += 8) r = __dadd_rn(r, l1_v(g, m, mask, e0 + i + k, h, mx));
+      // lane k owns accumulator r_k over elements k, k+8, ... of the leaf's
+      // full 8-groups (<= 16 of them): issue every load first, then add in
+      // numpy's order
+      const int ngrp = sz >> 3;
+      float gv[16], mv[16];
+      bool keep[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (i < ngrp) {
+          gv[i] = __ldcs(g + e0 + 8 * i + k);
+          mv[i] = __ldcs(m + e0 + 8 * i + k);
+          keep[i] = mask ? mask[e0 + 8 * i + k] != 0 : true;
+        }
+      }
+      double r = 0.0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (i < ngrp) {
+          double c = keep[i] ? lc::lion_c(mv[i], gv[i], h) : 0.0;
+          const double v = __ddiv_rn(fabs(c), mx);
+          r = i == 0 ? v : __dadd_rn(r, v);
+        }
+      }
       // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)); IEEE addition is commutative
       r = __dadd_rn(r, __shfl_xor_sync(gm, r, 1));
       r = __dadd_rn(r, __shfl_xor_sync(gm, r, 2));
       r = __dadd_rn(r, __shfl_xor_sync(gm, r, 4));
       res = r;
       if (k == 0)
-        for (int i = full; i < sz; ++i) res = __dadd_rn(res, l1_v(g, m, mask, e0 + i, h, mx));
+        for (int i = ngrp * 8; i < sz; ++i) res = __dadd_rn(res, l1_v(g, m, mask, e0 + i, h, mx));
     }
     if (k == 0) slots[lf] = res;
   }
@@ -428,7 +476,7 @@ int lc_l1_scales(lc_l1_plan_t p, const float* g, const float* m, const uint8_t* 
   const int64_t n = p->n_total;
   int64_t nct = (int64_t)lc::sm_count() * 8;
   int64_t per = (n + nct - 1) / nct;
-  per = std::max<int64_t>(per, 4096);
+  per = std::max<int64_t>((per + 4095) / 4096 * 4096, 4096);  // 16-byte aligned ranges
   int grid = (int)((n + per - 1) / per);
   k_l1_max<<<grid, kThreads, 0, st>>>(g, m, mask, p->d_seg_start, p->nseg, n, per, h, p->d_max);
   LC_LAUNCH_CHECK();
