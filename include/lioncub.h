@@ -180,6 +180,11 @@ int lc_l1_plan_destroy(lc_l1_plan_t plan);
 int lc_l1_scales(lc_l1_plan_t plan, const float* g, const float* m,
                  const uint8_t* mask, const lc_hyper* h, int32_t qmax,
                  double* norms, double* scales, void* stream);
+/* Self-check of the reciprocal-based correctly rounded division the norm
+ * kernel uses for |c|/max (counts bit mismatches vs IEEE division over
+ * pairs with |a| clamped to b). */
+int lc_debug_div_check(const double* a, const double* b, int64_t n,
+                       uint64_t* mismatches, void* stream);
 
 /* ---- metrics / operator helpers ---- */
 /* c as float64 (metrics_out["c_local"], optimizer.py:209). */

@@ -73,6 +73,7 @@ SIGNATURES = {
     "lc_l1_plan_create": (INT, [P, P, I32]),
     "lc_l1_plan_destroy": (INT, [P]),
     "lc_l1_scales": (INT, [P, P, P, P, P, I32, P, P, P]),
+    "lc_debug_div_check": (INT, [P, P, I64, P, P]),
     "lc_compute_c": (INT, [P, P, P, I64, P, P, P]),
     "lc_count_bits_segmented": (INT, [P, P, I32, P, P]),
     "lc_bits_to_sign": (INT, [P, P, I64, P, P]),

@@ -203,15 +203,45 @@ k_l1_max(const float* __restrict__ g, const float* __restrict__ m,
       if (tab[i]) atomicMax(&gmax[s_first + i], tab[i]);
 }
 
+// a / b correctly rounded given y = RN(1/b): q = RN(a*y) is within one ulp
+// of a/b, the FMA residual a - b*q is exact, and one correction q + r*y
+// rounds to RN(a/b) (Markstein).  Valid for 0 <= a <= b with b normal and a
+// normal result; the (rare) subnormal results take __ddiv_rn.
+__device__ __forceinline__ double div_by(double a, double b, double y) {
+  const double q = __dmul_rn(a, y);
+  const double r = __fma_rn(-q, b, a);
+  const double q2 = __fma_rn(r, y, q);
+  if (q2 < 2.2250738585072014e-308 && a != 0.0) return __ddiv_rn(a, b);
+  return q2;
+}
+
+struct Recip {
+  double b, y;
+  bool fast;
+  __device__ __forceinline__ double operator()(double a) const {
+    return fast ? div_by(a, b, y) : __ddiv_rn(a, b);
+  }
+};
+
+__device__ __forceinline__ Recip make_recip(double mx) {
+  Recip r;
+  r.b = mx;
+  r.y = __drcp_rn(mx);
+  r.fast = mx >= 1e-300 && mx < 1e300;
+  return r;
+}
+
+template <bool MASK>
 __device__ __forceinline__ double l1_v(const float* g, const float* m, const uint8_t* mask,
-                                       int64_t e, const Hyp& h, double mx) {
+                                       int64_t e, const Hyp& h, const Recip& dv) {
   double c = lc::lion_c(m[e], g[e], h);
-  if (mask && !mask[e]) c = 0.0;
-  return __ddiv_rn(fabs(c), mx);  // (a / m) ** 1.0 == a / m
+  if (MASK && !mask[e]) c = 0.0;
+  return dv(fabs(c));  // (a / m) ** 1.0 == a / m
 }
 
 // One CTA per work item: leaves with 8 lanes each, then templated additions.
-__global__ void __launch_bounds__(kThreads)
+template <bool MASK>
+__global__ void __launch_bounds__(kThreads, 4)
 k_l1_items(const float* __restrict__ g, const float* __restrict__ m,
            const uint8_t* __restrict__ mask, Hyp h,
            const unsigned long long* __restrict__ gmax,
@@ -229,6 +259,7 @@ k_l1_items(const float* __restrict__ g, const float* __restrict__ m,
     if (threadIdx.x == 0) nodes[node] = 0.0;
     return;
   }
+  const Recip dv = make_recip(mx);
   const int lane = threadIdx.x & 31;
   const int k = lane & 7;
   const int group = threadIdx.x >> 3;
@@ -242,28 +273,29 @@ k_l1_items(const float* __restrict__ g, const float* __restrict__ m,
     if (sz < 8) {  // only a whole tiny layer: sequential from 0
       res = 0.0;
       if (k == 0)
-        for (int i = 0; i < sz; ++i) res = __dadd_rn(res, l1_v(g, m, mask, e0 + i, h, mx));
+        for (int i = 0; i < sz; ++i) res = __dadd_rn(res, l1_v<MASK>(g, m, mask, e0 + i, h, dv));
     } else {
       // lane k owns accumulator r_k over elements k, k+8, ... of the leaf's
       // full 8-groups (<= 16 of them): issue every load first, then add in
       // numpy's order
       const int ngrp = sz >> 3;
       float gv[16], mv[16];
-      bool keep[16];
+      uint32_t keep = 0xffffu;
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         if (i < ngrp) {
           gv[i] = __ldcs(g + e0 + 8 * i + k);
           mv[i] = __ldcs(m + e0 + 8 * i + k);
-          keep[i] = mask ? mask[e0 + 8 * i + k] != 0 : true;
+          if (MASK && !mask[e0 + 8 * i + k]) keep &= ~(1u << i);
         }
       }
       double r = 0.0;
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         if (i < ngrp) {
-          double c = keep[i] ? lc::lion_c(mv[i], gv[i], h) : 0.0;
-          const double v = __ddiv_rn(fabs(c), mx);
+          double c = lc::lion_c(mv[i], gv[i], h);
+          if (MASK && !((keep >> i) & 1u)) c = 0.0;
+          const double v = dv(fabs(c));
           r = i == 0 ? v : __dadd_rn(r, v);
         }
       }
@@ -273,7 +305,7 @@ k_l1_items(const float* __restrict__ g, const float* __restrict__ m,
       r = __dadd_rn(r, __shfl_xor_sync(gm, r, 4));
       res = r;
       if (k == 0)
-        for (int i = ngrp * 8; i < sz; ++i) res = __dadd_rn(res, l1_v(g, m, mask, e0 + i, h, mx));
+        for (int i = ngrp * 8; i < sz; ++i) res = __dadd_rn(res, l1_v<MASK>(g, m, mask, e0 + i, h, dv));
     }
     if (k == 0) slots[lf] = res;
   }
@@ -287,6 +319,17 @@ k_l1_items(const float* __restrict__ g, const float* __restrict__ m,
     __syncthreads();
   }
   if (threadIdx.x == 0) nodes[node] = slots[T.root];
+}
+
+__global__ void k_div_check(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
+                            unsigned long long* __restrict__ bad) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const Recip dv = make_recip(b[i]);
+    const double x = fabs(a[i]) <= b[i] ? fabs(a[i]) : b[i];
+    if (__double_as_longlong(dv(x)) != __double_as_longlong(__ddiv_rn(x, b[i])))
+      atomicAdd(bad, 1ull);
+  }
 }
 
 // One CTA per layer: additions above the work items, then M1 and the scale.
@@ -481,14 +524,26 @@ int lc_l1_scales(lc_l1_plan_t p, const float* g, const float* m, const uint8_t* 
   k_l1_max<<<grid, kThreads, 0, st>>>(g, m, mask, p->d_seg_start, p->nseg, n, per, h, p->d_max);
   LC_LAUNCH_CHECK();
   size_t smem = sizeof(double) * std::max(1, p->max_slots);
+  auto items = mask ? k_l1_items<true> : k_l1_items<false>;
   if (smem > 48 * 1024)
-    LC_CUDA_TRY(cudaFuncSetAttribute(k_l1_items, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_l1_items<<<p->n_items, kThreads, smem, st>>>(g, m, mask, h, p->d_max, p->d_wi_off, p->d_wi_meta,
-                                                 p->d_tmpl, p->d_leaf_rel, p->d_leaf_size, p->d_tops,
-                                                 p->d_tlvl, p->d_nodes);
+    LC_CUDA_TRY(cudaFuncSetAttribute(items, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  items<<<p->n_items, kThreads, smem, st>>>(g, m, mask, h, p->d_max, p->d_wi_off, p->d_wi_meta,
+                                            p->d_tmpl, p->d_leaf_rel, p->d_leaf_size, p->d_tops,
+                                            p->d_tlvl, p->d_nodes);
   LC_LAUNCH_CHECK();
   k_l1_upper<<<p->nseg, kThreads, 0, st>>>(p->d_seg, p->d_uops, p->d_ulvl, p->d_max, p->d_nodes,
                                            qmax, norms, scales);
+  LC_LAUNCH_CHECK();
+  return LC_OK;
+}
+
+int lc_debug_div_check(const double* a, const double* b, int64_t n, uint64_t* mismatches,
+                       void* stream) {
+  if (n < 0 || !a || !b || !mismatches) return lc::set_err(LC_E_ARG, "lc_debug_div_check: bad arguments");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  LC_CUDA_TRY(cudaMemsetAsync(mismatches, 0, sizeof(uint64_t), st));
+  if (n == 0) return LC_OK;
+  k_div_check<<<lc::sm_count() * 8, 256, 0, st>>>(a, b, n, reinterpret_cast<unsigned long long*>(mismatches));
   LC_LAUNCH_CHECK();
   return LC_OK;
 }

@@ -71,6 +71,22 @@ def main():
         "lc_fused_local_step", th.data_ptr(), m.data_ptr(), g.data_ptr(), None, n,
         C.byref(hyp), 1, _lib.LC_LOCAL_BINARY, None, None, None, None, flags.data_ptr(), s),
         20 * n)
+    # per-layer numpy-exact L1 norm on the GPT-2-small layout (148 layers)
+    sys.path.insert(0, ROOT)
+    from bench import gpt2_small_layout
+    import paper_2411_16462_b200 as lc
+    lay = lc.Layout(gpt2_small_layout())
+    nl = lay.n
+    gl = torch.randn(nl, device=dev)
+    ml = torch.randn(nl, device=dev) * 0.1
+    arr = (C.c_int64 * len(lay.seg_start))(*lay.seg_start)
+    plan = C.c_void_p()
+    _lib.check(_lib.load().lc_l1_plan_create(C.byref(plan), arr, len(lay.names)))
+    norms = torch.zeros(len(lay.names), dtype=torch.float64, device=dev)
+    scales = torch.zeros_like(norms)
+    timed("l1_scales_gpt2", lambda: _lib.call(
+        "lc_l1_scales", plan.value, gl.data_ptr(), ml.data_ptr(), None, C.byref(hyp), 15,
+        norms.data_ptr(), scales.data_ptr(), s), 16 * nl)
     print(json.dumps(res))
 
 

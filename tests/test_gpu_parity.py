@@ -329,3 +329,51 @@ def test_cpu_tensors_fail_loudly():
     topo = lc.Topology(1, 0, lc.LocalTransport(1))
     with pytest.raises(lc.ConfigError):
         lc.distributed_lion_step(st, {"w": torch.zeros(3)}, h, None, topo, "compressed1bit")
+
+
+def test_reciprocal_division_is_correctly_rounded():
+    """The norm kernel divides |c| by the layer max with a precomputed
+    reciprocal + one FMA correction; it must equal IEEE division bitwise."""
+    rng = np.random.default_rng(11)
+    n = 20_000_000
+    b = np.exp(rng.uniform(-700, 700, size=n)) * rng.choice([1.0, 3.0, 7.0], size=n)
+    a = b * rng.uniform(0.0, 1.0, size=n)
+    a[::7] = b[::7] * (1.0 - 2.0 ** -52)          # adversarial: just below b
+    a[::11] = np.nextafter(b[::11], 0.0)
+    a[::13] = b[::13]
+    a[::17] = 0.0
+    da, db = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    _lib.call("lc_debug_div_check", da.data_ptr(), db.data_ptr(), n, bad.data_ptr(), 0)
+    assert int(bad.item()) == 0
+
+
+@pytest.mark.parametrize("sizes", [
+    {"a": (1_000_003,), "b": (7,), "c": (3_000_000,), "d": (8191,), "e": (8193,), "f": (129,)},
+    {"w": (4_194_305,)},
+])
+def test_l1_norms_bit_exact_large(sizes):
+    """Per-layer numpy L1 norms (np.mean pairwise order) on multi-million
+    element layers with outliers, and the quantized ints."""
+    ranks = O.synth_rank_inputs(9, 1, sizes, "outliers")
+    names = sorted(sizes)
+    starts = [0]
+    for k in names:
+        starts.append(starts[-1] + int(np.prod(sizes[k])))
+    g = np.concatenate([ranks[0]["g"][k] for k in names])
+    m = np.concatenate([ranks[0]["m"][k] for k in names])
+    c = 0.9 * m.astype(np.float64) + (1.0 - 0.9) * g.astype(np.float64)
+    ref = [O.lp_mean_norm_l1(c[starts[i]:starts[i + 1]]) for i in range(len(names))]
+    arr = (C.c_int64 * len(starts))(*starts)
+    plan = C.c_void_p()
+    _lib.check(_lib.load().lc_l1_plan_create(C.byref(plan), arr, len(names)))
+    try:
+        gt, mt = torch.from_numpy(g).cuda(), torch.from_numpy(m).cuda()
+        norms = torch.zeros(len(names), dtype=torch.float64, device="cuda")
+        scales = torch.zeros_like(norms)
+        hyp = _hyper()
+        _lib.call("lc_l1_scales", plan.value, gt.data_ptr(), mt.data_ptr(), None, C.byref(hyp),
+                  127, norms.data_ptr(), scales.data_ptr(), 0)
+        assert norms.cpu().numpy().tolist() == ref
+    finally:
+        _lib.load().lc_l1_plan_destroy(plan.value)
