@@ -14,7 +14,7 @@ import threading
 from .errors import (CapacityError, CollectiveError, ConfigError, DeviceError)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "liblioncub.so")
+LIB_PATH = os.environ.get("LIONCUB_LIB") or os.path.join(HERE, "_lib", "liblioncub.so")
 
 LC_OK = 0
 LC_E_CONFIG = -1

@@ -162,13 +162,20 @@ __device__ __forceinline__ void stage_subtile(uint32_t* sw, int lane, const uint
   }
 }
 
+#ifndef LC_ENC_KU
+#define LC_ENC_KU 4
+#endif
+#ifndef LC_ENC_MINB
+#define LC_ENC_MINB 2
+#endif
+
 template <int ENC, int F, bool MASK>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, LC_ENC_MINB)
 k_encode(const float* __restrict__ g, float* __restrict__ m,
          const uint8_t* __restrict__ mask, int64_t n, Hyp h, int fill, SegQ sq,
          Dst dst, int64_t L, uint32_t* __restrict__ flags) {
   constexpr int WPS = (ENC == LC_ENC_F64) ? 1 : 32 * F;  // words per super-tile
-  constexpr int KU = 4;  // sub-tiles whose loads are in flight together
+  constexpr int KU = LC_ENC_KU;  // sub-tiles whose loads are in flight together
   __shared__ __align__(16) uint32_t stage[8][WPS];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
