@@ -293,7 +293,7 @@ class _Workspace:
             self.nz = sym("nz", P * cw) if ternary else None
             self.ties = sym("ties", P * cw) if metrics else None
             self.dst = _lib.table([self.recv.peers[j] + r * blk_bytes for j in range(P)])
-            if metrics or os.environ.get("LIONCUB_VOTE_PUSH") == "1":
+            if metrics or os.environ.get("LIONCUB_VOTE_PUSH", "1") == "1":
                 # metrics need every block locally: owners push to all ranks
                 outs = lambda b: None if b is None else _lib.table(  # noqa: E731
                     [b.peers[j] + r * cw * 4 for j in range(P)])
