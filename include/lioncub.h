@@ -63,6 +63,24 @@ typedef struct lc_hyper {
   double weight_decay;
 } lc_hyper;
 
+/* In-kernel cross-GPU barrier (peer-memory exchange).  A kernel given a
+ * sync with wait_epoch != 0 first waits (one thread per peer polling with
+ * ld.acquire.sys, timeout -> LC_FLAG_BARRIER_TIMEOUT in *err) until every
+ * peer published wait_epoch into my_flags; a kernel given arrive_epoch != 0
+ * publishes it into every peer's flag slot `rank` after its last CTA
+ * finished (per-CTA fence + atomic counter, st.release.sys).  This replaces
+ * a separate barrier launch between K1 -> vote -> K5.  NULL = no sync. */
+typedef struct lc_sync {
+  void* peer_flags[32]; /* rank j's uint64[P] flag array, mapped here     */
+  uint64_t* my_flags;   /* this rank's flag array                          */
+  uint32_t* counter;    /* zeroed device word, one per arrive site         */
+  uint32_t* err;
+  uint64_t wait_epoch;
+  uint64_t arrive_epoch;
+  int32_t P, rank;
+  double timeout_s;
+} lc_sync;
+
 /* Per-layer segment table of a flat buffer (layers in sorted-name order). */
 typedef struct lc_segments {
   const int64_t* start; /* device, nseg+1 offsets (elements)               */
@@ -95,7 +113,7 @@ int lc_device_sm_count(int device);
 int lc_encode(const float* g, float* m, const uint8_t* mask, int64_t n,
               const lc_hyper* h, int fill, int enc, int field_bits,
               const lc_segments* segs, void* const* dst, int32_t nblocks,
-              int64_t L, uint32_t* flags, void* stream);
+              int64_t L, uint32_t* flags, const lc_sync* sync, void* stream);
 
 /* Output tables of the owner-side vote kernels: voted/nz/tie_bits are host
  * arrays of `nout` word pointers; the owner's block is written to every one
@@ -113,7 +131,7 @@ int lc_encode(const float* g, float* m, const uint8_t* mask, int64_t n,
 int lc_vote_bits(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid,
                  int fill, int sum_mode, void* const* voted, void* const* nz,
                  void* const* tie_bits, int32_t nout, uint32_t* flags,
-                 void* stream);
+                 const lc_sync* sync, void* stream);
 
 /* ---- K6: owner-side p-bit sums -> signed aggregate -> 1-bit vote ----
  * Replaces collectives.py:241-249 (de-offset, ties) + :313-316
@@ -126,7 +144,7 @@ int lc_fields_vote(const uint32_t* sums, int32_t rows, int64_t row_stride,
                    int64_t n, int32_t field_bits, int32_t P, int32_t offset,
                    int32_t binary, int fill, void* const* voted, void* const* nz,
                    void* const* tie_bits, int32_t nout, int64_t* values,
-                   void* stream);
+                   const lc_sync* sync, void* stream);
 
 /* ---- full-precision arm: P float64 rows (row stride `stride`) -> sum of
  * the first `len` elements in the reference's rank order (flat,
@@ -135,7 +153,7 @@ int lc_fields_vote(const uint32_t* sums, int32_t rows, int64_t row_stride,
 int lc_f64_sum_vote(const double* recv, int32_t P, int64_t len, int64_t stride,
                     int tree, int fill, void* const* voted, void* const* nz,
                     void* const* tie_bits, int32_t nout, double* values,
-                    void* stream);
+                    const lc_sync* sync, void* stream);
 
 /* ---- K5: theta' = theta - eta*(s + wd*theta)  (optimizer.py:204) ----
  * s = +1/-1 from the voted sign bits; 0 where nz_bits has a 0 bit.
@@ -145,7 +163,7 @@ int lc_f64_sum_vote(const double* recv, int32_t P, int64_t len, int64_t stride,
  * owner's vote output over NVLink (the allgather pulled inside K5). */
 int lc_apply_update(float* theta, int64_t n, void* const* sign_bits,
                     void* const* nz_bits, int32_t nsrc, int64_t wpb, double lr,
-                    double weight_decay, void* stream);
+                    double weight_decay, const lc_sync* sync, void* stream);
 
 /* ---- one-pass step for P == 1 (no exchange: the vote of one rank is its
  * own aggregate): reads theta,m,g, writes theta',m' (20 B/param).

@@ -164,7 +164,7 @@ def compressed_allreduce_1bit(c_i, topo: Topology, policy: SignPolicy) -> VoteRe
         ties = _words(P * cw, dev)
         _lib.call("lc_vote_bits", recv.data_ptr(), P, cw, owner_valid(n, P, r), fill, 0,
                   _lib.table([_off(full, r * cw)]), None, _lib.table([_off(ties, r * cw)]), 1,
-                  flags.data_ptr(), s)
+                  flags.data_ptr(), None, s)
         if fill == 0 and _flags_check(flags, topo, gen) & _lib.LC_FLAG_TIE_TERNARY:
             raise ConfigError("1-bit path cannot carry exact zeros; use the alternating policy")
         if P > 1:
@@ -219,7 +219,7 @@ def direct_allreduce(q_i, topo: Topology, q_max: int, lane_bits: int | None = No
         voted, ties = _words(nw, dev), _words(nw, dev)
         _lib.call("lc_fields_vote", full.data_ptr(), 1, 0, n, F, P, offset, int(binary_signs),
                   1, _lib.table([voted.data_ptr()]), None, _lib.table([ties.data_ptr()]), 1,
-                  None, s)
+                  None, None, s)
         bound = P if binary_signs else P * q_max
         return VoteResult(values=values, range=(-float(bound), float(bound)),
                           ties=count_bits(ties, n, st))
@@ -248,7 +248,7 @@ def ps_gather_broadcast(c_i, topo: Topology, efficient: bool = False) -> VoteRes
         voted, ties = _words(P * nw, dev), _words(P * nw, dev)
         _lib.call("lc_f64_sum_vote", recv.data_ptr(), P, owner_valid(n, P, r), L,
                   int(efficient), 1, _lib.table([_off(voted, r * nw)]), None,
-                  _lib.table([_off(ties, r * nw)]), 1, _off(vals, r * L), s)
+                  _lib.table([_off(ties, r * nw)]), 1, _off(vals, r * L), None, s)
         if P > 1:
             topo.transport.allgather(r, gen, vals[r * L:], vals, L * 8)
             topo.transport.allgather(r, gen, ties[r * nw:], ties, nw * 4)

@@ -103,4 +103,75 @@ __device__ __forceinline__ int seg_find(const int64_t* __restrict__ start,
   return lo;
 }
 
+// Device view of lc_sync (kernel parameter, by value).
+struct SyncD {
+  uint64_t* peer[32];
+  uint64_t* mine;
+  uint32_t* counter;
+  uint32_t* err;
+  unsigned long long wait_epoch, arrive_epoch, timeout_ns;
+  int P, rank;
+};
+
+inline SyncD to_syncd(const lc_sync* s) {
+  SyncD d{};
+  if (!s) return d;
+  for (int j = 0; j < 32; ++j) d.peer[j] = reinterpret_cast<uint64_t*>(s->peer_flags[j]);
+  d.mine = s->my_flags;
+  d.counter = s->counter;
+  d.err = s->err;
+  d.wait_epoch = s->wait_epoch;
+  d.arrive_epoch = s->arrive_epoch;
+  d.timeout_ns = (unsigned long long)(s->timeout_s * 1e9);
+  d.P = s->P;
+  d.rank = s->rank;
+  return d;
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Every CTA: wait until all P peers published s.wait_epoch (acquire).
+__device__ __forceinline__ void sync_wait(const SyncD& s) {
+  if (!s.wait_epoch) return;
+  const int j = threadIdx.x;
+  if (j < s.P) {
+    const unsigned long long t0 = globaltimer();
+    while (true) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(s.mine + j) : "memory");
+      if (v >= s.wait_epoch) break;
+      if (globaltimer() - t0 > s.timeout_ns) {
+        atomicOr(s.err, (uint32_t)LC_FLAG_BARRIER_TIMEOUT);
+        break;
+      }
+      __nanosleep(32);
+    }
+  }
+  __syncthreads();
+}
+
+// End of a kernel: the last CTA to finish publishes s.arrive_epoch to every
+// peer (each CTA fences its stores -- local and peer -- before counting).
+__device__ __forceinline__ void sync_arrive(const SyncD& s) {
+  if (!s.arrive_epoch) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const unsigned prev = atomicAdd(s.counter, 1u);
+    if (prev == gridDim.x - 1) {
+      *s.counter = 0u;  // ready for the next launch of this site
+      __threadfence_system();
+      for (int j = 0; j < s.P; ++j) {
+        uint64_t* slot = s.peer[j] + s.rank;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(slot), "l"(s.arrive_epoch)
+                     : "memory");
+      }
+    }
+  }
+}
+
 }  // namespace lc

@@ -173,7 +173,7 @@ template <int ENC, int F, bool MASK>
 __global__ void __launch_bounds__(256, LC_ENC_MINB)
 k_encode(const float* __restrict__ g, float* __restrict__ m,
          const uint8_t* __restrict__ mask, int64_t n, Hyp h, int fill, SegQ sq,
-         Dst dst, int64_t L, uint32_t* __restrict__ flags) {
+         Dst dst, int64_t L, uint32_t* __restrict__ flags, SyncD sy) {
   constexpr int WPS = (ENC == LC_ENC_F64) ? 1 : 32 * F;  // words per super-tile
   constexpr int KU = LC_ENC_KU;  // sub-tiles whose loads are in flight together
   __shared__ __align__(16) uint32_t stage[8][WPS];
@@ -282,6 +282,7 @@ k_encode(const float* __restrict__ g, float* __restrict__ m,
     }
   }
   if (flag) atomicOr(flags, flag);
+  sync_arrive(sy);
 }
 
 // ---------------------------------------------------------------------------
@@ -295,8 +296,9 @@ k_encode(const float* __restrict__ g, float* __restrict__ m,
 template <bool NZ>
 __global__ void __launch_bounds__(256, 3)
 k_apply_update(float* __restrict__ theta, int64_t n, Dst sb, Dst nzb, int64_t wpb,
-               double lr, double wd) {
+               double lr, double wd, SyncD sy) {
   constexpr int KU = 4;
+  sync_wait(sy);
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -527,7 +529,8 @@ __device__ __forceinline__ void vote_word(uint32_t planes[NP], int P, int T, uin
 template <int NP>
 __global__ void __launch_bounds__(256)
 k_vote_bits(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_valid,
-            int fill, int sum_mode, VoteOut out, uint32_t* __restrict__ flags) {
+            int fill, int sum_mode, VoteOut out, uint32_t* __restrict__ flags, SyncD sy) {
+  sync_wait(sy);
   const int T = P >> 1;
   const uint32_t fillmask = fill > 0 ? ~0u : 0u;
   uint32_t flag = 0;
@@ -564,6 +567,7 @@ k_vote_bits(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_vali
                make_uint4(nz[0], nz[1], nz[2], nz[3]), make_uint4(tie[0], tie[1], tie[2], tie[3]));
   }
   if (flag) atomicOr(flags, flag);
+  sync_arrive(sy);
 }
 
 // ---------------------------------------------------------------------------
@@ -576,7 +580,8 @@ template <int F>
 __global__ void __launch_bounds__(256)
 k_fields_vote(const uint32_t* __restrict__ sums, int rows, int64_t row_stride, int64_t n,
               int P, int offset, int binary, int fill, VoteOut out,
-              int64_t* __restrict__ values) {
+              int64_t* __restrict__ values, SyncD sy) {
+  sync_wait(sy);
   constexpr int E = 32 / F;
   constexpr uint32_t FM = (F == 32) ? 0xffffffffu : ((1u << F) - 1u);
   const int lane = threadIdx.x & 31;
@@ -625,6 +630,7 @@ k_fields_vote(const uint32_t* __restrict__ sums, int rows, int64_t row_stride, i
       }
     }
   }
+  sync_arrive(sy);
 }
 
 // ---------------------------------------------------------------------------
@@ -632,7 +638,8 @@ k_fields_vote(const uint32_t* __restrict__ sums, int rows, int64_t row_stride, i
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256)
 k_f64_sum_vote(const double* __restrict__ recv, int P, int64_t len, int64_t stride, int tree,
-               int fill, VoteOut out, double* __restrict__ values) {
+               int fill, VoteOut out, double* __restrict__ values, SyncD sy) {
+  sync_wait(sy);
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -663,6 +670,7 @@ k_f64_sum_vote(const double* __restrict__ recv, int P, int64_t len, int64_t stri
       if (out.tie.p[0]) reinterpret_cast<uint32_t*>(out.tie.p[lane])[w] = zb;
     }
   }
+  sync_arrive(sy);
 }
 
 // K7: momentum mean, float64 accumulation in rank order, one fp32 rounding.
@@ -848,6 +856,8 @@ int generic_grid(int64_t n) {
   return b < 1 ? 1 : (int)b;
 }
 
+thread_local SyncD g_sync{};  // sync of the encode launch being dispatched
+
 template <int ENC, int F, bool MASK>
 int launch_encode(const float* g, float* m, const uint8_t* mask, int64_t n, Hyp h,
                   int fill, SegQ sq, const Dst& dst, int64_t L, uint32_t* flags,
@@ -855,7 +865,7 @@ int launch_encode(const float* g, float* m, const uint8_t* mask, int64_t n, Hyp 
   auto kern = k_encode<ENC, F, MASK>;
   int64_t nsup = (n + 1023) >> 10;
   int grid = stream_grid(kern, kBlock, nsup, kBlock / 32);
-  kern<<<grid, kBlock, 0, st>>>(g, m, mask, n, h, fill, sq, dst, L, flags);
+  kern<<<grid, kBlock, 0, st>>>(g, m, mask, n, h, fill, sq, dst, L, flags, g_sync);
   LC_LAUNCH_CHECK();
   return LC_OK;
 }
@@ -910,7 +920,7 @@ int lc_device_sm_count(int device) {
 int lc_encode(const float* g, float* m, const uint8_t* mask, int64_t n,
               const lc_hyper* hp, int fill, int enc, int field_bits,
               const lc_segments* segs, void* const* dst, int32_t nblocks, int64_t L,
-              uint32_t* flags, void* stream) {
+              uint32_t* flags, const lc_sync* sync, void* stream) {
   if (n < 0 || !hp || !flags) return set_err(LC_E_ARG, "lc_encode: bad arguments");
   if (n == 0) return LC_OK;
   if (!g || !m) return set_err(LC_E_ARG, "lc_encode: null pointer");
@@ -922,6 +932,7 @@ int lc_encode(const float* g, float* m, const uint8_t* mask, int64_t n,
   Hyp h = to_hyp(hp);
   SegQ sq = to_segq(segs);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  g_sync = to_syncd(sync);
   switch (enc) {
     case LC_ENC_SIGN1:
       return dispatch_mask<LC_ENC_SIGN1, 1>(g, m, mask, n, h, fill, sq, d, L, flags, st);
@@ -940,7 +951,8 @@ int lc_encode(const float* g, float* m, const uint8_t* mask, int64_t n,
 }
 
 int lc_apply_update(float* theta, int64_t n, void* const* sign_bits, void* const* nz_bits,
-                    int32_t nsrc, int64_t wpb, double lr, double wd, void* stream) {
+                    int32_t nsrc, int64_t wpb, double lr, double wd, const lc_sync* sync,
+                    void* stream) {
   if (n < 0) return set_err(LC_E_ARG, "lc_apply_update: n < 0");
   if (n == 0) return LC_OK;
   Dst sb, zb;
@@ -954,11 +966,11 @@ int lc_apply_update(float* theta, int64_t n, void* const* sign_bits, void* const
   if (nz_bits) {
     auto kern = k_apply_update<true>;
     int grid = stream_grid(kern, kBlock, nsup, kBlock / 32);
-    kern<<<grid, kBlock, 0, st>>>(theta, n, sb, zb, wpb, lr, wd);
+    kern<<<grid, kBlock, 0, st>>>(theta, n, sb, zb, wpb, lr, wd, to_syncd(sync));
   } else {
     auto kern = k_apply_update<false>;
     int grid = stream_grid(kern, kBlock, nsup, kBlock / 32);
-    kern<<<grid, kBlock, 0, st>>>(theta, n, sb, sb, wpb, lr, wd);
+    kern<<<grid, kBlock, 0, st>>>(theta, n, sb, sb, wpb, lr, wd, to_syncd(sync));
   }
   LC_LAUNCH_CHECK();
   return LC_OK;
@@ -1022,7 +1034,7 @@ bool make_out(VoteOut& o, void* const* v, void* const* nz, void* const* tie, int
 
 int lc_vote_bits(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid, int fill,
                  int sum_mode, void* const* voted, void* const* nz, void* const* tie_bits,
-                 int32_t nout, uint32_t* flags, void* stream) {
+                 int32_t nout, uint32_t* flags, const lc_sync* sync, void* stream) {
   if (P < 1 || P > 255 || cw < 0 || (cw % 4) != 0 || !flags)
     return set_err(LC_E_ARG, "lc_vote_bits: P must be in [1,255], cw a multiple of 4");
   if (cw == 0) return LC_OK;
@@ -1031,7 +1043,8 @@ int lc_vote_bits(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid, i
     return set_err(LC_E_ARG, "lc_vote_bits: bad pointers / output table");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int grid = generic_grid(cw / 4);
-#define LC_VOTE(NP) k_vote_bits<NP><<<grid, kBlock, 0, st>>>(recv, P, cw, n_valid, fill, sum_mode, o, flags)
+  const SyncD sy = to_syncd(sync);
+#define LC_VOTE(NP) k_vote_bits<NP><<<grid, kBlock, 0, st>>>(recv, P, cw, n_valid, fill, sum_mode, o, flags, sy)
   if (P <= 1) LC_VOTE(1);
   else if (P <= 3) LC_VOTE(2);
   else if (P <= 7) LC_VOTE(3);
@@ -1048,7 +1061,7 @@ int lc_vote_bits(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid, i
 int lc_fields_vote(const uint32_t* sums, int32_t rows, int64_t row_stride, int64_t n,
                    int32_t F, int32_t P, int32_t offset, int32_t binary, int fill,
                    void* const* voted, void* const* nz, void* const* tie_bits, int32_t nout,
-                   int64_t* values, void* stream) {
+                   int64_t* values, const lc_sync* sync, void* stream) {
   if (n < 0 || P < 1 || rows < 1) return set_err(LC_E_ARG, "lc_fields_vote: bad arguments");
   if (n == 0) return LC_OK;
   VoteOut o;
@@ -1057,7 +1070,8 @@ int lc_fields_vote(const uint32_t* sums, int32_t rows, int64_t row_stride, int64
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int64_t nin = (n * F + 31) / 32;
   int grid = generic_grid(nin);
-#define LC_FV(FF) k_fields_vote<FF><<<grid, kBlock, 0, st>>>(sums, rows, row_stride, n, P, offset, binary, fill, o, values)
+  const SyncD sy = to_syncd(sync);
+#define LC_FV(FF) k_fields_vote<FF><<<grid, kBlock, 0, st>>>(sums, rows, row_stride, n, P, offset, binary, fill, o, values, sy)
   switch (F) {
     case 1: LC_FV(1); break;
     case 2: LC_FV(2); break;
@@ -1074,7 +1088,7 @@ int lc_fields_vote(const uint32_t* sums, int32_t rows, int64_t row_stride, int64
 
 int lc_f64_sum_vote(const double* recv, int32_t P, int64_t len, int64_t stride, int tree, int fill,
                     void* const* voted, void* const* nz, void* const* tie_bits, int32_t nout,
-                    double* values, void* stream) {
+                    double* values, const lc_sync* sync, void* stream) {
   if (len < 0 || P < 1 || (tree && P > 64) || nout > 32)
     return set_err(LC_E_ARG, "lc_f64_sum_vote: bad arguments");
   if (len == 0) return LC_OK;
@@ -1083,7 +1097,8 @@ int lc_f64_sum_vote(const double* recv, int32_t P, int64_t len, int64_t stride, 
     return set_err(LC_E_ARG, "lc_f64_sum_vote: bad pointers / output table");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int grid = generic_grid(len);
-  k_f64_sum_vote<<<grid, kBlock, 0, st>>>(recv, P, len, stride, tree, fill, o, values);
+  k_f64_sum_vote<<<grid, kBlock, 0, st>>>(recv, P, len, stride, tree, fill, o, values,
+                                          to_syncd(sync));
   LC_LAUNCH_CHECK();
   return LC_OK;
 }

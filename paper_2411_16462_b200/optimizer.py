@@ -273,6 +273,8 @@ class _Workspace:
         self.p2p = p2p = P > 1 and tp.p2p
         z = lambda k, dt=torch.int32: torch.zeros(max(k, 1), dtype=dt, device=dev)  # noqa
         self.flags = z(1)
+        self.counters = z(4)   # arrive counters of the in-kernel barriers
+        self.k5_sync = None
         self.l1 = None
         self.norms = self.scales = None
         if kind == "f64":
@@ -504,7 +506,7 @@ def distributed_lion_step(state: WorkerState, grad_i, h: LionHyper,
                                         n, g, m, mflat, hyp, segs, s,
                                         tree=algo == "ps_efficient")
                 _lib.call("lc_apply_update", th.flat.data_ptr(), n, ws.src, ws.nzsrc,
-                          ws.nsrc, ws.wpb, eta, wd, s)
+                          ws.nsrc, ws.wpb, eta, wd, ws.k5_sync, s)
             if metrics:
                 _fill_metrics(metrics_out, layout, dev, ws, nz, c_local, s)
     return WorkerState(params=th, momentum=m, iteration=t)
@@ -531,7 +533,7 @@ def _ternary_precheck(topo, gen, g, m, mflat, n, hyp, dev, s, kind):
             topo.transport.alltoall(r, gen, words, recv, cw * 4)
         voted = torch.zeros(cw, dtype=torch.int32, device=dev)
         _lib.call("lc_vote_bits", recv.data_ptr(), P, cw, owner_valid(n, P, r), 0, 0,
-                  _lib.table([voted.data_ptr()]), None, None, 1, flags.data_ptr(), s)
+                  _lib.table([voted.data_ptr()]), None, None, 1, flags.data_ptr(), None, s)
     if topo.world_size > 1:
         topo.transport.allreduce_max_u32(topo.rank, gen, flags)
     _raise_flags(int(flags.item()), binary=kind == "1bit")
@@ -551,12 +553,23 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
         enc, fb = (_lib.LC_ENC_SIGN_FIELDS if binary else _lib.LC_ENC_QUANT_FIELDS), F
     else:
         enc, fb = _lib.LC_ENC_F64, 64
+    fused = ws.p2p and tp.fused_barriers
+    sy1 = sy2 = sy3 = None
+    if fused:
+        # the barriers live inside the kernels: K1's last CTA publishes e1,
+        # the vote waits for e1 and publishes e2, K5 waits for e2
+        e1, e2 = tp.take_epochs(r, 2)
+        sy1 = C.byref(tp.sync_struct(r, ws.counters[0:1], 0, e1))
+        sy2 = C.byref(tp.sync_struct(r, ws.counters[1:2], e1, e2))
+        sy3 = C.byref(tp.sync_struct(r, ws.counters[2:3], e2, 0))
+        ws.k5_sync = sy3
     _lib.call("lc_encode", gp, mp, mk, n, C.byref(hyp), fill, enc, fb,
               C.byref(segs) if segs is not None else None, ws.dst, P, L,
-              ws.flags.data_ptr(), s)
+              ws.flags.data_ptr(), sy1, s)
     rows = 1
     if ws.p2p:
-        tp.device_barrier(r, gen)          # every rank's blocks have landed
+        if not fused:
+            tp.device_barrier(r, gen)      # every rank's blocks have landed
         recv, rows = ws.recv.local, P
     elif kind == "1bit":
         tp.alltoall(r, gen, ws.send, ws.recv, cw * 4)
@@ -569,16 +582,17 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
         recv = ws.recv
     if kind == "1bit":
         _lib.call("lc_vote_bits", recv.data_ptr(), P, cw, nvalid, fill, sum_mode, ws.vout,
-                  ws.nzout, ws.tout, ws.nout, ws.flags.data_ptr(), s)
+                  ws.nzout, ws.tout, ws.nout, ws.flags.data_ptr(), sy2, s)
     elif kind == "fields":
         _lib.call("lc_fields_vote", recv.data_ptr(), rows, ws.cwf, nvalid, F, P,
                   0 if binary else qmax, int(binary), fill, ws.vout, ws.nzout, ws.tout,
-                  ws.nout, None, s)
+                  ws.nout, None, sy2, s)
     else:
         _lib.call("lc_f64_sum_vote", recv.data_ptr(), P, nvalid, L, int(tree), fill, ws.vout,
-                  ws.nzout, ws.tout, ws.nout, None, s)
+                  ws.nzout, ws.tout, ws.nout, None, sy2, s)
     if ws.p2p:
-        tp.device_barrier(r, gen)          # every owner's voted block has landed
+        if not fused:
+            tp.device_barrier(r, gen)      # every owner's voted block has landed
     else:
         full = ws.full
         tp.allgather(r, gen, full[r * cw:], full, cw * 4)

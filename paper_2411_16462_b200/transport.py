@@ -94,6 +94,16 @@ class DeviceTransport:
         """True if an earlier device barrier timed out (no host sync)."""
         return False
 
+    # In-kernel barriers: kernels publish/wait epochs themselves (lc_sync).
+    fused_barriers: bool = False
+
+    def sync_struct(self, rank: int, counter: torch.Tensor, wait_epoch: int,
+                    arrive_epoch: int):
+        raise NotImplementedError
+
+    def take_epochs(self, rank: int, k: int) -> list:
+        raise NotImplementedError
+
     def device(self, rank: int) -> torch.device:
         raise NotImplementedError
 
@@ -362,17 +372,43 @@ class NcclTransport(DeviceTransport):
         self._sym[k] = buf
         return buf
 
-    def device_barrier(self, rank, gen):
+    def _flags(self, rank):
         flags = self.sym_buffer(rank, ("__barrier__",), self.world_size, torch.int64)
         if rank not in self._err:
             dev = self._devices[rank]
             self._err[rank] = torch.zeros(1, dtype=torch.int32, device=dev)
             self._err_host[rank] = torch.zeros(1, dtype=torch.int32, pin_memory=True)
             self._epoch[rank] = 0
-        self._epoch[rank] += 1
+        return flags
+
+    def take_epochs(self, rank, k):
+        self._flags(rank)
+        first = self._epoch[rank] + 1
+        self._epoch[rank] += k
+        return list(range(first, first + k))
+
+    @property
+    def fused_barriers(self):
+        return self.p2p and os.environ.get("LIONCUB_FUSED_BARRIER", "1") == "1"
+
+    def sync_struct(self, rank, counter, wait_epoch, arrive_epoch):
+        flags = self._flags(rank)
+        sy = _lib.Sync()
+        for j, p in enumerate(flags.peers):
+            sy.peer_flags[j] = p
+        sy.my_flags = flags.local.data_ptr()
+        sy.counter = counter.data_ptr()
+        sy.err = self._err[rank].data_ptr()
+        sy.wait_epoch, sy.arrive_epoch = wait_epoch, arrive_epoch
+        sy.P, sy.rank, sy.timeout_s = self.world_size, rank, DEFAULT_TIMEOUT
+        return sy
+
+    def device_barrier(self, rank, gen):
+        flags = self._flags(rank)
+        (epoch,) = self.take_epochs(rank, 1)
         st = self.stream(rank).cuda_stream
         _lib.call("lc_barrier", _lib.table(flags.peers), self.world_size, rank,
-                  flags.local.data_ptr(), self._epoch[rank], DEFAULT_TIMEOUT,
+                  flags.local.data_ptr(), epoch, DEFAULT_TIMEOUT,
                   self._err[rank].data_ptr(), st)
 
     def poll_error(self, rank):

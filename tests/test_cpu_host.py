@@ -51,7 +51,7 @@ def test_error_codes_map_to_reference_exceptions():
     with pytest.raises(lc.DeviceError):
         _lib.check(_lib.LC_E_CUDA, "x")
     # argument validation happens before any device work
-    rc = _lib.load().lc_vote_bits(None, 0, 4, 0, 1, 0, None, None, None, 1, None, None)
+    rc = _lib.load().lc_vote_bits(None, 0, 4, 0, 1, 0, None, None, None, 1, None, None, None)
     assert rc == _lib.LC_E_ARG and "P must be" in _lib.last_error()
 
 

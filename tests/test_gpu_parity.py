@@ -82,7 +82,7 @@ def test_packed_sign_words_bit_exact(name):
             L = -(-n // 1024) * 1024
             _lib.call("lc_encode", g.data_ptr(), m.data_ptr(), _lib.ptr(mask), n,
                       C.byref(hyp), fill, _lib.LC_ENC_SIGN1, 1, None,
-                      _lib.table([out.data_ptr()]), 1, L, flags.data_ptr(), 0)
+                      _lib.table([out.data_ptr()]), 1, L, flags.data_ptr(), None, 0)
             got = out.cpu().numpy().view(np.uint32)
             nb = (n + 7) // 8  # reference payload bytes; compare the valid bits
             gb = got.view(np.uint8)[:nb].copy()
@@ -135,7 +135,7 @@ def test_l1_norm_and_quantized_ints_bit_exact(name):
             _lib.call("lc_encode", g.data_ptr(), m.clone().data_ptr(), _lib.ptr(mask), n,
                       C.byref(hyp), 1, _lib.LC_ENC_QUANT_FIELDS, 32, C.byref(segs),
                       _lib.table([out.data_ptr()]), 1, -(-n // 1024) * 1024,
-                      flags.data_ptr(), 0)
+                      flags.data_ptr(), None, 0)
             q = out.cpu().numpy().astype(np.int64) - qmax
             ref = np.concatenate([gc["q"][r][k].astype(np.int64) for k in names])
             assert np.array_equal(q, ref), (name, r)
