@@ -321,6 +321,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-chunk", type=int, default=1 << 23)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -470,21 +471,30 @@ def main():
     sr = step_roofline(n, P, F, kind, sync_frac, hbm_peak)
     sr["frac"] = max(sr["t_hbm_ms"], sr["t_nvlink_ms"]) / ms
 
-    # end to end through the public API with host buffers
+    # end to end through the public API with host buffers: pinned host
+    # gradients in, updated parameters out (distributed_lion_step_host
+    # pipelines both copies with the kernels chunk by chunk)
     e2e = None
     if not args.no_e2e:
         host_g = torch.empty(n, dtype=torch.float32, pin_memory=True)
         host_g.copy_(grad[:n].cpu())
         host_t = torch.empty(n, dtype=torch.float32, pin_memory=True)
+
+        def step_host(state):
+            state = lc.distributed_lion_step_host(state, host_g, h, spec, topo, algo,
+                                                  params_out=host_t, chunk=args.e2e_chunk)
+            if policy is not None:
+                state = lc.maybe_sync_momentum(state, policy, topo)
+            return state
+
+        for _ in range(2):
+            st = step_host(st)
         barrier()
         f0 = torch.cuda.Event(enable_timing=True)
         f1 = torch.cuda.Event(enable_timing=True)
         f0.record(stream)
-        with torch.cuda.stream(stream):
-            for _ in range(args.steps):
-                g.flat[:n].copy_(host_g, non_blocking=True)
-                st = step(st)
-                host_t.copy_(st.params.flat[:n], non_blocking=True)
+        for _ in range(args.steps):
+            st = step_host(st)
         f1.record(stream)
         barrier()
         ems = f0.elapsed_time(f1) / args.steps
@@ -494,7 +504,8 @@ def main():
             ems = float(t.item())
         e2e = {"value": P * n / (ems * 1e-3), "unit": "params/s", "ms_per_step": ems,
                "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n,
-               "path": "pinned host grads -> distributed_lion_step -> pinned host theta"}
+               "path": "distributed_lion_step_host: pinned host grads -> step -> pinned "
+                       f"host params, {args.e2e_chunk}-element chunks pipelined"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -109,11 +109,14 @@ int lc_device_sm_count(int device);
  *     A local send buffer ([P][L*F/32] for an NCCL exchange) or, for the
  *     NVLink path, the owner GPU's receive slot (peer pointer), so the
  *     all-to-all happens inside the kernel.  L is a multiple of 1024.
+ *   eoff: index of g[0]/m[0] in the full vector (multiple of 1024), so a
+ *     chunk of the vector can be encoded as soon as it arrives.
  *   g, m must be 16-byte aligned. mask may be NULL (uint8 per element). */
 int lc_encode(const float* g, float* m, const uint8_t* mask, int64_t n,
               const lc_hyper* h, int fill, int enc, int field_bits,
               const lc_segments* segs, void* const* dst, int32_t nblocks,
-              int64_t L, uint32_t* flags, const lc_sync* sync, void* stream);
+              int64_t L, int64_t eoff, uint32_t* flags, const lc_sync* sync,
+              void* stream);
 
 /* Output tables of the owner-side vote kernels: voted/nz/tie_bits are host
  * arrays of `nout` word pointers; the owner's block is written to every one
@@ -160,10 +163,12 @@ int lc_f64_sum_vote(const double* recv, int32_t P, int64_t len, int64_t stride,
  * sign_bits / nz_bits (nullable) are tables of nsrc word arrays indexed by
  * the GLOBAL word index; word w is read from table entry w / wpb -- the
  * owner of that block.  nsrc = 1: local gather buffer; nsrc = P: each
- * owner's vote output over NVLink (the allgather pulled inside K5). */
+ * owner's vote output over NVLink (the allgather pulled inside K5).
+ * woff: global word index of theta[0] / 32 (chunked updates). */
 int lc_apply_update(float* theta, int64_t n, void* const* sign_bits,
-                    void* const* nz_bits, int32_t nsrc, int64_t wpb, double lr,
-                    double weight_decay, const lc_sync* sync, void* stream);
+                    void* const* nz_bits, int32_t nsrc, int64_t wpb, int64_t woff,
+                    double lr, double weight_decay, const lc_sync* sync,
+                    void* stream);
 
 /* ---- one-pass step for P == 1 (no exchange: the vote of one rank is its
  * own aggregate): reads theta,m,g, writes theta',m' (20 B/param).

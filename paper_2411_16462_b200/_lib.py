@@ -70,11 +70,11 @@ SIGNATURES = {
     "lc_abi_version": (INT, []),
     "lc_last_error": (C.c_char_p, []),
     "lc_device_sm_count": (INT, [INT]),
-    "lc_encode": (INT, [P, P, P, I64, P, INT, INT, INT, P, P, I32, I64, P, P, P]),
+    "lc_encode": (INT, [P, P, P, I64, P, INT, INT, INT, P, P, I32, I64, I64, P, P, P]),
     "lc_vote_bits": (INT, [P, I32, I64, I64, INT, INT, P, P, P, I32, P, P, P]),
     "lc_fields_vote": (INT, [P, I32, I64, I64, I32, I32, I32, I32, INT, P, P, P, I32, P, P, P]),
     "lc_f64_sum_vote": (INT, [P, I32, I64, I64, INT, INT, P, P, P, I32, P, P, P]),
-    "lc_apply_update": (INT, [P, I64, P, P, I32, I64, D, D, P, P]),
+    "lc_apply_update": (INT, [P, I64, P, P, I32, I64, I64, D, D, P, P]),
     "lc_fused_local_step": (INT, [P, P, P, P, I64, P, INT, INT, P, P, P, P, P, P]),
     "lc_mean_f32": (INT, [P, I32, I64, I64, P, P]),
     "lc_l1_plan_create": (INT, [P, P, I32]),

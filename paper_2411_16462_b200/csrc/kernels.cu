@@ -173,7 +173,7 @@ template <int ENC, int F, bool MASK>
 __global__ void __launch_bounds__(256, LC_ENC_MINB)
 k_encode(const float* __restrict__ g, float* __restrict__ m,
          const uint8_t* __restrict__ mask, int64_t n, Hyp h, int fill, SegQ sq,
-         Dst dst, int64_t L, uint32_t* __restrict__ flags, SyncD sy) {
+         Dst dst, int64_t L, int64_t eoff, uint32_t* __restrict__ flags, SyncD sy) {
   constexpr int WPS = (ENC == LC_ENC_F64) ? 1 : 32 * F;  // words per super-tile
   constexpr int KU = LC_ENC_KU;  // sub-tiles whose loads are in flight together
   __shared__ __align__(16) uint32_t stage[8][WPS];
@@ -191,8 +191,9 @@ k_encode(const float* __restrict__ g, float* __restrict__ m,
 
   for (int64_t sidx = gw; sidx < nsup; sidx += nw) {
     const int64_t ebase = sidx << 10;
-    const int j = (int)(ebase / L);
-    const int64_t boff = ebase - (int64_t)j * L;  // element offset inside block j
+    const int64_t gbase = eoff + ebase;            // element index in the full vector
+    const int j = (int)(gbase / L);
+    const int64_t boff = gbase - (int64_t)j * L;  // element offset inside block j
     if (ebase + 1024 <= n) {
       // ---- fast path: a full super-tile, no per-element bounds ----
       const float4* gp = g4 + (ebase >> 2) + lane;
@@ -296,7 +297,7 @@ k_encode(const float* __restrict__ g, float* __restrict__ m,
 template <bool NZ>
 __global__ void __launch_bounds__(256, 3)
 k_apply_update(float* __restrict__ theta, int64_t n, Dst sb, Dst nzb, int64_t wpb,
-               double lr, double wd, SyncD sy) {
+               int64_t woff, double lr, double wd, SyncD sy) {
   constexpr int KU = 4;
   sync_wait(sy);
   const int lane = threadIdx.x & 31;
@@ -312,9 +313,10 @@ k_apply_update(float* __restrict__ theta, int64_t n, Dst sb, Dst nzb, int64_t wp
     sw_ = 0u;
     zw_ = ~0u;
     if (sidx < nsup && w < nwords) {
-      const int j = (int)(w / wpb);
-      sw_ = __ldcs(reinterpret_cast<const uint32_t*>(sb.p[j]) + w);
-      if (NZ) zw_ = __ldcs(reinterpret_cast<const uint32_t*>(nzb.p[j]) + w);
+      const int64_t wg = woff + w;  // word index in the full vector
+      const int j = (int)(wg / wpb);
+      sw_ = __ldcs(reinterpret_cast<const uint32_t*>(sb.p[j]) + wg);
+      if (NZ) zw_ = __ldcs(reinterpret_cast<const uint32_t*>(nzb.p[j]) + wg);
     }
   };
   uint32_t nxw, nxz;
@@ -856,7 +858,8 @@ int generic_grid(int64_t n) {
   return b < 1 ? 1 : (int)b;
 }
 
-thread_local SyncD g_sync{};  // sync of the encode launch being dispatched
+thread_local SyncD g_sync{};     // sync of the encode launch being dispatched
+thread_local int64_t g_eoff = 0;  // element offset of the encode launch
 
 template <int ENC, int F, bool MASK>
 int launch_encode(const float* g, float* m, const uint8_t* mask, int64_t n, Hyp h,
@@ -865,7 +868,7 @@ int launch_encode(const float* g, float* m, const uint8_t* mask, int64_t n, Hyp 
   auto kern = k_encode<ENC, F, MASK>;
   int64_t nsup = (n + 1023) >> 10;
   int grid = stream_grid(kern, kBlock, nsup, kBlock / 32);
-  kern<<<grid, kBlock, 0, st>>>(g, m, mask, n, h, fill, sq, dst, L, flags, g_sync);
+  kern<<<grid, kBlock, 0, st>>>(g, m, mask, n, h, fill, sq, dst, L, g_eoff, flags, g_sync);
   LC_LAUNCH_CHECK();
   return LC_OK;
 }
@@ -920,19 +923,20 @@ int lc_device_sm_count(int device) {
 int lc_encode(const float* g, float* m, const uint8_t* mask, int64_t n,
               const lc_hyper* hp, int fill, int enc, int field_bits,
               const lc_segments* segs, void* const* dst, int32_t nblocks, int64_t L,
-              uint32_t* flags, const lc_sync* sync, void* stream) {
+              int64_t eoff, uint32_t* flags, const lc_sync* sync, void* stream) {
   if (n < 0 || !hp || !flags) return set_err(LC_E_ARG, "lc_encode: bad arguments");
   if (n == 0) return LC_OK;
   if (!g || !m) return set_err(LC_E_ARG, "lc_encode: null pointer");
   if (!aligned16(g) || !aligned16(m)) return set_err(LC_E_ARG, "lc_encode: g/m must be 16-byte aligned");
-  if (L <= 0 || (L % 1024) != 0 || (int64_t)nblocks * L < n)
-    return set_err(LC_E_ARG, "lc_encode: block length must be a positive multiple of 1024 covering n");
+  if (L <= 0 || (L % 1024) != 0 || (int64_t)nblocks * L < eoff + n || eoff < 0 || (eoff % 1024) != 0)
+    return set_err(LC_E_ARG, "lc_encode: blocks (multiple of 1024) must cover [eoff, eoff+n), eoff % 1024 == 0");
   Dst d;
   if (!make_dst(d, dst, nblocks)) return set_err(LC_E_ARG, "lc_encode: bad destination table");
   Hyp h = to_hyp(hp);
   SegQ sq = to_segq(segs);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   g_sync = to_syncd(sync);
+  g_eoff = eoff;
   switch (enc) {
     case LC_ENC_SIGN1:
       return dispatch_mask<LC_ENC_SIGN1, 1>(g, m, mask, n, h, fill, sq, d, L, flags, st);
@@ -951,26 +955,26 @@ int lc_encode(const float* g, float* m, const uint8_t* mask, int64_t n,
 }
 
 int lc_apply_update(float* theta, int64_t n, void* const* sign_bits, void* const* nz_bits,
-                    int32_t nsrc, int64_t wpb, double lr, double wd, const lc_sync* sync,
-                    void* stream) {
+                    int32_t nsrc, int64_t wpb, int64_t woff, double lr, double wd,
+                    const lc_sync* sync, void* stream) {
   if (n < 0) return set_err(LC_E_ARG, "lc_apply_update: n < 0");
   if (n == 0) return LC_OK;
   Dst sb, zb;
   if (!theta || !make_dst(sb, sign_bits, nsrc) || (nz_bits && !make_dst(zb, nz_bits, nsrc)))
     return set_err(LC_E_ARG, "lc_apply_update: bad pointers / source table");
-  if (wpb <= 0 || (int64_t)nsrc * wpb * 32 < n)
-    return set_err(LC_E_ARG, "lc_apply_update: source blocks do not cover n");
+  if (wpb <= 0 || woff < 0 || (int64_t)nsrc * wpb * 32 < woff * 32 + n)
+    return set_err(LC_E_ARG, "lc_apply_update: source blocks do not cover [woff*32, woff*32+n)");
   if (!aligned16(theta)) return set_err(LC_E_ARG, "lc_apply_update: theta must be 16-byte aligned");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int64_t nsup = (n + 1023) >> 10;
   if (nz_bits) {
     auto kern = k_apply_update<true>;
     int grid = stream_grid(kern, kBlock, nsup, kBlock / 32);
-    kern<<<grid, kBlock, 0, st>>>(theta, n, sb, zb, wpb, lr, wd, to_syncd(sync));
+    kern<<<grid, kBlock, 0, st>>>(theta, n, sb, zb, wpb, woff, lr, wd, to_syncd(sync));
   } else {
     auto kern = k_apply_update<false>;
     int grid = stream_grid(kern, kBlock, nsup, kBlock / 32);
-    kern<<<grid, kBlock, 0, st>>>(theta, n, sb, sb, wpb, lr, wd, to_syncd(sync));
+    kern<<<grid, kBlock, 0, st>>>(theta, n, sb, sb, wpb, woff, lr, wd, to_syncd(sync));
   }
   LC_LAUNCH_CHECK();
   return LC_OK;

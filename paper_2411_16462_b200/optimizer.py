@@ -440,6 +440,82 @@ def distributed_lion_step(state: WorkerState, grad_i, h: LionHyper,
     sync and an f64 copy of c)."""
     _validate(spec, algo)
     _check_shapes(state.params, grad_i)
+    return _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out)
+
+
+class _HostPipe:
+    """Chunked host<->device pipeline of one step: the gradient H2D copies
+    (pinned host -> the device grad buffer) run on their own stream chunk by
+    chunk, each compute chunk waits only for its own chunk, and theta's D2H
+    copy of a chunk starts as soon as that chunk is updated."""
+
+    def __init__(self, dev, n: int, chunk: int):
+        chunk = max(1024, -(-chunk // 1024) * 1024)
+        self.ranges = [(a, min(n, a + chunk)) for a in range(0, max(n, 1), chunk)]
+        self.h2d = torch.cuda.Stream(dev)
+        self.d2h = torch.cuda.Stream(dev)
+        self.ev_in = [torch.cuda.Event() for _ in self.ranges]
+        self.ev_out = [torch.cuda.Event() for _ in self.ranges]
+        self.host_g = self.host_out = None
+
+    def start(self, g_dev: torch.Tensor, compute: torch.cuda.Stream):
+        self.h2d.wait_stream(compute)  # the previous step no longer reads g
+        with torch.cuda.stream(self.h2d):
+            for (a, b), ev in zip(self.ranges, self.ev_in):
+                g_dev[a:b].copy_(self.host_g[a:b], non_blocking=True)
+                ev.record()
+
+    def wait_in(self, c: int, stream):
+        stream.wait_event(self.ev_in[c])
+
+    def wait_all_in(self, stream):
+        stream.wait_event(self.ev_in[-1])
+
+    def emit_out(self, c: int, theta: torch.Tensor, stream):
+        if self.host_out is None:
+            return
+        a, b = self.ranges[c]
+        self.ev_out[c].record(stream)
+        self.d2h.wait_event(self.ev_out[c])
+        with torch.cuda.stream(self.d2h):
+            self.host_out[a:b].copy_(theta[a:b], non_blocking=True)
+
+    def finish(self, stream):
+        stream.wait_stream(self.d2h)
+
+
+def distributed_lion_step_host(state: WorkerState, grad_host: torch.Tensor, h: LionHyper,
+                               spec: QuantSpec | None, topo: Topology, algo: str,
+                               zero_mode: str = "alternating",
+                               params_out: torch.Tensor | None = None,
+                               chunk: int = 1 << 23) -> WorkerState:
+    """The step with HOST buffers, as a reference user holds them: the
+    gradient comes from ``grad_host`` (a flat fp32 CPU tensor in the
+    state's sorted-name layout; pin it for async copies) and, if given, the
+    updated parameters land in ``params_out`` (same layout).  The copies are
+    pipelined with the kernels in ``chunk``-element pieces; the step is
+    complete on ``topo.stream`` when the parameter copy has landed."""
+    _validate(spec, algo)
+    layout, th, m = state.flat()
+    n = layout.n
+    if grad_host.device.type != "cpu" or grad_host.dtype != torch.float32 \
+            or grad_host.numel() < n:
+        raise ConfigError("grad_host must be a flat float32 CPU tensor of the layout's size")
+    key = ("host_pipe", chunk)
+    pipe = th.workspace.get(key)
+    if pipe is None:
+        pipe = _HostPipe(th.flat.device, n, chunk)
+        th.workspace[key] = pipe
+    pipe.host_g = grad_host.reshape(-1)
+    pipe.host_out = None if params_out is None else params_out.reshape(-1)
+    g = th.workspace.get("host_grads")
+    if g is None:
+        g = FlatParamSet.empty_like(th)
+        th.workspace["host_grads"] = g
+    return _step_impl(state, g, h, spec, topo, algo, None, zero_mode, None, pipe=pipe)
+
+
+def _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out, pipe=None):
     layout, th, m = state.flat()
     dev = th.flat.device
     P = topo.world_size
@@ -477,6 +553,11 @@ def distributed_lion_step(state: WorkerState, grad_i, h: LionHyper,
         s = stream.cuda_stream
         with torch.cuda.stream(stream):
             g = _to_flat(grad_i, layout, dev)
+            if pipe is not None:
+                pipe.start(g.flat, stream)
+                # stages that need the whole gradient first
+                if (ternary and binary) or (kind == "fields" and not binary):
+                    pipe.wait_all_in(stream)
             mflat = _flat_mask(mask, layout, dev)
             ws = _workspace(th, topo, kind if P > 1 else "local", F,
                             ternary and (kind != "1bit" or sum_mode == 1), metrics)
@@ -494,19 +575,43 @@ def distributed_lion_step(state: WorkerState, grad_i, h: LionHyper,
             if P == 1:
                 mode = (_lib.LC_LOCAL_BINARY if binary else
                         _lib.LC_LOCAL_QUANT if kind == "fields" else _lib.LC_LOCAL_PS)
-                _lib.call("lc_fused_local_step", th.flat.data_ptr(), m.flat.data_ptr(),
-                          g.flat.data_ptr(), _lib.ptr(mflat), n, C.byref(hyp), fill, mode,
-                          C.byref(segs) if segs is not None else None,
-                          _loc(ws.full).data_ptr() if metrics else None,
-                          _loc(ws.nz).data_ptr() if (metrics and ws.nz is not None) else None,
-                          _lib.ptr(_loc(ws.ties)), ws.flags.data_ptr(), s)
+                if pipe is not None and mode != _lib.LC_LOCAL_QUANT:
+                    # elementwise: each chunk as soon as its gradient landed
+                    for c, (a, b) in enumerate(pipe.ranges):
+                        pipe.wait_in(c, stream)
+                        _lib.call("lc_fused_local_step", _off(th.flat, a), _off(m.flat, a),
+                                  _off(g.flat, a), None, b - a, C.byref(hyp), fill, mode,
+                                  None, None, None, None, ws.flags.data_ptr(), s)
+                        pipe.emit_out(c, th.flat, stream)
+                else:
+                    if pipe is not None:
+                        pipe.wait_all_in(stream)
+                    _lib.call("lc_fused_local_step", th.flat.data_ptr(), m.flat.data_ptr(),
+                              g.flat.data_ptr(), _lib.ptr(mflat), n, C.byref(hyp), fill, mode,
+                              C.byref(segs) if segs is not None else None,
+                              _loc(ws.full).data_ptr() if metrics else None,
+                              _loc(ws.nz).data_ptr() if (metrics and ws.nz is not None)
+                              else None,
+                              _lib.ptr(_loc(ws.ties)), ws.flags.data_ptr(), s)
+                    if pipe is not None:
+                        for c in range(len(pipe.ranges)):
+                            pipe.emit_out(c, th.flat, stream)
                 nz = _loc(ws.nz) if metrics else None
             else:
                 nz = _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill,
                                         n, g, m, mflat, hyp, segs, s,
-                                        tree=algo == "ps_efficient")
-                _lib.call("lc_apply_update", th.flat.data_ptr(), n, ws.src, ws.nzsrc,
-                          ws.nsrc, ws.wpb, eta, wd, ws.k5_sync, s)
+                                        tree=algo == "ps_efficient", pipe=pipe)
+                if pipe is None:
+                    _lib.call("lc_apply_update", th.flat.data_ptr(), n, ws.src, ws.nzsrc,
+                              ws.nsrc, ws.wpb, 0, eta, wd, ws.k5_sync, s)
+                else:
+                    for c, (a, b) in enumerate(pipe.ranges):
+                        _lib.call("lc_apply_update", _off(th.flat, a), b - a, ws.src, ws.nzsrc,
+                                  ws.nsrc, ws.wpb, a // 32, eta, wd,
+                                  ws.k5_sync if c == 0 else None, s)
+                        pipe.emit_out(c, th.flat, stream)
+            if pipe is not None:
+                pipe.finish(stream)
             if metrics:
                 _fill_metrics(metrics_out, layout, dev, ws, nz, c_local, s)
     return WorkerState(params=th, momentum=m, iteration=t)
@@ -540,7 +645,7 @@ def _ternary_precheck(topo, gen, g, m, mflat, n, hyp, dev, s, kind):
 
 
 def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, g, m, mflat,
-                       hyp, segs, s, tree=False):
+                       hyp, segs, s, tree=False, pipe=None):
     """K1 encode -> exchange -> owner vote into the gather buffer (+nz, ties)."""
     P, r = topo.world_size, topo.rank
     tp = topo.transport
@@ -563,9 +668,22 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
         sy2 = C.byref(tp.sync_struct(r, ws.counters[1:2], e1, e2))
         sy3 = C.byref(tp.sync_struct(r, ws.counters[2:3], e2, 0))
         ws.k5_sync = sy3
-    _lib.call("lc_encode", gp, mp, mk, n, C.byref(hyp), fill, enc, fb,
-              C.byref(segs) if segs is not None else None, ws.dst, P, L,
-              ws.flags.data_ptr(), sy1, s)
+    if pipe is not None and segs is None and mflat is None:
+        # encode each gradient chunk as soon as it landed; the last chunk's
+        # launch publishes the barrier epoch
+        stream = torch.cuda.ExternalStream(s)
+        last = len(pipe.ranges) - 1
+        for c, (a, b) in enumerate(pipe.ranges):
+            pipe.wait_in(c, stream)
+            _lib.call("lc_encode", _off(g.flat, a), _off(m.flat, a), None, b - a,
+                      C.byref(hyp), fill, enc, fb, None, ws.dst, P, L, a,
+                      ws.flags.data_ptr(), sy1 if c == last else None, s)
+    else:
+        if pipe is not None:
+            pipe.wait_all_in(torch.cuda.ExternalStream(s))
+        _lib.call("lc_encode", gp, mp, mk, n, C.byref(hyp), fill, enc, fb,
+                  C.byref(segs) if segs is not None else None, ws.dst, P, L, 0,
+                  ws.flags.data_ptr(), sy1, s)
     rows = 1
     if ws.p2p:
         if not fused:

@@ -59,13 +59,13 @@ def main():
 
     timed("encode_1bit", lambda: _lib.call(
         "lc_encode", g.data_ptr(), m.data_ptr(), None, n, C.byref(hyp), 1,
-        _lib.LC_ENC_SIGN1, 1, None, dst, P, L, flags.data_ptr(), None, s), 12 * n + n / 8)
+        _lib.LC_ENC_SIGN1, 1, None, dst, P, L, 0, flags.data_ptr(), None, s), 12 * n + n / 8)
     timed("vote_bits", lambda: _lib.call(
         "lc_vote_bits", send.data_ptr(), P, cw, L, 1, 0, vout, None, None, 1,
         flags.data_ptr(), None, s), (P + 1) * cw * 4)
     timed("apply_update", lambda: _lib.call(
         "lc_apply_update", th.data_ptr(), n, _lib.table([send.data_ptr()]), None, 1,
-        P * cw, 1e-4, 0.0, None, s),
+        P * cw, 0, 1e-4, 0.0, None, s),
         8 * n + n / 8)
     timed("fused_local", lambda: _lib.call(
         "lc_fused_local_step", th.data_ptr(), m.data_ptr(), g.data_ptr(), None, n,

@@ -82,7 +82,7 @@ def test_packed_sign_words_bit_exact(name):
             L = -(-n // 1024) * 1024
             _lib.call("lc_encode", g.data_ptr(), m.data_ptr(), _lib.ptr(mask), n,
                       C.byref(hyp), fill, _lib.LC_ENC_SIGN1, 1, None,
-                      _lib.table([out.data_ptr()]), 1, L, flags.data_ptr(), None, 0)
+                      _lib.table([out.data_ptr()]), 1, L, 0, flags.data_ptr(), None, 0)
             got = out.cpu().numpy().view(np.uint32)
             nb = (n + 7) // 8  # reference payload bytes; compare the valid bits
             gb = got.view(np.uint8)[:nb].copy()
@@ -134,7 +134,7 @@ def test_l1_norm_and_quantized_ints_bit_exact(name):
             flags = torch.zeros(1, dtype=torch.int32, device="cuda")
             _lib.call("lc_encode", g.data_ptr(), m.clone().data_ptr(), _lib.ptr(mask), n,
                       C.byref(hyp), 1, _lib.LC_ENC_QUANT_FIELDS, 32, C.byref(segs),
-                      _lib.table([out.data_ptr()]), 1, -(-n // 1024) * 1024,
+                      _lib.table([out.data_ptr()]), 1, -(-n // 1024) * 1024, 0,
                       flags.data_ptr(), None, 0)
             q = out.cpu().numpy().astype(np.int64) - qmax
             ref = np.concatenate([gc["q"][r][k].astype(np.int64) for k in names])
@@ -377,3 +377,43 @@ def test_l1_norms_bit_exact_large(sizes):
         assert norms.cpu().numpy().tolist() == ref
     finally:
         _lib.load().lc_l1_plan_destroy(plan.value)
+
+
+@pytest.mark.parametrize("p2p", [True, False], ids=["peer-memory", "collectives"])
+@pytest.mark.parametrize("algo,bits,world,chunk", [
+    ("compressed1bit", None, 1, 65536), ("direct", 1, 1, 1 << 20), ("direct", 5, 1, 4096),
+    ("compressed1bit", None, 3, 65536), ("direct", 1, 4, 3 * 1024), ("direct", 5, 2, 65536),
+    ("ps", None, 2, 100_000),
+])
+def test_host_buffer_step_matches_device_step(algo, bits, world, chunk, p2p):
+    """distributed_lion_step_host (pipelined pinned-host grads in, theta out)
+    == distributed_lion_step on device buffers, bit for bit."""
+    sizes = {"a": (150_001,), "b": (7,), "c": (65_536,)}
+    ranks = O.synth_rank_inputs(21, world, sizes, "laplace")
+    case = dict(world=world, lr=1e-3, wd=0.1, bits=bits, algo=algo, iteration=4,
+                zero_mode="alternating")
+    ref = run_step_case(case, ranks[0]["theta"], [r["m"] for r in ranks],
+                        [r["g"] for r in ranks], metrics=False,
+                        transport=lc.LocalTransport(world, p2p=p2p))
+    h = lc.LionHyper(0.9, 0.99, 1e-3, 0.1)
+    spec = None if bits is None else lc.QuantSpec(bits=bits)
+    names = sorted(sizes)
+
+    def fn(topo):
+        from tests.gpu_helpers import make_state
+        r = ranks[topo.rank]
+        st = make_state(r["theta"], r["m"], 4)
+        host_g = torch.from_numpy(np.concatenate([r["g"][k] for k in names])).pin_memory()
+        out = torch.empty(host_g.numel(), dtype=torch.float32).pin_memory()
+        st = lc.distributed_lion_step_host(st, host_g, h, spec, topo, algo,
+                                           params_out=out, chunk=chunk)
+        topo.stream.synchronize()
+        return out.numpy().copy(), {k: v.cpu().numpy() for k, v in st.momentum.items()}
+
+    got = lc.run_ranks(world, fn, transport=lc.LocalTransport(world, p2p=p2p))
+    for r in range(world):
+        th_flat, mom = got[r]
+        exp_th = np.concatenate([ref[r][0][k] for k in names])
+        assert np.array_equal(th_flat.view(np.int32), exp_th.view(np.int32))
+        for k in names:
+            assert np.array_equal(mom[k].view(np.int32), ref[r][1][k].view(np.int32))
