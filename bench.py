@@ -398,6 +398,8 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    sampler = ClockSampler(local)
+    sampler.start()
     for _ in range(args.warmup):
         st = step(st)
     barrier()
@@ -409,9 +411,7 @@ def main():
     probe = torch.tensor([time.perf_counter() - t_probe], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(probe, op=dist.ReduceOp.MAX)
-    soak = max(1, min(200, int(0.3 / max(float(probe.item()), 1e-4))))
-    sampler = ClockSampler(local)
-    sampler.start()
+    soak = max(1, min(5000, int(0.4 / max(float(probe.item()), 1e-5))))
     for _ in range(soak):
         st = step(st)
     barrier()
