@@ -17,6 +17,7 @@ from .optimizer import (VOTE_ALGOS, FlatParamSet, Layout, LionHyper,  # noqa: F4
                         distributed_lion_step_host,
                         hash_params, lion_step, maybe_sync_momentum)
 from .quant import INF, QuantSpec, SignPolicy  # noqa: F401
+from .torch_optim import LionCub, lioncub_comm_hook  # noqa: F401
 from .transport import (DeviceTransport, LocalTransport,  # noqa: F401
                         NcclTransport)
 

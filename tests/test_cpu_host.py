@@ -174,3 +174,36 @@ def test_bench_reference_arm_under_torchrun_two_ranks():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "port" and d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def _ddp_worker(rank, world, port, q):
+    import torch.distributed as dist
+    from torch.nn.parallel import DistributedDataParallel as DDP
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.manual_seed(0)
+    model = torch.nn.Linear(4, 2)
+    ddp = DDP(model)
+    ddp.register_comm_hook(None, lc.lioncub_comm_hook)
+    x = torch.full((3, 4), float(rank + 1))
+    ddp(x).sum().backward()
+    # gradients stay local (no averaging): each rank sees its own input's grad
+    expect = torch.full((2, 4), 3.0 * (rank + 1))
+    q.put((rank, bool(torch.allclose(model.weight.grad, expect))))
+    dist.destroy_process_group()
+
+
+def test_ddp_comm_hook_keeps_local_gradients_gloo():
+    """The DDP hook returns buckets untouched: Lion Cub votes with LOCAL
+    gradients, so DDP's all-reduce must not average them."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + os.getpid() % 150
+    procs = [ctx.Process(target=_ddp_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res

@@ -417,3 +417,60 @@ def test_host_buffer_step_matches_device_step(algo, bits, world, chunk, p2p):
         assert np.array_equal(th_flat.view(np.int32), exp_th.view(np.int32))
         for k in names:
             assert np.array_equal(mom[k].view(np.int32), ref[r][1][k].view(np.int32))
+
+
+def test_torch_optim_lioncub_trains_and_matches_step():
+    """LionCub (torch.optim front end) on a small MLP: the model's params
+    are the flat state; one step equals distributed_lion_step on the same
+    gradient; replicas stay bit-identical across simulated ranks."""
+    torch.manual_seed(0)
+
+    def make():
+        return torch.nn.Sequential(torch.nn.Linear(16, 32), torch.nn.Tanh(),
+                                   torch.nn.Linear(32, 1)).cuda()
+
+    init = {k: v.clone() for k, v in make().state_dict().items()}  # same replica everywhere
+    world = 3
+    xs = [torch.randn(64, 16, device="cuda") for _ in range(world)]
+    ys = [x.sum(dim=1, keepdim=True).sin() for x in xs]
+
+    def fn(topo):
+        model = make()
+        model.load_state_dict(init)
+        opt = lc.LionCub(model.named_parameters(), topo, lr=1e-2,
+                         spec=lc.QuantSpec(bits=1), algo="direct")
+        losses = []
+        for _ in range(30):
+            opt.zero_grad()
+            loss = torch.nn.functional.mse_loss(model(xs[topo.rank]), ys[topo.rank])
+            loss.backward()
+            opt.step()
+            losses.append(float(loss.detach()))
+        torch.cuda.synchronize()
+        flat = opt.lion_state.params.flat.cpu().numpy()
+        return losses, flat
+
+    res = lc.run_ranks(world, fn)
+    for _, flat in res[1:]:
+        assert np.array_equal(flat.view(np.int32), res[0][1].view(np.int32))
+    for losses, _ in res:
+        assert losses[-1] < 0.7 * losses[0]
+
+
+def test_torch_optim_step_equals_functional_step():
+    model = torch.nn.Linear(8, 4).cuda()
+    topo = lc.Topology(1, 0, lc.LocalTransport(1))
+    opt = lc.LionCub(model.named_parameters(), topo, lr=1e-3, weight_decay=0.1,
+                     spec=None, algo="compressed1bit")
+    x = torch.randn(5, 8, device="cuda")
+    opt.zero_grad()
+    model(x).square().sum().backward()
+    g = {k: v.clone() for k, v in opt.grads.items()}
+    theta0 = {k: v.clone() for k, v in opt.lion_state.params.items()}
+    opt.step()
+    st = lc.WorkerState.initial(theta0)
+    st = lc.distributed_lion_step(st, g, lc.LionHyper(0.9, 0.99, 1e-3, 0.1), None, topo,
+                                  "compressed1bit")
+    for k in g:
+        assert torch.equal(st.params[k], opt.lion_state.params[k])
+    assert torch.equal(model.weight.detach(), opt.lion_state.params["weight"])
