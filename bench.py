@@ -111,22 +111,22 @@ def kernel_bytes(name: str, n: int, P: int, F: int, kind: str) -> float:
         return L * F / 8.0 + L / 8.0
     if name == "lc_f64_sum_vote":
         return P * L * 8.0 + L / 8.0
-    if name == "lc_mean_f32":
-        return 0.0
+    if name == "lc_l1_scales":
+        return 16.0 * n  # g, m read twice: max pass, then the pairwise sum
     return 0.0
 
 
 def step_roofline(n: int, P: int, F: int, kind: str, sync_frac: float,
-                  hbm_gbs: float, nvl_gbs: float = 770.0) -> dict:
+                  hbm_gbs: float, nvl_gbs: float = 770.0, l1: bool = False) -> dict:
     """Whole-step lower bound: max(HBM bytes / HBM BW, NVLink bytes / link BW)."""
     if P == 1:
-        hbm = 20.0 * n
+        hbm = 20.0 * n + (16.0 * n if l1 else 0.0)
         nvl = 0.0
     elif kind == "1bit":
         hbm = 20.0 * n + 2 * n / 8.0
         nvl = 2 * (P - 1) / P * n / 8.0
     elif kind == "fields":
-        hbm = 20.0 * n + 2 * n * F / 8.0 + 2 * n / 8.0
+        hbm = 20.0 * n + 2 * n * F / 8.0 + 2 * n / 8.0 + (16.0 * n if l1 else 0.0)
         nvl = (P - 1) / P * n * (F + 1) / 8.0
     else:
         hbm = 36.0 * n
@@ -468,7 +468,7 @@ def main():
                 "avg_launch_ms": kern[dominant]["avg_ms"],
                 "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs" if peak_src ==
                 "measured" else "fallback 6650 GB/s (B200_PROFILING.md)"}
-    sr = step_roofline(n, P, F, kind, sync_frac, hbm_peak)
+    sr = step_roofline(n, P, F, kind, sync_frac, hbm_peak, l1=bits is not None and bits > 1)
     sr["frac"] = max(sr["t_hbm_ms"], sr["t_nvlink_ms"]) / ms
 
     # end to end through the public API with host buffers: pinned host
