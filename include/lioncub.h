@@ -121,7 +121,9 @@ int lc_encode(const float* g, float* m, const uint8_t* mask, int64_t n,
 /* Output tables of the owner-side vote kernels: voted/nz/tie_bits are host
  * arrays of `nout` word pointers; the owner's block is written to every one
  * (nout = 1: local gather buffer before an NCCL allgather; nout = P: every
- * rank's gather buffer over NVLink, i.e. the allgather inside the kernel).
+ * rank's gather buffer over NVLink, i.e. the allgather inside the kernel;
+ * nout = -1: each table holds ONE NVLS multicast address and a single
+ * multimem.st reaches every rank's gather buffer through the NVSwitch).
  * nz / tie_bits may be NULL.  nz marks non-zero aggregates (exact-ternary),
  * tie_bits marks aggregates that are exactly 0 (VoteResult.ties). */
 

@@ -7,6 +7,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <string>
+#include <utility>
 
 #include "lioncub.h"
 
@@ -101,6 +102,30 @@ __device__ __forceinline__ int seg_find(const int64_t* __restrict__ start,
       hi = mid - 1;
   }
   return lo;
+}
+
+// Programmatic dependent launch (Hopper+/Blackwell): the step kernels are
+// launched with programmatic stream serialization so a kernel's CTAs are
+// scheduled while its predecessor drains; each kernel first waits for the
+// predecessor's completion (griddepcontrol.wait, a no-op without PDL).
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 // Device view of lc_sync (kernel parameter, by value).

@@ -174,6 +174,7 @@ __global__ void __launch_bounds__(256, LC_ENC_MINB)
 k_encode(const float* __restrict__ g, float* __restrict__ m,
          const uint8_t* __restrict__ mask, int64_t n, Hyp h, int fill, SegQ sq,
          Dst dst, int64_t L, int64_t eoff, uint32_t* __restrict__ flags, SyncD sy) {
+  griddep_wait();
   constexpr int WPS = (ENC == LC_ENC_F64) ? 1 : 32 * F;  // words per super-tile
   constexpr int KU = LC_ENC_KU;  // sub-tiles whose loads are in flight together
   __shared__ __align__(16) uint32_t stage[8][WPS];
@@ -299,6 +300,7 @@ __global__ void __launch_bounds__(256, 3)
 k_apply_update(float* __restrict__ theta, int64_t n, Dst sb, Dst nzb, int64_t wpb,
                int64_t woff, double lr, double wd, SyncD sy) {
   constexpr int KU = 4;
+  griddep_wait();
   sync_wait(sy);
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -373,6 +375,7 @@ k_fused_local(float* __restrict__ theta, float* __restrict__ m,
               int64_t n, Hyp h, double lr, double wd, int fill, SegQ sq,
               uint32_t* __restrict__ sbits, uint32_t* __restrict__ nzbits,
               uint32_t* __restrict__ tbits, uint32_t* __restrict__ flags) {
+  griddep_wait();
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -490,16 +493,45 @@ k_fused_local(float* __restrict__ theta, float* __restrict__ m,
 // ---------------------------------------------------------------------------
 struct VoteOut {
   Dst v, nz, tie;
-  int nout;
+  int nout;  // > 0: that many destinations; -1: p[0] is an NVLS multicast address
 };
+
+// NVLS: one store to a multicast address is replicated by the NVSwitch into
+// the bound buffer of every GPU (the allgather as a single store).
+__device__ __forceinline__ void mc_st4(uint32_t* mc, uint4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};"
+               ::"l"(mc), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ void mc_st1(uint32_t* mc, uint32_t v) {
+  asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(mc), "r"(v) : "memory");
+}
 
 __device__ __forceinline__ void vote_store(const VoteOut& o, int64_t i, uint4 v, uint4 nz,
                                            uint4 tie) {
+  if (o.nout < 0) {
+    mc_st4(reinterpret_cast<uint32_t*>(o.v.p[0]) + i, v);
+    if (o.nz.p[0]) mc_st4(reinterpret_cast<uint32_t*>(o.nz.p[0]) + i, nz);
+    if (o.tie.p[0]) mc_st4(reinterpret_cast<uint32_t*>(o.tie.p[0]) + i, tie);
+    return;
+  }
   for (int k = 0; k < o.nout; ++k) {
     *reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(o.v.p[k]) + i) = v;
     if (o.nz.p[0]) *reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(o.nz.p[k]) + i) = nz;
     if (o.tie.p[0]) *reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(o.tie.p[k]) + i) = tie;
   }
+}
+
+__device__ __forceinline__ void vote_store1(const VoteOut& o, int k, int64_t i, uint32_t v,
+                                            uint32_t nz, uint32_t tie) {
+  if (o.nout < 0) {
+    mc_st1(reinterpret_cast<uint32_t*>(o.v.p[0]) + i, v);
+    if (o.nz.p[0]) mc_st1(reinterpret_cast<uint32_t*>(o.nz.p[0]) + i, nz);
+    if (o.tie.p[0]) mc_st1(reinterpret_cast<uint32_t*>(o.tie.p[0]) + i, tie);
+    return;
+  }
+  reinterpret_cast<uint32_t*>(o.v.p[k])[i] = v;
+  if (o.nz.p[0]) reinterpret_cast<uint32_t*>(o.nz.p[k])[i] = nz;
+  if (o.tie.p[0]) reinterpret_cast<uint32_t*>(o.tie.p[k])[i] = tie;
 }
 
 template <int NP>
@@ -532,6 +564,7 @@ template <int NP>
 __global__ void __launch_bounds__(256)
 k_vote_bits(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_valid,
             int fill, int sum_mode, VoteOut out, uint32_t* __restrict__ flags, SyncD sy) {
+  griddep_wait();
   sync_wait(sy);
   const int T = P >> 1;
   const uint32_t fillmask = fill > 0 ? ~0u : 0u;
@@ -583,6 +616,7 @@ __global__ void __launch_bounds__(256)
 k_fields_vote(const uint32_t* __restrict__ sums, int rows, int64_t row_stride, int64_t n,
               int P, int offset, int binary, int fill, VoteOut out,
               int64_t* __restrict__ values, SyncD sy) {
+  griddep_wait();
   sync_wait(sy);
   constexpr int E = 32 / F;
   constexpr uint32_t FM = (F == 32) ? 0xffffffffu : ((1u << F) - 1u);
@@ -625,11 +659,8 @@ k_fields_vote(const uint32_t* __restrict__ sums, int rows, int64_t row_stride, i
     const int64_t o = i / F;
     if ((lane % F) == 0 && o < nout) {
       const uint32_t v = pos | (fill > 0 ? zer : 0u);
-      for (int k = 0; k < out.nout; ++k) {
-        reinterpret_cast<uint32_t*>(out.v.p[k])[o] = v;
-        if (out.nz.p[0]) reinterpret_cast<uint32_t*>(out.nz.p[k])[o] = ~zer & val;
-        if (out.tie.p[0]) reinterpret_cast<uint32_t*>(out.tie.p[k])[o] = zer & val;
-      }
+      const int nk = out.nout < 0 ? 1 : out.nout;
+      for (int k = 0; k < nk; ++k) vote_store1(out, k, o, v, ~zer & val, zer & val);
     }
   }
   sync_arrive(sy);
@@ -641,6 +672,7 @@ k_fields_vote(const uint32_t* __restrict__ sums, int rows, int64_t row_stride, i
 __global__ void __launch_bounds__(256)
 k_f64_sum_vote(const double* __restrict__ recv, int P, int64_t len, int64_t stride, int tree,
                int fill, VoteOut out, double* __restrict__ values, SyncD sy) {
+  griddep_wait();
   sync_wait(sy);
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -666,11 +698,8 @@ k_f64_sum_vote(const double* __restrict__ recv, int P, int64_t len, int64_t stri
     const uint32_t pb = __ballot_sync(kFull, valid && tot > 0.0);
     const uint32_t zb = __ballot_sync(kFull, valid && tot == 0.0);
     const uint32_t vb = __ballot_sync(kFull, valid);
-    if (lane < out.nout) {
-      reinterpret_cast<uint32_t*>(out.v.p[lane])[w] = pb | (fill > 0 ? zb : 0u);
-      if (out.nz.p[0]) reinterpret_cast<uint32_t*>(out.nz.p[lane])[w] = ~zb & vb;
-      if (out.tie.p[0]) reinterpret_cast<uint32_t*>(out.tie.p[lane])[w] = zb;
-    }
+    if (lane < (out.nout < 0 ? 1 : out.nout))
+      vote_store1(out, lane, w, pb | (fill > 0 ? zb : 0u), ~zb & vb, zb);
   }
   sync_arrive(sy);
 }
@@ -868,7 +897,8 @@ int launch_encode(const float* g, float* m, const uint8_t* mask, int64_t n, Hyp 
   auto kern = k_encode<ENC, F, MASK>;
   int64_t nsup = (n + 1023) >> 10;
   int grid = stream_grid(kern, kBlock, nsup, kBlock / 32);
-  kern<<<grid, kBlock, 0, st>>>(g, m, mask, n, h, fill, sq, dst, L, g_eoff, flags, g_sync);
+  LC_CUDA_TRY(launch_pdl(kern, grid, kBlock, 0, st, g, m, mask, n, h, fill, sq, dst, L, g_eoff,
+                         flags, g_sync));
   LC_LAUNCH_CHECK();
   return LC_OK;
 }
@@ -970,11 +1000,13 @@ int lc_apply_update(float* theta, int64_t n, void* const* sign_bits, void* const
   if (nz_bits) {
     auto kern = k_apply_update<true>;
     int grid = stream_grid(kern, kBlock, nsup, kBlock / 32);
-    kern<<<grid, kBlock, 0, st>>>(theta, n, sb, zb, wpb, woff, lr, wd, to_syncd(sync));
+    LC_CUDA_TRY(launch_pdl(kern, grid, kBlock, 0, st, theta, n, sb, zb, wpb, woff, lr, wd,
+                           to_syncd(sync)));
   } else {
     auto kern = k_apply_update<false>;
     int grid = stream_grid(kern, kBlock, nsup, kBlock / 32);
-    kern<<<grid, kBlock, 0, st>>>(theta, n, sb, sb, wpb, woff, lr, wd, to_syncd(sync));
+    LC_CUDA_TRY(launch_pdl(kern, grid, kBlock, 0, st, theta, n, sb, sb, wpb, woff, lr, wd,
+                           to_syncd(sync)));
   }
   LC_LAUNCH_CHECK();
   return LC_OK;
@@ -1002,7 +1034,7 @@ int lc_fused_local_step(float* theta, float* m, const float* g, const uint8_t* m
   do {                                                                                 \
     auto kern = k_fused_local<MODE, MASK, MET, U>;                                     \
     int grid = stream_grid(kern, kBlock, ntiles, (kBlock / 32) * U);                   \
-    kern<<<grid, kBlock, 0, st>>>(theta, m, g, mask, n, h, hp->lr, hp->weight_decay,   \
+    launch_pdl(kern, grid, kBlock, 0, st, theta, m, g, mask, n, h, hp->lr, hp->weight_decay, \
                                   fill, sq, sign_bits, nz_bits, tie_bits, flags);      \
   } while (0)
 #define LC_FUSED_M(MODE)                         \
@@ -1028,11 +1060,12 @@ int lc_fused_local_step(float* theta, float* m, const float* g, const uint8_t* m
 }
 
 bool make_out(VoteOut& o, void* const* v, void* const* nz, void* const* tie, int nout) {
-  if (!make_dst(o.v, v, nout)) return false;
+  const int nt = nout < 0 ? 1 : nout;  // nout == -1: one multicast address each
+  if (nout < -1 || nout == 0 || !make_dst(o.v, v, nt)) return false;
   o.nout = nout;
   for (int i = 0; i < LC_MAX_BLOCKS; ++i) o.nz.p[i] = o.tie.p[i] = nullptr;
-  if (nz && !make_dst(o.nz, nz, nout)) return false;
-  if (tie && !make_dst(o.tie, tie, nout)) return false;
+  if (nz && !make_dst(o.nz, nz, nt)) return false;
+  if (tie && !make_dst(o.tie, tie, nt)) return false;
   return true;
 }
 
@@ -1048,7 +1081,7 @@ int lc_vote_bits(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid, i
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int grid = generic_grid(cw / 4);
   const SyncD sy = to_syncd(sync);
-#define LC_VOTE(NP) k_vote_bits<NP><<<grid, kBlock, 0, st>>>(recv, P, cw, n_valid, fill, sum_mode, o, flags, sy)
+#define LC_VOTE(NP) LC_CUDA_TRY(launch_pdl(k_vote_bits<NP>, grid, kBlock, 0, st, recv, P, cw, n_valid, fill, sum_mode, o, flags, sy))
   if (P <= 1) LC_VOTE(1);
   else if (P <= 3) LC_VOTE(2);
   else if (P <= 7) LC_VOTE(3);
@@ -1075,7 +1108,7 @@ int lc_fields_vote(const uint32_t* sums, int32_t rows, int64_t row_stride, int64
   int64_t nin = (n * F + 31) / 32;
   int grid = generic_grid(nin);
   const SyncD sy = to_syncd(sync);
-#define LC_FV(FF) k_fields_vote<FF><<<grid, kBlock, 0, st>>>(sums, rows, row_stride, n, P, offset, binary, fill, o, values, sy)
+#define LC_FV(FF) LC_CUDA_TRY(launch_pdl(k_fields_vote<FF>, grid, kBlock, 0, st, sums, rows, row_stride, n, P, offset, binary, fill, o, values, sy))
   switch (F) {
     case 1: LC_FV(1); break;
     case 2: LC_FV(2); break;
@@ -1101,8 +1134,8 @@ int lc_f64_sum_vote(const double* recv, int32_t P, int64_t len, int64_t stride, 
     return set_err(LC_E_ARG, "lc_f64_sum_vote: bad pointers / output table");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int grid = generic_grid(len);
-  k_f64_sum_vote<<<grid, kBlock, 0, st>>>(recv, P, len, stride, tree, fill, o, values,
-                                          to_syncd(sync));
+  LC_CUDA_TRY(launch_pdl(k_f64_sum_vote, grid, kBlock, 0, st, recv, P, len, stride, tree, fill, o,
+                         values, to_syncd(sync)));
   LC_LAUNCH_CHECK();
   return LC_OK;
 }

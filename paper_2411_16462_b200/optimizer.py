@@ -184,6 +184,9 @@ def _to_flat(ps: Mapping[str, torch.Tensor], layout: Layout, dev) -> FlatParamSe
 
 
 def _check_shapes(params: Mapping, grad: Mapping):
+    if isinstance(params, FlatParamSet) and isinstance(grad, FlatParamSet) and (
+            grad.layout is params.layout or grad.layout.key == params.layout.key):
+        return  # same flat layout: names and shapes agree by construction
     if set(params) != set(grad):
         raise ConfigError(f"layer mismatch: {sorted(params)} vs {sorted(grad)}")
     for name in params:
@@ -275,6 +278,7 @@ class _Workspace:
         self.flags = z(1)
         self.counters = z(4)   # arrive counters of the in-kernel barriers
         self.k5_sync = None
+        self.syncs = None
         self.l1 = None
         self.norms = self.scales = None
         if kind == "f64":
@@ -295,6 +299,18 @@ class _Workspace:
             self.nz = sym("nz", P * cw) if ternary else None
             self.ties = sym("ties", P * cw) if metrics else None
             self.dst = _lib.table([self.recv.peers[j] + r * blk_bytes for j in range(P)])
+            used = [b for b in (self.full, self.nz, self.ties) if b is not None]
+            if all(getattr(b, "mc", 0) for b in used):
+                # NVLS: the owner stores its voted block once to the multicast
+                # address; the NVSwitch writes it into every rank's buffer
+                mco = lambda b: None if b is None else _lib.table(  # noqa: E731
+                    [b.mc + r * cw * 4])
+                self.vout, self.nzout, self.tout = mco(self.full), mco(self.nz), mco(self.ties)
+                self.nout = -1
+                self.src = _lib.table([self.full.local.data_ptr()])
+                self.nzsrc = None if self.nz is None else _lib.table([self.nz.local.data_ptr()])
+                self.nsrc, self.wpb = 1, P * cw
+                return
             if metrics or os.environ.get("LIONCUB_VOTE_PUSH", "1") == "1":
                 # metrics need every block locally: owners push to all ranks
                 outs = lambda b: None if b is None else _lib.table(  # noqa: E731
@@ -664,9 +680,13 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
         # the barriers live inside the kernels: K1's last CTA publishes e1,
         # the vote waits for e1 and publishes e2, K5 waits for e2
         e1, e2 = tp.take_epochs(r, 2)
-        sy1 = C.byref(tp.sync_struct(r, ws.counters[0:1], 0, e1))
-        sy2 = C.byref(tp.sync_struct(r, ws.counters[1:2], e1, e2))
-        sy3 = C.byref(tp.sync_struct(r, ws.counters[2:3], e2, 0))
+        if ws.syncs is None:   # built once per workspace; only epochs change
+            ws.syncs = [tp.sync_struct(r, ws.counters[i:i + 1], 0, 0) for i in range(3)]
+        a, b, c = ws.syncs
+        a.wait_epoch, a.arrive_epoch = 0, e1
+        b.wait_epoch, b.arrive_epoch = e1, e2
+        c.wait_epoch, c.arrive_epoch = e2, 0
+        sy1, sy2, sy3 = C.byref(a), C.byref(b), C.byref(c)
         ws.k5_sync = sy3
     if pipe is not None and segs is None and mflat is None:
         # encode each gradient chunk as soon as it landed; the last chunk's

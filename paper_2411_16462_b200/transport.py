@@ -45,11 +45,14 @@ DEFAULT_TIMEOUT = 30.0
 
 class SymBuffer:
     """A buffer mapped on every rank: ``local`` is this rank's tensor,
-    ``peers[j]`` the device address of rank j's buffer (usable here)."""
+    ``peers[j]`` the device address of rank j's buffer (usable here), and
+    ``mc`` (0 if unavailable) an NVLS multicast address: one multimem store
+    there lands in every rank's buffer through the NVSwitch."""
 
-    def __init__(self, local: torch.Tensor, peers: list, keep=None):
+    def __init__(self, local: torch.Tensor, peers: list, keep=None, mc: int = 0):
         self.local = local
         self.peers = peers
+        self.mc = mc
         self._keep = keep
 
     def peer(self, j: int, byte_offset: int = 0) -> int:
@@ -285,6 +288,8 @@ class NcclTransport(DeviceTransport):
         if p2p is None:
             p2p = os.environ.get("LIONCUB_P2P", "1") != "0" and world_size > 1
         self.p2p = bool(p2p)
+        # NVLS multicast gather buffers (process-per-GPU, torch symmetric memory)
+        self._nvls_ok = (not threaded) and os.environ.get("LIONCUB_NVLS", "1") != "0"
         if self.p2p and threaded:
             lib = _lib.load()
             devs = [devices[r].index for r in range(world_size)]
@@ -341,11 +346,15 @@ class NcclTransport(DeviceTransport):
         dev = self._devices[rank]
         if self._threaded:
             t = torch.zeros(max(numel, 1), dtype=dtype, device=dev)
+            torch.cuda.synchronize(dev)  # zeroed before any peer may write into it
             self._posts[rank] = t.data_ptr()
             self._rv.wait(rank, 0, "sym_buffer:post", DEFAULT_TIMEOUT)
             peers = list(self._posts)
             self._rv.wait(rank, 0, "sym_buffer:done", DEFAULT_TIMEOUT)
             buf = SymBuffer(t, peers)
+        elif self._nvls_ok and key[-1] in ("full", "nz", "ties", "momentum") \
+                and self._try_torch_symm(rank, k, numel, dtype):
+            return self._sym[k]
         else:
             import torch.distributed as dist
             lib = _lib.load()
@@ -371,6 +380,38 @@ class NcclTransport(DeviceTransport):
             buf = SymBuffer(_wrap(p.value, max(numel, 1), dtype, dev), peers)
         self._sym[k] = buf
         return buf
+
+    def _try_torch_symm(self, rank, k, numel, dtype) -> bool:
+        """Allocate through torch's symmetric memory to obtain an NVLS
+        multicast address (process-per-GPU only).  False -> fall back."""
+        import torch.distributed as dist
+        try:
+            import torch.distributed._symmetric_memory as symm
+            import warnings
+            group = self._group or dist.group.WORLD
+            name = group.group_name
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                if not symm.is_symm_mem_enabled_for_group(name):
+                    symm.enable_symm_mem_for_group(name)
+            dev = self._devices[rank]
+            nbytes = max(numel, 1) * torch.empty((), dtype=dtype).element_size()
+            nbytes = -(-nbytes // 16) * 16
+            t = symm.empty(nbytes, dtype=torch.uint8, device=dev)
+            hdl = symm.rendezvous(t, name)
+            mc = int(hdl.multicast_ptr) if hdl.has_multicast_support() else 0
+            if not mc:
+                return False
+            t.zero_()
+            torch.cuda.synchronize(dev)
+            dist.barrier(group=group)  # every rank zeroed before anyone writes
+            self._sym[k] = SymBuffer(t[:max(numel, 1) * torch.empty((), dtype=dtype)
+                                       .element_size()].view(dtype),
+                                     [int(p) for p in hdl.buffer_ptrs], keep=(t, hdl), mc=mc)
+            return True
+        except Exception:
+            self._nvls_ok = False
+            return False
 
     def _flags(self, rank):
         flags = self.sym_buffer(rank, ("__barrier__",), self.world_size, torch.int64)
