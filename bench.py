@@ -369,7 +369,6 @@ def main():
     # synthetic state: theta shared (seed 0), m and g per rank; g = base + noise
     gen = torch.Generator(device=dev)
     gen.manual_seed(0)
-    st = lc.WorkerState.initial({"_": torch.zeros(1, device=dev)})  # placeholder
     layout = lc.Layout(shapes)
     theta = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
     theta.normal_(generator=gen)
@@ -382,6 +381,7 @@ def main():
     grad = base.add_(noise)
     del noise
     st = lc.WorkerState(params=layout.views(theta), momentum=layout.views(mom), iteration=0)
+    del mom  # the state owns it (a P2P sync may re-home it; do not pin the old buffer)
     g = layout.views(grad)
     stream = topo.stream
     torch.cuda.synchronize()

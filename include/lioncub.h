@@ -289,7 +289,8 @@ int lc_barrier(void* const* peer_flags, int32_t P, int32_t rank, uint64_t* my_fl
                uint64_t epoch, double timeout_s, uint32_t* err, void* stream);
 /* Momentum sync over peer memory (collectives.py:319-344): push block j of a
  * fp32 vector (blocks of s) to dst[j]; the owner then averages its P rows in
- * float64 rank order and stores the fp32 mean to every out[k]. */
+ * float64 rank order and stores the fp32 mean to every out[k] (nout = -1:
+ * out[0] is an NVLS multicast address, one store reaches every rank). */
 int lc_push_blocks_f32(const float* src, int64_t len, int64_t s, void* const* dst,
                        int32_t P, void* stream);
 int lc_mean_bcast_f32(const float* recv, int32_t P, int64_t cnt, int64_t s,

@@ -72,7 +72,12 @@ k_mean_bcast(const float* __restrict__ recv, int P, int64_t cnt, int64_t s, Ptrs
     double acc = (double)__ldcs(recv + i);
     for (int j = 1; j < P; ++j) acc = __dadd_rn(acc, (double)__ldcs(recv + (int64_t)j * s + i));
     const float v = __double2float_rn(__ddiv_rn(acc, dp));
-    for (int k = 0; k < nout; ++k) reinterpret_cast<float*>(out.p[k])[i] = v;
+    if (nout < 0) {  // NVLS multicast: one store reaches every rank
+      asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;"
+                   ::"l"(reinterpret_cast<float*>(out.p[0]) + i), "f"(v) : "memory");
+    } else {
+      for (int k = 0; k < nout; ++k) reinterpret_cast<float*>(out.p[k])[i] = v;
+    }
   }
 }
 
@@ -173,7 +178,7 @@ int lc_push_blocks_f32(const float* src, int64_t len, int64_t s, void* const* ds
 int lc_mean_bcast_f32(const float* recv, int32_t P, int64_t cnt, int64_t s, void* const* out,
                       int32_t nout, void* stream) {
   Ptrs o;
-  if (cnt < 0 || P < 1 || !recv || !make_ptrs(o, out, nout))
+  if (cnt < 0 || P < 1 || !recv || nout == 0 || nout < -1 || !make_ptrs(o, out, nout < 0 ? 1 : nout))
     return lc::set_err(LC_E_ARG, "lc_mean_bcast_f32: bad arguments");
   if (cnt == 0) return LC_OK;
   k_mean_bcast<<<grid_for(cnt), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(recv, P, cnt, s, o, nout);

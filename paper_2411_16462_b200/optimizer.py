@@ -46,6 +46,7 @@ from .errors import CollectiveError, ConfigError
 from .quant import QuantSpec, SignPolicy
 
 LrSchedule = Union[float, Callable[[int], float]]
+SYNC_PIECE = 1 << 27   # elements per momentum-sync exchange piece
 VOTE_ALGOS = ("ps", "ps_efficient", "direct", "compressed1bit")
 
 
@@ -765,7 +766,7 @@ def _symmetric_momentum(m: FlatParamSet, topo: Topology) -> FlatParamSet:
     if getattr(m, "sym", None) is not None:
         return m
     layout = m.layout
-    buf = topo.transport.sym_buffer(topo.rank, ("momentum", layout.key), max(layout.n, 1),
+    buf = topo.transport.sym_buffer(topo.rank, (layout.key, "momentum"), max(layout.n, 1),
                                     torch.float32)
     buf.local.copy_(m.flat)
     out = FlatParamSet(buf.local, layout)
@@ -798,8 +799,13 @@ def maybe_sync_momentum(state: WorkerState, policy: SyncPolicy,
             st = topo.stream.cuda_stream
             if tp.p2p:
                 m = _symmetric_momentum(m, topo)
+                # pieces bound the staging buffer (7B all-layer sync fits HBM)
+                pieces = [(a0, min(b, a0 + SYNC_PIECE)) for a, b in runs
+                          for a0 in range(a, b, SYNC_PIECE)]
+                smax = -(-max(b - a for a, b in pieces) // P)
                 stage = tp.sym_buffer(r, ("sync_stage", P, smax), P * smax, torch.float32)
-                for a, b in runs:
+                mc = getattr(m.sym, "mc", 0)
+                for a, b in pieces:
                     gen = topo.next_generation()
                     ln = b - a
                     sr = -(-ln // P)
@@ -808,9 +814,13 @@ def maybe_sync_momentum(state: WorkerState, policy: SyncPolicy,
                               _lib.table([stage.peers[j] + r * sr * 4 for j in range(P)]),
                               P, st)
                     tp.device_barrier(r, gen)
-                    _lib.call("lc_mean_bcast_f32", stage.local.data_ptr(), P, cnt, sr,
-                              _lib.table([m.sym.peers[j] + (a + r * sr) * 4
-                                          for j in range(P)]), P, st)
+                    if mc:   # NVLS: one multimem store reaches every rank's m
+                        outs, nout = _lib.table([mc + (a + r * sr) * 4]), -1
+                    else:
+                        outs = _lib.table([m.sym.peers[j] + (a + r * sr) * 4 for j in range(P)])
+                        nout = P
+                    _lib.call("lc_mean_bcast_f32", stage.local.data_ptr(), P, cnt, sr, outs,
+                              nout, st)
                     tp.device_barrier(r, gen)
             else:
                 key = ("sync", P, smax)
