@@ -50,28 +50,79 @@ __global__ void k_barrier(Ptrs peer_flags, uint64_t* __restrict__ my_flags, int 
 }
 
 // dst[j][i] = src[j*s + i] for i < min(s, len - j*s): an owner-blocked
-// scatter of one fp32 vector to P destinations (peer receive slots).
+// scatter of one fp32 vector to P destinations (peer receive slots).  With
+// src 16-byte aligned and s % 4 == 0 every quad stays inside one block and
+// moves as one 128-bit load / (peer) store.
 __global__ void __launch_bounds__(256)
-k_push_blocks(const float* __restrict__ src, int64_t len, int64_t s, Ptrs dst, int P) {
-  const int64_t total = len;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
+k_push_blocks(const float* __restrict__ src, int64_t len, int64_t s, Ptrs dst, int P, int vec) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t done = 0;
+  if (vec) {
+    const int64_t nq = len >> 2;
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += stride) {
+      const int64_t e = q << 2;
+      const int j = (int)(e / s);
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(dst.p[j]) + (e - (int64_t)j * s)) =
+          __ldcs(s4 + q);
+    }
+    done = nq << 2;
+  }
+  for (int64_t e = done + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < len; e += stride) {
     const int j = (int)(e / s);
     reinterpret_cast<float*>(dst.p[j])[e - (int64_t)j * s] = __ldcs(src + e);
   }
 }
 
+__device__ __forceinline__ float mean_rows(const float* __restrict__ recv, int P, int64_t s,
+                                           int64_t i, double dp) {
+  double acc = (double)__ldcs(recv + i);
+  for (int j = 1; j < P; ++j) acc = __dadd_rn(acc, (double)__ldcs(recv + (int64_t)j * s + i));
+  return __double2float_rn(__ddiv_rn(acc, dp));
+}
+
 // out[k][i] = fp32( (sum_j f64(recv[j][i])) / P ) for every destination k:
 // the reference's rank-ordered float64 mean (collectives.py:336-340), with
-// the broadcast (:344) fused as peer stores.
+// the broadcast (:344) fused as peer stores, or as ONE NVLS multicast store
+// (nout = -1).  Quads (128-bit rows/stores) when s and the outputs allow.
 __global__ void __launch_bounds__(256)
-k_mean_bcast(const float* __restrict__ recv, int P, int64_t cnt, int64_t s, Ptrs out, int nout) {
+k_mean_bcast(const float* __restrict__ recv, int P, int64_t cnt, int64_t s, Ptrs out, int nout,
+             int vec) {
   const double dp = (double)P;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    double acc = (double)__ldcs(recv + i);
-    for (int j = 1; j < P; ++j) acc = __dadd_rn(acc, (double)__ldcs(recv + (int64_t)j * s + i));
-    const float v = __double2float_rn(__ddiv_rn(acc, dp));
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t done = 0;
+  if (vec) {
+    const int64_t nq = cnt >> 2;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += stride) {
+      const int64_t i = q << 2;
+      double acc[4];
+      float4 x = __ldcs(reinterpret_cast<const float4*>(recv + i));
+      acc[0] = x.x; acc[1] = x.y; acc[2] = x.z; acc[3] = x.w;
+      for (int j = 1; j < P; ++j) {
+        x = __ldcs(reinterpret_cast<const float4*>(recv + (int64_t)j * s + i));
+        acc[0] = __dadd_rn(acc[0], (double)x.x);
+        acc[1] = __dadd_rn(acc[1], (double)x.y);
+        acc[2] = __dadd_rn(acc[2], (double)x.z);
+        acc[3] = __dadd_rn(acc[3], (double)x.w);
+      }
+      float4 v;
+      v.x = __double2float_rn(__ddiv_rn(acc[0], dp));
+      v.y = __double2float_rn(__ddiv_rn(acc[1], dp));
+      v.z = __double2float_rn(__ddiv_rn(acc[2], dp));
+      v.w = __double2float_rn(__ddiv_rn(acc[3], dp));
+      if (nout < 0) {
+        asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};"
+                     ::"l"(reinterpret_cast<float*>(out.p[0]) + i), "f"(v.x), "f"(v.y),
+                     "f"(v.z), "f"(v.w) : "memory");
+      } else {
+        for (int k = 0; k < nout; ++k)
+          *reinterpret_cast<float4*>(reinterpret_cast<float*>(out.p[k]) + i) = v;
+      }
+    }
+    done = nq << 2;
+  }
+  for (int64_t i = done + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += stride) {
+    const float v = mean_rows(recv, P, s, i, dp);
     if (nout < 0) {  // NVLS multicast: one store reaches every rank
       asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;"
                    ::"l"(reinterpret_cast<float*>(out.p[0]) + i), "f"(v) : "memory");
@@ -164,13 +215,18 @@ int lc_barrier(void* const* peer_flags, int32_t P, int32_t rank, uint64_t* my_fl
   return LC_OK;
 }
 
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
 int lc_push_blocks_f32(const float* src, int64_t len, int64_t s, void* const* dst, int32_t P,
                        void* stream) {
   Ptrs d;
   if (len < 0 || s <= 0 || (len + s - 1) / s > P || !make_ptrs(d, dst, P))
     return lc::set_err(LC_E_ARG, "lc_push_blocks_f32: bad arguments");
   if (len == 0) return LC_OK;
-  k_push_blocks<<<grid_for(len), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(src, len, s, d, P);
+  int vec = aligned16(src) && (s % 4) == 0;
+  for (int j = 0; j < P && vec; ++j) vec = aligned16(d.p[j]);
+  k_push_blocks<<<grid_for(vec ? len / 4 : len), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      src, len, s, d, P, vec);
   LC_LAUNCH_CHECK();
   return LC_OK;
 }
@@ -178,10 +234,14 @@ int lc_push_blocks_f32(const float* src, int64_t len, int64_t s, void* const* ds
 int lc_mean_bcast_f32(const float* recv, int32_t P, int64_t cnt, int64_t s, void* const* out,
                       int32_t nout, void* stream) {
   Ptrs o;
-  if (cnt < 0 || P < 1 || !recv || nout == 0 || nout < -1 || !make_ptrs(o, out, nout < 0 ? 1 : nout))
+  const int nt = nout < 0 ? 1 : nout;
+  if (cnt < 0 || P < 1 || !recv || nout == 0 || nout < -1 || !make_ptrs(o, out, nt))
     return lc::set_err(LC_E_ARG, "lc_mean_bcast_f32: bad arguments");
   if (cnt == 0) return LC_OK;
-  k_mean_bcast<<<grid_for(cnt), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(recv, P, cnt, s, o, nout);
+  int vec = aligned16(recv) && (s % 4) == 0;
+  for (int k = 0; k < nt && vec; ++k) vec = aligned16(o.p[k]);
+  k_mean_bcast<<<grid_for(vec ? cnt / 4 : cnt), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      recv, P, cnt, s, o, nout, vec);
   LC_LAUNCH_CHECK();
   return LC_OK;
 }

@@ -46,7 +46,7 @@ from .errors import CollectiveError, ConfigError
 from .quant import QuantSpec, SignPolicy
 
 LrSchedule = Union[float, Callable[[int], float]]
-SYNC_PIECE = 1 << 27   # elements per momentum-sync exchange piece
+SYNC_PIECE = 1 << 28   # elements per momentum-sync exchange piece
 VOTE_ALGOS = ("ps", "ps_efficient", "direct", "compressed1bit")
 
 
@@ -802,13 +802,15 @@ def maybe_sync_momentum(state: WorkerState, policy: SyncPolicy,
                 # pieces bound the staging buffer (7B all-layer sync fits HBM)
                 pieces = [(a0, min(b, a0 + SYNC_PIECE)) for a, b in runs
                           for a0 in range(a, b, SYNC_PIECE)]
-                smax = -(-max(b - a for a, b in pieces) // P)
+                smax = -(-(-(-max(b - a for a, b in pieces) // P)) // 4) * 4
                 stage = tp.sym_buffer(r, ("sync_stage", P, smax), P * smax, torch.float32)
                 mc = getattr(m.sym, "mc", 0)
                 for a, b in pieces:
                     gen = topo.next_generation()
                     ln = b - a
                     sr = -(-ln // P)
+                    if a % 4 == 0:
+                        sr = -(-sr // 4) * 4   # 16-byte aligned owner blocks
                     cnt = max(0, min(sr, ln - r * sr))
                     _lib.call("lc_push_blocks_f32", _off(m.flat, a), ln, sr,
                               _lib.table([stage.peers[j] + r * sr * 4 for j in range(P)]),
