@@ -295,6 +295,12 @@ int lc_push_blocks_f32(const float* src, int64_t len, int64_t s, void* const* ds
                        int32_t P, void* stream);
 int lc_mean_bcast_f32(const float* recv, int32_t P, int64_t cnt, int64_t s,
                       void* const* out, int32_t nout, void* stream);
+/* Same mean without staging: the owner loads elements [off, off+cnt) of
+ * every rank's momentum directly (src[j] = rank j's buffer, peer pointers)
+ * and stores the fp32 mean to out (nout = -1: NVLS multicast base; else
+ * nout per-rank base pointers).  Ranks' buffers must be final (barrier). */
+int lc_mean_pull_f32(void* const* src, int32_t P, int64_t off, int64_t cnt,
+                     void* const* out, int32_t nout, void* stream);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

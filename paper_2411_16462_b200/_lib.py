@@ -109,6 +109,7 @@ SIGNATURES = {
     "lc_barrier": (INT, [P, I32, I32, P, C.c_uint64, D, P, P]),
     "lc_push_blocks_f32": (INT, [P, I64, I64, P, I32, P]),
     "lc_mean_bcast_f32": (INT, [P, I32, I64, I64, P, I32, P]),
+    "lc_mean_pull_f32": (INT, [P, I32, I64, I64, P, I32, P]),
 }
 
 _lock = threading.Lock()
@@ -159,7 +160,7 @@ def check(rc: int, what: str = "", rank=None, generation=None):
 # Entry points that enqueue one of OUR kernels (for launch accounting).
 KERNEL_CALLS = frozenset({
     "lc_encode", "lc_vote_bits", "lc_fields_vote", "lc_f64_sum_vote",
-    "lc_barrier", "lc_push_blocks_f32", "lc_mean_bcast_f32",
+    "lc_barrier", "lc_push_blocks_f32", "lc_mean_bcast_f32", "lc_mean_pull_f32",
     "lc_apply_update", "lc_fused_local_step", "lc_mean_f32", "lc_compute_c",
     "lc_count_bits_segmented", "lc_bits_to_sign", "lc_pack_i64_fields",
     "lc_fields_decode", "lc_sign_pack_f64", "lc_sum_u32_rows"})

@@ -132,6 +132,60 @@ k_mean_bcast(const float* __restrict__ recv, int P, int64_t cnt, int64_t s, Ptrs
   }
 }
 
+// Owner-side momentum mean pulled straight from every rank's momentum over
+// NVLink (no staging): element i of the owner's block, from P rows m_j[i],
+// summed in float64 in rank order, divided once, rounded once to fp32, and
+// stored to every rank (NVLS multicast, or one store per rank).
+__global__ void __launch_bounds__(256)
+k_mean_pull(Ptrs src, int P, int64_t off, int64_t cnt, Ptrs out, int nout, int vec) {
+  const double dp = (double)P;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t done = 0;
+  if (vec) {
+    const int64_t nq = cnt >> 2;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += stride) {
+      const int64_t i = off + (q << 2);
+      double acc[4];
+      float4 x = __ldcv(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(src.p[0]) + i));
+      acc[0] = x.x; acc[1] = x.y; acc[2] = x.z; acc[3] = x.w;
+      for (int j = 1; j < P; ++j) {
+        x = __ldcv(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(src.p[j]) + i));
+        acc[0] = __dadd_rn(acc[0], (double)x.x);
+        acc[1] = __dadd_rn(acc[1], (double)x.y);
+        acc[2] = __dadd_rn(acc[2], (double)x.z);
+        acc[3] = __dadd_rn(acc[3], (double)x.w);
+      }
+      float4 v;
+      v.x = __double2float_rn(__ddiv_rn(acc[0], dp));
+      v.y = __double2float_rn(__ddiv_rn(acc[1], dp));
+      v.z = __double2float_rn(__ddiv_rn(acc[2], dp));
+      v.w = __double2float_rn(__ddiv_rn(acc[3], dp));
+      if (nout < 0) {
+        asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};"
+                     ::"l"(reinterpret_cast<float*>(out.p[0]) + i), "f"(v.x), "f"(v.y),
+                     "f"(v.z), "f"(v.w) : "memory");
+      } else {
+        for (int k = 0; k < nout; ++k)
+          *reinterpret_cast<float4*>(reinterpret_cast<float*>(out.p[k]) + i) = v;
+      }
+    }
+    done = nq << 2;
+  }
+  for (int64_t t = done + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += stride) {
+    const int64_t i = off + t;
+    double acc = (double)__ldcv(reinterpret_cast<const float*>(src.p[0]) + i);
+    for (int j = 1; j < P; ++j)
+      acc = __dadd_rn(acc, (double)__ldcv(reinterpret_cast<const float*>(src.p[j]) + i));
+    const float v = __double2float_rn(__ddiv_rn(acc, dp));
+    if (nout < 0) {
+      asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;"
+                   ::"l"(reinterpret_cast<float*>(out.p[0]) + i), "f"(v) : "memory");
+    } else {
+      for (int k = 0; k < nout; ++k) reinterpret_cast<float*>(out.p[k])[i] = v;
+    }
+  }
+}
+
 bool make_ptrs(Ptrs& d, void* const* src, int n) {
   if (n < 1 || n > LC_MAX_BLOCKS || !src) return false;
   for (int i = 0; i < LC_MAX_BLOCKS; ++i) d.p[i] = i < n ? src[i] : nullptr;
@@ -242,6 +296,23 @@ int lc_mean_bcast_f32(const float* recv, int32_t P, int64_t cnt, int64_t s, void
   for (int k = 0; k < nt && vec; ++k) vec = aligned16(o.p[k]);
   k_mean_bcast<<<grid_for(vec ? cnt / 4 : cnt), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       recv, P, cnt, s, o, nout, vec);
+  LC_LAUNCH_CHECK();
+  return LC_OK;
+}
+
+int lc_mean_pull_f32(void* const* src, int32_t P, int64_t off, int64_t cnt, void* const* out,
+                     int32_t nout, void* stream) {
+  Ptrs sp, o;
+  const int nt = nout < 0 ? 1 : nout;
+  if (cnt < 0 || off < 0 || P < 1 || nout == 0 || nout < -1 || !make_ptrs(sp, src, P) ||
+      !make_ptrs(o, out, nt))
+    return lc::set_err(LC_E_ARG, "lc_mean_pull_f32: bad arguments");
+  if (cnt == 0) return LC_OK;
+  int vec = (off % 4) == 0;
+  for (int j = 0; j < P && vec; ++j) vec = aligned16(sp.p[j]);
+  for (int k = 0; k < nt && vec; ++k) vec = aligned16(o.p[k]);
+  k_mean_pull<<<grid_for(vec ? cnt / 4 : cnt), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      sp, P, off, cnt, o, nout, vec);
   LC_LAUNCH_CHECK();
   return LC_OK;
 }

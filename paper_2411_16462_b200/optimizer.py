@@ -798,32 +798,25 @@ def maybe_sync_momentum(state: WorkerState, policy: SyncPolicy,
             smax = -(-longest // P)
             st = topo.stream.cuda_stream
             if tp.p2p:
+                # owner r pulls block r of every selected range from every
+                # rank's momentum over NVLink, averages (f64, rank order) and
+                # stores the mean into every rank's momentum -- one kernel per
+                # range, one barrier before (all m' final) and one after
                 m = _symmetric_momentum(m, topo)
-                # pieces bound the staging buffer (7B all-layer sync fits HBM)
-                pieces = [(a0, min(b, a0 + SYNC_PIECE)) for a, b in runs
-                          for a0 in range(a, b, SYNC_PIECE)]
-                smax = -(-(-(-max(b - a for a, b in pieces) // P)) // 4) * 4
-                stage = tp.sym_buffer(r, ("sync_stage", P, smax), P * smax, torch.float32)
                 mc = getattr(m.sym, "mc", 0)
-                for a, b in pieces:
-                    gen = topo.next_generation()
+                gen = topo.next_generation()
+                tp.device_barrier(r, gen)
+                src = _lib.table(m.sym.peers)
+                outs, nout = ((_lib.table([mc]), -1) if mc else
+                              (_lib.table(m.sym.peers), P))
+                for a, b in runs:
                     ln = b - a
                     sr = -(-ln // P)
                     if a % 4 == 0:
                         sr = -(-sr // 4) * 4   # 16-byte aligned owner blocks
                     cnt = max(0, min(sr, ln - r * sr))
-                    _lib.call("lc_push_blocks_f32", _off(m.flat, a), ln, sr,
-                              _lib.table([stage.peers[j] + r * sr * 4 for j in range(P)]),
-                              P, st)
-                    tp.device_barrier(r, gen)
-                    if mc:   # NVLS: one multimem store reaches every rank's m
-                        outs, nout = _lib.table([mc + (a + r * sr) * 4]), -1
-                    else:
-                        outs = _lib.table([m.sym.peers[j] + (a + r * sr) * 4 for j in range(P)])
-                        nout = P
-                    _lib.call("lc_mean_bcast_f32", stage.local.data_ptr(), P, cnt, sr, outs,
-                              nout, st)
-                    tp.device_barrier(r, gen)
+                    _lib.call("lc_mean_pull_f32", src, P, a + r * sr, cnt, outs, nout, st)
+                tp.device_barrier(r, gen)
             else:
                 key = ("sync", P, smax)
                 scratch = m.workspace.get(key)
