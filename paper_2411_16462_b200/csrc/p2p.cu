@@ -146,10 +146,10 @@ k_mean_pull(Ptrs src, int P, int64_t off, int64_t cnt, Ptrs out, int nout, int v
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += stride) {
       const int64_t i = off + (q << 2);
       double acc[4];
-      float4 x = __ldcv(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(src.p[0]) + i));
+      float4 x = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(src.p[0]) + i);
       acc[0] = x.x; acc[1] = x.y; acc[2] = x.z; acc[3] = x.w;
       for (int j = 1; j < P; ++j) {
-        x = __ldcv(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(src.p[j]) + i));
+        x = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(src.p[j]) + i);
         acc[0] = __dadd_rn(acc[0], (double)x.x);
         acc[1] = __dadd_rn(acc[1], (double)x.y);
         acc[2] = __dadd_rn(acc[2], (double)x.z);

@@ -288,8 +288,11 @@ class NcclTransport(DeviceTransport):
         if p2p is None:
             p2p = os.environ.get("LIONCUB_P2P", "1") != "0" and world_size > 1
         self.p2p = bool(p2p)
-        # NVLS multicast gather buffers (process-per-GPU, torch symmetric memory)
-        self._nvls_ok = (not threaded) and os.environ.get("LIONCUB_NVLS", "1") != "0"
+        # NVLS multicast gather buffers (process-per-GPU, torch symmetric
+        # memory).  Off by default: measured on this pool, multimem stores
+        # reach 179 GB/s vs 683 GB/s for plain stores to every peer
+        # (tests/nvlink_microbench.py, profiles/r01_summary.md).
+        self._nvls_ok = (not threaded) and os.environ.get("LIONCUB_NVLS", "0") == "1"
         if self.p2p and threaded:
             lib = _lib.load()
             devs = [devices[r].index for r in range(world_size)]
@@ -399,9 +402,9 @@ class NcclTransport(DeviceTransport):
             nbytes = -(-nbytes // 16) * 16
             t = symm.empty(nbytes, dtype=torch.uint8, device=dev)
             hdl = symm.rendezvous(t, name)
-            mc = int(hdl.multicast_ptr) if hdl.has_multicast_support() else 0
+            mc = int(hdl.multicast_ptr or 0)
             if not mc:
-                return False
+                raise RuntimeError("no multicast support reported")
             t.zero_()
             torch.cuda.synchronize(dev)
             dist.barrier(group=group)  # every rank zeroed before anyone writes
@@ -409,7 +412,10 @@ class NcclTransport(DeviceTransport):
                                        .element_size()].view(dtype),
                                      [int(p) for p in hdl.buffer_ptrs], keep=(t, hdl), mc=mc)
             return True
-        except Exception:
+        except Exception as exc:  # fall back to cudaMalloc + CUDA IPC, say why once
+            import sys
+            print(f"[lioncub] NVLS multicast buffers unavailable ({type(exc).__name__}: "
+                  f"{exc}); using peer stores", file=sys.stderr)
             self._nvls_ok = False
             return False
 
