@@ -187,11 +187,24 @@ k_l1_max(const float* __restrict__ g, const float* __restrict__ m,
 #pragma unroll
     for (int u = 0; u < QU; ++u) {
       const int64_t q = q0 + (int64_t)u * blockDim.x;
-      if (q < q_hi) {
-        take(4 * q, gv[u].x, mv[u].x);
-        take(4 * q + 1, gv[u].y, mv[u].y);
-        take(4 * q + 2, gv[u].z, mv[u].z);
-        take(4 * q + 3, gv[u].w, mv[u].w);
+      if (q >= q_hi) continue;
+      const int64_t e = 4 * q;
+      if (!mask && e >= seg_lo && e + 4 <= seg_hi) {
+        // the whole quad lies in the current segment: no per-element checks
+        const double c0 = fabs(lc::lion_c(mv[u].x, gv[u].x, h));
+        const double c1 = fabs(lc::lion_c(mv[u].y, gv[u].y, h));
+        const double c2 = fabs(lc::lion_c(mv[u].z, gv[u].z, h));
+        const double c3 = fabs(lc::lion_c(mv[u].w, gv[u].w, h));
+        // max on the bit patterns (non-negative doubles order as unsigned;
+        // a NaN propagates like numpy's max)
+        auto bits = [](double x) { return (unsigned long long)__double_as_longlong(x); };
+        const unsigned long long b = max(max(bits(c0), bits(c1)), max(bits(c2), bits(c3)));
+        cur = b > cur ? b : cur;
+      } else {
+        take(e, gv[u].x, mv[u].x);
+        take(e + 1, gv[u].y, mv[u].y);
+        take(e + 2, gv[u].z, mv[u].z);
+        take(e + 3, gv[u].w, mv[u].w);
       }
     }
   }
