@@ -424,6 +424,7 @@ def main():
     for _ in range(args.steps):
         st = step(st)
     e1.record(stream)
+    host_ms = (time.perf_counter() - w0) * 1e3 / args.steps  # enqueue cost per step
     barrier()
     w1 = time.perf_counter()
     launches = _lib.launches - l0
@@ -525,6 +526,7 @@ def main():
                            "l2": "inputs larger than L2 (no flush needed)"},
                 "roofline": roof, "step_roofline": sr, "kernels": kern,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "host_enqueue_ms_per_step": host_ms,
                 "clocks": clocks}
         print(json.dumps(line))
     if world > 1:

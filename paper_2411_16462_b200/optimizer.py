@@ -30,6 +30,7 @@ Step pipelines (P = topo.world_size, n = params in the flat buffer):
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import hashlib
 import math
@@ -407,6 +408,20 @@ def _off(t: torch.Tensor, elems: int) -> int:
     return t.data_ptr() + elems * t.element_size()
 
 
+_NULL = contextlib.nullcontext()
+
+
+def _on_device(dev):
+    """torch.cuda.device(dev) only when dev is not already current (the
+    context managers are a measurable part of a small step's host cost)."""
+    return _NULL if torch.cuda.current_device() == dev.index else torch.cuda.device(dev)
+
+
+def _on_stream(stream, dev):
+    cur = torch.cuda.current_stream(dev)
+    return _NULL if cur.cuda_stream == stream.cuda_stream else torch.cuda.stream(stream)
+
+
 def _raise_flags(bits: int, binary: bool):
     if bits & (_lib.LC_FLAG_ZERO_SIGN | _lib.LC_FLAG_TIE_TERNARY):
         if binary:
@@ -565,10 +580,10 @@ def _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out,
                               generation=topo.generation)
     metrics = metrics_out is not None
     n = layout.n
-    with torch.cuda.device(dev):
+    with _on_device(dev):
         stream = topo.stream
         s = stream.cuda_stream
-        with torch.cuda.stream(stream):
+        with _on_stream(stream, dev):
             g = _to_flat(grad_i, layout, dev)
             if pipe is not None:
                 pipe.start(g.flat, stream)

@@ -173,6 +173,7 @@ class LocalTransport(DeviceTransport):
                     else torch.device("cuda", torch.cuda.current_device()))
         self.timeout = timeout
         self.p2p = p2p
+        self._stream = torch.cuda.default_stream(self.dev)
         self._posts = [None] * world_size
         self._rv = _Rendezvous(world_size)
         self._sym = {}
@@ -196,7 +197,7 @@ class LocalTransport(DeviceTransport):
         return self.dev
 
     def stream(self, rank):
-        return torch.cuda.default_stream(self.dev)
+        return self._stream
 
     def _exchange(self, rank, gen, phase, post):
         self._posts[rank] = post
@@ -293,6 +294,7 @@ class NcclTransport(DeviceTransport):
         # reach 179 GB/s vs 683 GB/s for plain stores to every peer
         # (tests/nvlink_microbench.py, profiles/r01_summary.md).
         self._nvls_ok = (not threaded) and os.environ.get("LIONCUB_NVLS", "0") == "1"
+        self._fused_env = os.environ.get("LIONCUB_FUSED_BARRIER", "1") == "1"
         if self.p2p and threaded:
             lib = _lib.load()
             devs = [devices[r].index for r in range(world_size)]
@@ -436,7 +438,7 @@ class NcclTransport(DeviceTransport):
 
     @property
     def fused_barriers(self):
-        return self.p2p and os.environ.get("LIONCUB_FUSED_BARRIER", "1") == "1"
+        return self.p2p and self._fused_env
 
     def sync_struct(self, rank, counter, wait_epoch, arrive_epoch):
         flags = self._flags(rank)
