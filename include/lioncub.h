@@ -138,6 +138,18 @@ int lc_vote_bits(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid,
                  void* const* tie_bits, int32_t nout, uint32_t* flags,
                  const lc_sync* sync, void* stream);
 
+/* ---- K4+K5 fused (peer-memory path, 1-bit words): vote this owner's block
+ * (as lc_vote_bits, voted/nz pushed through the nout table), publish
+ * sync->arrive_epoch, then update theta (as lc_apply_update from the local
+ * gather buffer `full`/`nz_full`), each warp waiting only for the owner of
+ * the block it reads (peer flag >= arrive_epoch).  sync->wait_epoch: all
+ * ranks' encode finished.  P <= 32. */
+int lc_vote_apply(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid,
+                  int fill, int sum_mode, void* const* voted, void* const* nz,
+                  int32_t nout, uint32_t* flags, const lc_sync* sync, float* theta,
+                  int64_t n, const uint32_t* full, const uint32_t* nz_full, double lr,
+                  double weight_decay, void* stream);
+
 /* ---- K6: owner-side p-bit sums -> signed aggregate -> 1-bit vote ----
  * Replaces collectives.py:241-249 (de-offset, ties) + :313-316
  * (majority_sign).  sums: `rows` rows (stride row_stride words) of F-bit

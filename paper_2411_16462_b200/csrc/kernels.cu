@@ -606,6 +606,151 @@ k_vote_bits(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_vali
 }
 
 // ---------------------------------------------------------------------------
+// K4+K5 fused (peer-memory path): the owner votes its block and pushes the
+// voted words into every rank's gather buffer, its last CTA publishes epoch
+// e2, and the same grid then updates theta super-tile by super-tile, each
+// warp waiting only for the owner of the block it is about to read (so the
+// update of already-voted blocks overlaps the slowest owner's vote).  All
+// CTAs of the grid are co-resident (occupancy-sized grid), so CTAs that wait
+// for their own rank's block never starve the CTAs still voting.
+// ---------------------------------------------------------------------------
+struct ApplyArgs {
+  float* theta;
+  int64_t n;
+  const uint32_t* sb;   // local gather buffer (all blocks land here)
+  const uint32_t* nzb;  // nullable
+  double lr, wd;
+  int64_t blk_words;    // words per owner block (cw)
+};
+
+template <int NP, bool NZ>
+__global__ void __launch_bounds__(256)
+k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_valid, int fill,
+             int sum_mode, VoteOut out, uint32_t* __restrict__ flags, SyncD sy, ApplyArgs a) {
+  griddep_wait();
+  sync_wait(sy);
+  // ---- vote (same as k_vote_bits) ----
+  {
+    const int T = P >> 1;
+    const uint32_t fillmask = fill > 0 ? ~0u : 0u;
+    uint32_t flag = 0;
+    const int64_t nq = cw >> 2;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq;
+         q += (int64_t)gridDim.x * blockDim.x) {
+      uint32_t pl[4][NP];
+#pragma unroll
+      for (int w = 0; w < 4; ++w)
+#pragma unroll
+        for (int pp = 0; pp < NP; ++pp) pl[w][pp] = 0u;
+      for (int j = 0; j < P; ++j) {
+        uint4 x = __ldcs(reinterpret_cast<const uint4*>(recv + (int64_t)j * cw) + q);
+        uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          uint32_t carry = xs[w];
+#pragma unroll
+          for (int pp = 0; pp < NP; ++pp) {
+            uint32_t t = pl[w][pp] & carry;
+            pl[w][pp] ^= carry;
+            carry = t;
+          }
+        }
+      }
+      uint32_t v[4], nz[4], tie[4];
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        int64_t rem = n_valid - (4 * q + w) * 32;
+        uint32_t vm = rem >= 32 ? ~0u : (rem <= 0 ? 0u : ((1u << rem) - 1u));
+        vote_word<NP>(pl[w], P, T, fillmask, vm, fill, sum_mode, v[w], nz[w], tie[w], flag);
+      }
+      vote_store(out, 4 * q, make_uint4(v[0], v[1], v[2], v[3]),
+                 make_uint4(nz[0], nz[1], nz[2], nz[3]), make_uint4(tie[0], tie[1], tie[2], tie[3]));
+    }
+    if (flag) atomicOr(flags, flag);
+  }
+  sync_arrive(sy);  // last CTA: every peer learns this owner's block is out
+  // ---- theta update, waiting per owner block ----
+  constexpr int KU = 4;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nsup = (a.n + 1023) >> 10;
+  const int64_t nwords = (a.n + 31) >> 5;
+  float4* th4 = reinterpret_cast<float4*>(a.theta);
+  uint32_t ready = 0u;  // owners whose voted block this warp has seen land
+  auto fetch = [&](int64_t sidx, uint32_t& sw_, uint32_t& zw_) {
+    sw_ = 0u;
+    zw_ = ~0u;
+    if (sidx >= nsup) return;
+    const int j = (int)((sidx * 32) / a.blk_words);  // owner of this super-tile
+    if (!((ready >> j) & 1u)) {
+      if (lane == 0) {
+        const unsigned long long t0 = globaltimer();
+        while (true) {
+          unsigned long long v;
+          asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(sy.mine + j) : "memory");
+          if (v >= sy.arrive_epoch) break;
+          if (globaltimer() - t0 > sy.timeout_ns) {
+            atomicOr(sy.err, (uint32_t)LC_FLAG_BARRIER_TIMEOUT);
+            break;
+          }
+          __nanosleep(32);
+        }
+      }
+      __syncwarp();
+      ready |= 1u << j;
+    }
+    const int64_t w = sidx * 32 + lane;
+    if (w < nwords) {
+      sw_ = __ldcv(a.sb + w);
+      if (NZ) zw_ = __ldcv(a.nzb + w);
+    }
+  };
+  uint32_t nxw, nxz;
+  fetch(gw, nxw, nxz);
+  for (int64_t sidx = gw; sidx < nsup; sidx += nw) {
+    const uint32_t myw = nxw, myz = nxz;
+    fetch(sidx + nw, nxw, nxz);
+#pragma unroll 1
+    for (int k0 = 0; k0 < 8; k0 += KU) {
+      float4 tv[KU];
+#pragma unroll
+      for (int u = 0; u < KU; ++u) {
+        const int64_t t = sidx * 8 + k0 + u;
+        if ((t + 1) * 128 <= a.n) tv[u] = ld_stream(th4 + t * 32 + lane);
+      }
+#pragma unroll
+      for (int u = 0; u < KU; ++u) {
+        const int k = k0 + u;
+        const int64_t t = sidx * 8 + k;
+        const uint32_t sw = __shfl_sync(kFull, myw, 4 * k + (lane >> 3));
+        const uint32_t zw = NZ ? __shfl_sync(kFull, myz, 4 * k + (lane >> 3)) : ~0u;
+        if (t * 128 >= a.n) continue;  // warp-uniform
+        const int sh = 4 * (lane & 7);
+        const uint32_t sn = (sw >> sh) & 0xF, zn = (zw >> sh) & 0xF;
+        double sg[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          sg[q] = ((zn >> q) & 1) ? (((sn >> q) & 1) ? 1.0 : -1.0) : 0.0;
+        if ((t + 1) * 128 <= a.n) {
+          float4 v = tv[u];
+          v.x = lion_theta(v.x, sg[0], a.lr, a.wd);
+          v.y = lion_theta(v.y, sg[1], a.lr, a.wd);
+          v.z = lion_theta(v.z, sg[2], a.lr, a.wd);
+          v.w = lion_theta(v.w, sg[3], a.lr, a.wd);
+          st_stream(th4 + t * 32 + lane, v);
+        } else {
+          const int64_t e0 = t * 128 + lane * 4;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (e0 + q < a.n) a.theta[e0 + q] = lion_theta(a.theta[e0 + q], sg[q], a.lr, a.wd);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K6: p-bit field sums -> signed aggregate -> sign words (+ ties, values).
 // `rows` partial-sum rows of the owner block are added first (1 after an
 // NCCL reduce-scatter; P when peers wrote their fields over NVLink).  Each
@@ -1091,6 +1236,40 @@ int lc_vote_bits(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid, i
   else if (P <= 127) LC_VOTE(7);
   else LC_VOTE(8);
 #undef LC_VOTE
+  LC_LAUNCH_CHECK();
+  return LC_OK;
+}
+
+int lc_vote_apply(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid, int fill,
+                  int sum_mode, void* const* voted, void* const* nz, int32_t nout,
+                  uint32_t* flags, const lc_sync* sync, float* theta, int64_t n,
+                  const uint32_t* full, const uint32_t* nz_full, double lr, double wd,
+                  void* stream) {
+  if (P < 1 || P > 32 || cw <= 0 || (cw % 4) != 0 || !flags || !sync || !sync->arrive_epoch)
+    return set_err(LC_E_ARG, "lc_vote_apply: P in [1,32], cw % 4 == 0, sync with arrive_epoch");
+  VoteOut o;
+  if (!recv || !theta || !full || !make_out(o, voted, nz, nullptr, nout) || (nz && !nz_full))
+    return set_err(LC_E_ARG, "lc_vote_apply: bad pointers / output table");
+  if (!aligned16(theta)) return set_err(LC_E_ARG, "lc_vote_apply: theta must be 16-byte aligned");
+  if ((int64_t)P * cw * 32 < n) return set_err(LC_E_ARG, "lc_vote_apply: blocks do not cover n");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const SyncD sy = to_syncd(sync);
+  ApplyArgs a{theta, n, full, nz_full, lr, wd, cw};
+#define LC_VA(NP, NZ)                                                                      \
+  do {                                                                                     \
+    auto kern = k_vote_apply<NP, NZ>;                                                      \
+    int grid = stream_grid(kern, kBlock, (n + 1023) >> 10, kBlock / 32);                   \
+    LC_CUDA_TRY(launch_pdl(kern, grid, kBlock, 0, st, recv, P, cw, n_valid, fill, sum_mode, \
+                           o, flags, sy, a));                                              \
+  } while (0)
+#define LC_VA_NZ(NP) do { if (nz) LC_VA(NP, true); else LC_VA(NP, false); } while (0)
+  if (P <= 1) LC_VA_NZ(1);
+  else if (P <= 3) LC_VA_NZ(2);
+  else if (P <= 7) LC_VA_NZ(3);
+  else if (P <= 15) LC_VA_NZ(4);
+  else LC_VA_NZ(5);
+#undef LC_VA_NZ
+#undef LC_VA
   LC_LAUNCH_CHECK();
   return LC_OK;
 }

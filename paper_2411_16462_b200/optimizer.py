@@ -281,6 +281,7 @@ class _Workspace:
         self.counters = z(4)   # arrive counters of the in-kernel barriers
         self.k5_sync = None
         self.syncs = None
+        self.applied = False
         self.l1 = None
         self.norms = self.scales = None
         if kind == "f64":
@@ -632,8 +633,11 @@ def _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out,
             else:
                 nz = _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill,
                                         n, g, m, mflat, hyp, segs, s,
-                                        tree=algo == "ps_efficient", pipe=pipe)
-                if pipe is None:
+                                        tree=algo == "ps_efficient", pipe=pipe,
+                                        theta=th.flat)
+                if ws.applied:
+                    pass
+                elif pipe is None:
                     _lib.call("lc_apply_update", th.flat.data_ptr(), n, ws.src, ws.nzsrc,
                               ws.nsrc, ws.wpb, 0, eta, wd, ws.k5_sync, s)
                 else:
@@ -677,8 +681,11 @@ def _ternary_precheck(topo, gen, g, m, mflat, n, hyp, dev, s, kind):
 
 
 def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, g, m, mflat,
-                       hyp, segs, s, tree=False, pipe=None):
-    """K1 encode -> exchange -> owner vote into the gather buffer (+nz, ties)."""
+                       hyp, segs, s, tree=False, pipe=None, theta=None):
+    """K1 encode -> exchange -> owner vote into the gather buffer (+nz, ties).
+    With ``theta`` on the fused peer-memory path the theta update runs in
+    the vote's grid (``ws.applied`` is set)."""
+    ws.applied = False
     P, r = topo.world_size, topo.rank
     tp = topo.transport
     cw, L = ws.cw, ws.L
@@ -734,6 +741,15 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
     else:
         tp.alltoall(r, gen, ws.send, ws.recv, L * 8)
         recv = ws.recv
+    if kind == "1bit" and fused and ws.tout is None and pipe is None and ws.nsrc == 1 \
+            and theta is not None:
+        # vote + theta update in one grid: each warp waits only for the owner
+        # of the block it updates (the allgather and K5 overlap the skew)
+        _lib.call("lc_vote_apply", recv.data_ptr(), P, cw, nvalid, fill, sum_mode, ws.vout,
+                  ws.nzout, ws.nout, ws.flags.data_ptr(), sy2, theta.data_ptr(), n,
+                  _loc(ws.full).data_ptr(), _lib.ptr(_loc(ws.nz)), hyp.lr, hyp.weight_decay, s)
+        ws.applied = True
+        return _loc(ws.nz)
     if kind == "1bit":
         _lib.call("lc_vote_bits", recv.data_ptr(), P, cw, nvalid, fill, sum_mode, ws.vout,
                   ws.nzout, ws.tout, ws.nout, ws.flags.data_ptr(), sy2, s)
