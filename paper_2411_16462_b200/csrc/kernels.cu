@@ -811,6 +811,57 @@ k_fields_vote(const uint32_t* __restrict__ sums, int rows, int64_t row_stride, i
   sync_arrive(sy);
 }
 
+// K6 without per-element values (the step path): one thread per output sign
+// word -- it adds its F input words over the rows with 128-bit loads and
+// decodes 32 fields in registers (no shuffles).
+template <int F>
+__global__ void __launch_bounds__(256)
+k_fields_vote_words(const uint32_t* __restrict__ sums, int rows, int64_t row_stride, int64_t n,
+                    int P, int offset, int binary, int fill, VoteOut out, SyncD sy) {
+  griddep_wait();
+  sync_wait(sy);
+  constexpr int E = 32 / F;  // fields per input word
+  constexpr uint32_t FM = (F == 32) ? 0xffffffffu : ((1u << F) - 1u);
+  const int64_t nout = (n + 31) / 32;
+  const int64_t nin = (n * F + 31) / 32;
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < nout;
+       o += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t w[F];
+#pragma unroll
+    for (int k = 0; k < F; ++k) w[k] = 0u;
+    const int64_t i0 = o * F;
+    const bool vec = (F >= 4) && (i0 + F <= nin);
+    for (int r = 0; r < rows; ++r) {
+      const uint32_t* src = sums + (int64_t)r * row_stride + i0;
+      if (vec) {
+#pragma unroll
+        for (int k = 0; k < F; k += 4) {
+          const uint4 x = __ldcs(reinterpret_cast<const uint4*>(src + k));
+          w[k] += x.x; w[k + 1] += x.y; w[k + 2] += x.z; w[k + 3] += x.w;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < F; ++k)
+          if (i0 + k < nin) w[k] += __ldcs(src + k);
+      }
+    }
+    uint32_t pos = 0u, zer = 0u;
+#pragma unroll
+    for (int b = 0; b < 32; ++b) {
+      const int64_t cnt = (int64_t)((w[b / E] >> (F * (b % E))) & FM);
+      const int64_t sv = binary ? 2 * cnt - P : cnt - (int64_t)P * offset;
+      pos |= (uint32_t)(sv > 0) << b;
+      zer |= (uint32_t)(sv == 0) << b;
+    }
+    const int64_t rem = n - o * 32;
+    const uint32_t val = rem >= 32 ? ~0u : ((1u << rem) - 1u);
+    zer &= val;
+    const int nk = out.nout < 0 ? 1 : out.nout;
+    for (int k = 0; k < nk; ++k) vote_store1(out, k, o, pos | (fill > 0 ? zer : 0u), ~zer & val, zer);
+  }
+  sync_arrive(sy);
+}
+
 // ---------------------------------------------------------------------------
 // Full-precision arm: rank-ordered float64 sum (flat or binomial tree).
 // ---------------------------------------------------------------------------
@@ -1287,6 +1338,22 @@ int lc_fields_vote(const uint32_t* sums, int32_t rows, int64_t row_stride, int64
   int64_t nin = (n * F + 31) / 32;
   int grid = generic_grid(nin);
   const SyncD sy = to_syncd(sync);
+  if (!values && (row_stride % 4) == 0 && (reinterpret_cast<uintptr_t>(sums) & 15u) == 0) {
+    const int gw = generic_grid((n + 31) / 32);
+#define LC_FW(FF) LC_CUDA_TRY(launch_pdl(k_fields_vote_words<FF>, gw, kBlock, 0, st, sums, rows, row_stride, n, P, offset, binary, fill, o, sy))
+    switch (F) {
+      case 1: LC_FW(1); break;
+      case 2: LC_FW(2); break;
+      case 4: LC_FW(4); break;
+      case 8: LC_FW(8); break;
+      case 16: LC_FW(16); break;
+      case 32: LC_FW(32); break;
+      default: return set_err(LC_E_ARG, "lc_fields_vote: field_bits %d", F);
+    }
+#undef LC_FW
+    LC_LAUNCH_CHECK();
+    return LC_OK;
+  }
 #define LC_FV(FF) LC_CUDA_TRY(launch_pdl(k_fields_vote<FF>, grid, kBlock, 0, st, sums, rows, row_stride, n, P, offset, binary, fill, o, values, sy))
   switch (F) {
     case 1: LC_FV(1); break;

@@ -275,7 +275,10 @@ class _Workspace:
         self.cw = cw = L // 32
         self.F = F
         self.cwf = L * F // 32
-        self.p2p = p2p = P > 1 and tp.p2p
+        # the full-precision arm moves 8 B/param: NCCL's all-to-all beats SM
+        # stores into peer memory for that volume (measured), so it stays on
+        # the collective path; the 1-bit / p-bit payloads use peer memory
+        self.p2p = p2p = P > 1 and tp.p2p and kind != "f64"
         z = lambda k, dt=torch.int32: torch.zeros(max(k, 1), dtype=dt, device=dev)  # noqa
         self.flags = z(1)
         self.counters = z(4)   # arrive counters of the in-kernel barriers
