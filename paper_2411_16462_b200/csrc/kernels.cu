@@ -368,8 +368,15 @@ k_apply_update(float* __restrict__ theta, int64_t n, Dst sb, Dst nzb, int64_t wp
 // ---------------------------------------------------------------------------
 // Fused single-rank step (P == 1): one pass, theta/m/g in, theta'/m' out.
 // ---------------------------------------------------------------------------
+#ifndef LC_FUSED_U
+#define LC_FUSED_U 2
+#endif
+#ifndef LC_FUSED_MINB
+#define LC_FUSED_MINB 1
+#endif
+
 template <int MODE, bool MASK, bool METRICS, int U>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, LC_FUSED_MINB)
 k_fused_local(float* __restrict__ theta, float* __restrict__ m,
               const float* __restrict__ g, const uint8_t* __restrict__ mask,
               int64_t n, Hyp h, double lr, double wd, int fill, SegQ sq,
@@ -1224,7 +1231,7 @@ int lc_fused_local_step(float* theta, float* m, const float* g, const uint8_t* m
   SegQ sq = to_segq(segs);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const bool metrics = sign_bits || nz_bits || tie_bits;
-  constexpr int U = 2;
+  constexpr int U = LC_FUSED_U;
   const int64_t ntiles = (n + 127) >> 7;
 #define LC_FUSED(MODE, MASK, MET)                                                      \
   do {                                                                                 \
