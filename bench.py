@@ -322,6 +322,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-chunk", type=int, default=1 << 23)
+    ap.add_argument("--graph", action="store_true",
+                    help="replay the single-GPU step as a CUDA graph (launch-bound sizes)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -386,7 +388,13 @@ def main():
     stream = topo.stream
     torch.cuda.synchronize()
 
+    graph = None
+    if args.graph and world == 1 and (bits is None or bits == 1):
+        graph = lc.StepGraph(st, g, h, spec, topo, algo)  # CUDA-graph replay of the P=1 step
+
     def step(state):
+        if graph is not None:
+            return graph.step()
         state = lc.distributed_lion_step(state, g, h, spec, topo, algo)
         if policy is not None:
             state = lc.maybe_sync_momentum(state, policy, topo)
@@ -443,6 +451,12 @@ def main():
     for name, evs in phases.items():
         d = [a.elapsed_time(b) for a, b in evs]
         kern[name] = {"launches": len(d), "avg_ms": sum(d) / len(d), "total_ms": sum(d)}
+    if graph is not None:
+        # one fused kernel per replay: its duration is bounded by the step time
+        launches = args.steps
+        kern["lc_fused_local_step"] = {"launches": args.steps, "avg_ms": ms,
+                                       "total_ms": ms * args.steps,
+                                       "note": "CUDA-graph replay; step time used as kernel time"}
     cand = {k: v for k, v in kern.items() if k != "lc_barrier"}
     dominant = max(cand, key=lambda k: cand[k]["total_ms"]) if cand else None
 
@@ -521,6 +535,7 @@ def main():
                 "config": {"workload": args.workload, "description": desc, "params": n,
                            "tensors": len(shapes), "algo": algo, "bits": bits,
                            "parallelism": f"dp{world}", "field_bits": F,
+                           "cuda_graph": graph is not None,
                            "exchange": ("nvlink peer memory" if world > 1 and transport.p2p
                                         else "nccl" if world > 1 else "none (P=1)"),
                            "l2": "inputs larger than L2 (no flush needed)"},

@@ -13,7 +13,7 @@ from .errors import (CapacityError, CollectiveError, ConfigError,  # noqa: F401
                      DeviceError, LionCommError, PackFormatError,
                      PackRangeError)
 from .optimizer import (VOTE_ALGOS, FlatParamSet, Layout, LionHyper,  # noqa: F401
-                        SyncPolicy, WorkerState, distributed_lion_step,
+                        StepGraph, SyncPolicy, WorkerState, distributed_lion_step,
                         distributed_lion_step_host,
                         hash_params, lion_step, maybe_sync_momentum)
 from .quant import INF, QuantSpec, SignPolicy  # noqa: F401

@@ -862,3 +862,61 @@ def maybe_sync_momentum(state: WorkerState, policy: SyncPolicy,
                     seg = m.flat[a:b]
                     mean_into(topo, gen, seg, seg, scratch)
     return replace(state, params=th, momentum=m)
+
+
+class StepGraph:
+    """CUDA-graph replay of the single-rank (P = 1) Lion Cub step.
+
+    A small step is launch-bound: the Python dispatch of
+    ``distributed_lion_step`` costs more than the fused kernel.  The step
+    kernel's arguments depend only on the buffers, the constant learning
+    rate and the parity of t (the alternating zero fill), so two graphs --
+    odd and even t -- are captured once and replayed; ``step()`` advances
+    ``state.iteration`` exactly like ``distributed_lion_step``.  Constant lr
+    only (a schedule changes the kernel arguments every step); multi-rank
+    steps are not captured (their in-kernel barrier epochs advance).
+    """
+
+    def __init__(self, state: WorkerState, grads: FlatParamSet, h: LionHyper,
+                 spec: QuantSpec | None, topo: Topology, algo: str,
+                 zero_mode: str = "alternating"):
+        _validate(spec, algo)
+        if topo.world_size != 1:
+            raise ConfigError("StepGraph captures the single-rank step (world_size == 1)")
+        if callable(h.lr):
+            raise ConfigError("StepGraph needs a constant learning rate")
+        if spec is not None and spec.bits > 1:
+            raise ConfigError("StepGraph: the L1 p-bit step needs per-step norms; use "
+                              "distributed_lion_step")
+        layout, th, m = state.flat()
+        _check_shapes(th, grads)
+        g = _to_flat(grads, layout, th.flat.device)
+        self.state, self.grads = state, g
+        binary = algo == "compressed1bit" or spec is not None
+        mode = _lib.LC_LOCAL_BINARY if binary else _lib.LC_LOCAL_PS
+        dev = th.flat.device
+        self.flags = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.graphs = {}
+        with _on_device(dev):
+            for parity in (0, 1):
+                t = parity if parity else 2
+                hyp = h.c_struct(t)
+                fill = SignPolicy(mode=zero_mode, iteration=t).kernel_fill()
+                graph = torch.cuda.CUDAGraph()
+                side = torch.cuda.Stream(dev)
+                side.wait_stream(torch.cuda.current_stream(dev))
+                with torch.cuda.stream(side):
+                    with torch.cuda.graph(graph, stream=side):
+                        _lib.call("lc_fused_local_step", th.flat.data_ptr(), m.flat.data_ptr(),
+                                  g.flat.data_ptr(), None, layout.n, C.byref(hyp), fill, mode,
+                                  None, None, None, None, self.flags.data_ptr(),
+                                  torch.cuda.current_stream(dev).cuda_stream)
+                torch.cuda.current_stream(dev).wait_stream(side)
+                self.graphs[parity] = graph
+
+    def step(self) -> WorkerState:
+        t = self.state.iteration + 1
+        self.graphs[t % 2].replay()
+        self.state = WorkerState(params=self.state.params, momentum=self.state.momentum,
+                                 iteration=t)
+        return self.state

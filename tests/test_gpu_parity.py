@@ -474,3 +474,27 @@ def test_torch_optim_step_equals_functional_step():
     for k in g:
         assert torch.equal(st.params[k], opt.lion_state.params[k])
     assert torch.equal(model.weight.detach(), opt.lion_state.params["weight"])
+
+
+@pytest.mark.parametrize("algo,bits", [("compressed1bit", None), ("direct", 1), ("ps", None)])
+def test_step_graph_replay_equals_eager(algo, bits):
+    """StepGraph (CUDA-graph replay of the P=1 step, odd/even fill graphs)
+    == distributed_lion_step, bit for bit, over several steps."""
+    sizes = {"a": (70_001,), "b": (129,)}
+    ranks = O.synth_rank_inputs(4, 1, sizes, "zeros")
+    h = lc.LionHyper(0.9, 0.99, 1e-3, 0.1)
+    spec = None if bits is None else lc.QuantSpec(bits=bits)
+    topo = lc.Topology(1, 0, lc.LocalTransport(1))
+    from tests.gpu_helpers import grads_like, make_state
+    zm = "exact-ternary" if algo == "ps" else "alternating"
+    a = make_state(ranks[0]["theta"], ranks[0]["m"], 0)
+    b = make_state(ranks[0]["theta"], ranks[0]["m"], 0)
+    ga, gb = grads_like(a, ranks[0]["g"]), grads_like(b, ranks[0]["g"])
+    graph = lc.StepGraph(b, gb, h, spec, topo, algo, zero_mode=zm)
+    for _ in range(5):
+        a = lc.distributed_lion_step(a, ga, h, spec, topo, algo, zero_mode=zm)
+        b = graph.step()
+    torch.cuda.synchronize()
+    assert a.iteration == b.iteration == 5
+    assert torch.equal(a.params.flat, b.params.flat)
+    assert torch.equal(a.momentum.flat, b.momentum.flat)
