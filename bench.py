@@ -11,7 +11,9 @@ resident in HBM.  Rank 0 prints ONE JSON line.
 Default workload = BASELINE.json configs[1]: the GPT-2-small-sized buffer
 (124,439,808 params in its 148 tensors) with the p-bit sum-of-signs vote
 (algo="direct", QuantSpec(bits=1)).  Every array (498 MB each) is larger
-than the 126 MB L2, so no L2 flush is needed between steps.
+than the 126 MB L2, so no L2 flush is needed between steps.  Workloads whose
+12 B/param working set is under 2x L2 (c1_1bit_1m) flush L2 before every
+step and time each step alone with its own event pair.
 """
 
 from __future__ import annotations
@@ -310,6 +312,9 @@ METRIC = "Lion Cub step time (ms) & params/s at 1/2/4/8 B200, % of HBM/NVLink ro
 # The B200 arm
 # ---------------------------------------------------------------------------
 
+L2_BYTES = 126 * 1000 * 1000
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -423,22 +428,41 @@ def main():
     for _ in range(soak):
         st = step(st)
     barrier()
+    # state + gradient bytes a step touches; below 2x the 126 MB L2 every
+    # timed step is preceded by an (untimed) L2 flush and timed alone
+    flush = None
+    if 12 * n < 2 * L2_BYTES:
+        flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
     _lib.phase_events = {}
     l0 = _lib.launches
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
     w0 = time.perf_counter()
-    e0.record(stream)
-    for _ in range(args.steps):
-        st = step(st)
-    e1.record(stream)
+    if flush is None:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            st = step(st)
+        e1.record(stream)
+    else:
+        evs = []
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(1.0)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            st = step(st)
+            b.record(stream)
+            evs.append((a, b))
     host_ms = (time.perf_counter() - w0) * 1e3 / args.steps  # enqueue cost per step
     barrier()
     w1 = time.perf_counter()
     launches = _lib.launches - l0
     phases = _lib.phase_events
     _lib.phase_events = None
-    ms = e0.elapsed_time(e1) / args.steps
+    if flush is None:
+        ms = e0.elapsed_time(e1) / args.steps
+    else:
+        ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -538,7 +562,9 @@ def main():
                            "cuda_graph": graph is not None,
                            "exchange": ("nvlink peer memory" if world > 1 and transport.p2p
                                         else "nccl" if world > 1 else "none (P=1)"),
-                           "l2": "inputs larger than L2 (no flush needed)"},
+                           "l2": ("inputs larger than L2 (no flush needed)" if flush is None
+                                  else "L2 flushed (252 MB write) before every timed step; "
+                                       "steps timed individually, flush excluded")},
                 "roofline": roof, "step_roofline": sr, "kernels": kern,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "host_enqueue_ms_per_step": host_ms,

@@ -15,7 +15,8 @@ from .errors import (CapacityError, CollectiveError, ConfigError,  # noqa: F401
 from .optimizer import (VOTE_ALGOS, FlatParamSet, Layout, LionHyper,  # noqa: F401
                         StepGraph, SyncPolicy, WorkerState, distributed_lion_step,
                         distributed_lion_step_host,
-                        hash_params, lion_step, maybe_sync_momentum)
+                        hash_params, lion_step, load_checkpoint,
+                        maybe_sync_momentum, save_checkpoint)
 from .quant import INF, QuantSpec, SignPolicy  # noqa: F401
 from .torch_optim import LionCub, lioncub_comm_hook  # noqa: F401
 from .transport import (DeviceTransport, LocalTransport,  # noqa: F401

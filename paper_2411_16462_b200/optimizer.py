@@ -920,3 +920,58 @@ class StepGraph:
         self.state = WorkerState(params=self.state.params, momentum=self.state.momentum,
                                  iteration=t)
         return self.state
+
+
+def save_checkpoint(path: str, state: WorkerState, h: LionHyper | None = None):
+    """The reference's checkpoint format (optimizer.py:279-303): per layer in
+    sorted order theta then momentum as little-endian float32, plus a JSON
+    sidecar with name/kind/shape/offset/nbytes, the iteration and the hyper-
+    parameters.  The GPU state is already fp32 in sorted-name order, so the
+    blob is two device->host copies interleaved per layer."""
+    import json
+    layout, th, m = state.flat()
+    tflat, mflat = th.flat[:layout.n].cpu(), m.flat[:layout.n].cpu()
+    blob = bytearray()
+    layers = []
+    for name in layout.names:
+        o, c = layout.offset[name], layout.numel[name]
+        for kind, flat in (("theta", tflat), ("momentum", mflat)):
+            data = flat[o:o + c].numpy().astype("<f4").tobytes()
+            layers.append({"name": name, "kind": kind, "shape": list(layout.shapes[name]),
+                           "offset": len(blob), "nbytes": len(data)})
+            blob.extend(data)
+    side = {"layers": layers, "iteration": state.iteration,
+            "hyperparameters": None if h is None else {
+                "beta1": h.beta1, "beta2": h.beta2,
+                "lr": h.lr if not callable(h.lr) else "<schedule>",
+                "weight_decay": h.weight_decay}}
+    with open(path, "wb") as f:
+        f.write(bytes(blob))
+    with open(path + ".json", "w") as f:
+        json.dump(side, f, indent=2)
+
+
+def load_checkpoint(path: str, device=None) -> tuple:
+    """Inverse of save_checkpoint (optimizer.py:306-320): a flat device
+    WorkerState plus the sidecar dict.  Reads checkpoints written by the
+    reference as well."""
+    import json
+
+    import numpy as np
+    with open(path + ".json") as f:
+        side = json.load(f)
+    with open(path, "rb") as f:
+        blob = f.read()
+    shapes = {e["name"]: tuple(e["shape"]) for e in side["layers"]}
+    layout = Layout(shapes)
+    dev = torch.device(device) if device is not None else \
+        torch.device("cuda", torch.cuda.current_device())
+    host = {"theta": np.zeros(max(layout.n, 1), np.float32),
+            "momentum": np.zeros(max(layout.n, 1), np.float32)}
+    for e in side["layers"]:
+        arr = np.frombuffer(blob, dtype="<f4", count=e["nbytes"] // 4, offset=e["offset"])
+        o = layout.offset[e["name"]]
+        host[e["kind"]][o:o + arr.size] = arr
+    th = FlatParamSet(torch.from_numpy(host["theta"]).to(dev), layout)
+    m = FlatParamSet(torch.from_numpy(host["momentum"]).to(dev), layout)
+    return WorkerState(params=th, momentum=m, iteration=side["iteration"]), side

@@ -29,7 +29,8 @@ from lioncomm.collectives import (allreduce_mean_f32,  # noqa: E402
                                   compressed_allreduce_1bit, direct_allreduce,
                                   run_ranks)
 from lioncomm.optimizer import (LionHyper, SyncPolicy, WorkerState,  # noqa: E402
-                                distributed_lion_step, maybe_sync_momentum)
+                                distributed_lion_step, maybe_sync_momentum,
+                                save_checkpoint)
 from lioncomm.quant import (QuantSpec, SignPolicy, apply_sign,  # noqa: E402
                             lp_mean_norm, pack, quantize)
 from lioncomm.transport import InprocTransport  # noqa: E402
@@ -155,6 +156,18 @@ def run_collective_case(case: dict, out: dict):
         out[p + "out/ties"] = np.int64(res[0].ties)
 
 
+def make_checkpoint():
+    """A checkpoint written by the reference's save_checkpoint
+    (optimizer.py:279) for the byte-level format test."""
+    rng = np.random.default_rng(7)
+    shapes = {"w.weight": (3, 5), "a.bias": (4,), "z": (1, 2, 3)}
+    f32 = lambda s: rng.standard_normal(s).astype(np.float32).astype(np.float64)  # noqa: E731
+    state = WorkerState(params={k: f32(v) for k, v in shapes.items()},
+                        momentum={k: f32(v) for k, v in shapes.items()}, iteration=17)
+    save_checkpoint(os.path.join(HERE, "ref_ckpt.bin"), state,
+                    LionHyper(lr=3e-4, beta1=0.9, beta2=0.99, weight_decay=0.1))
+
+
 def main():
     steps: dict = {}
     for case in STEP_CASES:
@@ -169,6 +182,7 @@ def main():
     colls["meta"] = np.frombuffer(json.dumps({"cases": COLLECTIVE_CASES}).encode(),
                                   dtype=np.uint8)
     np.savez_compressed(os.path.join(HERE, "golden_collectives.npz"), **colls)
+    make_checkpoint()
     print(f"{len(STEP_CASES)} step cases, {len(COLLECTIVE_CASES)} collective cases")
 
 

@@ -30,9 +30,11 @@ def grads_like(st: lc.WorkerState, g: dict) -> FlatParamSet:
 
 
 def run_step_case(case: dict, theta, ms, gs, mask=None, transport=None,
-                  metrics=True, sizes=None):
+                  metrics=True, sizes=None, steps=1):
     """Run one distributed step (+ optional sync) on ``case['world']`` ranks
-    through the public API; returns per-rank (theta', m', metrics) numpy."""
+    through the public API; returns per-rank (theta', m', metrics) numpy.
+    ``steps`` > 1 repeats the step on the device-resident state (same
+    gradients), exercising workspace/epoch reuse across steps."""
     world = case["world"]
     h = lc.LionHyper(beta1=0.9, beta2=0.99, lr=case["lr"], weight_decay=case["wd"])
     spec = None if case["bits"] is None else lc.QuantSpec(bits=case["bits"], norm_p=1.0)
@@ -49,11 +51,13 @@ def run_step_case(case: dict, theta, ms, gs, mask=None, transport=None,
         r = topo.rank
         st = make_state(theta, ms[r], case["iteration"])
         g = grads_like(st, gs[r])
-        met = {} if metrics else None
-        st2 = lc.distributed_lion_step(st, g, h, spec, topo, case["algo"], mask=cmask,
-                                       zero_mode=case["zero_mode"], metrics_out=met)
-        if sync is not None:
-            st2 = lc.maybe_sync_momentum(st2, sync, topo)
+        st2 = st
+        for _ in range(steps):
+            met = {} if metrics else None
+            st2 = lc.distributed_lion_step(st2, g, h, spec, topo, case["algo"], mask=cmask,
+                                           zero_mode=case["zero_mode"], metrics_out=met)
+            if sync is not None:
+                st2 = lc.maybe_sync_momentum(st2, sync, topo)
         torch.cuda.synchronize()
         out_t = {k: v.detach().cpu().numpy().copy() for k, v in st2.params.items()}
         out_m = {k: v.detach().cpu().numpy().copy() for k, v in st2.momentum.items()}

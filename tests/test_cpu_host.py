@@ -207,3 +207,29 @@ def test_ddp_comm_hook_keeps_local_gradients_gloo():
     for p in procs:
         p.join(timeout=60)
     assert all(ok for _, ok in res), res
+
+
+def test_checkpoint_reference_format_roundtrip(tmp_path):
+    """load_checkpoint reads a checkpoint written by the reference's
+    save_checkpoint (optimizer.py:279-303, fixture from make_golden.py) and
+    save_checkpoint writes it back byte-identical, sidecar included."""
+    import json
+
+    import numpy as np
+
+    import paper_2411_16462_b200 as lc
+    gold = os.path.join(ROOT, "tests", "golden", "ref_ckpt.bin")
+    state, side = lc.load_checkpoint(gold, device="cpu")
+    assert state.iteration == 17
+    blob = open(gold, "rb").read()
+    for e in side["layers"]:
+        want = np.frombuffer(blob, "<f4", e["nbytes"] // 4, e["offset"]).reshape(e["shape"])
+        got = (state.params if e["kind"] == "theta" else state.momentum)[e["name"]]
+        assert tuple(got.shape) == tuple(e["shape"])
+        assert np.array_equal(got.numpy(), want)
+    h = lc.LionHyper(lr=3e-4, beta1=0.9, beta2=0.99, weight_decay=0.1)
+    out = str(tmp_path / "ckpt.bin")
+    lc.save_checkpoint(out, state, h)
+    assert open(out, "rb").read() == blob
+    assert json.load(open(out + ".json")) == json.load(open(gold + ".json"))
+    assert open(out + ".json").read() == open(gold + ".json").read()

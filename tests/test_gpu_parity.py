@@ -225,6 +225,90 @@ def test_momentum_sync_matches_oracle_large(p2p):
             assert_f32_equal(m[k], synced[r][k], f"m {k} r{r}")
 
 
+# ---- edge sizes and multi-step trajectories --------------------------------
+
+EDGE_SIZES = [
+    {"x": (1,)},
+    {"x": (33,)},
+    {"a": (1,), "b": (1025,), "c": (4097,)},
+    {"a": (31,), "b": (32,), "c": (1023,), "d": (1024,), "e": (3, 7)},
+]
+
+
+@pytest.mark.parametrize("p2p", [True, False], ids=["peer-memory", "collectives"])
+@pytest.mark.parametrize("si", range(len(EDGE_SIZES)))
+@pytest.mark.parametrize("algo,bits,world,zm", [
+    ("compressed1bit", None, 3, "alternating"),
+    ("direct", 1, 4, "alternating"),
+    ("direct", 6, 5, "exact-ternary"),
+    ("ps", None, 2, "exact-ternary"),
+    ("ps_efficient", None, 4, "alternating"),
+    ("direct", 5, 1, "alternating"),
+])
+def test_edge_sizes_match_oracle(algo, bits, world, zm, si, p2p):
+    """Vectors smaller than one owner block / one warp tile / one word, and
+    layer boundaries off the 32- and 1024-element grids: most ranks own
+    nothing and every tail path runs."""
+    sizes = EDGE_SIZES[si]
+    ranks = O.synth_rank_inputs(11 + si, world, sizes, "ties")
+    h = O.Hyper(0.9, 0.99, 1e-3, 0.1)
+    spec = None if bits is None else O.Spec(bits)
+    nt, nm, sign, ties, _, _ = O.distributed_step(
+        [rk["theta"] for rk in ranks], [rk["m"] for rk in ranks], [rk["g"] for rk in ranks],
+        h, spec, algo, 4, zero_mode=zm)
+    case = dict(world=world, lr=1e-3, wd=0.1, bits=bits, algo=algo, iteration=4, zero_mode=zm)
+    res = run_step_case(case, ranks[0]["theta"], [rk["m"] for rk in ranks],
+                        [rk["g"] for rk in ranks], transport=lc.LocalTransport(world, p2p=p2p))
+    for r, (th, m, met, _) in enumerate(res):
+        for k in sizes:
+            assert_f32_equal(th[k], nt[0][k], f"theta {k}")
+            assert_f32_equal(m[k], nm[r][k], f"m {k}")
+            assert np.array_equal(met["vote_sign"][k].reshape(-1), sign[k].reshape(-1))
+            assert met["ties"][k] == ties[k]
+
+
+@pytest.mark.parametrize("p2p", [True, False], ids=["peer-memory", "collectives"])
+@pytest.mark.parametrize("algo,bits,world,zm,sync", [
+    ("compressed1bit", None, 4, "alternating", (2, ["emb"])),
+    ("direct", 1, 3, "alternating", None),
+    ("direct", 5, 4, "exact-ternary", (3, "all")),
+    ("ps", None, 2, "exact-ternary", None),
+])
+def test_multi_step_trajectory_matches_oracle(algo, bits, world, zm, sync, p2p):
+    """Six consecutive steps on the device-resident state (workspaces,
+    epochs and symmetric buffers reused) against the oracle fed the fp32-
+    rounded state each step -- the fp32-state contract of DESIGN.md."""
+    sizes = {"emb": (5_003,), "w": (70_000,), "b": (96,)}
+    ranks = O.synth_rank_inputs(23, world, sizes, "laplace")
+    h = O.Hyper(0.9, 0.99, 1e-3, 0.1)
+    spec = None if bits is None else O.Spec(bits)
+    f32 = lambda d: {k: np.asarray(v, np.float32).astype(np.float64) for k, v in d.items()}  # noqa: E731
+    thetas = [f32(ranks[0]["theta"])] * world
+    moms = [f32(rk["m"]) for rk in ranks]
+    steps, it0 = 6, 0
+    for i in range(steps):
+        nt, nm, sign, ties, _, _ = O.distributed_step(
+            thetas, moms, [rk["g"] for rk in ranks], h, spec, algo, it0 + i, zero_mode=zm)
+        nm = [f32(m) for m in nm]
+        if sync is not None:
+            layers = "all" if sync[1] == "all" else frozenset(sync[1])
+            nm = O.sync_momentum(nm, sync[0], layers, it0 + i + 1)
+        thetas = [f32(t) for t in nt]
+        moms = [f32(m) for m in nm]
+    case = dict(world=world, lr=1e-3, wd=0.1, bits=bits, algo=algo, iteration=it0,
+                zero_mode=zm, sync=sync)
+    res = run_step_case(case, ranks[0]["theta"], [rk["m"] for rk in ranks],
+                        [rk["g"] for rk in ranks], transport=lc.LocalTransport(world, p2p=p2p),
+                        steps=steps)
+    for r, (th, m, met, it) in enumerate(res):
+        assert it == it0 + steps
+        for k in sizes:
+            assert_f32_equal(th[k], thetas[r][k], f"theta {k} r{r}")
+            assert_f32_equal(m[k], moms[r][k], f"m {k} r{r}")
+            assert np.array_equal(met["vote_sign"][k], sign[k])
+            assert met["ties"][k] == ties[k]
+
+
 # ---- reference error behaviour ---------------------------------------------
 
 def test_capacity_guard_before_any_communication():
@@ -498,3 +582,30 @@ def test_step_graph_replay_equals_eager(algo, bits):
     assert a.iteration == b.iteration == 5
     assert torch.equal(a.params.flat, b.params.flat)
     assert torch.equal(a.momentum.flat, b.momentum.flat)
+
+
+@pytest.mark.gpu
+def test_checkpoint_resume_equals_continuous(tmp_path):
+    """save_checkpoint / load_checkpoint (reference format) mid-run: resuming
+    from the checkpoint continues bit-identically to the uninterrupted run."""
+    sizes = {"a": (3, 1001), "b": (17,)}
+    ranks = O.synth_rank_inputs(5, 1, sizes, "laplace")
+    h = lc.LionHyper(0.9, 0.99, 1e-3, 0.1)
+    topo = lc.Topology(1, 0, lc.LocalTransport(1))
+    from tests.gpu_helpers import grads_like, make_state
+    a = make_state(ranks[0]["theta"], ranks[0]["m"], 0)
+    ga = grads_like(a, ranks[0]["g"])
+    for _ in range(3):
+        a = lc.distributed_lion_step(a, ga, h, None, topo, "compressed1bit")
+    path = str(tmp_path / "ck.bin")
+    lc.save_checkpoint(path, a, h)
+    b, side = lc.load_checkpoint(path)
+    assert side["iteration"] == 3 and b.params.flat.is_cuda
+    gb = grads_like(b, ranks[0]["g"])
+    for _ in range(3):
+        a = lc.distributed_lion_step(a, ga, h, None, topo, "compressed1bit")
+        b = lc.distributed_lion_step(b, gb, h, None, topo, "compressed1bit")
+    torch.cuda.synchronize()
+    assert a.iteration == b.iteration == 6
+    assert torch.equal(a.params.flat[:a.params.layout.n], b.params.flat[:b.params.layout.n])
+    assert torch.equal(a.momentum.flat[:a.params.layout.n], b.momentum.flat[:b.params.layout.n])
