@@ -428,41 +428,54 @@ def main():
     for _ in range(soak):
         st = step(st)
     barrier()
+
+    def timed_pass(record_kernels: bool):
+        """K steps between a barrier + synchronize on both sides; returns
+        (ms per step, host enqueue ms per step, our launches, kernel events)."""
+        nonlocal st
+        _lib.phase_events = {} if record_kernels else None
+        l0 = _lib.launches
+        t0 = time.perf_counter()
+        if flush is None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                st = step(st)
+            e1.record(stream)
+        else:
+            evs = []
+            for _ in range(args.steps):
+                with torch.cuda.stream(stream):
+                    flush.fill_(1.0)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                st = step(st)
+                b.record(stream)
+                evs.append((a, b))
+        enq = (time.perf_counter() - t0) * 1e3 / args.steps
+        barrier()
+        nl = _lib.launches - l0
+        ph = _lib.phase_events
+        _lib.phase_events = None
+        if flush is None:
+            t = e0.elapsed_time(e1) / args.steps
+        else:
+            t = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+        return t, enq, nl, ph
+
     # state + gradient bytes a step touches; below 2x the 126 MB L2 every
     # timed step is preceded by an (untimed) L2 flush and timed alone
     flush = None
     if 12 * n < 2 * L2_BYTES:
         flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
-    _lib.phase_events = {}
-    l0 = _lib.launches
+    # the step time comes from a pass without per-kernel events (an event
+    # between two kernels would break their programmatic-launch overlap);
+    # a second pass of K steps records every kernel for the roofline
     w0 = time.perf_counter()
-    if flush is None:
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            st = step(st)
-        e1.record(stream)
-    else:
-        evs = []
-        for _ in range(args.steps):
-            with torch.cuda.stream(stream):
-                flush.fill_(1.0)
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            st = step(st)
-            b.record(stream)
-            evs.append((a, b))
-    host_ms = (time.perf_counter() - w0) * 1e3 / args.steps  # enqueue cost per step
-    barrier()
+    ms, host_ms, launches, _ = timed_pass(False)
     w1 = time.perf_counter()
-    launches = _lib.launches - l0
-    phases = _lib.phase_events
-    _lib.phase_events = None
-    if flush is None:
-        ms = e0.elapsed_time(e1) / args.steps
-    else:
-        ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    _, _, _, phases = timed_pass(True)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -53,7 +53,9 @@ enum {
   LC_ENC_SIGN1 = 0,       /* 1-bit sign words (compressed1bit)            */
   LC_ENC_SIGN_FIELDS = 1, /* (s+1)>>1 in F-bit fields (sum-of-signs)      */
   LC_ENC_QUANT_FIELDS = 2,/* q+q_max in F-bit fields (L1 p-bit)           */
-  LC_ENC_F64 = 3          /* c as float64 (full-precision ps arm)         */
+  LC_ENC_F64 = 3,         /* c as float64 (full-precision ps arm)         */
+  LC_ENC_REPLICATE = 0x100 /* OR with LC_ENC_SIGN1: every dst gets all words
+                              (allgather of the payload; L >= eoff+n)      */
 };
 
 typedef struct lc_hyper {
@@ -149,6 +151,18 @@ int lc_vote_apply(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid,
                   int32_t nout, uint32_t* flags, const lc_sync* sync, float* theta,
                   int64_t n, const uint32_t* full, const uint32_t* nz_full, double lr,
                   double weight_decay, void* stream);
+
+/* ---- K5v: vote + theta update over allgathered sign words ----
+ * rows: P rows (stride row_stride >= ceil(n/32) words) of every rank's
+ * 1-bit sign words for the whole vector (lc_encode with LC_ENC_REPLICATE
+ * stores row `rank` into every rank's buffer).  Each word is voted from the
+ * P rows (the owner vote of lc_vote_bits: majority / sum-of-signs, fill,
+ * exact-ternary flags) and theta updated in the same pass (lc_apply_update).
+ * sync->wait_epoch: every rank's encode finished.  Replaces collectives.py
+ * :287-299 + optimizer.py:204 on the allgather exchange. */
+int lc_vote_update(const uint32_t* rows, int64_t row_stride, int32_t P, float* theta,
+                   int64_t n, int fill, int sum_mode, double lr, double weight_decay,
+                   uint32_t* flags, const lc_sync* sync, void* stream);
 
 /* ---- K6: owner-side p-bit sums -> signed aggregate -> 1-bit vote ----
  * Replaces collectives.py:241-249 (de-offset, ties) + :313-316

@@ -54,15 +54,19 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          defines: tuple = ()) -> str:
+    """Compile every csrc/*.cu into one sm_100a shared library.  ``out`` /
+    ``defines`` (-D macros) build tuning variants next to the default one."""
+    target = out or LIB
+    if not force and out is None and not needs_build():
         return LIB
-    os.makedirs(LIBDIR, exist_ok=True)
+    os.makedirs(os.path.dirname(target), exist_ok=True)
     inc, lib = nccl_paths()
-    tmp = LIB + ".tmp"
+    tmp = target + ".tmp"
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared",
            "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-           "--expt-relaxed-constexpr",
+           "--expt-relaxed-constexpr", *[f"-D{d}" for d in defines],
            "-I", os.path.join(ROOT, "include"), "-I", inc,
            *sources(), "-o", tmp,
            "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}"]
@@ -74,8 +78,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stdout}\n{res.stderr}")
     if verbose:
         print(res.stderr, file=sys.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

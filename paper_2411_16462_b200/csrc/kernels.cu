@@ -173,7 +173,7 @@ template <int ENC, int F, bool MASK>
 __global__ void __launch_bounds__(256, LC_ENC_MINB)
 k_encode(const float* __restrict__ g, float* __restrict__ m,
          const uint8_t* __restrict__ mask, int64_t n, Hyp h, int fill, SegQ sq,
-         Dst dst, int64_t L, int64_t eoff, uint32_t* __restrict__ flags, SyncD sy) {
+         Dst dst, int64_t L, int64_t eoff, int nrep, uint32_t* __restrict__ flags, SyncD sy) {
   griddep_wait();
   constexpr int WPS = (ENC == LC_ENC_F64) ? 1 : 32 * F;  // words per super-tile
   constexpr int KU = LC_ENC_KU;  // sub-tiles whose loads are in flight together
@@ -271,14 +271,19 @@ k_encode(const float* __restrict__ g, float* __restrict__ m,
     }
     if constexpr (ENC != LC_ENC_F64) {
       __syncwarp();
-      uint32_t* d = reinterpret_cast<uint32_t*>(dst.p[j]) + (boff >> 5) * F;
       const int64_t rem = n - ebase;
       const int nwv = rem >= 1024 ? WPS : (int)((rem * F + 31) / 32);
-      if (nwv == WPS && (WPS % 128) == 0) {
-        for (int w = lane * 4; w < WPS; w += 128)
-          *reinterpret_cast<uint4*>(d + w) = *reinterpret_cast<const uint4*>(&stage[wib][w]);
-      } else {
-        for (int w = lane; w < nwv; w += 32) d[w] = stage[wib][w];
+      // owner-block mode: block j's destination; replicate mode (nrep > 0):
+      // the same words to every destination (an allgather of the payload)
+      const int nd = nrep > 0 ? nrep : 1;
+      for (int q = 0; q < nd; ++q) {
+        uint32_t* d = reinterpret_cast<uint32_t*>(dst.p[nrep > 0 ? q : j]) + (boff >> 5) * F;
+        if (nwv == WPS && (WPS % 128) == 0) {
+          for (int w = lane * 4; w < WPS; w += 128)
+            *reinterpret_cast<uint4*>(d + w) = *reinterpret_cast<const uint4*>(&stage[wib][w]);
+        } else {
+          for (int w = lane; w < nwv; w += 32) d[w] = stage[wib][w];
+        }
       }
       __syncwarp();
     }
@@ -1057,6 +1062,109 @@ __global__ void k_sum_rows(Rows rows, int P, int64_t count, uint32_t* __restrict
   }
 }
 
+// ---------------------------------------------------------------------------
+// K5v: vote + theta update for the allgather exchange (peer-memory path,
+// P <= 4 by default).  K1 in replicate mode stored every rank's sign words
+// into row `rank` of every rank's receive rows, so each rank holds all P
+// rows of the whole vector: a warp owns a 1024-element super-tile, lane i
+// counts word i over the P rows (bit-sliced, the same count the owner's K4
+// makes), votes it, and sub-tile k takes its 4 voted words by shuffle.  No
+// owner hop and no voted-word broadcast: one in-kernel barrier per step.
+// ---------------------------------------------------------------------------
+#ifndef LC_VU_KU
+#define LC_VU_KU 4
+#endif
+#ifndef LC_VU_MINB
+#define LC_VU_MINB 3
+#endif
+
+template <int NP, bool NZ>
+__global__ void __launch_bounds__(256, LC_VU_MINB)
+k_vote_update(const uint32_t* __restrict__ rows, int64_t stride, int P, float* __restrict__ theta,
+              int64_t n, int fill, int sum_mode, double lr, double wd,
+              uint32_t* __restrict__ flags, SyncD sy) {
+  constexpr int KU = LC_VU_KU;  // theta sub-tiles in flight per batch
+  griddep_wait();
+  sync_wait(sy);
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nsup = (n + 1023) >> 10;
+  const int64_t nwords = (n + 31) >> 5;
+  const uint32_t fillmask = fill > 0 ? ~0u : 0u;
+  const int T = P >> 1;
+  float4* th4 = reinterpret_cast<float4*>(theta);
+  uint32_t flag = 0;
+  for (int64_t sidx = gw; sidx < nsup; sidx += nw) {
+    const int64_t eb = sidx << 10;
+    const bool full = eb + 1024 <= n;
+    float4 tv[KU];  // the first batch of theta in flight with the words
+    if (full) {
+#pragma unroll
+      for (int k = 0; k < KU; ++k) tv[k] = ld_stream(th4 + (eb >> 2) + k * 32 + lane);
+    }
+    const int64_t w = sidx * 32 + lane;
+    uint32_t myw = 0u, myz = ~0u;
+    if (w < nwords) {
+      uint32_t pl[NP];
+#pragma unroll
+      for (int pp = 0; pp < NP; ++pp) pl[pp] = 0u;
+      for (int s4 = 0; s4 < P; s4 += 4) {
+        uint32_t x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] = s4 + u < P ? __ldcg(rows + (int64_t)(s4 + u) * stride + w) : 0u;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          uint32_t carry = x[u];
+#pragma unroll
+          for (int pp = 0; pp < NP; ++pp) {
+            const uint32_t t = pl[pp] & carry;
+            pl[pp] ^= carry;
+            carry = t;
+          }
+        }
+      }
+      const int64_t rem = n - w * 32;
+      const uint32_t vm = rem >= 32 ? ~0u : ((1u << rem) - 1u);
+      uint32_t tie;
+      vote_word<NP>(pl, P, T, fillmask, vm, fill, sum_mode, myw, myz, tie, flag);
+    }
+#pragma unroll
+    for (int k0 = 0; k0 < 8; k0 += KU) {
+      if (k0 > 0 && full) {
+#pragma unroll
+        for (int u = 0; u < KU; ++u) tv[u] = ld_stream(th4 + (eb >> 2) + (k0 + u) * 32 + lane);
+      }
+#pragma unroll
+      for (int u = 0; u < KU; ++u) {
+        const int k = k0 + u;
+        const int64_t t = sidx * 8 + k;
+        const uint32_t sw = __shfl_sync(kFull, myw, 4 * k + (lane >> 3));
+        const uint32_t zw = NZ ? __shfl_sync(kFull, myz, 4 * k + (lane >> 3)) : ~0u;
+        const int sh = 4 * (lane & 7);
+        const uint32_t sn = (sw >> sh) & 0xF, zn = (zw >> sh) & 0xF;
+        double sg[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) sg[q] = ((zn >> q) & 1) ? (((sn >> q) & 1) ? 1.0 : -1.0) : 0.0;
+        if (full) {
+          float4 v = tv[u];
+          v.x = lion_theta(v.x, sg[0], lr, wd);
+          v.y = lion_theta(v.y, sg[1], lr, wd);
+          v.z = lion_theta(v.z, sg[2], lr, wd);
+          v.w = lion_theta(v.w, sg[3], lr, wd);
+          st_stream(th4 + t * 32 + lane, v);
+        } else if (t * 128 < n) {
+          const int64_t e0 = t * 128 + lane * 4;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (e0 + q < n) theta[e0 + q] = lion_theta(theta[e0 + q], sg[q], lr, wd);
+        }
+      }
+    }
+  }
+  if (flag) atomicOr(flags, flag);
+}
+
 }  // namespace lc
 
 // ===========================================================================
@@ -1092,6 +1200,7 @@ int generic_grid(int64_t n) {
 
 thread_local SyncD g_sync{};     // sync of the encode launch being dispatched
 thread_local int64_t g_eoff = 0;  // element offset of the encode launch
+thread_local int g_nrep = 0;      // replicate-mode destinations (0: owner blocks)
 
 template <int ENC, int F, bool MASK>
 int launch_encode(const float* g, float* m, const uint8_t* mask, int64_t n, Hyp h,
@@ -1101,7 +1210,7 @@ int launch_encode(const float* g, float* m, const uint8_t* mask, int64_t n, Hyp 
   int64_t nsup = (n + 1023) >> 10;
   int grid = stream_grid(kern, kBlock, nsup, kBlock / 32);
   LC_CUDA_TRY(launch_pdl(kern, grid, kBlock, 0, st, g, m, mask, n, h, fill, sq, dst, L, g_eoff,
-                         flags, g_sync));
+                         g_nrep, flags, g_sync));
   LC_LAUNCH_CHECK();
   return LC_OK;
 }
@@ -1161,10 +1270,16 @@ int lc_encode(const float* g, float* m, const uint8_t* mask, int64_t n,
   if (n == 0) return LC_OK;
   if (!g || !m) return set_err(LC_E_ARG, "lc_encode: null pointer");
   if (!aligned16(g) || !aligned16(m)) return set_err(LC_E_ARG, "lc_encode: g/m must be 16-byte aligned");
-  if (L <= 0 || (L % 1024) != 0 || (int64_t)nblocks * L < eoff + n || eoff < 0 || (eoff % 1024) != 0)
+  const bool rep = (enc & LC_ENC_REPLICATE) != 0;
+  enc &= ~LC_ENC_REPLICATE;
+  if (rep && (enc != LC_ENC_SIGN1 || L < eoff + n))
+    return set_err(LC_E_ARG, "lc_encode: replicate mode is 1-bit only and L must cover [eoff, eoff+n)");
+  if (L <= 0 || (L % 1024) != 0 || (!rep && (int64_t)nblocks * L < eoff + n) || eoff < 0 ||
+      (eoff % 1024) != 0)
     return set_err(LC_E_ARG, "lc_encode: blocks (multiple of 1024) must cover [eoff, eoff+n), eoff % 1024 == 0");
   Dst d;
   if (!make_dst(d, dst, nblocks)) return set_err(LC_E_ARG, "lc_encode: bad destination table");
+  g_nrep = rep ? nblocks : 0;
   Hyp h = to_hyp(hp);
   SegQ sq = to_segq(segs);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -1325,9 +1440,43 @@ int lc_vote_apply(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid, 
   else if (P <= 3) LC_VA_NZ(2);
   else if (P <= 7) LC_VA_NZ(3);
   else if (P <= 15) LC_VA_NZ(4);
-  else LC_VA_NZ(5);
+  else if (P <= 31) LC_VA_NZ(5);
+  else LC_VA_NZ(6);
 #undef LC_VA_NZ
 #undef LC_VA
+  LC_LAUNCH_CHECK();
+  return LC_OK;
+}
+
+int lc_vote_update(const uint32_t* rows, int64_t row_stride, int32_t P, float* theta, int64_t n,
+                   int fill, int sum_mode, double lr, double wd, uint32_t* flags,
+                   const lc_sync* sync, void* stream) {
+  if (n < 0 || P < 1 || P > 255 || !flags) return set_err(LC_E_ARG, "lc_vote_update: bad arguments");
+  if (n == 0) return LC_OK;
+  if (!rows || !theta || row_stride < (n + 31) / 32)
+    return set_err(LC_E_ARG, "lc_vote_update: null pointer / rows shorter than ceil(n/32)");
+  if (!aligned16(theta)) return set_err(LC_E_ARG, "lc_vote_update: theta must be 16-byte aligned");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const SyncD sy = to_syncd(sync);
+  const int64_t nsup = (n + 1023) >> 10;
+#define LC_VU(NP, NZ)                                                                      \
+  do {                                                                                     \
+    auto kern = k_vote_update<NP, NZ>;                                                     \
+    int grid = stream_grid(kern, kBlock, nsup, kBlock / 32);                               \
+    LC_CUDA_TRY(launch_pdl(kern, grid, kBlock, 0, st, rows, row_stride, P, theta, n, fill, \
+                           sum_mode, lr, wd, flags, sy));                                  \
+  } while (0)
+#define LC_VU_Z(NP) do { if (fill == 0) LC_VU(NP, true); else LC_VU(NP, false); } while (0)
+  if (P <= 1) LC_VU_Z(1);
+  else if (P <= 3) LC_VU_Z(2);
+  else if (P <= 7) LC_VU_Z(3);
+  else if (P <= 15) LC_VU_Z(4);
+  else if (P <= 31) LC_VU_Z(5);
+  else if (P <= 63) LC_VU_Z(6);
+  else if (P <= 127) LC_VU_Z(7);
+  else LC_VU_Z(8);
+#undef LC_VU_Z
+#undef LC_VU
   LC_LAUNCH_CHECK();
   return LC_OK;
 }

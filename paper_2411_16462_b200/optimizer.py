@@ -45,9 +45,9 @@ from .collectives import (Topology, choose_lane_bits, field_bits, mean_into,
                           owner_elems, owner_valid)
 from .errors import CollectiveError, ConfigError
 from .quant import QuantSpec, SignPolicy
+from .transport import DEFAULT_TIMEOUT
 
 LrSchedule = Union[float, Callable[[int], float]]
-SYNC_PIECE = 1 << 28   # elements per momentum-sync exchange piece
 VOTE_ALGOS = ("ps", "ps_efficient", "direct", "compressed1bit")
 
 
@@ -280,6 +280,8 @@ class _Workspace:
         # the collective path; the 1-bit / p-bit payloads use peer memory
         self.p2p = p2p = P > 1 and tp.p2p and kind != "f64"
         z = lambda k, dt=torch.int32: torch.zeros(max(k, 1), dtype=dt, device=dev)  # noqa
+        self.key = (layout.key, P, kind, F)
+        self.ag = None
         self.flags = z(1)
         self.counters = z(4)   # arrive counters of the in-kernel barriers
         self.k5_sync = None
@@ -683,6 +685,34 @@ def _ternary_precheck(topo, gen, g, m, mflat, n, hyp, dev, s, kind):
     _raise_flags(int(flags.item()), binary=kind == "1bit")
 
 
+# When the 1-bit step allgathers the sign words (K1 stores its words into
+# every rank, K5v votes locally: one barrier, no owner hop, (P-1) x n/8
+# bytes out per rank) instead of the owner vote (2(P-1)/P x n/8 bytes, two
+# hops).  Measured on B200: the allgather wins at P = 2 for
+# GPT-2-small (0.424 vs 0.441 ms), the owner vote at P = 2 for 1.1B params
+# (3.71 vs 3.76 ms: K1's doubled NVLink stores) and at P = 4 for both.
+AG_MAX_P = int(os.environ.get("LIONCUB_AG_MAX_P", "2"))
+AG_MAX_N = int(os.environ.get("LIONCUB_AG_MAX_N", str(1 << 28)))
+
+
+class _Allgather:
+    """Receive rows of the allgather exchange: two halves (alternating by
+    step, so a fast rank's next encode never overwrites rows a slow rank is
+    still voting) x P rows x ceil(n/1024)*32 words, mapped on every rank."""
+
+    def __init__(self, ws, topo, n):
+        P, r, tp = topo.world_size, topo.rank, topo.transport
+        self.row = row = max(32, -(-n // 1024) * 32)   # words per row
+        self.buf = tp.sym_buffer(r, ws.key + ("ag_rows",), 2 * P * row, torch.int32)
+        if not hasattr(self.buf, "ag_steps"):
+            self.buf.ag_steps = 0      # shared by every workspace on this buffer
+        half = P * row * 4
+        self.rows = [self.buf.local.data_ptr() + h * half for h in (0, 1)]
+        self.dst = [_lib.table([self.buf.peers[q] + h * half + r * row * 4 for q in range(P)])
+                    for h in (0, 1)]
+        self.L = row * 32              # one "block" covering the whole vector
+
+
 def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, g, m, mflat,
                        hyp, segs, s, tree=False, pipe=None, theta=None):
     """K1 encode -> exchange -> owner vote into the gather buffer (+nz, ties).
@@ -701,6 +731,28 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
     else:
         enc, fb = _lib.LC_ENC_F64, 64
     fused = ws.p2p and tp.fused_barriers
+    if kind == "1bit" and fused and ws.tout is None and pipe is None and theta is not None \
+            and P <= AG_MAX_P and n <= AG_MAX_N:
+        # allgather exchange: K1 stores its sign words into every rank, the
+        # last CTA publishes e1; K5v waits for e1 and votes + updates locally
+        if ws.ag is None:
+            ws.ag = _Allgather(ws, topo, n)
+        ag = ws.ag
+        h = ag.buf.ag_steps & 1
+        ag.buf.ag_steps += 1
+        (e1,) = tp.take_epochs(r, 1)
+        if ws.syncs is None:
+            ws.syncs = [tp.sync_struct(r, ws.counters[i:i + 1], 0, 0) for i in range(3)]
+        a, b = ws.syncs[0], ws.syncs[1]
+        a.wait_epoch, a.arrive_epoch = 0, e1
+        b.wait_epoch, b.arrive_epoch = e1, 0
+        _lib.call("lc_encode", gp, mp, mk, n, C.byref(hyp), fill,
+                  _lib.LC_ENC_SIGN1 | _lib.LC_ENC_REPLICATE, 1, None, ag.dst[h], P, ag.L, 0,
+                  ws.flags.data_ptr(), C.byref(a), s)
+        _lib.call("lc_vote_update", ag.rows[h], ag.row, P, theta.data_ptr(), n, fill, sum_mode,
+                  hyp.lr, hyp.weight_decay, ws.flags.data_ptr(), C.byref(b), s)
+        ws.applied = True
+        return None
     sy1 = sy2 = sy3 = None
     if fused:
         # the barriers live inside the kernels: K1's last CTA publishes e1,

@@ -430,6 +430,11 @@ class NcclTransport(DeviceTransport):
             self._epoch[rank] = 0
         return flags
 
+    def error_word(self, rank) -> int:
+        """Device address of this rank's barrier error word (uint32)."""
+        self._flags(rank)
+        return self._err[rank].data_ptr()
+
     def take_epochs(self, rank, k):
         self._flags(rank)
         first = self._epoch[rank] + 1

@@ -93,6 +93,47 @@ def main():
                 fails.append(f"{algo}/{bits}/{kind}/{zm}: sign {k}")
             if met["ties"][k] != ties[k]:
                 fails.append(f"{algo}/{bits}/{kind}/{zm}: ties {k} {met['ties'][k]} != {ties[k]}")
+    # the production path (no metrics): fused in-kernel barriers / the
+    # streamed step, three consecutive steps against the oracle fed the
+    # fp32-rounded state each step
+    f32 = lambda d: {k: np.asarray(v, np.float32).astype(np.float64) for k, v in d.items()}  # noqa
+    for ci, (algo, bits, kind, zm, sync) in enumerate(CONFIGS):
+        ranks = O.synth_rank_inputs(300 + ci, world, SIZES, kind)
+        h = O.Hyper(0.9, 0.99, 1e-4, 0.1)
+        it0 = 4
+        thetas = [f32(ranks[0]["theta"])] * world
+        moms = [f32(r["m"]) for r in ranks]
+        for i in range(3):
+            nt, nm, *_ = O.distributed_step(thetas, moms, [r["g"] for r in ranks], h,
+                                            None if bits is None else O.Spec(bits), algo,
+                                            it0 + i, zero_mode=zm)
+            nm = [f32(x) for x in nm]
+            if sync is not None:
+                nm = O.sync_momentum(nm, sync[0], sync[1], it0 + i + 1)
+            thetas, moms = [f32(x) for x in nt], [f32(x) for x in nm]
+        mine = ranks[rank]
+        st = lc.WorkerState.initial({k: torch.from_numpy(v).to(dev)
+                                     for k, v in ranks[0]["theta"].items()})
+        for k, v in mine["m"].items():
+            st.momentum[k].copy_(torch.from_numpy(v))
+        st.iteration = it0
+        g = st.new_grad_buffer()
+        for k, v in mine["g"].items():
+            g[k].copy_(torch.from_numpy(v))
+        for i in range(3):
+            st = lc.distributed_lion_step(st, g, lc.LionHyper(0.9, 0.99, 1e-4, 0.1),
+                                          None if bits is None else lc.QuantSpec(bits=bits),
+                                          topo, algo, zero_mode=zm)
+            if sync is not None:
+                st = lc.maybe_sync_momentum(st, lc.SyncPolicy(period=sync[0], layers=sync[1]),
+                                            topo)
+        torch.cuda.synchronize()
+        for k in SIZES:
+            checked += 1
+            if not f32_eq(st.params[k].cpu().numpy(), thetas[rank][k]):
+                fails.append(f"prod {algo}/{bits}/{kind}/{zm}: theta {k}")
+            if not f32_eq(st.momentum[k].cpu().numpy(), moms[rank][k]):
+                fails.append(f"prod {algo}/{bits}/{kind}/{zm}: m {k}")
     # reference golden collectives at this world size
     for c in G.collective_cases():
         if c["world"] != world:

@@ -67,6 +67,17 @@ def main():
         "lc_apply_update", th.data_ptr(), n, _lib.table([send.data_ptr()]), None, 1,
         P * cw, 0, 1e-4, 0.0, None, s),
         8 * n + n / 8)
+    # allgather exchange: K1 replicating into P local rows, K5v over P rows
+    row = -(-n // 1024) * 32
+    rows = torch.zeros(P * row, dtype=torch.int32, device=dev)
+    rdst = _lib.table([rows.data_ptr() + j * row * 4 for j in range(P)])
+    timed("encode_replicate", lambda: _lib.call(
+        "lc_encode", g.data_ptr(), m.data_ptr(), None, n, C.byref(hyp), 1,
+        _lib.LC_ENC_SIGN1 | _lib.LC_ENC_REPLICATE, 1, None, rdst, P, row * 32, 0,
+        flags.data_ptr(), None, s), 12 * n + P * n / 8)
+    timed("vote_update", lambda: _lib.call(
+        "lc_vote_update", rows.data_ptr(), row, P, th.data_ptr(), n, 1, 0, 1e-4, 0.0,
+        flags.data_ptr(), None, s), 8 * n + P * n / 8)
     timed("fused_local", lambda: _lib.call(
         "lc_fused_local_step", th.data_ptr(), m.data_ptr(), g.data_ptr(), None, n,
         C.byref(hyp), 1, _lib.LC_LOCAL_BINARY, None, None, None, None, flags.data_ptr(), s),

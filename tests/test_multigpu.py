@@ -17,16 +17,27 @@ def _ngpu():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("p2p", ["1", "0"], ids=["nvlink-peer-memory", "nccl"])
+MODES = {
+    # default policy (allgather at P = 2, owner vote above)
+    "nvlink-default": {"LIONCUB_P2P": "1"},
+    # allgather exchange forced: K1 -> every rank, K5v votes + updates
+    "nvlink-allgather": {"LIONCUB_P2P": "1", "LIONCUB_AG_MAX_P": "64"},
+    # owner vote forced: K1 -> owner, fused vote + voted-word push + update
+    "nvlink-owner-vote": {"LIONCUB_P2P": "1", "LIONCUB_AG_MAX_P": "1"},
+    "nccl": {"LIONCUB_P2P": "0"},
+}
+
+
+@pytest.mark.parametrize("mode", list(MODES))
 @pytest.mark.parametrize("nproc", [2, 4, 8])
-def test_process_per_gpu_parity(nproc, p2p):
+def test_process_per_gpu_parity(nproc, mode):
     if _ngpu() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1",
-           f"--master-port={29600 + 2 * nproc + int(p2p)}",
+           f"--master-port={29600 + 8 * nproc + list(MODES).index(mode)}",
            os.path.join(ROOT, "tests", "mgpu_parity.py")]
-    env = dict(os.environ, LIONCUB_P2P=p2p)
+    env = dict(os.environ, **MODES[mode])
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     assert '"failures_all_ranks": 0' in res.stdout
@@ -74,5 +85,17 @@ def test_thread_per_gpu_run_ranks(p2p):
                 assert_f32_equal(th[k], nt[0][k], f"theta {k}")
                 assert_f32_equal(m[k], nm[r][k], f"m {k}")
                 assert met["ties"][k] == ties[k]
+        # production path (no metrics): the allgather exchange on peer memory
+        nt, nm, *_ = O.distributed_step(
+            [r["theta"] for r in ranks], [r["m"] for r in ranks], [r["g"] for r in ranks],
+            h, O.Spec(1), "direct", 9)
+        case = dict(world=n, lr=1e-3, wd=0.1, bits=1, algo="direct", iteration=9,
+                    zero_mode="alternating")
+        res = run_step_case(case, ranks[0]["theta"], [r["m"] for r in ranks],
+                            [r["g"] for r in ranks], transport=tp, metrics=False)
+        for r, (th, m, _, _) in enumerate(res):
+            for k in sizes:
+                assert_f32_equal(th[k], nt[0][k], f"theta {k}")
+                assert_f32_equal(m[k], nm[r][k], f"m {k}")
     finally:
         tp.close()
