@@ -32,24 +32,19 @@ int set_err(int code, const char* fmt, ...);
 // SMs of the current device (cached per device).
 int sm_count();
 
-// Grid size for a grid-stride streaming kernel: enough resident CTAs to fill
-// every SM (occupancy-derived), never more than the work needs.
-// Resident CTAs per SM of `kernel` at `block` threads, cached per kernel and
-// device (the occupancy query is not free on the launch path).
+// Resident CTAs per SM of `kernel` at `block` threads (occupancy query),
+// cached per (device, kernel) -- the query is not free on the launch path.
+// Keyed by the kernel's address: template instances share a type but not
+// their register counts.  Thread-safe (one host thread per GPU may launch).
+int resident_ctas_of(const void* kernel, int block);
+
 template <typename K>
 int resident_ctas(K kernel, int block) {
-  static int cache[64] = {0};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) dev = 0;
-  if (!cache[dev]) {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0);
-    cache[dev] = per_sm < 1 ? 1 : per_sm;
-  }
-  return cache[dev];
+  return resident_ctas_of(reinterpret_cast<const void*>(kernel), block);
 }
 
+// Grid size for a grid-stride streaming kernel: enough resident CTAs to fill
+// every SM (occupancy-derived), never more than the work needs.
 template <typename K>
 int stream_grid(K kernel, int block, int64_t work_items, int items_per_cta) {
   int per_sm = resident_ctas(kernel, block);

@@ -7,6 +7,10 @@
 // Math that decides a sign (c, the p-bit scale, the update) runs in float64
 // with every product/sum rounded separately (no FMA contraction) so results
 // equal the float64 numpy reference bit-for-bit; fp32 state is rounded once.
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #include "common.cuh"
 
 namespace lc {
@@ -37,6 +41,22 @@ int sm_count() {
     cache[dev] = v > 0 ? v : 148;
   }
   return cache[dev];
+}
+
+int resident_ctas_of(const void* kernel, int block) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void*, int>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(dev, kernel, block);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0);
+  if (per_sm < 1) per_sm = 1;
+  cache.emplace(key, per_sm);
+  return per_sm;
 }
 
 struct SegQ {
@@ -377,7 +397,7 @@ k_apply_update(float* __restrict__ theta, int64_t n, Dst sb, Dst nzb, int64_t wp
 #define LC_FUSED_U 2
 #endif
 #ifndef LC_FUSED_MINB
-#define LC_FUSED_MINB 1
+#define LC_FUSED_MINB 3
 #endif
 
 template <int MODE, bool MASK, bool METRICS, int U>
