@@ -25,7 +25,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define LIONCUB_ABI_VERSION 1
+#define LIONCUB_ABI_VERSION 2
 
 enum {
   LC_OK = 0,
@@ -83,12 +83,28 @@ typedef struct lc_sync {
   double timeout_s;
 } lc_sync;
 
-/* Per-layer segment table of a flat buffer (layers in sorted-name order). */
+/* Quantizer variant flags (QuantSpec, quant.py:28-55). */
+enum {
+  LC_Q_STOCHASTIC = 1u << 0, /* rounding="stochastic": floor(v) + (u < frac),
+                                u from the counter-based stream lc::uniform01(seed, e)
+                                (reference: PCG64 draws, quant.py:107-116)   */
+  LC_Q_NO_ZERO = 1u << 1     /* no_zero: q == 0 and c != 0 -> sign(c) (:171-173) */
+};
+
+/* Per-layer segment table of a flat buffer (layers in sorted-name order).
+ * The quantizer (quant.py:127-173) is q = clip(round(scale[s] * y), +-qmax)
+ * with y = c, or y = sign(c) log1p(|c| / log_scale[s]) when log_scale is
+ * given and log_scale[s] > 0 (log_transform, quant.py:146-150). */
 typedef struct lc_segments {
   const int64_t* start; /* device, nseg+1 offsets (elements)               */
-  const double* scale;  /* device, nseg quant scales qmax/(2 M1) or NULL   */
+  const double* scale;  /* device, nseg scales: qmax/(2 M_p), or qmax/M_inf
+                           for norm_p = inf; NULL when not quantizing      */
   int32_t nseg;
   int32_t qmax;
+  const double* log_scale; /* device, nseg M1(c) for log_transform, or NULL */
+  uint32_t qflags;         /* LC_Q_* bits                                   */
+  uint32_t reserved;
+  uint64_t seed;           /* stochastic-rounding stream of this rank/step  */
 } lc_segments;
 
 int lc_abi_version(void);
@@ -231,6 +247,24 @@ int lc_l1_plan_destroy(lc_l1_plan_t plan);
 int lc_l1_scales(lc_l1_plan_t plan, const float* g, const float* m,
                  const uint8_t* mask, const lc_hyper* h, int32_t qmax,
                  double* norms, double* scales, void* stream);
+/* ---- per-segment mean p-norm of every order (quant.py:81-104) and the
+ * quantizer scale, for y = c or the log-mapped c (log_scale != NULL):
+ *   p = 1    exact (the lc_l1_scales schedule);
+ *   p = 2, 0.5  exact: (a/max)**2 = square, **0.5 = sqrt, as numpy does;
+ *   other finite p  max * mean(pow(a/max, p))**(1/p) in numpy's pairwise
+ *            order, CUDA pow (<= 2 ulp; numpy's own pow is not glibc's);
+ *   p = 0    exp(sum(log a) / #nonzero) (tree order, CUDA log/exp);
+ *   p = inf  max|y|, scale = qmax / M.
+ * norms/scales: nseg doubles each. */
+typedef struct lc_norm_spec {
+  double p;                /* 0, finite > 0, or +inf                        */
+  int32_t qmax;
+  int32_t reserved;
+  const double* log_scale; /* device, nseg M1(c) (from lc_l1_scales), or NULL */
+} lc_norm_spec;
+int lc_norm_scales(lc_l1_plan_t plan, const float* g, const float* m,
+                   const uint8_t* mask, const lc_hyper* h, const lc_norm_spec* spec,
+                   double* norms, double* scales, void* stream);
 /* Self-check of the reciprocal-based correctly rounded division the norm
  * kernel uses for |c|/max (counts bit mismatches vs IEEE division over
  * pairs with |a| clamped to b). */

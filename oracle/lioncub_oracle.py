@@ -117,6 +117,122 @@ def quantize_l1(x, bits: int) -> np.ndarray:
     return np.clip(q, -qmax, qmax)
 
 
+INF = float("inf")
+
+
+def lp_mean_norm(x, p: float) -> float:
+    """``lp_mean_norm`` (quant.py:81-104), every order: p = inf -> max|x|;
+    p = 0 -> exp(mean(log|x_j|)) over the nonzero entries (0 if none);
+    finite p -> max * mean((|x|/max)**p)**(1/p)."""
+    x = np.asarray(x, dtype=np.float64)
+    if x.size == 0:
+        raise OracleConfigError("lp_mean_norm of an empty vector")
+    a = np.abs(x)
+    if p == INF:
+        return float(a.max())
+    if p == 0:
+        nz = a[a > 0]
+        if nz.size == 0:
+            return 0.0
+        return float(np.exp(np.mean(np.log(nz))))
+    if p <= 0:
+        raise OracleConfigError(f"invalid norm order {p}")
+    m = a.max()
+    if m == 0:
+        return 0.0
+    return float(m * np.mean((a / m) ** p) ** (1.0 / p))
+
+
+_GOLDEN = 0x9E3779B97F4A7C15
+
+
+def splitmix_uniforms(seed: int, index) -> np.ndarray:
+    """The CUDA path's stochastic-rounding stream (csrc/common.cuh
+    ``lc::uniform01``): element e draws u = (splitmix64(seed + (e+1)*golden)
+    >> 11) * 2**-53, a counter-based stream (no sequential state, so any
+    element range of any rank can be drawn independently).  The reference
+    draws from numpy's PCG64 (quant.py:107-116); parity of stochastic
+    rounding with the reference is statistical, with this stream exact."""
+    e = np.asarray(index, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = np.uint64(seed & 0xFFFFFFFFFFFFFFFF) + (e + np.uint64(1)) * np.uint64(_GOLDEN)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return (z >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+
+
+def sround(v, u) -> np.ndarray:
+    """``sround`` (quant.py:107-116) with the uniforms supplied: floor(v) +
+    (u < v - floor(v))."""
+    v = np.asarray(v, dtype=np.float64)
+    lo = np.floor(v)
+    frac = v - lo
+    return (lo + (np.asarray(u) < frac)).astype(np.int64)
+
+
+def quantize(x, spec: "Spec", uniforms=None) -> np.ndarray:
+    """``quantize`` (quant.py:127-173), every variant: optional log map
+    y = sign(x) log1p(|x|/M1(x)) (:146-150, :119-120), scale qmax/M_inf
+    (p = inf, :153-161) or qmax/(2 M_p) (:162-170), nearest (half-even) or
+    stochastic rounding (``uniforms`` = the per-element draws), clip,
+    then no_zero (:171-173)."""
+    x = np.asarray(x, dtype=np.float64)
+    if x.size == 0:
+        raise OracleConfigError("quantize of an empty vector")
+    qmax = spec.qmax
+    y = x
+    if spec.log_transform:
+        s = lp_mean_norm(x, 1.0)
+        if s > 0:
+            y = np.sign(x) * np.log1p(np.abs(x) / s)
+    m = lp_mean_norm(y, spec.norm_p)
+    if m == 0 or qmax == 0:
+        q = np.zeros(x.shape, dtype=np.int64)
+    else:
+        scaled = (qmax / m) * y if spec.norm_p == INF else (qmax / (2.0 * m)) * y
+        if spec.rounding == "stochastic":
+            if uniforms is None:
+                raise OracleConfigError("stochastic rounding needs an rng")
+            q = sround(scaled, np.asarray(uniforms).reshape(x.shape))
+        else:
+            q = np.round(scaled).astype(np.int64)
+        q = np.clip(q, -qmax, qmax)
+    if spec.no_zero:
+        fix = (q == 0) & (x != 0)
+        q = np.where(fix, np.sign(x).astype(np.int64), q)
+    return q
+
+
+def quant_scale(x, spec: "Spec") -> tuple:
+    """(scale, log_scale) the quantizer multiplies by: the per-layer scalars
+    the CUDA norm kernels produce (quant.py:146-170)."""
+    x = np.asarray(x, dtype=np.float64)
+    y, s = x, None
+    if spec.log_transform:
+        s = lp_mean_norm(x, 1.0)
+        if s > 0:
+            y = np.sign(x) * np.log1p(np.abs(x) / s)
+    m = lp_mean_norm(y, spec.norm_p)
+    if m == 0 or spec.qmax == 0:
+        return 0.0, s, m
+    return (spec.qmax / m if spec.norm_p == INF else spec.qmax / (2.0 * m)), s, m
+
+
+def dequantize(q, spec: "Spec", norm: float, log_scale: float | None = None) -> np.ndarray:
+    """``dequantize`` (quant.py:176-195)."""
+    q = np.asarray(q, dtype=np.float64)
+    qmax = spec.qmax
+    if qmax == 0 or norm == 0:
+        return np.zeros_like(q)
+    y = q * (norm / qmax) if spec.norm_p == INF else q * (2.0 * norm / qmax)
+    if spec.log_transform:
+        if log_scale is None:
+            raise OracleConfigError("dequantize of a log-transformed vector needs log_scale")
+        return np.sign(y) * log_scale * np.expm1(np.abs(y))
+    return y
+
+
 def pack_words(stored, width: int) -> np.ndarray:
     """``pack(values, width)`` payload (quant.py:330-356) viewed as
     little-endian uint32 words: element i sits at bits
@@ -278,9 +394,13 @@ class Hyper:
 
 @dataclass
 class Spec:
-    """The subset of ``QuantSpec`` (quant.py:102-130) on the hot path:
-    bits with norm_p=1, nearest rounding."""
+    """``QuantSpec`` (quant.py:28-55): bits, norm order, rounding, log map,
+    no_zero."""
     bits: int = 8
+    norm_p: float = 1.0
+    rounding: str = "nearest"
+    log_transform: bool = False
+    no_zero: bool = False
 
     @property
     def qmax(self) -> int:
@@ -288,8 +408,9 @@ class Spec:
 
 
 def _vote_layer(cs: Sequence[np.ndarray], spec: Spec | None, algo: str,
-                mode: str, t: int):
-    """``_vote`` (optimizer.py:137-169): returns (sign, Vote)."""
+                mode: str, t: int, uniforms=None):
+    """``_vote`` (optimizer.py:137-169): returns (sign, Vote).  ``uniforms``:
+    per-rank stochastic-rounding draws of this layer."""
     if algo == "compressed1bit":
         v = vote_1bit(cs, mode, t)
         return v.values, v
@@ -300,7 +421,8 @@ def _vote_layer(cs: Sequence[np.ndarray], spec: Spec | None, algo: str,
     elif spec.bits == 1:
         qs = [apply_sign(c, mode, t) for c in cs]
     else:
-        qs = [quantize_l1(c, spec.bits) for c in cs]
+        qs = [quantize(c, spec, None if uniforms is None else uniforms[r])
+              for r, c in enumerate(cs)]
     if algo in ("ps", "ps_efficient"):
         if spec is None:
             v = ps_sum(qs, efficient=algo == "ps_efficient")
@@ -320,12 +442,16 @@ def distributed_step(thetas: Sequence[Mapping[str, np.ndarray]],
                      grads: Sequence[Mapping[str, np.ndarray]],
                      h: Hyper, spec: Spec | None, algo: str, iteration: int,
                      zero_mode: str = "alternating",
-                     masks: Mapping[str, np.ndarray] | Sequence | None = None):
+                     masks: Mapping[str, np.ndarray] | Sequence | None = None,
+                     seeds: Sequence[int] | None = None):
     """``distributed_lion_step`` for all P ranks at once
     (optimizer.py:172-210).  Per layer in sorted order: c = b1*m + (1-b1)*g
     (:199), optional mask (:200-201), vote (:202), theta' (:204), m' (:205).
 
     ``masks`` is one mapping shared by all ranks or a per-rank sequence.
+    ``seeds``: per-rank stochastic-rounding seeds of this step (the CUDA
+    path's stream is indexed by the element's offset in the sorted-name flat
+    buffer).
     Returns (thetas', moms', vote_sign{layer}, ties{layer}, c{rank}{layer},
     vote{layer})."""
     p = len(thetas)
@@ -335,6 +461,7 @@ def distributed_step(thetas: Sequence[Mapping[str, np.ndarray]],
     new_m = [dict() for _ in range(p)]
     signs, ties, votes = {}, {}, {}
     cs_all = [dict() for _ in range(p)]
+    offset = 0
     for name in sorted(thetas[0]):
         cs = []
         for r in range(p):
@@ -349,7 +476,12 @@ def distributed_step(thetas: Sequence[Mapping[str, np.ndarray]],
             cs.append(c)
             cs_all[r][name] = c
         flat = [c.ravel() for c in cs]
-        sign, vote = _vote_layer(flat, spec, algo, zero_mode, t)
+        uni = None
+        if seeds is not None:
+            idx = offset + np.arange(flat[0].size)
+            uni = [splitmix_uniforms(seeds[r], idx) for r in range(p)]
+        offset += flat[0].size
+        sign, vote = _vote_layer(flat, spec, algo, zero_mode, t, uniforms=uni)
         sign = np.asarray(sign).reshape(cs[0].shape)
         for r in range(p):
             theta = np.asarray(thetas[r][name], dtype=np.float64)

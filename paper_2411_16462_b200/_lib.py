@@ -48,9 +48,20 @@ class Hyper(C.Structure):
                 ("lr", C.c_double), ("weight_decay", C.c_double)]
 
 
+LC_Q_STOCHASTIC = 1 << 0
+LC_Q_NO_ZERO = 1 << 1
+
+
 class Segments(C.Structure):
     _fields_ = [("start", C.c_void_p), ("scale", C.c_void_p),
-                ("nseg", C.c_int32), ("qmax", C.c_int32)]
+                ("nseg", C.c_int32), ("qmax", C.c_int32),
+                ("log_scale", C.c_void_p), ("qflags", C.c_uint32),
+                ("reserved", C.c_uint32), ("seed", C.c_uint64)]
+
+
+class NormSpec(C.Structure):
+    _fields_ = [("p", C.c_double), ("qmax", C.c_int32), ("reserved", C.c_int32),
+                ("log_scale", C.c_void_p)]
 
 
 class Sync(C.Structure):
@@ -83,6 +94,7 @@ SIGNATURES = {
     "lc_l1_plan_create": (INT, [P, P, I32]),
     "lc_l1_plan_destroy": (INT, [P]),
     "lc_l1_scales": (INT, [P, P, P, P, P, I32, P, P, P]),
+    "lc_norm_scales": (INT, [P, P, P, P, P, P, P, P, P]),
     "lc_debug_div_check": (INT, [P, P, I64, P, P]),
     "lc_compute_c": (INT, [P, P, P, I64, P, P, P]),
     "lc_count_bits_segmented": (INT, [P, P, I32, P, P]),
@@ -167,7 +179,7 @@ KERNEL_CALLS = frozenset({
     "lc_apply_update", "lc_fused_local_step", "lc_mean_f32", "lc_compute_c",
     "lc_count_bits_segmented", "lc_bits_to_sign", "lc_pack_i64_fields",
     "lc_fields_decode", "lc_sign_pack_f64", "lc_sum_u32_rows"})
-KERNELS_PER_CALL = {"lc_l1_scales": 3}
+KERNELS_PER_CALL = {"lc_l1_scales": 3, "lc_norm_scales": 3}
 
 launches = 0  # kernels enqueued through call(); read by bench.py
 

@@ -78,6 +78,19 @@ __device__ __forceinline__ float lion_theta(float th, double s, double lr,
       __dsub_rn(t, __dmul_rn(lr, __dadd_rn(s, __dmul_rn(wd, t)))));
 }
 
+// Stochastic-rounding stream: element e of a rank's flat buffer draws
+// u = (splitmix64(seed + (e+1) * golden) >> 11) * 2^-53 in [0, 1) -- a
+// counter-based generator (no per-thread state; any element range can be
+// drawn independently).  oracle/lioncub_oracle.py splitmix_uniforms
+// restates it.
+__device__ __forceinline__ double uniform01(uint64_t seed, int64_t e) {
+  uint64_t z = seed + (uint64_t)(e + 1) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return (double)(z >> 11) * 0x1.0p-53;
+}
+
 __device__ __forceinline__ float4 ld_stream(const float4* p) {
   return __ldcs(p);
 }

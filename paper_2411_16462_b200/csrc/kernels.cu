@@ -10,6 +10,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -64,7 +65,15 @@ struct SegQ {
   const double* scale;
   int nseg;
   int qmax;
+  const double* logs;  // per-segment log_transform scale, or null
+  uint32_t qflags;     // LC_Q_*
+  uint64_t seed;
 };
+
+// Internal variants picked when the segment table asks for a quantizer
+// other than nearest-rounding L1 without log map / no_zero.
+constexpr int kEncQuantX = 4;    // lc_encode: QUANT_FIELDS with quant_x
+constexpr int kLocalQuantX = 3;  // lc_fused_local_step: QUANT with quant_x
 
 // Destination table: block j of a packed vector goes to p[j] (local send
 // buffer, or the owner GPU's receive slot over NVLink).
@@ -86,6 +95,51 @@ struct SegCursor {
     return scale;
   }
 };
+
+// Cursor of the general quantizer: scale and log scale of the segment.
+struct SegCursorX {
+  int64_t lo = 0, hi = -1;
+  double scale = 0.0, logs = 0.0;
+  __device__ __forceinline__ void at(const SegQ& sq, int64_t e) {
+    if (e < lo || e >= hi) {
+      int s = seg_find(sq.start, sq.nseg, e);
+      lo = __ldg(sq.start + s);
+      hi = __ldg(sq.start + s + 1);
+      scale = __ldg(sq.scale + s);
+      logs = sq.logs ? __ldg(sq.logs + s) : 0.0;
+    }
+  }
+  __device__ __forceinline__ double get(const SegQ& sq, int64_t e) {
+    at(sq, e);
+    return scale;
+  }
+};
+
+// Every quantizer variant (quant.py:127-173): y = c or sign(c) log1p(|c|/s)
+// (s > 0), v = scale * y, nearest (half-even) or stochastic rounding
+// floor(v) + (u < v - floor(v)), clip to +-qmax, then no_zero: a zero q of
+// a nonzero c becomes sign(c).  e: element index of the rank's flat buffer
+// (the stochastic stream position).
+__device__ __forceinline__ int quant_x(double c, const SegQ& sq, SegCursorX& cur, int64_t e) {
+  cur.at(sq, e);
+  double y = c;
+  if (cur.logs > 0.0) {
+    const double l = log1p(__ddiv_rn(fabs(c), cur.logs));
+    y = c > 0.0 ? l : (c < 0.0 ? -l : 0.0);
+  }
+  const double v = __dmul_rn(cur.scale, y);
+  double r;
+  if (sq.qflags & LC_Q_STOCHASTIC) {
+    const double lo = floor(v);
+    r = lo + (uniform01(sq.seed, e) < __dsub_rn(v, lo) ? 1.0 : 0.0);
+  } else {
+    r = rint(v);
+  }
+  r = fmin(fmax(r, -(double)sq.qmax), (double)sq.qmax);
+  int q = (int)r;
+  if ((sq.qflags & LC_Q_NO_ZERO) && q == 0 && c != 0.0) q = c > 0.0 ? 1 : -1;
+  return q;
+}
 
 // q = clip(round_half_even(scale*c), +-qmax)   (quant.py:236-243)
 __device__ __forceinline__ int quant_l1(double c, double scale, int qmax) {
@@ -139,10 +193,10 @@ __device__ __forceinline__ void pack_store(uint32_t* __restrict__ out,
 // Encode 4 consecutive elements of one lane: c and m' in float64, m' back as
 // fp32, and the stored value of each element (sign bit / field).  VALID is
 // false only for the last, partial sub-tile.
-template <int ENC, bool MASK>
+template <int ENC, bool MASK, class CUR>
 __device__ __forceinline__ void encode4(const float ge[4], const float me[4], const bool keep[4],
                                         const bool valid[4], const Hyp& h, uint32_t fillbit,
-                                        uint32_t zflag, const SegQ& sq, SegCursor& cur,
+                                        uint32_t zflag, const SegQ& sq, CUR& cur,
                                         int64_t e0, double c[4], float mn[4], uint32_t st[4],
                                         uint32_t& flag) {
 #pragma unroll
@@ -152,6 +206,8 @@ __device__ __forceinline__ void encode4(const float ge[4], const float me[4], co
     mn[q] = lion_m(me[q], ge[q], h);
     if constexpr (ENC == LC_ENC_QUANT_FIELDS) {
       st[q] = valid[q] ? (uint32_t)(quant_l1(c[q], cur.get(sq, e0 + q), sq.qmax) + sq.qmax) : 0u;
+    } else if constexpr (ENC == kEncQuantX) {
+      st[q] = valid[q] ? (uint32_t)(quant_x(c[q], sq, cur, e0 + q) + sq.qmax) : 0u;
     } else if constexpr (ENC != LC_ENC_F64) {
       // sign with the zero fill; -0.0 == 0 (np.sign(-0.0) == 0); NaN -> 0
       const bool pos = c[q] > 0.0, zero = c[q] == 0.0;
@@ -207,7 +263,7 @@ k_encode(const float* __restrict__ g, float* __restrict__ m,
   const float4* g4 = reinterpret_cast<const float4*>(g);
   float4* m4 = reinterpret_cast<float4*>(m);
   uint32_t flag = 0;
-  SegCursor cur;
+  std::conditional_t<ENC == kEncQuantX, SegCursorX, SegCursor> cur;
   const bool valid_all[4] = {true, true, true, true};
 
   for (int64_t sidx = gw; sidx < nsup; sidx += nw) {
@@ -419,7 +475,7 @@ k_fused_local(float* __restrict__ theta, float* __restrict__ m,
   float4* m4 = reinterpret_cast<float4*>(m);
   float4* th4 = reinterpret_cast<float4*>(theta);
   uint32_t flag = 0;
-  SegCursor cur;
+  std::conditional_t<MODE == kLocalQuantX, SegCursorX, SegCursor> cur;
   for (int64_t t0 = gw; t0 < ntiles; t0 += nw * U) {
     float4 gv[U], mv[U], tv[U];
     uchar4 mk[U];
@@ -468,8 +524,10 @@ k_fused_local(float* __restrict__ theta, float* __restrict__ m,
         if (MASK && !keep[k]) c = 0.0;
         mn[k] = lion_m(me[k], ge[k], h);
         double agg;  // the single-rank aggregate the vote signs
-        if (MODE == LC_LOCAL_QUANT) {
+        if constexpr (MODE == LC_LOCAL_QUANT) {
           agg = valid[k] ? (double)quant_l1(c, cur.get(sq, e0 + k), sq.qmax) : 1.0;
+        } else if constexpr (MODE == kLocalQuantX) {
+          agg = valid[k] ? (double)quant_x(c, sq, cur, e0 + k) : 1.0;
         } else {
           agg = c;
         }
@@ -1199,15 +1257,21 @@ constexpr int kBlock = 256;
 Hyp to_hyp(const lc_hyper* h) { return Hyp{h->beta1, h->one_minus_beta1, h->beta2, h->one_minus_beta2}; }
 
 SegQ to_segq(const lc_segments* s) {
-  SegQ q{nullptr, nullptr, 0, 0};
+  SegQ q{nullptr, nullptr, 0, 0, nullptr, 0u, 0ull};
   if (s) {
     q.start = s->start;
     q.scale = s->scale;
     q.nseg = s->nseg;
     q.qmax = s->qmax;
+    q.logs = s->log_scale;
+    q.qflags = s->qflags;
+    q.seed = s->seed;
   }
   return q;
 }
+
+// The segment table asks for a quantizer beyond nearest-rounding L1.
+bool needs_quant_x(const lc_segments* s) { return s && (s->log_scale || s->qflags); }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -1314,6 +1378,8 @@ int lc_encode(const float* g, float* m, const uint8_t* mask, int64_t n,
       if (!segs || !segs->start || !segs->scale || segs->nseg < 1)
         return set_err(LC_E_ARG, "lc_encode: quant needs a segment table with scales");
       if (field_bits < 2) return set_err(LC_E_ARG, "lc_encode: quant fields need >= 2 bits");
+      if (needs_quant_x(segs))
+        return dispatch_fields<kEncQuantX>(field_bits, g, m, mask, n, h, fill, sq, d, L, flags, st);
       return dispatch_fields<LC_ENC_QUANT_FIELDS>(field_bits, g, m, mask, n, h, fill, sq, d, L, flags, st);
     case LC_ENC_F64:
       return dispatch_mask<LC_ENC_F64, 1>(g, m, mask, n, h, fill, sq, d, L, flags, st);
@@ -1388,7 +1454,10 @@ int lc_fused_local_step(float* theta, float* m, const float* g, const uint8_t* m
   switch (mode) {
     case LC_LOCAL_BINARY: LC_FUSED_M(LC_LOCAL_BINARY); break;
     case LC_LOCAL_PS: LC_FUSED_M(LC_LOCAL_PS); break;
-    case LC_LOCAL_QUANT: LC_FUSED_M(LC_LOCAL_QUANT); break;
+    case LC_LOCAL_QUANT:
+      if (needs_quant_x(segs)) LC_FUSED_M(kLocalQuantX);
+      else LC_FUSED_M(LC_LOCAL_QUANT);
+      break;
     default: return set_err(LC_E_ARG, "lc_fused_local_step: unknown mode %d", mode);
   }
 #undef LC_FUSED_M

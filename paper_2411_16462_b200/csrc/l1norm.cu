@@ -14,6 +14,7 @@
 // Every addition happens in exactly numpy's order, so the norm and therefore
 // the quantized integers are bit-identical to the reference.
 #include <algorithm>
+#include <cmath>
 #include <functional>
 #include <map>
 #include <vector>
@@ -128,14 +129,29 @@ namespace {
 
 using lc::Hyp;
 
-// Per-segment max|c| as uint64 bit patterns (non-negative doubles order as
-// unsigned integers).  Each CTA walks a contiguous, 16-byte aligned element
-// range (so it meets few segments) with 128-bit loads, 4 quads per thread in
-// flight; per-lane maxima are merged in shared memory first.
+// Norm orders (lc_norm_scales): the per-element term of numpy's mean and the
+// final root (quant.py:94-104).
+enum { PK_1 = 0, PK_2 = 1, PK_HALF = 2, PK_GEN = 3, PK_0 = 4, PK_INF = 5 };
+
+// |y| for y = c, or the log map y = sign(c) log1p(|c|/s) when s > 0
+// (quant.py:119-120, :146-150): |y| = log1p(|c|/s).
+template <bool LOG>
+__device__ __forceinline__ double abs_y(double c, double s) {
+  double a = fabs(c);
+  if (LOG && s > 0.0) a = log1p(__ddiv_rn(a, s));
+  return a;
+}
+
+// Per-segment max|y| as uint64 bit patterns (non-negative doubles order as
+// unsigned integers), or with COUNT the number of nonzero |y| (p = 0).
+// Each CTA walks a contiguous, 16-byte aligned element range (so it meets
+// few segments) with 128-bit loads, 4 quads per thread in flight; per-lane
+// results are merged in shared memory first.
+template <bool LOG, bool COUNT>
 __global__ void __launch_bounds__(kThreads)
 k_l1_max(const float* __restrict__ g, const float* __restrict__ m,
          const uint8_t* __restrict__ mask, const int64_t* __restrict__ start,
-         int nseg, int64_t n, int64_t per_cta, Hyp h,
+         int nseg, int64_t n, int64_t per_cta, Hyp h, const double* __restrict__ logs,
          unsigned long long* __restrict__ gmax) {
   constexpr int kTab = 256;
   constexpr int QU = 4;
@@ -150,13 +166,26 @@ k_l1_max(const float* __restrict__ g, const float* __restrict__ m,
   __syncthreads();
   int seg = -1;
   int64_t seg_lo = 1, seg_hi = 0;
+  double sv = 0.0;  // log scale of the current segment
   unsigned long long cur = 0ull;
+  auto bits = [](double x) { return (unsigned long long)__double_as_longlong(x); };
+  auto acc = [&](double a) {
+    if (COUNT) {
+      cur += a > 0.0 ? 1ull : 0ull;
+    } else {
+      const unsigned long long b = bits(a);
+      cur = b > cur ? b : cur;
+    }
+  };
   auto flush = [&]() {
     if (seg < 0 || !cur) return;
-    if (use_tab)
-      atomicMax(&tab[seg - s_first], cur);
-    else
-      atomicMax(&gmax[seg], cur);
+    if (use_tab) {
+      if (COUNT) atomicAdd(&tab[seg - s_first], cur);
+      else atomicMax(&tab[seg - s_first], cur);
+    } else {
+      if (COUNT) atomicAdd(&gmax[seg], cur);
+      else atomicMax(&gmax[seg], cur);
+    }
   };
   auto take = [&](int64_t e, float gv, float mv) {
     if (e < seg_lo || e >= seg_hi) {
@@ -165,11 +194,11 @@ k_l1_max(const float* __restrict__ g, const float* __restrict__ m,
       seg = lc::seg_find(start, nseg, e);
       seg_lo = start[seg];
       seg_hi = start[seg + 1];
+      if (LOG) sv = logs[seg];
     }
     double c = lc::lion_c(mv, gv, h);
     if (mask && !mask[e]) c = 0.0;
-    unsigned long long b = (unsigned long long)__double_as_longlong(fabs(c));
-    cur = b > cur ? b : cur;
+    acc(abs_y<LOG>(c, sv));
   };
   const float4* g4 = reinterpret_cast<const float4*>(g);
   const float4* m4 = reinterpret_cast<const float4*>(m);
@@ -191,15 +220,17 @@ k_l1_max(const float* __restrict__ g, const float* __restrict__ m,
       const int64_t e = 4 * q;
       if (!mask && e >= seg_lo && e + 4 <= seg_hi) {
         // the whole quad lies in the current segment: no per-element checks
-        const double c0 = fabs(lc::lion_c(mv[u].x, gv[u].x, h));
-        const double c1 = fabs(lc::lion_c(mv[u].y, gv[u].y, h));
-        const double c2 = fabs(lc::lion_c(mv[u].z, gv[u].z, h));
-        const double c3 = fabs(lc::lion_c(mv[u].w, gv[u].w, h));
-        // max on the bit patterns (non-negative doubles order as unsigned;
-        // a NaN propagates like numpy's max)
-        auto bits = [](double x) { return (unsigned long long)__double_as_longlong(x); };
-        const unsigned long long b = max(max(bits(c0), bits(c1)), max(bits(c2), bits(c3)));
-        cur = b > cur ? b : cur;
+        const double c0 = abs_y<LOG>(lc::lion_c(mv[u].x, gv[u].x, h), sv);
+        const double c1 = abs_y<LOG>(lc::lion_c(mv[u].y, gv[u].y, h), sv);
+        const double c2 = abs_y<LOG>(lc::lion_c(mv[u].z, gv[u].z, h), sv);
+        const double c3 = abs_y<LOG>(lc::lion_c(mv[u].w, gv[u].w, h), sv);
+        if (COUNT) {
+          acc(c0); acc(c1); acc(c2); acc(c3);
+        } else {
+          // max on the bit patterns (a NaN propagates like numpy's max)
+          const unsigned long long b = max(max(bits(c0), bits(c1)), max(bits(c2), bits(c3)));
+          cur = b > cur ? b : cur;
+        }
       } else {
         take(e, gv[u].x, mv[u].x);
         take(e + 1, gv[u].y, mv[u].y);
@@ -213,7 +244,10 @@ k_l1_max(const float* __restrict__ g, const float* __restrict__ m,
   __syncthreads();
   if (use_tab)
     for (int i = threadIdx.x; i <= s_last - s_first; i += blockDim.x)
-      if (tab[i]) atomicMax(&gmax[s_first + i], tab[i]);
+      if (tab[i]) {
+        if (COUNT) atomicAdd(&gmax[s_first + i], tab[i]);
+        else atomicMax(&gmax[s_first + i], tab[i]);
+      }
 }
 
 // a / b correctly rounded given y = RN(1/b): q = RN(a*y) is within one ulp
@@ -244,21 +278,35 @@ __device__ __forceinline__ Recip make_recip(double mx) {
   return r;
 }
 
-template <bool MASK>
+// The summed term of segment order PK for |y| = a: (a/max)**p with numpy's
+// fast paths for p = 1 (copy), 2 (square), 0.5 (sqrt), else pow; p = 0:
+// log(a) of the nonzero entries (zeros add +0.0, which leaves a sum as is).
+template <int PK>
+__device__ __forceinline__ double term(double a, const Recip& dv, double p) {
+  if (PK == PK_0) return a > 0.0 ? log(a) : 0.0;
+  const double t = dv(a);
+  if (PK == PK_1) return t;
+  if (PK == PK_2) return __dmul_rn(t, t);
+  if (PK == PK_HALF) return __dsqrt_rn(t);
+  return pow(t, p);
+}
+
+template <bool MASK, int PK, bool LOG>
 __device__ __forceinline__ double l1_v(const float* g, const float* m, const uint8_t* mask,
-                                       int64_t e, const Hyp& h, const Recip& dv) {
+                                       int64_t e, const Hyp& h, const Recip& dv, double sv,
+                                       double p) {
   double c = lc::lion_c(m[e], g[e], h);
   if (MASK && !mask[e]) c = 0.0;
-  return dv(fabs(c));  // (a / m) ** 1.0 == a / m
+  return term<PK>(abs_y<LOG>(c, sv), dv, p);
 }
 
 // One CTA per work item: leaves with 8 lanes each, then templated additions.
-template <bool MASK>
+template <bool MASK, int PK, bool LOG>
 __global__ void __launch_bounds__(kThreads, 4)
 k_l1_items(const float* __restrict__ g, const float* __restrict__ m,
            const uint8_t* __restrict__ mask, Hyp h,
-           const unsigned long long* __restrict__ gmax,
-           const int64_t* __restrict__ wi_off, const int* __restrict__ wi_meta,
+           const unsigned long long* __restrict__ gmax, const double* __restrict__ logs,
+           double p, const int64_t* __restrict__ wi_off, const int* __restrict__ wi_meta,
            const DevTmpl* __restrict__ tmpl, const int* __restrict__ leaf_rel,
            const int* __restrict__ leaf_size, const int4* __restrict__ tops,
            const int* __restrict__ tlvl, double* __restrict__ nodes) {
@@ -267,12 +315,14 @@ k_l1_items(const float* __restrict__ g, const float* __restrict__ m,
   const int64_t base = wi_off[item];
   const int seg = wi_meta[3 * item], ti = wi_meta[3 * item + 1], node = wi_meta[3 * item + 2];
   const DevTmpl T = tmpl[ti];
-  const double mx = __longlong_as_double((long long)gmax[seg]);
-  if (mx == 0.0) {  // lp_mean_norm returns 0 before summing (quant.py:176-178)
+  // max|y| (or, for p = 0, the nonzero count: only its being 0 matters here)
+  const double mx = PK == PK_0 ? (double)gmax[seg] : __longlong_as_double((long long)gmax[seg]);
+  if (mx == 0.0) {  // lp_mean_norm returns 0 before summing (quant.py:96-102)
     if (threadIdx.x == 0) nodes[node] = 0.0;
     return;
   }
-  const Recip dv = make_recip(mx);
+  const double sv = LOG ? logs[seg] : 0.0;
+  const Recip dv = make_recip(PK == PK_0 ? 1.0 : mx);
   const int lane = threadIdx.x & 31;
   const int k = lane & 7;
   const int group = threadIdx.x >> 3;
@@ -286,7 +336,8 @@ k_l1_items(const float* __restrict__ g, const float* __restrict__ m,
     if (sz < 8) {  // only a whole tiny layer: sequential from 0
       res = 0.0;
       if (k == 0)
-        for (int i = 0; i < sz; ++i) res = __dadd_rn(res, l1_v<MASK>(g, m, mask, e0 + i, h, dv));
+        for (int i = 0; i < sz; ++i)
+          res = __dadd_rn(res, l1_v<MASK, PK, LOG>(g, m, mask, e0 + i, h, dv, sv, p));
     } else {
       // lane k owns accumulator r_k over elements k, k+8, ... of the leaf's
       // full 8-groups (<= 16 of them): issue every load first, then add in
@@ -308,7 +359,7 @@ k_l1_items(const float* __restrict__ g, const float* __restrict__ m,
         if (i < ngrp) {
           double c = lc::lion_c(mv[i], gv[i], h);
           if (MASK && !((keep >> i) & 1u)) c = 0.0;
-          const double v = dv(fabs(c));
+          const double v = term<PK>(abs_y<LOG>(c, sv), dv, p);
           r = i == 0 ? v : __dadd_rn(r, v);
         }
       }
@@ -318,7 +369,8 @@ k_l1_items(const float* __restrict__ g, const float* __restrict__ m,
       r = __dadd_rn(r, __shfl_xor_sync(gm, r, 4));
       res = r;
       if (k == 0)
-        for (int i = ngrp * 8; i < sz; ++i) res = __dadd_rn(res, l1_v<MASK>(g, m, mask, e0 + i, h, dv));
+        for (int i = ngrp * 8; i < sz; ++i)
+          res = __dadd_rn(res, l1_v<MASK, PK, LOG>(g, m, mask, e0 + i, h, dv, sv, p));
     }
     if (k == 0) slots[lf] = res;
   }
@@ -345,16 +397,17 @@ __global__ void k_div_check(const double* __restrict__ a, const double* __restri
   }
 }
 
-// One CTA per layer: additions above the work items, then M1 and the scale.
+// One CTA per layer: additions above the work items, then M_p and the scale
+// (quant.py:94-104, :153-170).
 __global__ void __launch_bounds__(kThreads)
 k_l1_upper(const DevSeg* __restrict__ segs, const int4* __restrict__ uops,
            const int* __restrict__ ulvl, const unsigned long long* __restrict__ gmax,
-           double* __restrict__ nodes, int qmax, double* __restrict__ norms,
-           double* __restrict__ scales) {
+           double* __restrict__ nodes, int pk, double p, int qmax,
+           double* __restrict__ norms, double* __restrict__ scales) {
   const int s = blockIdx.x;
   const DevSeg S = segs[s];
-  const double mx = __longlong_as_double((long long)gmax[s]);
-  if (mx != 0.0) {
+  const double mx = pk == PK_0 ? (double)gmax[s] : __longlong_as_double((long long)gmax[s]);
+  if (mx != 0.0 && pk != PK_INF) {
     for (int lv = 0; lv < S.nlvl; ++lv) {
       const int b = ulvl[S.lvl_begin + lv], e = ulvl[S.lvl_begin + lv + 1];
       for (int o = b + threadIdx.x; o < e; o += blockDim.x) {
@@ -367,12 +420,33 @@ k_l1_upper(const DevSeg* __restrict__ segs, const int4* __restrict__ uops,
   if (threadIdx.x == 0) {
     double M = 0.0;
     if (mx != 0.0) {
-      const double mean = __ddiv_rn(nodes[S.root], (double)S.n);  // np.mean
-      M = __dmul_rn(mx, mean);                                   // m * mean**(1/1)
+      if (pk == PK_INF) {
+        M = mx;                                                  // max|y|
+      } else if (pk == PK_0) {
+        M = exp(__ddiv_rn(nodes[S.root], mx));                   // exp(mean(log nz))
+      } else {
+        const double mean = __ddiv_rn(nodes[S.root], (double)S.n);  // np.mean
+        double r = mean;                                             // mean ** (1/p)
+        if (pk == PK_2) r = __dsqrt_rn(mean);
+        else if (pk == PK_HALF) r = __dmul_rn(mean, mean);
+        else if (pk == PK_GEN) r = pow(mean, __ddiv_rn(1.0, p));
+        M = __dmul_rn(mx, r);
+      }
     }
     norms[s] = M;
-    scales[s] = (M == 0.0 || qmax == 0) ? 0.0 : __ddiv_rn((double)qmax, __dmul_rn(2.0, M));
+    scales[s] = (M == 0.0 || qmax == 0) ? 0.0
+                : pk == PK_INF ? __ddiv_rn((double)qmax, M)
+                               : __ddiv_rn((double)qmax, __dmul_rn(2.0, M));
   }
+}
+
+int norm_kind(double p) {
+  if (p == 1.0) return PK_1;
+  if (p == 2.0) return PK_2;
+  if (p == 0.5) return PK_HALF;
+  if (p == 0.0) return PK_0;
+  if (std::isinf(p) && p > 0) return PK_INF;
+  return PK_GEN;
 }
 
 template <typename T>
@@ -522,32 +596,97 @@ int lc_l1_plan_create(lc_l1_plan_t* out, const int64_t* seg_start, int32_t nseg)
   return LC_OK;
 }
 
-int lc_l1_scales(lc_l1_plan_t p, const float* g, const float* m, const uint8_t* mask,
-                 const lc_hyper* hp, int32_t qmax, double* norms, double* scales,
-                 void* stream) {
-  if (!p || !g || !m || !hp || !norms || !scales) return lc::set_err(LC_E_ARG, "lc_l1_scales: bad arguments");
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  Hyp h{hp->beta1, hp->one_minus_beta1, hp->beta2, hp->one_minus_beta2};
-  LC_CUDA_TRY(cudaMemsetAsync(p->d_max, 0, sizeof(unsigned long long) * p->nseg, st));
+}  // extern "C"
+
+namespace {
+
+template <bool LOG, bool COUNT>
+void launch_max(lc_l1_plan_t p, const float* g, const float* m, const uint8_t* mask, Hyp h,
+                const double* logs, cudaStream_t st) {
   const int64_t n = p->n_total;
   int64_t nct = (int64_t)lc::sm_count() * 8;
   int64_t per = (n + nct - 1) / nct;
   per = std::max<int64_t>((per + 4095) / 4096 * 4096, 4096);  // 16-byte aligned ranges
   int grid = (int)((n + per - 1) / per);
-  k_l1_max<<<grid, kThreads, 0, st>>>(g, m, mask, p->d_seg_start, p->nseg, n, per, h, p->d_max);
-  LC_LAUNCH_CHECK();
+  k_l1_max<LOG, COUNT><<<grid, kThreads, 0, st>>>(g, m, mask, p->d_seg_start, p->nseg, n, per,
+                                                  h, logs, p->d_max);
+}
+
+template <bool MASK, int PK, bool LOG>
+int launch_items(lc_l1_plan_t p, const float* g, const float* m, const uint8_t* mask, Hyp h,
+                 const double* logs, double pv, cudaStream_t st) {
   size_t smem = sizeof(double) * std::max(1, p->max_slots);
-  auto items = mask ? k_l1_items<true> : k_l1_items<false>;
+  auto items = k_l1_items<MASK, PK, LOG>;
   if (smem > 48 * 1024)
     LC_CUDA_TRY(cudaFuncSetAttribute(items, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  items<<<p->n_items, kThreads, smem, st>>>(g, m, mask, h, p->d_max, p->d_wi_off, p->d_wi_meta,
-                                            p->d_tmpl, p->d_leaf_rel, p->d_leaf_size, p->d_tops,
-                                            p->d_tlvl, p->d_nodes);
+  items<<<p->n_items, kThreads, smem, st>>>(g, m, mask, h, p->d_max, logs, pv, p->d_wi_off,
+                                            p->d_wi_meta, p->d_tmpl, p->d_leaf_rel,
+                                            p->d_leaf_size, p->d_tops, p->d_tlvl, p->d_nodes);
+  return LC_OK;
+}
+
+template <int PK>
+int items_pk(lc_l1_plan_t p, const float* g, const float* m, const uint8_t* mask, Hyp h,
+             const double* logs, double pv, cudaStream_t st) {
+  if (mask)
+    return logs ? launch_items<true, PK, true>(p, g, m, mask, h, logs, pv, st)
+                : launch_items<true, PK, false>(p, g, m, mask, h, logs, pv, st);
+  return logs ? launch_items<false, PK, true>(p, g, m, mask, h, logs, pv, st)
+              : launch_items<false, PK, false>(p, g, m, mask, h, logs, pv, st);
+}
+
+int norm_scales(lc_l1_plan_t p, const float* g, const float* m, const uint8_t* mask,
+                const lc_hyper* hp, double pv, int qmax, const double* logs, double* norms,
+                double* scales, cudaStream_t st) {
+  Hyp h{hp->beta1, hp->one_minus_beta1, hp->beta2, hp->one_minus_beta2};
+  const int pk = norm_kind(pv);
+  LC_CUDA_TRY(cudaMemsetAsync(p->d_max, 0, sizeof(unsigned long long) * p->nseg, st));
+  if (pk == PK_0) {
+    if (logs) launch_max<true, true>(p, g, m, mask, h, logs, st);
+    else launch_max<false, true>(p, g, m, mask, h, logs, st);
+  } else {
+    if (logs) launch_max<true, false>(p, g, m, mask, h, logs, st);
+    else launch_max<false, false>(p, g, m, mask, h, logs, st);
+  }
+  LC_LAUNCH_CHECK();
+  int rc = LC_OK;
+  switch (pk) {
+    case PK_1: rc = items_pk<PK_1>(p, g, m, mask, h, logs, pv, st); break;
+    case PK_2: rc = items_pk<PK_2>(p, g, m, mask, h, logs, pv, st); break;
+    case PK_HALF: rc = items_pk<PK_HALF>(p, g, m, mask, h, logs, pv, st); break;
+    case PK_GEN: rc = items_pk<PK_GEN>(p, g, m, mask, h, logs, pv, st); break;
+    case PK_0: rc = items_pk<PK_0>(p, g, m, mask, h, logs, pv, st); break;
+    default: break;  // p = inf: the max is the norm
+  }
+  if (rc) return rc;
   LC_LAUNCH_CHECK();
   k_l1_upper<<<p->nseg, kThreads, 0, st>>>(p->d_seg, p->d_uops, p->d_ulvl, p->d_max, p->d_nodes,
-                                           qmax, norms, scales);
+                                           pk, pv, qmax, norms, scales);
   LC_LAUNCH_CHECK();
   return LC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lc_l1_scales(lc_l1_plan_t p, const float* g, const float* m, const uint8_t* mask,
+                 const lc_hyper* hp, int32_t qmax, double* norms, double* scales,
+                 void* stream) {
+  if (!p || !g || !m || !hp || !norms || !scales) return lc::set_err(LC_E_ARG, "lc_l1_scales: bad arguments");
+  return norm_scales(p, g, m, mask, hp, 1.0, qmax, nullptr, norms, scales,
+                     reinterpret_cast<cudaStream_t>(stream));
+}
+
+int lc_norm_scales(lc_l1_plan_t p, const float* g, const float* m, const uint8_t* mask,
+                   const lc_hyper* hp, const lc_norm_spec* spec, double* norms,
+                   double* scales, void* stream) {
+  if (!p || !g || !m || !hp || !spec || !norms || !scales)
+    return lc::set_err(LC_E_ARG, "lc_norm_scales: bad arguments");
+  const double pv = spec->p;
+  if (std::isnan(pv) || pv < 0) return lc::set_err(LC_E_CONFIG, "invalid norm order %g", pv);
+  return norm_scales(p, g, m, mask, hp, pv, spec->qmax, spec->log_scale, norms, scales,
+                     reinterpret_cast<cudaStream_t>(stream));
 }
 
 int lc_debug_div_check(const double* a, const double* b, int64_t n, uint64_t* mismatches,

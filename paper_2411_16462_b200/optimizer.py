@@ -288,7 +288,7 @@ class _Workspace:
         self.syncs = None
         self.applied = False
         self.l1 = None
-        self.norms = self.scales = None
+        self.norms = self.scales = self.logs = None
         if kind == "f64":
             blk_bytes, rdt, rlen = L * 8, torch.float64, P * L
         elif kind == "fields":
@@ -382,15 +382,36 @@ class _L1Plan:
             pass
 
 
-def _l1_scales(ws: _Workspace, layout: Layout, dev, g, m, mask, hyp, qmax, stream):
+def _quant_scales(ws: _Workspace, layout: Layout, dev, g, m, mask, hyp, spec: QuantSpec,
+                  stream, seed: int = 0):
+    """Per-layer quantizer scalars on the device (quant.py:127-170): the
+    log-map scale M1(c) when ``log_transform``, then M_p of y and the scale
+    qmax/(2 M_p) (qmax/M_inf for p = inf).  Returns the segment table K1
+    quantizes with."""
+    qmax = spec.qmax
+    nseg = len(layout.names)
     if ws.l1 is None:
         ws.l1 = _L1Plan(layout)
-        ws.norms = torch.zeros(len(layout.names), dtype=torch.float64, device=dev)
-        ws.scales = torch.zeros(len(layout.names), dtype=torch.float64, device=dev)
-    _lib.call("lc_l1_scales", ws.l1.handle, g.data_ptr(), m.data_ptr(), _lib.ptr(mask),
-              C.byref(hyp), qmax, ws.norms.data_ptr(), ws.scales.data_ptr(), stream)
+        ws.norms = torch.zeros(nseg, dtype=torch.float64, device=dev)
+        ws.scales = torch.zeros(nseg, dtype=torch.float64, device=dev)
+    args = (ws.l1.handle, g.data_ptr(), m.data_ptr(), _lib.ptr(mask), C.byref(hyp))
+    logs = None
+    if spec.log_transform:
+        if ws.logs is None:
+            ws.logs = torch.zeros(2 * nseg, dtype=torch.float64, device=dev)
+        logs = ws.logs[:nseg]
+        _lib.call("lc_l1_scales", *args, qmax, logs.data_ptr(), ws.logs[nseg:].data_ptr(),
+                  stream)
+    if spec.norm_p == 1.0 and logs is None:
+        _lib.call("lc_l1_scales", *args, qmax, ws.norms.data_ptr(), ws.scales.data_ptr(),
+                  stream)
+    else:
+        ns = _lib.NormSpec(float(spec.norm_p), qmax, 0, _lib.ptr(logs))
+        _lib.call("lc_norm_scales", *args, C.byref(ns), ws.norms.data_ptr(),
+                  ws.scales.data_ptr(), stream)
     return _lib.Segments(layout.seg_start_dev(dev).data_ptr(), ws.scales.data_ptr(),
-                         len(layout.names), qmax)
+                         nseg, qmax, _lib.ptr(logs), spec.kernel_flags(), 0,
+                         seed & 0xFFFFFFFFFFFFFFFF)
 
 
 def _flat_mask(mask, layout: Layout, dev):
@@ -461,9 +482,6 @@ def _validate(spec, algo):
         raise ConfigError(f"unknown vote algorithm {algo!r}")
     if algo == "direct" and spec is None:
         raise ConfigError("direct allreduce needs an integer QuantSpec")
-    if spec is not None and not spec.cuda_supported():
-        raise ConfigError(f"{spec} is not implemented on the CUDA path "
-                          "(finite norm_p=1 with nearest rounding, or bits=1)")
 
 
 def distributed_lion_step(state: WorkerState, grad_i, h: LionHyper,
@@ -478,7 +496,8 @@ def distributed_lion_step(state: WorkerState, grad_i, h: LionHyper,
     sync and an f64 copy of c)."""
     _validate(spec, algo)
     _check_shapes(state.params, grad_i)
-    return _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out)
+    return _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out,
+                      rng=rng)
 
 
 class _HostPipe:
@@ -526,7 +545,7 @@ def distributed_lion_step_host(state: WorkerState, grad_host: torch.Tensor, h: L
                                spec: QuantSpec | None, topo: Topology, algo: str,
                                zero_mode: str = "alternating",
                                params_out: torch.Tensor | None = None,
-                               chunk: int = 1 << 23) -> WorkerState:
+                               chunk: int = 1 << 23, rng=None) -> WorkerState:
     """The step with HOST buffers, as a reference user holds them: the
     gradient comes from ``grad_host`` (a flat fp32 CPU tensor in the
     state's sorted-name layout; pin it for async copies) and, if given, the
@@ -550,10 +569,12 @@ def distributed_lion_step_host(state: WorkerState, grad_host: torch.Tensor, h: L
     if g is None:
         g = FlatParamSet.empty_like(th)
         th.workspace["host_grads"] = g
-    return _step_impl(state, g, h, spec, topo, algo, None, zero_mode, None, pipe=pipe)
+    return _step_impl(state, g, h, spec, topo, algo, None, zero_mode, None, pipe=pipe,
+                      rng=rng)
 
 
-def _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out, pipe=None):
+def _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out, pipe=None,
+               rng=None):
     layout, th, m = state.flat()
     dev = th.flat.device
     P = topo.world_size
@@ -572,6 +593,9 @@ def _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out,
         kind, binary, qmax = "fields", True, 1
     else:
         kind, binary, qmax = "fields", False, spec.qmax
+    # quantize() raises before any exchange when stochastic rounding has no
+    # rng (quant.py:163-165); this step's stream position comes from rng
+    seed = spec.draw_seed(rng) if (kind == "fields" and not binary) else 0
     F = 1
     if kind == "fields":
         # reference capacity rule first: CapacityError before any exchange
@@ -609,7 +633,7 @@ def _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out,
                                   "1bit" if algo == "compressed1bit" else "fields")
             segs = None
             if kind == "fields" and not binary:
-                segs = _l1_scales(ws, layout, dev, g.flat, m.flat, mflat, hyp, qmax, s)
+                segs = _quant_scales(ws, layout, dev, g.flat, m.flat, mflat, hyp, spec, s, seed)
             if P == 1:
                 mode = (_lib.LC_LOCAL_BINARY if binary else
                         _lib.LC_LOCAL_QUANT if kind == "fields" else _lib.LC_LOCAL_PS)

@@ -3,9 +3,10 @@
 ``QuantSpec`` and ``SignPolicy`` take the reference's constructor arguments
 and validation (lioncomm/quant.py:102-153).  On the CUDA path the quantizer
 itself runs inside the fused interpolate kernel (csrc/kernels.cu, K1) and the
-per-layer L1 norm in csrc/l1norm.cu; only the finite-p=1 nearest-rounding
-quantizer (the paper's Lion Cub p-bit scheme) is on the hot path, other
-variants raise ``ConfigError`` from the step.
+per-layer mean p-norm in csrc/l1norm.cu.  Every variant of the reference is
+implemented: norm_p 1 (the paper's Lion Cub p-bit scheme), any finite p,
+0 (geometric mean) and inf (max norm); nearest or stochastic rounding;
+log_transform; no_zero.
 """
 
 from __future__ import annotations
@@ -13,6 +14,24 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 from .errors import ConfigError
+
+LC_Q_STOCHASTIC = 1 << 0   # include/lioncub.h
+LC_Q_NO_ZERO = 1 << 1
+
+
+def draw_seed(rng) -> int:
+    """A 64-bit seed for the counter-based stochastic-rounding stream."""
+    if rng is None:
+        raise ConfigError("stochastic rounding needs an rng")
+    if isinstance(rng, int):
+        return rng & 0xFFFFFFFFFFFFFFFF
+    if hasattr(rng, "integers"):         # numpy Generator
+        return int(rng.integers(0, 1 << 63, dtype="int64"))
+    import torch
+    if isinstance(rng, torch.Generator):
+        return int(torch.randint(0, 1 << 62, (1,), generator=rng).item())
+    raise ConfigError(f"unsupported rng {type(rng).__name__}")
+
 
 PACKABLE_WIDTHS = (1, 2, 4, 8)
 INF = float("inf")
@@ -44,10 +63,20 @@ class QuantSpec:
     def qmax(self) -> int:
         return (1 << (self.bits - 1)) - 1
 
-    def cuda_supported(self) -> bool:
-        """The quantizer variants the fused CUDA encoder implements."""
-        return self.bits == 1 or (self.norm_p == 1.0 and self.rounding == "nearest"
-                                  and not self.log_transform and not self.no_zero)
+    def kernel_flags(self) -> int:
+        """``lc_segments.qflags`` of this spec (include/lioncub.h LC_Q_*)."""
+        return ((LC_Q_STOCHASTIC if self.rounding == "stochastic" else 0)
+                | (LC_Q_NO_ZERO if self.no_zero else 0))
+
+    def draw_seed(self, rng) -> int:
+        """This call's stochastic-rounding stream seed, drawn from ``rng``
+        (0 for nearest rounding).  ``rng``: a ``numpy.random.Generator`` (as
+        the reference takes, quant.py:127-128), a CPU ``torch.Generator``, or
+        an int (a fixed stream).  Missing rng -> ConfigError like the
+        reference (quant.py:163-165)."""
+        if self.rounding != "stochastic":
+            return 0
+        return draw_seed(rng)
 
 
 @dataclass(frozen=True)

@@ -46,6 +46,18 @@ STEP_CASES = [
     _c("q5", "direct", 3, "zeros", bits=8, zero_mode="exact-ternary", seed=35),
     _c("q6", "direct", 4, "laplace", bits=2, seed=36),
     _c("q7", "direct", 2, "ties", bits=3, iteration=1, seed=37, mask="d"),
+    # quantizer variants (quant.py:127-173): max norm, other p, geometric
+    # mean, log map, no_zero (nearest rounding; stochastic is statistical)
+    _c("x1", "direct", 4, "outliers", bits=5, seed=61, quant=dict(norm_p=float("inf"))),
+    _c("x2", "direct", 2, "laplace", iteration=1, bits=4, seed=62, quant=dict(norm_p=2.0)),
+    _c("x3", "direct", 3, "zeros", bits=8, seed=63, quant=dict(norm_p=0.0)),
+    _c("x4", "direct", 8, "laplace", bits=5, seed=64, quant=dict(log_transform=True)),
+    _c("x5", "direct", 4, "ties", bits=3, seed=65, quant=dict(no_zero=True)),
+    _c("x6", "direct", 1, "outliers", bits=5, seed=66, quant=dict(norm_p=3.0)),
+    _c("x7", "direct", 2, "laplace", bits=5, seed=67, mask="d",
+       quant=dict(norm_p=0.5, no_zero=True)),
+    _c("x8", "direct", 4, "laplace", iteration=1, wd=0.1, bits=6, seed=68,
+       quant=dict(norm_p=float("inf"), log_transform=True)),
     # full precision (ps / ps_efficient, spec=None)
     _c("p1", "ps", 1, "zeros", zero_mode="exact-ternary", seed=41),
     _c("p2", "ps", 2, "laplace", seed=42),
@@ -76,3 +88,12 @@ COLLECTIVE_CASES.append(dict(name="dirbin_w4_n100", kind="direct", world=4,
                              n=100, q_max=1, binary=True, seed=3))
 COLLECTIVE_CASES.append(dict(name="dir15_w8_n257", kind="direct", world=8,
                              n=257, q_max=15, seed=5))
+
+
+def quant_kwargs(case: dict) -> dict | None:
+    """QuantSpec keyword arguments of a step case (None: spec=None)."""
+    if case["bits"] is None:
+        return None
+    kw = dict(bits=case["bits"], norm_p=1.0)
+    kw.update(case.get("quant") or {})
+    return kw

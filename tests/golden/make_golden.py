@@ -31,11 +31,13 @@ from lioncomm.collectives import (allreduce_mean_f32,  # noqa: E402
 from lioncomm.optimizer import (LionHyper, SyncPolicy, WorkerState,  # noqa: E402
                                 distributed_lion_step, maybe_sync_momentum,
                                 save_checkpoint)
-from lioncomm.quant import (QuantSpec, SignPolicy, apply_sign,  # noqa: E402
-                            lp_mean_norm, pack, quantize)
+from lioncomm.quant import (PackedBits, QuantSpec, SignPolicy,  # noqa: E402
+                            apply_sign, dequantize, lp_mean_norm, pack,
+                            quantize, unpack)
 from lioncomm.transport import InprocTransport  # noqa: E402
 
-from tests.golden.cases import COLLECTIVE_CASES, SIZES, STEP_CASES  # noqa: E402
+from tests.golden.cases import (COLLECTIVE_CASES, SIZES, STEP_CASES,  # noqa: E402
+                                quant_kwargs)
 from oracle.lioncub_oracle import synth_rank_inputs  # noqa: E402
 
 
@@ -52,7 +54,8 @@ def run_step_case(case: dict, out: dict):
     ranks = synth_rank_inputs(case["seed"], world, SIZES, case["kind"])
     h = LionHyper(beta1=0.9, beta2=0.99, lr=case["lr"],
                   weight_decay=case["wd"])
-    spec = None if case["bits"] is None else QuantSpec(bits=case["bits"], norm_p=1.0)
+    kw = quant_kwargs(case)
+    spec = None if kw is None else QuantSpec(**kw)
     mask = None
     if case.get("mask"):
         mrng = np.random.default_rng(case["seed"] + 77)
@@ -104,7 +107,8 @@ def run_step_case(case: dict, out: dict):
                 out[p + f"out/words/{r}/{layer}"] = sign_words(s)
             if spec is not None and spec.bits > 1:
                 out[p + f"out/q/{r}/{layer}"] = quantize(c.ravel(), spec).astype(np.int16)
-                out[p + f"out/norm/{r}/{layer}"] = np.float64(lp_mean_norm(c.ravel(), 1.0))
+                out[p + f"out/norm/{r}/{layer}"] = np.float64(
+                    lp_mean_norm(c.ravel(), spec.norm_p))
     if mask is not None:
         for k, v in mask.items():
             out[p + f"in/mask/{k}"] = v
@@ -168,6 +172,79 @@ def make_checkpoint():
                     LionHyper(lr=3e-4, beta1=0.9, beta2=0.99, weight_decay=0.1))
 
 
+QUANT_INPUTS = ("lap", "halves", "zeros", "one", "spiky")
+QUANT_PS = (1.0, 2.0, 0.5, 3.0, float("inf"), 0.0)
+QUANT_BITS = (2, 5, 8)
+PACK_CASES = [  # (width, offset, low, high, count)
+    (1, 1, None, None, 1001), (1, 0, 0, 1, 77), (2, 1, -1, 2, 1000), (2, 0, 0, 3, 5),
+    (4, 7, -7, 8, 999), (4, 0, 0, 15, 1), (8, 128, -128, 127, 1003), (8, 0, 0, 255, 0),
+]
+
+
+def quant_input(kind: str) -> np.ndarray:
+    rng = np.random.default_rng(len(kind) * 7919)
+    if kind == "lap":
+        x = rng.laplace(size=3001)
+        x[rng.random(3001) < 0.05] = 0.0
+        x[3] = -0.0
+        x[17] = 250.0
+    elif kind == "halves":   # exact half-way points of the scaled grid
+        x = np.array([0.5, -0.5, 1.5, -1.5, 2.5, -2.5, 3.5, 0.0, -0.0, 1.0, 7.0, -7.0])
+    elif kind == "zeros":
+        x = np.zeros(10)
+    elif kind == "one":
+        x = np.array([-3.25])
+    else:
+        x = rng.standard_normal(2048) * 1e-3
+        x[::97] = rng.choice([-1.0, 1.0], size=x[::97].size) * 40.0
+    return np.asarray(x, dtype=np.float32).astype(np.float64)
+
+
+def make_quant_golden():
+    """Standalone quant.py functions of the reference on fixed inputs:
+    lp_mean_norm (every p), quantize/dequantize (every variant, nearest),
+    apply_sign (both policies), pack/unpack/PackedBits wire bytes."""
+    out: dict = {}
+    for kind in QUANT_INPUTS:
+        x = quant_input(kind)
+        out[f"x/{kind}"] = x
+        for p in QUANT_PS:
+            out[f"norm/{kind}/{p}"] = np.float64(lp_mean_norm(x, p))
+            for bits in QUANT_BITS:
+                for lt in (False, True):
+                    for nz in (False, True):
+                        spec = QuantSpec(bits=bits, norm_p=p, log_transform=lt, no_zero=nz)
+                        key = f"{kind}/{p}/{bits}/{int(lt)}/{int(nz)}"
+                        q = quantize(x, spec)
+                        out[f"q/{key}"] = q.astype(np.int16)
+                        y, s = x, None
+                        if lt:
+                            s = lp_mean_norm(x, 1.0)
+                            if s > 0:
+                                y = np.sign(x) * np.log1p(np.abs(x) / s)
+                        norm = lp_mean_norm(y, p)
+                        out[f"deq/{key}"] = dequantize(q, spec, norm, s)
+        for mode, it in (("alternating", 1), ("alternating", 2), ("exact-ternary", 1)):
+            out[f"sign/{kind}/{mode}/{it}"] = apply_sign(
+                x, SignPolicy(mode=mode, iteration=it)).astype(np.int8)
+    rng = np.random.default_rng(99)
+    for i, (w, off, lo, hi, count) in enumerate(PACK_CASES):
+        if lo is None:
+            v = rng.choice([-1, 1], size=count).astype(np.int64)
+        else:
+            v = rng.integers(lo, hi + 1, size=count).astype(np.int64)
+        pk = pack(v, w, off)
+        assert np.array_equal(unpack(pk), v)
+        assert PackedBits.from_bytes(pk.to_bytes()) == pk
+        out[f"pack/{i}/values"] = v
+        out[f"pack/{i}/wire"] = np.frombuffer(pk.to_bytes(), dtype=np.uint8).copy()
+    meta = {"inputs": list(QUANT_INPUTS), "ps": list(QUANT_PS), "bits": list(QUANT_BITS),
+            "pack": PACK_CASES}
+    out["meta"] = np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(HERE, "golden_quant.npz"), **out)
+    return len(out)
+
+
 def main():
     steps: dict = {}
     for case in STEP_CASES:
@@ -183,6 +260,8 @@ def main():
                                   dtype=np.uint8)
     np.savez_compressed(os.path.join(HERE, "golden_collectives.npz"), **colls)
     make_checkpoint()
+    nq = make_quant_golden()
+    print(f"{nq} standalone quant arrays")
     print(f"{len(STEP_CASES)} step cases, {len(COLLECTIVE_CASES)} collective cases")
 
 

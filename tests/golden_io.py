@@ -69,3 +69,8 @@ def collective_case(name: str) -> dict:
                 inputs=[data[p + f"in/{r}"] for r in range(case["world"])],
                 values=data[p + "out/values"],
                 ties=int(data[p + "out/ties"]) if (p + "out/ties") in data else None)
+
+
+def quant_golden():
+    """golden_quant.npz: the reference's standalone quant.py outputs."""
+    return _load("golden_quant.npz")

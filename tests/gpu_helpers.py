@@ -7,6 +7,7 @@ import torch
 
 import paper_2411_16462_b200 as lc
 from paper_2411_16462_b200.optimizer import FlatParamSet
+from tests.golden.cases import quant_kwargs
 
 
 def cuda_params(d: dict) -> dict:
@@ -37,7 +38,9 @@ def run_step_case(case: dict, theta, ms, gs, mask=None, transport=None,
     gradients), exercising workspace/epoch reuse across steps."""
     world = case["world"]
     h = lc.LionHyper(beta1=0.9, beta2=0.99, lr=case["lr"], weight_decay=case["wd"])
-    spec = None if case["bits"] is None else lc.QuantSpec(bits=case["bits"], norm_p=1.0)
+    kw = quant_kwargs(case)
+    spec = None if kw is None else lc.QuantSpec(**kw)
+    rng_seed = case.get("rng_seed")
     sync = None
     if case.get("sync"):
         period, layers = case["sync"]
@@ -54,8 +57,10 @@ def run_step_case(case: dict, theta, ms, gs, mask=None, transport=None,
         st2 = st
         for _ in range(steps):
             met = {} if metrics else None
+            rng = None if rng_seed is None else np.random.default_rng(rng_seed + r)
             st2 = lc.distributed_lion_step(st2, g, h, spec, topo, case["algo"], mask=cmask,
-                                           zero_mode=case["zero_mode"], metrics_out=met)
+                                           zero_mode=case["zero_mode"], metrics_out=met,
+                                           rng=rng)
             if sync is not None:
                 st2 = lc.maybe_sync_momentum(st2, sync, topo)
         torch.cuda.synchronize()
@@ -84,3 +89,9 @@ def assert_f32_equal(got, ref64, what=""):
         i = int(bad[0])
         raise AssertionError(f"{what}: {bad.size} mismatches, first at {i}: "
                              f"got {got.ravel()[i]!r} ref {ref.ravel()[i]!r}")
+
+
+def step_seeds(rng_seed: int, world: int) -> list:
+    """The per-rank stochastic-rounding seeds run_step_case's steps draw."""
+    from paper_2411_16462_b200.quant import draw_seed
+    return [draw_seed(np.random.default_rng(rng_seed + r)) for r in range(world)]

@@ -10,6 +10,7 @@ import pytest
 
 from oracle import lioncub_oracle as O
 from tests import golden_io as G
+from tests.golden.cases import quant_kwargs
 
 
 # ---- known-answer tests of the reference test-suite ------------------------
@@ -108,7 +109,8 @@ def test_oracle_matches_reference_step(name):
     case = gc["case"]
     world = case["world"]
     h = O.Hyper(0.9, 0.99, case["lr"], case["wd"])
-    spec = None if case["bits"] is None else O.Spec(case["bits"])
+    kw = quant_kwargs(case)
+    spec = None if kw is None else O.Spec(**kw)
     thetas = [dict(gc["theta"]) for _ in range(world)]
     nt, nm, sign, ties, cs, _ = O.distributed_step(
         thetas, gc["m"], gc["g"], h, spec, case["algo"], case["iteration"],
@@ -129,9 +131,13 @@ def test_oracle_matches_reference_step(name):
                 s = O.apply_sign(cs[r][k], case["zero_mode"], t)
                 assert np.array_equal(O.pack_signs(s), gc["words"][r][k])
             if gc["q"][r][k] is not None:
-                assert np.array_equal(O.quantize_l1(cs[r][k], case["bits"]),
+                assert np.array_equal(O.quantize(cs[r][k], spec),
                                       gc["q"][r][k].astype(np.int64))
-                assert O.lp_mean_norm_l1(cs[r][k]) == float(gc["norm"][r][k])
+                assert O.lp_mean_norm(cs[r][k], spec.norm_p) == float(gc["norm"][r][k])
+                if spec.norm_p == 1.0 and not spec.log_transform and not spec.no_zero:
+                    assert np.array_equal(O.quantize_l1(cs[r][k], case["bits"]),
+                                          gc["q"][r][k].astype(np.int64))
+                    assert O.lp_mean_norm_l1(cs[r][k]) == float(gc["norm"][r][k])
 
 
 @pytest.mark.parametrize("name", [c["name"] for c in G.collective_cases()])
@@ -148,3 +154,66 @@ def test_oracle_matches_reference_collective(name):
         assert v.ties == gc["ties"]
     else:
         assert np.array_equal(O.mean_f32(gc["inputs"]), gc["values"])
+
+
+# ---- standalone quant.py functions (golden_quant.npz) ----------------------
+
+def _quant_keys():
+    _, meta = G.quant_golden()
+    for kind in meta["inputs"]:
+        for p in meta["ps"]:
+            for bits in meta["bits"]:
+                for lt in (0, 1):
+                    for nz in (0, 1):
+                        yield kind, p, bits, lt, nz
+
+
+def test_oracle_lp_mean_norm_matches_reference():
+    data, meta = G.quant_golden()
+    for kind in meta["inputs"]:
+        for p in meta["ps"]:
+            assert O.lp_mean_norm(data[f"x/{kind}"], p) == float(data[f"norm/{kind}/{p}"]), \
+                (kind, p)
+
+
+def test_oracle_quantize_dequantize_match_reference():
+    data, _ = G.quant_golden()
+    for kind, p, bits, lt, nz in _quant_keys():
+        x = data[f"x/{kind}"]
+        spec = O.Spec(bits=bits, norm_p=p, log_transform=bool(lt), no_zero=bool(nz))
+        key = f"{kind}/{p}/{bits}/{lt}/{nz}"
+        q = O.quantize(x, spec)
+        assert np.array_equal(q, data[f"q/{key}"].astype(np.int64)), key
+        _, s, norm = O.quant_scale(x, spec)
+        assert np.array_equal(O.dequantize(q, spec, norm, s), data[f"deq/{key}"]), key
+
+
+def test_oracle_apply_sign_and_pack_match_reference():
+    data, meta = G.quant_golden()
+    for kind in meta["inputs"]:
+        x = data[f"x/{kind}"]
+        for mode, it in (("alternating", 1), ("alternating", 2), ("exact-ternary", 1)):
+            assert np.array_equal(O.apply_sign(x, mode, it),
+                                  data[f"sign/{kind}/{mode}/{it}"].astype(np.int64))
+    for i, (w, off, *_rest) in enumerate(meta["pack"]):
+        v = data[f"pack/{i}/values"]
+        wire = data[f"pack/{i}/wire"].tobytes()
+        stored = (v + 1) >> 1 if (w == 1 and off == 1) else v + off
+        words = O.pack_words(stored, w)
+        nbytes = (v.size * w + 7) // 8
+        assert words.astype("<u4").tobytes()[:nbytes] == wire[9:], i
+        assert wire[:9] == np.array([v.size], "<u4").tobytes() + bytes([w]) + \
+            np.array([off], "<i4").tobytes()
+
+
+def test_splitmix_stream_is_uniform_and_sround_unbiased():
+    u = O.splitmix_uniforms(12345, np.arange(1 << 20))
+    assert u.min() >= 0.0 and u.max() < 1.0
+    assert abs(u.mean() - 0.5) < 2e-3 and abs(u.var() - 1 / 12) < 2e-3
+    # different seeds / offsets give different streams
+    assert not np.array_equal(u[:100], O.splitmix_uniforms(12346, np.arange(100)))
+    assert np.array_equal(u[50:60], O.splitmix_uniforms(12345, np.arange(50, 60)))
+    v = np.full(u.size, 2.3)
+    q = O.sround(v, u)
+    assert set(np.unique(q)) == {2, 3}
+    assert abs(q.mean() - 2.3) < 2e-3          # E[sround(v)] = v (quant.py:107-116)
