@@ -271,6 +271,27 @@ int lc_norm_scales(lc_l1_plan_t plan, const float* g, const float* m,
 int lc_debug_div_check(const double* a, const double* b, int64_t n,
                        uint64_t* mismatches, void* stream);
 
+/* ---- standalone quantizer operators (quant.py; csrc/quant.cu) ----
+ * lc_quantize_values: q = quantize(x) elementwise (quant.py:151-173) with the
+ *   segment table of lc_norm_scales (qmax, scale, log_scale, qflags, seed);
+ *   the stochastic stream position of x[e] is e.
+ * lc_dequantize: y = q * mult (mult = norm/qmax for p = inf, else
+ *   2 norm/qmax, computed by the caller as numpy does); log != 0 undoes the
+ *   log map: sign(y) * log_scale * expm1(|y|) (quant.py:176-195).
+ * lc_apply_sign_values: apply_sign (quant.py:198-204) of a float32
+ *   (is_f64 = 0) or float64 vector: +-1, zeros (and -0.0) -> fill in
+ *   {+1, -1, 0}; NaN -> 0.
+ * lc_f64_to_f32_exact: float64 -> float32, LC_FLAG_RANGE when a value is
+ *   not exactly representable (the CUDA operators compute from fp32). */
+int lc_quantize_values(const float* x, int64_t n, const lc_segments* segs,
+                       int64_t* q, void* stream);
+int lc_dequantize(const int64_t* q, int64_t n, double mult, double log_scale,
+                  int32_t log, double* out, void* stream);
+int lc_apply_sign_values(const void* x, int32_t is_f64, int64_t n, int fill,
+                         int8_t* out, void* stream);
+int lc_f64_to_f32_exact(const double* x, int64_t n, float* out, uint32_t* flags,
+                        void* stream);
+
 /* ---- metrics / operator helpers ---- */
 /* c as float64 (metrics_out["c_local"], optimizer.py:209). */
 int lc_compute_c(const float* g, const float* m, const uint8_t* mask,

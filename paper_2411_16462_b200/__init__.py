@@ -17,7 +17,8 @@ from .optimizer import (VOTE_ALGOS, FlatParamSet, Layout, LionHyper,  # noqa: F4
                         distributed_lion_step_host,
                         hash_params, lion_step, load_checkpoint,
                         maybe_sync_momentum, save_checkpoint)
-from .quant import INF, QuantSpec, SignPolicy  # noqa: F401
+from .quant import (INF, PackedBits, QuantSpec, SignPolicy, apply_sign,  # noqa: F401
+                    dequantize, lp_mean_norm, pack, quantize, unpack)
 from .torch_optim import LionCub, lioncub_comm_hook  # noqa: F401
 from .transport import (DeviceTransport, LocalTransport,  # noqa: F401
                         NcclTransport)

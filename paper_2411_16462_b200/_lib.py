@@ -96,6 +96,10 @@ SIGNATURES = {
     "lc_l1_scales": (INT, [P, P, P, P, P, I32, P, P, P]),
     "lc_norm_scales": (INT, [P, P, P, P, P, P, P, P, P]),
     "lc_debug_div_check": (INT, [P, P, I64, P, P]),
+    "lc_quantize_values": (INT, [P, I64, P, P, P]),
+    "lc_dequantize": (INT, [P, I64, D, D, I32, P, P]),
+    "lc_apply_sign_values": (INT, [P, I32, I64, INT, P, P]),
+    "lc_f64_to_f32_exact": (INT, [P, I64, P, P, P]),
     "lc_compute_c": (INT, [P, P, P, I64, P, P, P]),
     "lc_count_bits_segmented": (INT, [P, P, I32, P, P]),
     "lc_bits_to_sign": (INT, [P, P, I64, P, P]),
@@ -178,7 +182,8 @@ KERNEL_CALLS = frozenset({
     "lc_barrier", "lc_push_blocks_f32", "lc_mean_bcast_f32", "lc_mean_pull_f32",
     "lc_apply_update", "lc_fused_local_step", "lc_mean_f32", "lc_compute_c",
     "lc_count_bits_segmented", "lc_bits_to_sign", "lc_pack_i64_fields",
-    "lc_fields_decode", "lc_sign_pack_f64", "lc_sum_u32_rows"})
+    "lc_fields_decode", "lc_sign_pack_f64", "lc_sum_u32_rows", "lc_quantize_values",
+    "lc_dequantize", "lc_apply_sign_values", "lc_f64_to_f32_exact"})
 KERNELS_PER_CALL = {"lc_l1_scales": 3, "lc_norm_scales": 3}
 
 launches = 0  # kernels enqueued through call(); read by bench.py

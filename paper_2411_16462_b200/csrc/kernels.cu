@@ -60,16 +60,6 @@ int resident_ctas_of(const void* kernel, int block) {
   return per_sm;
 }
 
-struct SegQ {
-  const int64_t* start;
-  const double* scale;
-  int nseg;
-  int qmax;
-  const double* logs;  // per-segment log_transform scale, or null
-  uint32_t qflags;     // LC_Q_*
-  uint64_t seed;
-};
-
 // Internal variants picked when the segment table asks for a quantizer
 // other than nearest-rounding L1 without log map / no_zero.
 constexpr int kEncQuantX = 4;    // lc_encode: QUANT_FIELDS with quant_x
@@ -95,51 +85,6 @@ struct SegCursor {
     return scale;
   }
 };
-
-// Cursor of the general quantizer: scale and log scale of the segment.
-struct SegCursorX {
-  int64_t lo = 0, hi = -1;
-  double scale = 0.0, logs = 0.0;
-  __device__ __forceinline__ void at(const SegQ& sq, int64_t e) {
-    if (e < lo || e >= hi) {
-      int s = seg_find(sq.start, sq.nseg, e);
-      lo = __ldg(sq.start + s);
-      hi = __ldg(sq.start + s + 1);
-      scale = __ldg(sq.scale + s);
-      logs = sq.logs ? __ldg(sq.logs + s) : 0.0;
-    }
-  }
-  __device__ __forceinline__ double get(const SegQ& sq, int64_t e) {
-    at(sq, e);
-    return scale;
-  }
-};
-
-// Every quantizer variant (quant.py:127-173): y = c or sign(c) log1p(|c|/s)
-// (s > 0), v = scale * y, nearest (half-even) or stochastic rounding
-// floor(v) + (u < v - floor(v)), clip to +-qmax, then no_zero: a zero q of
-// a nonzero c becomes sign(c).  e: element index of the rank's flat buffer
-// (the stochastic stream position).
-__device__ __forceinline__ int quant_x(double c, const SegQ& sq, SegCursorX& cur, int64_t e) {
-  cur.at(sq, e);
-  double y = c;
-  if (cur.logs > 0.0) {
-    const double l = log1p(__ddiv_rn(fabs(c), cur.logs));
-    y = c > 0.0 ? l : (c < 0.0 ? -l : 0.0);
-  }
-  const double v = __dmul_rn(cur.scale, y);
-  double r;
-  if (sq.qflags & LC_Q_STOCHASTIC) {
-    const double lo = floor(v);
-    r = lo + (uniform01(sq.seed, e) < __dsub_rn(v, lo) ? 1.0 : 0.0);
-  } else {
-    r = rint(v);
-  }
-  r = fmin(fmax(r, -(double)sq.qmax), (double)sq.qmax);
-  int q = (int)r;
-  if ((sq.qflags & LC_Q_NO_ZERO) && q == 0 && c != 0.0) q = c > 0.0 ? 1 : -1;
-  return q;
-}
 
 // q = clip(round_half_even(scale*c), +-qmax)   (quant.py:236-243)
 __device__ __forceinline__ int quant_l1(double c, double scale, int qmax) {

@@ -44,7 +44,7 @@ from . import _lib
 from .collectives import (Topology, choose_lane_bits, field_bits, mean_into,
                           owner_elems, owner_valid)
 from .errors import CollectiveError, ConfigError
-from .quant import QuantSpec, SignPolicy
+from .quant import QuantSpec, SignPolicy, scale_tables
 from .transport import DEFAULT_TIMEOUT
 
 LrSchedule = Union[float, Callable[[int], float]]
@@ -394,21 +394,10 @@ def _quant_scales(ws: _Workspace, layout: Layout, dev, g, m, mask, hyp, spec: Qu
         ws.l1 = _L1Plan(layout)
         ws.norms = torch.zeros(nseg, dtype=torch.float64, device=dev)
         ws.scales = torch.zeros(nseg, dtype=torch.float64, device=dev)
-    args = (ws.l1.handle, g.data_ptr(), m.data_ptr(), _lib.ptr(mask), C.byref(hyp))
-    logs = None
-    if spec.log_transform:
-        if ws.logs is None:
-            ws.logs = torch.zeros(2 * nseg, dtype=torch.float64, device=dev)
-        logs = ws.logs[:nseg]
-        _lib.call("lc_l1_scales", *args, qmax, logs.data_ptr(), ws.logs[nseg:].data_ptr(),
-                  stream)
-    if spec.norm_p == 1.0 and logs is None:
-        _lib.call("lc_l1_scales", *args, qmax, ws.norms.data_ptr(), ws.scales.data_ptr(),
-                  stream)
-    else:
-        ns = _lib.NormSpec(float(spec.norm_p), qmax, 0, _lib.ptr(logs))
-        _lib.call("lc_norm_scales", *args, C.byref(ns), ws.norms.data_ptr(),
-                  ws.scales.data_ptr(), stream)
+    if spec.log_transform and ws.logs is None:
+        ws.logs = torch.zeros(2 * nseg, dtype=torch.float64, device=dev)
+    scale_tables(ws.l1.handle, g, m, mask, hyp, spec, ws.norms, ws.scales, ws.logs, stream)
+    logs = ws.logs[:nseg] if spec.log_transform else None
     return _lib.Segments(layout.seg_start_dev(dev).data_ptr(), ws.scales.data_ptr(),
                          nseg, qmax, _lib.ptr(logs), spec.kernel_flags(), 0,
                          seed & 0xFFFFFFFFFFFFFFFF)
