@@ -293,6 +293,12 @@ int lc_f64_to_f32_exact(const double* x, int64_t n, float* out, uint32_t* flags,
                         void* stream);
 
 /* ---- metrics / operator helpers ---- */
+/* Momentum divergence (optimizer.py:261-276): per segment, the max over its
+ * elements of the population std across P fp32 rows (row r at rows + r*stride),
+ * numpy's rank-ordered float64 mean / sum of squares; bit-exact. */
+int lc_std_max_segmented(const float* rows, int32_t P, int64_t n, int64_t stride,
+                         const int64_t* seg_start, int32_t nseg, double* out_max,
+                         void* stream);
 /* c as float64 (metrics_out["c_local"], optimizer.py:209). */
 int lc_compute_c(const float* g, const float* m, const uint8_t* mask,
                  int64_t n, const lc_hyper* h, double* c, void* stream);

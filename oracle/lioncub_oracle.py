@@ -495,6 +495,38 @@ def distributed_step(thetas: Sequence[Mapping[str, np.ndarray]],
     return new_t, new_m, signs, ties, cs_all, votes
 
 
+def signsgd_step(thetas: Sequence[Mapping[str, np.ndarray]],
+                 grads: Sequence[Mapping[str, np.ndarray]], lr: float, algo: str,
+                 iteration: int, zero_mode: str = "alternating"):
+    """``signsgd_majority_step`` for all P ranks (optimizer.py:213-241):
+    theta' = theta - lr * majority(sign(g_r)), momentum untouched."""
+    t = iteration + 1
+    out = {}
+    for name in sorted(thetas[0]):
+        gs = [np.asarray(g[name], dtype=np.float64).ravel() for g in grads]
+        if algo == "compressed1bit":
+            maj = vote_1bit(gs, zero_mode, t).values
+        else:
+            ss = [apply_sign(g, zero_mode, t) for g in gs]
+            if algo == "direct":
+                v = direct_sum(ss, q_max=1, binary_signs=True)
+            else:
+                v = ps_sum([s.astype(np.float64) for s in ss],
+                           efficient=algo == "ps_efficient")
+            maj = apply_sign(v.values, zero_mode, t)
+        th = np.asarray(thetas[0][name], dtype=np.float64)
+        out[name] = th - lr * np.asarray(maj).reshape(th.shape)
+    return out
+
+
+def divergence(moms: Sequence[Mapping[str, np.ndarray]]) -> dict:
+    """``divergence_from_momenta`` (optimizer.py:270-276): per layer, max over
+    elements of the population std across ranks."""
+    return {name: float(np.stack([np.asarray(m[name], np.float64) for m in moms])
+                        .std(axis=0, ddof=0).max())
+            for name in sorted(moms[0])}
+
+
 def lion_step(theta: Mapping[str, np.ndarray], mom: Mapping[str, np.ndarray],
               grad: Mapping[str, np.ndarray], h: Hyper):
     """``lion_step`` (optimizer.py:114-131): single worker, np.sign (zeros

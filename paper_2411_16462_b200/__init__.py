@@ -6,7 +6,7 @@ optimizer / collective API over CUDA tensors, executed by sm_100a kernels
 """
 
 from .collectives import (Topology, VoteResult, allreduce_mean_f32,  # noqa: F401
-                          choose_lane_bits, compressed_allreduce_1bit,
+                          allgather_f64, choose_lane_bits, compressed_allreduce_1bit,
                           direct_allreduce, field_bits, majority_sign,
                           ps_gather_broadcast, run_ranks)
 from .errors import (CapacityError, CollectiveError, ConfigError,  # noqa: F401
@@ -14,7 +14,8 @@ from .errors import (CapacityError, CollectiveError, ConfigError,  # noqa: F401
                      PackRangeError)
 from .optimizer import (VOTE_ALGOS, FlatParamSet, Layout, LionHyper,  # noqa: F401
                         StepGraph, SyncPolicy, WorkerState, distributed_lion_step,
-                        distributed_lion_step_host,
+                        distributed_lion_step_host, divergence_from_momenta,
+                        momentum_divergence, signsgd_majority_step,
                         hash_params, lion_step, load_checkpoint,
                         maybe_sync_momentum, save_checkpoint)
 from .quant import (INF, PackedBits, QuantSpec, SignPolicy, apply_sign,  # noqa: F401

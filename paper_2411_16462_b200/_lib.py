@@ -100,6 +100,7 @@ SIGNATURES = {
     "lc_dequantize": (INT, [P, I64, D, D, I32, P, P]),
     "lc_apply_sign_values": (INT, [P, I32, I64, INT, P, P]),
     "lc_f64_to_f32_exact": (INT, [P, I64, P, P, P]),
+    "lc_std_max_segmented": (INT, [P, I32, I64, I64, P, I32, P, P]),
     "lc_compute_c": (INT, [P, P, P, I64, P, P, P]),
     "lc_count_bits_segmented": (INT, [P, P, I32, P, P]),
     "lc_bits_to_sign": (INT, [P, P, I64, P, P]),
@@ -183,7 +184,7 @@ KERNEL_CALLS = frozenset({
     "lc_apply_update", "lc_fused_local_step", "lc_mean_f32", "lc_compute_c",
     "lc_count_bits_segmented", "lc_bits_to_sign", "lc_pack_i64_fields",
     "lc_fields_decode", "lc_sign_pack_f64", "lc_sum_u32_rows", "lc_quantize_values",
-    "lc_dequantize", "lc_apply_sign_values", "lc_f64_to_f32_exact"})
+    "lc_dequantize", "lc_apply_sign_values", "lc_f64_to_f32_exact", "lc_std_max_segmented"})
 KERNELS_PER_CALL = {"lc_l1_scales": 3, "lc_norm_scales": 3}
 
 launches = 0  # kernels enqueued through call(); read by bench.py

@@ -311,6 +311,34 @@ def allreduce_mean_f32(x, topo: Topology) -> torch.Tensor:
         return out
 
 
+def allgather_rows(x: torch.Tensor, topo: Topology, gen: int) -> torch.Tensor:
+    """[P, n] stack of every rank's flat ``x`` (same dtype), rank order."""
+    P, r = topo.world_size, topo.rank
+    n = x.numel()
+    rows = torch.empty((P, n), dtype=x.dtype, device=x.device)
+    if P == 1 or n == 0:
+        rows[0].copy_(x) if n else None
+        return rows
+    topo.transport.allgather(r, gen, x, rows.reshape(-1), n * x.element_size())
+    return rows
+
+
+def allgather_f64(x, topo: Topology) -> list:
+    """Every rank returns [x_0, ..., x_{P-1}] in rank order as float64
+    (collectives.py:347-360).  fp32 inputs travel as fp32 (half the bytes;
+    the float64 values are identical)."""
+    dev, st = topo.device, topo.stream
+    with torch.cuda.device(dev), torch.cuda.stream(st):
+        if not isinstance(x, torch.Tensor) or not x.is_cuda:
+            raise ConfigError("CUDA path needs CUDA tensors; no CPU fallback")
+        v = x.reshape(-1)
+        if v.dtype not in (torch.float32, torch.float64):
+            v = v.to(torch.float64)
+        v = _as_device(v, dev, v.dtype)
+        rows = allgather_rows(v, topo, topo.next_generation())
+        return [rows[j].to(torch.float64) for j in range(topo.world_size)]
+
+
 def run_ranks(world_size: int, fn, transport: DeviceTransport | None = None,
               transport_factory=None, timeout: float = DEFAULT_TIMEOUT) -> list:
     """Run ``fn(topo)`` on ``world_size`` threads (collectives.py:363-403).

@@ -929,6 +929,86 @@ def maybe_sync_momentum(state: WorkerState, policy: SyncPolicy,
     return replace(state, params=th, momentum=m)
 
 
+# ---------------------------------------------------------------------------
+# Divergence metrics (optimizer.py:261-276) and signSGD (optimizer.py:213-241)
+# ---------------------------------------------------------------------------
+
+def _std_max(rows: torch.Tensor, layout: Layout, stream) -> dict:
+    P, n = rows.shape
+    out = torch.zeros(len(layout.names), dtype=torch.float64, device=rows.device)
+    _lib.call("lc_std_max_segmented", rows.data_ptr(), P, n, n,
+              layout.seg_start_dev(rows.device).data_ptr(), len(layout.names),
+              out.data_ptr(), stream)
+    return dict(zip(layout.names, out.tolist()))
+
+
+def momentum_divergence(state: WorkerState, topo: Topology) -> dict:
+    """Per layer, the max over elements of the population std of momentum
+    across ranks (optimizer.py:261-267), bit-identical to the reference's
+    np.stack(...).std(axis=0, ddof=0).max().  One allgather of the fp32
+    momentum (P x 4 B/param per rank) + one kernel."""
+    from .collectives import allgather_rows
+    layout, _, m = state.flat()
+    dev = m.flat.device
+    with _on_device(dev), _on_stream(topo.stream, dev):
+        rows = allgather_rows(m.flat[:layout.n], topo, topo.next_generation())
+        return _std_max(rows, layout, topo.stream.cuda_stream)
+
+
+def divergence_from_momenta(momenta) -> dict:
+    """Single-process counterpart of ``momentum_divergence``
+    (optimizer.py:270-276): ``momenta`` is a list of per-rank ParamSets of
+    CUDA tensors (one device)."""
+    names = sorted(momenta[0])
+    layout = Layout({k: tuple(momenta[0][k].shape) for k in names})
+    dev = momenta[0][names[0]].device
+    if dev.type != "cuda":
+        raise ConfigError("divergence_from_momenta needs CUDA tensors; no CPU fallback")
+    rows = torch.empty((len(momenta), layout.n), dtype=torch.float32, device=dev)
+    for r, ms in enumerate(momenta):
+        for k in names:
+            o = layout.offset[k]
+            rows[r, o:o + layout.numel[k]].copy_(ms[k].reshape(-1))
+    return _std_max(rows, layout, torch.cuda.current_stream(dev).cuda_stream)
+
+
+class _SignHyper:
+    """c = 0*m + 1*g = g and m' = 1*m + 0*g = m with m aliased to g, so the
+    Lion kernels compute sign(g) and leave the gradient bit-identical; no
+    weight decay (optimizer.py:231-241)."""
+
+    def __init__(self, h: LionHyper):
+        self.h = h
+
+    def c_struct(self, t: int) -> _lib.Hyper:
+        return _lib.Hyper(0.0, 1.0, 1.0, 0.0, float(self.h.lr_at(t)), 0.0)
+
+
+def signsgd_majority_step(state: WorkerState, grad_i, h: LionHyper, topo: Topology,
+                          algo: str = "ps", zero_mode: str = "alternating") -> WorkerState:
+    """signSGD with majority vote (optimizer.py:213-241):
+    theta -= lr * sign(sum_i sign(g_i)), momentum untouched.  Runs the Lion
+    Cub kernels on sign(g): compressed1bit -> the 1-bit vote; ps /
+    ps_efficient / direct -> the exact sum of signs (alternating: binary
+    fields; exact-ternary ps: ternary signs as a 2-bit max-norm no_zero
+    quantizer, which is exactly sign(g)); direct keeps the reference's
+    rejection of zeros in exact-ternary mode.  In place."""
+    if algo not in VOTE_ALGOS:
+        raise ConfigError(f"unknown vote algorithm {algo!r}")
+    _check_shapes(state.params, grad_i)
+    layout, th, m = state.flat()
+    g = _to_flat(grad_i, layout, th.flat.device)
+    if algo == "compressed1bit":
+        spec, run_algo = None, "compressed1bit"
+    elif zero_mode == "exact-ternary" and algo != "direct":
+        spec, run_algo = QuantSpec(bits=2, norm_p=float("inf"), no_zero=True), "direct"
+    else:
+        spec, run_algo = QuantSpec(bits=1), "direct"
+    tmp = WorkerState(params=th, momentum=g, iteration=state.iteration)
+    out = _step_impl(tmp, g, _SignHyper(h), spec, topo, run_algo, None, zero_mode, None)
+    return WorkerState(params=out.params, momentum=m, iteration=out.iteration)
+
+
 class StepGraph:
     """CUDA-graph replay of the single-rank (P = 1) Lion Cub step.
 

@@ -29,8 +29,9 @@ from lioncomm.collectives import (allreduce_mean_f32,  # noqa: E402
                                   compressed_allreduce_1bit, direct_allreduce,
                                   run_ranks)
 from lioncomm.optimizer import (LionHyper, SyncPolicy, WorkerState,  # noqa: E402
-                                distributed_lion_step, maybe_sync_momentum,
-                                save_checkpoint)
+                                distributed_lion_step, divergence_from_momenta,
+                                maybe_sync_momentum, momentum_divergence,
+                                save_checkpoint, signsgd_majority_step)
 from lioncomm.quant import (PackedBits, QuantSpec, SignPolicy,  # noqa: E402
                             apply_sign, dequantize, lp_mean_norm, pack,
                             quantize, unpack)
@@ -245,6 +246,51 @@ def make_quant_golden():
     return len(out)
 
 
+SIGNSGD_CASES = [  # (algo, world, kind, zero_mode, iteration)
+    ("ps", 3, "laplace", "alternating", 0), ("ps", 4, "zeros", "exact-ternary", 1),
+    ("ps_efficient", 5, "ties", "alternating", 1), ("direct", 2, "laplace", "alternating", 0),
+    ("direct", 8, "ties", "alternating", 3), ("compressed1bit", 4, "zeros", "alternating", 0),
+    ("compressed1bit", 1, "laplace", "alternating", 1), ("ps", 1, "zeros", "exact-ternary", 0),
+]
+
+
+def make_metrics_golden():
+    """signsgd_majority_step and the momentum-divergence metrics of the
+    reference on seeded inputs."""
+    out: dict = {}
+    for i, (algo, world, kind, zm, it) in enumerate(SIGNSGD_CASES):
+        ranks = synth_rank_inputs(300 + i, world, SIZES, kind)
+        h = LionHyper(beta1=0.9, beta2=0.99, lr=1e-3, weight_decay=0.1)
+
+        def fn(topo, ranks=ranks):
+            r = topo.rank
+            st = WorkerState(
+                params={k: v.astype(np.float64) for k, v in ranks[r]["theta"].items()},
+                momentum={k: v.astype(np.float64) for k, v in ranks[r]["m"].items()},
+                iteration=it)
+            grads = {k: v.astype(np.float64) for k, v in ranks[r]["g"].items()}
+            st2 = signsgd_majority_step(st, grads, h, topo, algo=algo, zero_mode=zm)
+            return st2, momentum_divergence(st2, topo)
+
+        res = run_ranks(world, fn, transport=InprocTransport(world))
+        p = f"sgd{i}/"
+        for k in SIZES:
+            out[p + f"in/theta/{k}"] = ranks[0]["theta"][k]
+            for r in range(world):
+                out[p + f"in/m/{r}/{k}"] = ranks[r]["m"][k]
+                out[p + f"in/g/{r}/{k}"] = ranks[r]["g"][k]
+                assert np.array_equal(res[r][0].params[k], res[0][0].params[k])
+            out[p + f"out/theta/{k}"] = res[0][0].params[k]
+            out[p + f"out/div/{k}"] = np.float64(res[0][1][k])
+        moms = [{k: v.astype(np.float64) for k, v in rk["m"].items()} for rk in ranks]
+        div = divergence_from_momenta(moms)
+        for k in SIZES:
+            out[p + f"out/divm/{k}"] = np.float64(div[k])
+    meta = {"signsgd": SIGNSGD_CASES}
+    out["meta"] = np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(HERE, "golden_metrics.npz"), **out)
+
+
 def main():
     steps: dict = {}
     for case in STEP_CASES:
@@ -260,6 +306,7 @@ def main():
                                   dtype=np.uint8)
     np.savez_compressed(os.path.join(HERE, "golden_collectives.npz"), **colls)
     make_checkpoint()
+    make_metrics_golden()
     nq = make_quant_golden()
     print(f"{nq} standalone quant arrays")
     print(f"{len(STEP_CASES)} step cases, {len(COLLECTIVE_CASES)} collective cases")

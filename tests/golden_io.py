@@ -74,3 +74,23 @@ def collective_case(name: str) -> dict:
 def quant_golden():
     """golden_quant.npz: the reference's standalone quant.py outputs."""
     return _load("golden_quant.npz")
+
+
+def metrics_golden():
+    """golden_metrics.npz: the reference's signsgd_majority_step and
+    momentum-divergence outputs."""
+    return _load("golden_metrics.npz")
+
+
+def signsgd_case(i: int, sizes: dict):
+    data, meta = metrics_golden()
+    algo, world, kind, zm, it = meta["signsgd"][i]
+    p = f"sgd{i}/"
+    return dict(
+        algo=algo, world=world, zero_mode=zm, iteration=it,
+        theta={k: data[p + f"in/theta/{k}"] for k in sizes},
+        m=[{k: data[p + f"in/m/{r}/{k}"] for k in sizes} for r in range(world)],
+        g=[{k: data[p + f"in/g/{r}/{k}"] for k in sizes} for r in range(world)],
+        theta_out={k: data[p + f"out/theta/{k}"] for k in sizes},
+        div={k: float(data[p + f"out/div/{k}"]) for k in sizes},
+        divm={k: float(data[p + f"out/divm/{k}"]) for k in sizes})

@@ -217,3 +217,18 @@ def test_splitmix_stream_is_uniform_and_sround_unbiased():
     q = O.sround(v, u)
     assert set(np.unique(q)) == {2, 3}
     assert abs(q.mean() - 2.3) < 2e-3          # E[sround(v)] = v (quant.py:107-116)
+
+
+# ---- signSGD majority and divergence metrics (golden_metrics.npz) ----------
+
+@pytest.mark.parametrize("i", range(len(G.metrics_golden()[1]["signsgd"])))
+def test_oracle_signsgd_and_divergence_match_reference(i):
+    sizes = G.step_sizes()
+    c = G.signsgd_case(i, sizes)
+    out = O.signsgd_step([c["theta"]] * c["world"], c["g"], 1e-3, c["algo"], c["iteration"],
+                         c["zero_mode"])
+    for k in sizes:
+        assert np.array_equal(out[k], c["theta_out"][k]), k
+    div = O.divergence(c["m"])
+    for k in sizes:
+        assert div[k] == c["div"][k] == c["divm"][k], k
