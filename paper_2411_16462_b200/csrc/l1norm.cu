@@ -301,8 +301,13 @@ __device__ __forceinline__ double l1_v(const float* g, const float* m, const uin
 }
 
 // One CTA per work item: leaves with 8 lanes each, then templated additions.
+#ifndef LC_L1_ITEM_THREADS
+#define LC_L1_ITEM_THREADS 256
+#endif
+constexpr int kItemThreads = LC_L1_ITEM_THREADS;
+
 template <bool MASK, int PK, bool LOG>
-__global__ void __launch_bounds__(kThreads, 4)
+__global__ void __launch_bounds__(kItemThreads, 1024 / kItemThreads)
 k_l1_items(const float* __restrict__ g, const float* __restrict__ m,
            const uint8_t* __restrict__ mask, Hyp h,
            const unsigned long long* __restrict__ gmax, const double* __restrict__ logs,
@@ -397,22 +402,20 @@ __global__ void k_div_check(const double* __restrict__ a, const double* __restri
   }
 }
 
-// One CTA per layer: additions above the work items, then M_p and the scale
-// (quant.py:94-104, :153-170).
-__global__ void __launch_bounds__(kThreads)
-k_l1_upper(const DevSeg* __restrict__ segs, const int4* __restrict__ uops,
-           const int* __restrict__ ulvl, const unsigned long long* __restrict__ gmax,
-           double* __restrict__ nodes, int pk, double p, int qmax,
-           double* __restrict__ norms, double* __restrict__ scales) {
-  const int s = blockIdx.x;
-  const DevSeg S = segs[s];
-  const double mx = pk == PK_0 ? (double)gmax[s] : __longlong_as_double((long long)gmax[s]);
+// Additions above the work items of segment S (level by level, one CTA),
+// then M_p and the quantizer scale (quant.py:94-104, :153-170).  Every
+// thread of the CTA calls it.
+__device__ __forceinline__ void seg_upper(const DevSeg& S, int s, const int4* __restrict__ uops,
+                                          const int* __restrict__ ulvl, double mx,
+                                          double* __restrict__ nodes, int pk, double p,
+                                          int qmax, double* __restrict__ norms,
+                                          double* __restrict__ scales) {
   if (mx != 0.0 && pk != PK_INF) {
     for (int lv = 0; lv < S.nlvl; ++lv) {
       const int b = ulvl[S.lvl_begin + lv], e = ulvl[S.lvl_begin + lv + 1];
       for (int o = b + threadIdx.x; o < e; o += blockDim.x) {
         const int4 op = uops[S.op_begin + o];
-        nodes[op.x] = __dadd_rn(nodes[op.y], nodes[op.z]);
+        __stcg(nodes + op.x, __dadd_rn(__ldcg(nodes + op.y), __ldcg(nodes + op.z)));
       }
       __syncthreads();
     }
@@ -423,10 +426,10 @@ k_l1_upper(const DevSeg* __restrict__ segs, const int4* __restrict__ uops,
       if (pk == PK_INF) {
         M = mx;                                                  // max|y|
       } else if (pk == PK_0) {
-        M = exp(__ddiv_rn(nodes[S.root], mx));                   // exp(mean(log nz))
+        M = exp(__ddiv_rn(__ldcg(nodes + S.root), mx));          // exp(mean(log nz))
       } else {
-        const double mean = __ddiv_rn(nodes[S.root], (double)S.n);  // np.mean
-        double r = mean;                                             // mean ** (1/p)
+        const double mean = __ddiv_rn(__ldcg(nodes + S.root), (double)S.n);  // np.mean
+        double r = mean;                                                     // mean ** (1/p)
         if (pk == PK_2) r = __dsqrt_rn(mean);
         else if (pk == PK_HALF) r = __dmul_rn(mean, mean);
         else if (pk == PK_GEN) r = pow(mean, __ddiv_rn(1.0, p));
@@ -438,6 +441,20 @@ k_l1_upper(const DevSeg* __restrict__ segs, const int4* __restrict__ uops,
                 : pk == PK_INF ? __ddiv_rn((double)qmax, M)
                                : __ddiv_rn((double)qmax, __dmul_rn(2.0, M));
   }
+}
+
+__device__ __forceinline__ double seg_mx(const unsigned long long* gmax, int s, int pk) {
+  return pk == PK_0 ? (double)gmax[s] : __longlong_as_double((long long)gmax[s]);
+}
+
+// One CTA per layer: additions above the work items, then M_p and the scale.
+__global__ void __launch_bounds__(kThreads)
+k_l1_upper(const DevSeg* __restrict__ segs, const int4* __restrict__ uops,
+           const int* __restrict__ ulvl, const unsigned long long* __restrict__ gmax,
+           double* __restrict__ nodes, int pk, double p, int qmax,
+           double* __restrict__ norms, double* __restrict__ scales) {
+  const int s = blockIdx.x;
+  seg_upper(segs[s], s, uops, ulvl, seg_mx(gmax, s, pk), nodes, pk, p, qmax, norms, scales);
 }
 
 int norm_kind(double p) {
@@ -619,7 +636,7 @@ int launch_items(lc_l1_plan_t p, const float* g, const float* m, const uint8_t* 
   auto items = k_l1_items<MASK, PK, LOG>;
   if (smem > 48 * 1024)
     LC_CUDA_TRY(cudaFuncSetAttribute(items, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  items<<<p->n_items, kThreads, smem, st>>>(g, m, mask, h, p->d_max, logs, pv, p->d_wi_off,
+  items<<<p->n_items, kItemThreads, smem, st>>>(g, m, mask, h, p->d_max, logs, pv, p->d_wi_off,
                                             p->d_wi_meta, p->d_tmpl, p->d_leaf_rel,
                                             p->d_leaf_size, p->d_tops, p->d_tlvl, p->d_nodes);
   return LC_OK;
