@@ -81,11 +81,31 @@ WORKLOADS = {
                        "TinyLlama-1.1B layout, 1-bit vote, no sync"),
     "gpt2s_l1_5bit": (gpt2_small_layout, "direct", 5, None,
                       "GPT-2-small-sized buffer, L1 5-bit p-bit vote (paper's 8-bit Lion Cub)"),
+    "gpt2s_qinf_stoch_5bit": (gpt2_small_layout, "direct",
+                              dict(bits=5, norm_p=float("inf"), rounding="stochastic"), None,
+                              "GPT-2-small-sized buffer, 5-bit max-norm quantizer with "
+                              "stochastic rounding (QuantSpec variant)"),
     "gpt2s_ps": (gpt2_small_layout, "ps", None, None,
                  "GPT-2-small-sized buffer, full-precision (ps) vote"),
     "flat7b_1bit_sync": (lambda: {"w": (7_000_000_000,)}, "compressed1bit", None,
                          (1, "all"), "7e9 flat buffer, 1-bit vote + all-layer sync (configs[4])"),
 }
+
+
+def quant_kwargs(bits) -> dict | None:
+    """QuantSpec kwargs of a workload's ``bits`` entry (int: L1, nearest)."""
+    if bits is None:
+        return None
+    return dict(bits) if isinstance(bits, dict) else dict(bits=bits, norm_p=1.0)
+
+
+def norm_bytes(bits) -> float:
+    """HBM bytes/param of the per-layer norm pass(es) of a quantizer."""
+    kw = quant_kwargs(bits)
+    if kw is None or kw["bits"] == 1:
+        return 0.0
+    b = 8.0 if kw.get("norm_p") == float("inf") else 16.0  # max pass (+ pairwise sum)
+    return b + (16.0 if kw.get("log_transform") else 0.0)
 
 
 def numel(shapes: dict) -> int:
@@ -96,7 +116,7 @@ def numel(shapes: dict) -> int:
 # Algorithmic bytes
 # ---------------------------------------------------------------------------
 
-def kernel_bytes(name: str, n: int, P: int, F: int, kind: str) -> float:
+def kernel_bytes(name: str, n: int, P: int, F: int, kind: str, nb: float = 16.0) -> float:
     """Algorithmic HBM bytes of ONE launch of our kernel on an n-param step."""
     L = -(-max(-(-n // P), 1) // 1024) * 1024
     if name == "lc_fused_local_step":
@@ -115,20 +135,22 @@ def kernel_bytes(name: str, n: int, P: int, F: int, kind: str) -> float:
         return P * L * 8.0 + L / 8.0
     if name == "lc_l1_scales":
         return 16.0 * n  # g, m read twice: max pass, then the pairwise sum
+    if name == "lc_norm_scales":
+        return nb * n
     return 0.0
 
 
 def step_roofline(n: int, P: int, F: int, kind: str, sync_frac: float,
-                  hbm_gbs: float, nvl_gbs: float = 770.0, l1: bool = False) -> dict:
+                  hbm_gbs: float, nvl_gbs: float = 770.0, nb: float = 0.0) -> dict:
     """Whole-step lower bound: max(HBM bytes / HBM BW, NVLink bytes / link BW)."""
     if P == 1:
-        hbm = 20.0 * n + (16.0 * n if l1 else 0.0)
+        hbm = 20.0 * n + nb * n
         nvl = 0.0
     elif kind == "1bit":
         hbm = 20.0 * n + 2 * n / 8.0
         nvl = 2 * (P - 1) / P * n / 8.0
     elif kind == "fields":
-        hbm = 20.0 * n + 2 * n * F / 8.0 + 2 * n / 8.0 + (16.0 * n if l1 else 0.0)
+        hbm = 20.0 * n + 2 * n * F / 8.0 + 2 * n / 8.0 + nb * n
         nvl = (P - 1) / P * n * (F + 1) / 8.0
     else:
         hbm = 36.0 * n
@@ -240,7 +262,10 @@ class CpuReference:
         self.cores = threads or len(os.sched_getaffinity(0))
         ranks = O.synth_rank_inputs(0, world, {"w": (sample,)}, "laplace")
         self.h = O.Hyper(0.9, 0.99, 1e-4, 0.0)
-        self.spec = None if bits is None else O.Spec(bits)
+        kw = quant_kwargs(bits)
+        self.spec = None if kw is None else O.Spec(**kw)
+        self.seeds = list(range(1, world + 1)) \
+            if kw and kw.get("rounding") == "stochastic" else None
         chunk = -(-sample // self.cores)
         self.pieces = []
         for a in range(0, sample, chunk):
@@ -252,7 +277,7 @@ class CpuReference:
 
     def _one(self, piece):
         th, m, g = piece
-        self.O.distributed_step(th, m, g, self.h, self.spec, self.algo, 0)
+        self.O.distributed_step(th, m, g, self.h, self.spec, self.algo, 0, seeds=self.seeds)
 
     def step(self) -> float:
         t0 = time.perf_counter()
@@ -335,6 +360,7 @@ def main():
     if args.impl == "reference":
         return run_reference_arm(args)
 
+    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -362,7 +388,11 @@ def main():
     layout_fn, algo, bits, sync, desc = WORKLOADS[args.workload]
     shapes = layout_fn()
     n = numel(shapes)
-    spec = None if bits is None else lc.QuantSpec(bits=bits, norm_p=1.0)
+    qkw = quant_kwargs(bits)
+    spec = None if qkw is None else lc.QuantSpec(**qkw)
+    nbits = None if qkw is None else qkw["bits"]
+    rng = np.random.default_rng(rank) if spec is not None and spec.rounding == "stochastic" \
+        else None
     policy = None
     sync_frac = 0.0
     if sync is not None:
@@ -394,13 +424,13 @@ def main():
     torch.cuda.synchronize()
 
     graph = None
-    if args.graph and world == 1 and (bits is None or bits == 1):
+    if args.graph and world == 1 and (nbits is None or nbits == 1):
         graph = lc.StepGraph(st, g, h, spec, topo, algo)  # CUDA-graph replay of the P=1 step
 
     def step(state):
         if graph is not None:
             return graph.step()
-        state = lc.distributed_lion_step(state, g, h, spec, topo, algo)
+        state = lc.distributed_lion_step(state, g, h, spec, topo, algo, rng=rng)
         if policy is not None:
             state = lc.maybe_sync_momentum(state, policy, topo)
         return state
@@ -502,16 +532,16 @@ def main():
     P = world
     if algo == "compressed1bit":
         kind, F = "1bit", 1
-    elif bits is None:
+    elif nbits is None:
         kind, F = "f64", 64
-    elif bits == 1 and P > 1 and transport.p2p:
+    elif nbits == 1 and P > 1 and transport.p2p:
         kind, F = "1bit", 1   # sum-of-signs ships 1-bit signs over peer memory
     else:
         kind = "fields"
-        F = lc.field_bits(P, 1 if bits == 1 else 2 * ((1 << (bits - 1)) - 1))
+        F = lc.field_bits(P, 1 if nbits == 1 else 2 * ((1 << (nbits - 1)) - 1))
     roof = None
     if dominant:
-        bpl = kernel_bytes(dominant, n, P, F, kind)
+        bpl = kernel_bytes(dominant, n, P, F, kind, norm_bytes(bits))
         ach = bpl / (kern[dominant]["avg_ms"] * 1e-3) / 1e9
         tt = traffic_table().get(f"{args.workload}/P{P}/{dominant}")
         roof = {"kernel": dominant, "bound": "hbm", "achieved": ach, "peak": hbm_peak,
@@ -520,7 +550,7 @@ def main():
                 "avg_launch_ms": kern[dominant]["avg_ms"],
                 "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs" if peak_src ==
                 "measured" else "fallback 6650 GB/s (B200_PROFILING.md)"}
-    sr = step_roofline(n, P, F, kind, sync_frac, hbm_peak, l1=bits is not None and bits > 1)
+    sr = step_roofline(n, P, F, kind, sync_frac, hbm_peak, nb=norm_bytes(bits))
     sr["frac"] = max(sr["t_hbm_ms"], sr["t_nvlink_ms"]) / ms
 
     # end to end through the public API with host buffers: pinned host
@@ -534,7 +564,8 @@ def main():
 
         def step_host(state):
             state = lc.distributed_lion_step_host(state, host_g, h, spec, topo, algo,
-                                                  params_out=host_t, chunk=args.e2e_chunk)
+                                                  params_out=host_t, chunk=args.e2e_chunk,
+                                                  rng=rng)
             if policy is not None:
                 state = lc.maybe_sync_momentum(state, policy, topo)
             return state

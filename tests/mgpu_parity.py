@@ -27,18 +27,38 @@ from tests import golden_io as G  # noqa: E402
 
 SIZES = {"emb": (50_000,), "h0.w": (300_017,), "h1.w": (262_144,), "norm": (7,)}
 
-CONFIGS = [
+INF = float("inf")
+CONFIGS = [  # (algo, QuantSpec kwargs or None, input kind, zero mode, sync)
     ("compressed1bit", None, "laplace", "alternating", None),
     ("compressed1bit", None, "ties", "alternating", None),
-    ("direct", 1, "laplace", "alternating", None),
-    ("direct", 1, "ties", "exact-ternary", None),
-    ("direct", 5, "outliers", "alternating", None),
-    ("direct", 8, "laplace", "exact-ternary", None),
+    ("direct", dict(bits=1), "laplace", "alternating", None),
+    ("direct", dict(bits=1), "ties", "exact-ternary", None),
+    ("direct", dict(bits=5), "outliers", "alternating", None),
+    ("direct", dict(bits=8), "laplace", "exact-ternary", None),
     ("ps", None, "cancel", "exact-ternary", None),
     ("ps_efficient", None, "laplace", "alternating", None),
     ("compressed1bit", None, "laplace", "alternating", (10, frozenset({"emb", "h1.w"}))),
-    ("direct", 1, "zeros", "alternating", (10, "all")),
+    ("direct", dict(bits=1), "zeros", "alternating", (10, "all")),
+    # quantizer variants (stochastic: the oracle is fed the same stream)
+    ("direct", dict(bits=5, norm_p=INF), "outliers", "alternating", None),
+    ("direct", dict(bits=4, rounding="stochastic"), "laplace", "alternating", None),
+    ("direct", dict(bits=6, norm_p=2.0, log_transform=True, no_zero=True), "zeros",
+     "alternating", None),
 ]
+SEED_BASE = 1000
+
+
+def step_seeds(qkw, world):
+    if not qkw or qkw.get("rounding") != "stochastic":
+        return None
+    from paper_2411_16462_b200.quant import draw_seed
+    return [draw_seed(np.random.default_rng(SEED_BASE + r)) for r in range(world)]
+
+
+def rng_for(qkw, rank):
+    if not qkw or qkw.get("rounding") != "stochastic":
+        return None
+    return np.random.default_rng(SEED_BASE + rank)
 
 
 def f32_eq(a, b):
@@ -58,13 +78,15 @@ def main():
     topo = lc.Topology(world_size=world, rank=rank, transport=tp)
     fails = []
     checked = 0
-    for ci, (algo, bits, kind, zm, sync) in enumerate(CONFIGS):
+    for ci, (algo, qkw, kind, zm, sync) in enumerate(CONFIGS):
+        bits = None if qkw is None else qkw["bits"]
         ranks = O.synth_rank_inputs(100 + ci, world, SIZES, kind)
         h = O.Hyper(0.9, 0.99, 1e-4, 0.1)
         it = 9
         nt, nm, sign, ties, _, _ = O.distributed_step(
             [r["theta"] for r in ranks], [r["m"] for r in ranks], [r["g"] for r in ranks],
-            h, None if bits is None else O.Spec(bits), algo, it, zero_mode=zm)
+            h, None if qkw is None else O.Spec(**qkw), algo, it, zero_mode=zm,
+            seeds=step_seeds(qkw, world))
         if sync is not None:
             nm = O.sync_momentum(nm, sync[0], sync[1], it + 1)
         mine = ranks[rank]
@@ -78,8 +100,9 @@ def main():
             g[k].copy_(torch.from_numpy(v))
         met = {}
         st = lc.distributed_lion_step(st, g, lc.LionHyper(0.9, 0.99, 1e-4, 0.1),
-                                      None if bits is None else lc.QuantSpec(bits=bits),
-                                      topo, algo, zero_mode=zm, metrics_out=met)
+                                      None if qkw is None else lc.QuantSpec(**qkw),
+                                      topo, algo, zero_mode=zm, metrics_out=met,
+                                      rng=rng_for(qkw, rank))
         if sync is not None:
             st = lc.maybe_sync_momentum(st, lc.SyncPolicy(period=sync[0], layers=sync[1]), topo)
         torch.cuda.synchronize()
@@ -97,7 +120,10 @@ def main():
     # streamed step, three consecutive steps against the oracle fed the
     # fp32-rounded state each step
     f32 = lambda d: {k: np.asarray(v, np.float32).astype(np.float64) for k, v in d.items()}  # noqa
-    for ci, (algo, bits, kind, zm, sync) in enumerate(CONFIGS):
+    for ci, (algo, qkw, kind, zm, sync) in enumerate(CONFIGS):
+        if qkw is not None and qkw.get("rounding") == "stochastic":
+            continue   # one stream per step: covered by the metrics pass above
+        bits = None if qkw is None else qkw["bits"]
         ranks = O.synth_rank_inputs(300 + ci, world, SIZES, kind)
         h = O.Hyper(0.9, 0.99, 1e-4, 0.1)
         it0 = 4
@@ -105,7 +131,7 @@ def main():
         moms = [f32(r["m"]) for r in ranks]
         for i in range(3):
             nt, nm, *_ = O.distributed_step(thetas, moms, [r["g"] for r in ranks], h,
-                                            None if bits is None else O.Spec(bits), algo,
+                                            None if qkw is None else O.Spec(**qkw), algo,
                                             it0 + i, zero_mode=zm)
             nm = [f32(x) for x in nm]
             if sync is not None:
@@ -122,7 +148,7 @@ def main():
             g[k].copy_(torch.from_numpy(v))
         for i in range(3):
             st = lc.distributed_lion_step(st, g, lc.LionHyper(0.9, 0.99, 1e-4, 0.1),
-                                          None if bits is None else lc.QuantSpec(bits=bits),
+                                          None if qkw is None else lc.QuantSpec(**qkw),
                                           topo, algo, zero_mode=zm)
             if sync is not None:
                 st = lc.maybe_sync_momentum(st, lc.SyncPolicy(period=sync[0], layers=sync[1]),
@@ -152,6 +178,29 @@ def main():
             ok = np.array_equal(v.cpu().numpy().view(np.int32), gc["values"].view(np.int32))
         if not ok:
             fails.append(f"golden {c['name']}")
+    # signSGD majority and the divergence metric (golden_metrics.npz) at this world size
+    gsizes = G.step_sizes()
+    for i, case in enumerate(G.metrics_golden()[1]["signsgd"]):
+        if case[1] != world:
+            continue
+        c = G.signsgd_case(i, gsizes)
+        st = lc.WorkerState.initial({k: torch.from_numpy(v).to(dev)
+                                     for k, v in c["theta"].items()})
+        for k, v in c["m"][rank].items():
+            st.momentum[k].copy_(torch.from_numpy(v))
+        st.iteration = c["iteration"]
+        g = st.new_grad_buffer()
+        for k, v in c["g"][rank].items():
+            g[k].copy_(torch.from_numpy(v))
+        st = lc.signsgd_majority_step(st, g, lc.LionHyper(0.9, 0.99, 1e-3, 0.1), topo,
+                                      algo=c["algo"], zero_mode=c["zero_mode"])
+        div = lc.momentum_divergence(st, topo)
+        for k in gsizes:
+            checked += 1
+            if not f32_eq(st.params[k].cpu().numpy(), c["theta_out"][k]):
+                fails.append(f"signsgd {i}: theta {k}")
+            if div[k] != c["div"][k]:
+                fails.append(f"signsgd {i}: divergence {k}")
     nfail = torch.tensor([len(fails)], device=dev)
     dist.all_reduce(nfail)
     if fails:
