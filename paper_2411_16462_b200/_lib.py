@@ -185,7 +185,7 @@ KERNEL_CALLS = frozenset({
     "lc_count_bits_segmented", "lc_bits_to_sign", "lc_pack_i64_fields",
     "lc_fields_decode", "lc_sign_pack_f64", "lc_sum_u32_rows", "lc_quantize_values",
     "lc_dequantize", "lc_apply_sign_values", "lc_f64_to_f32_exact", "lc_std_max_segmented"})
-KERNELS_PER_CALL = {"lc_l1_scales": 3, "lc_norm_scales": 3}
+KERNELS_PER_CALL = {"lc_l1_scales": 4, "lc_norm_scales": 4}
 
 launches = 0  # kernels enqueued through call(); read by bench.py
 

@@ -15,6 +15,7 @@
 // the quantized integers are bit-identical to the reference.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <functional>
 #include <map>
 #include <vector>
@@ -121,6 +122,11 @@ struct lc_l1_plan_s {
   int* d_ulvl = nullptr;      // upper level starts
   int64_t* d_wi_off = nullptr;  // work-item absolute element offset
   int* d_wi_meta = nullptr;     // (seg, tmpl, node) triples
+  int* d_wi_leaf0 = nullptr;    // first global leaf of each work item
+  int64_t n_leaves = 0;
+  int64_t* d_lf_start = nullptr;  // global leaves: absolute element offset
+  uint32_t* d_lf_meta = nullptr;  // size (8 bits) | segment << 8
+  double* d_lf_sum = nullptr;     // leaf sums
   double* d_nodes = nullptr;
   unsigned long long* d_max = nullptr;
 };
@@ -391,6 +397,167 @@ k_l1_items(const float* __restrict__ g, const float* __restrict__ m,
   if (threadIdx.x == 0) nodes[node] = slots[T.root];
 }
 
+// ---------------------------------------------------------------------------
+// Leaf-parallel pipeline: every numpy leaf (<= 128 elements, 8 strided
+// accumulators) of every layer is summed by an 8-lane group in one flat
+// grid-stride pass (no per-item trees, all 16 loads per lane in flight), then
+// one warp per work item combines its leaves with the item's template tree.
+// ---------------------------------------------------------------------------
+// (a/max)**p etc. of |y| = a; FAST divides by the reciprocal y = RN(1/max)
+// with one Markstein correction (RN(a/max) whenever the quotient is normal,
+// validated bitwise by lc_debug_div_check), else IEEE __ddiv_rn.  FAST
+// flags (bad) a nonzero a whose quotient could be subnormal (a < thr =
+// max * 2^-1021); the caller then redoes the leaf with IEEE division.
+template <int PK, bool FAST>
+__device__ __forceinline__ double term_div(double a, double b, double y, double thr, double p,
+                                           bool& bad) {
+  if (PK == PK_0) return a > 0.0 ? log(a) : 0.0;
+  double t;
+  if (FAST) {
+    const double q = __dmul_rn(a, y);
+    t = __fma_rn(__fma_rn(-q, b, a), y, q);
+    bad |= (a < thr) & (a > 0.0);
+  } else {
+    t = __ddiv_rn(a, b);
+  }
+  if (PK == PK_1) return t;
+  if (PK == PK_2) return __dmul_rn(t, t);
+  if (PK == PK_HALF) return __dsqrt_rn(t);
+  return pow(t, p);
+}
+
+// Sum of one numpy leaf (group of 8 lanes, lane k = accumulator k).
+template <bool MASK, int PK, bool LOG, bool FAST>
+__device__ __forceinline__ double leaf_sum(const float* __restrict__ g, const float* __restrict__ m,
+                                           const uint8_t* __restrict__ mask, const Hyp& h,
+                                           int64_t e0, int sz, int k, unsigned gm, double b,
+                                           double y, double thr, double sv, double p, bool& bad) {
+  auto one = [&](int64_t e) {
+    double c = lc::lion_c(m[e], g[e], h);
+    if (MASK && !mask[e]) c = 0.0;
+    return term_div<PK, FAST>(abs_y<LOG>(c, sv), b, y, thr, p, bad);
+  };
+  double res = 0.0;
+  if (sz < 8) {  // only a whole tiny layer: sequential from 0
+    if (k == 0)
+      for (int i = 0; i < sz; ++i) res = __dadd_rn(res, one(e0 + i));
+    return res;
+  }
+  // one predicated group per step: the compiler keeps the loads of several
+  // groups in flight (measured faster than staging all 32 loads in
+  // registers first, which spills at 64 registers)
+  const int ngrp = sz >> 3;
+  double r = 0.0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    if (i < ngrp) {
+      const int64_t e = e0 + 8 * i + k;
+      double c = lc::lion_c(__ldcs(m + e), __ldcs(g + e), h);
+      if (MASK && !mask[e]) c = 0.0;
+      const double v = term_div<PK, FAST>(abs_y<LOG>(c, sv), b, y, thr, p, bad);
+      r = i == 0 ? v : __dadd_rn(r, v);
+    }
+  }
+  r = __dadd_rn(r, __shfl_xor_sync(gm, r, 1));
+  r = __dadd_rn(r, __shfl_xor_sync(gm, r, 2));
+  r = __dadd_rn(r, __shfl_xor_sync(gm, r, 4));
+  res = r;
+  if (k == 0)
+    for (int i = ngrp * 8; i < sz; ++i) res = __dadd_rn(res, one(e0 + i));
+  return res;
+}
+
+// The rare general case (log map, extreme max, possibly subnormal
+// quotients) out of line, so the IEEE division does not weigh on the fast
+// path's registers.
+template <bool MASK, int PK, bool LOG>
+__device__ __noinline__ double leaf_sum_ieee(const float* __restrict__ g,
+                                             const float* __restrict__ m,
+                                             const uint8_t* __restrict__ mask, Hyp h, int64_t e0,
+                                             int sz, int k, unsigned gm, double b, double sv,
+                                             double p) {
+  bool unused = false;
+  return leaf_sum<MASK, PK, LOG, false>(g, m, mask, h, e0, sz, k, gm, b, 0.0, 0.0, sv, p, unused);
+}
+
+#ifndef LC_L1_LEAF_MINB
+#define LC_L1_LEAF_MINB 4
+#endif
+template <bool MASK, int PK, bool LOG>
+__global__ void __launch_bounds__(kThreads, LC_L1_LEAF_MINB)
+k_l1_leaves(const float* __restrict__ g, const float* __restrict__ m,
+            const uint8_t* __restrict__ mask, Hyp h,
+            const unsigned long long* __restrict__ gmax, const double* __restrict__ logs,
+            double p, int64_t n_leaves, const int64_t* __restrict__ lf_start,
+            const uint32_t* __restrict__ lf_meta, double* __restrict__ lf_sum) {
+  const int lane = threadIdx.x & 31;
+  const int k = lane & 7;
+  const unsigned gm = 0xffu << (lane & 24);
+  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) >> 3;
+  for (int64_t lf = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3; lf < n_leaves;
+       lf += ngroups) {
+    const int64_t e0 = __ldg(lf_start + lf);
+    const uint32_t meta = __ldg(lf_meta + lf);
+    const int sz = (int)(meta & 0xffu);
+    const int seg = (int)(meta >> 8);
+    const double mx = PK == PK_0 ? (double)gmax[seg] : __longlong_as_double((long long)gmax[seg]);
+    if (mx == 0.0) {  // the tree writes 0 for this segment; nothing to sum
+      if (k == 0) lf_sum[lf] = 0.0;
+      continue;
+    }
+    const double sv = LOG ? logs[seg] : 0.0;
+    // reciprocal division unless max is extreme or the log map is on; a
+    // leaf with a possibly subnormal quotient is redone with IEEE division
+    const bool fast = !LOG && mx >= 1e-300 && mx < 1e300;
+    double res;
+    bool bad = !fast;
+    if (fast) {
+      const double y = __drcp_rn(mx);
+      res = leaf_sum<MASK, PK, LOG, true>(g, m, mask, h, e0, sz, k, gm, mx, y,
+                                          __dmul_rn(mx, 0x1.0p-1021), sv, p, bad);
+    }
+    if (__any_sync(gm, bad))
+      res = leaf_sum_ieee<MASK, PK, LOG>(g, m, mask, h, e0, sz, k, gm, mx, sv, p);
+    if (k == 0) lf_sum[lf] = res;
+  }
+}
+
+// One warp per work item: its leaf sums -> the item's template tree (numpy's
+// additions above the leaves) -> the item's node.  Slots live in shared
+// memory, one region per warp; levels are ordered by __syncwarp.
+constexpr int kTreeWarps = 8;
+__global__ void __launch_bounds__(kTreeWarps * 32)
+k_l1_item_trees(int n_items, const unsigned long long* __restrict__ gmax, int pk,
+                const int* __restrict__ wi_meta, const int* __restrict__ wi_leaf0,
+                const DevTmpl* __restrict__ tmpl, const int4* __restrict__ tops,
+                const int* __restrict__ tlvl, const double* __restrict__ lf_sum,
+                int max_slots, double* __restrict__ nodes) {
+  extern __shared__ double tslots[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item = blockIdx.x * kTreeWarps + w;
+  if (item >= n_items) return;
+  double* slots = tslots + (size_t)w * max_slots;
+  const int seg = wi_meta[3 * item], ti = wi_meta[3 * item + 1], node = wi_meta[3 * item + 2];
+  const DevTmpl T = tmpl[ti];
+  const double mx = pk == PK_0 ? (double)gmax[seg] : __longlong_as_double((long long)gmax[seg]);
+  if (mx == 0.0) {
+    if (lane == 0) nodes[node] = 0.0;
+    return;
+  }
+  const int l0 = wi_leaf0[item];
+  for (int lf = lane; lf < T.nleaf; lf += 32) slots[lf] = lf_sum[l0 + lf];
+  __syncwarp();
+  for (int lv = 0; lv < T.nlvl; ++lv) {
+    const int b = tlvl[T.lvl_begin + lv], e = tlvl[T.lvl_begin + lv + 1];
+    for (int o = b + lane; o < e; o += 32) {
+      const int4 op = tops[T.op_begin + o];
+      slots[op.x] = __dadd_rn(slots[op.y], slots[op.z]);
+    }
+    __syncwarp();
+  }
+  if (lane == 0) nodes[node] = slots[T.root];
+}
+
 __global__ void k_div_check(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
                             unsigned long long* __restrict__ bad) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -402,23 +569,31 @@ __global__ void k_div_check(const double* __restrict__ a, const double* __restri
   }
 }
 
-// Additions above the work items of segment S (level by level, one CTA),
-// then M_p and the quantizer scale (quant.py:94-104, :153-170).  Every
-// thread of the CTA calls it.
-__device__ __forceinline__ void seg_upper(const DevSeg& S, int s, const int4* __restrict__ uops,
-                                          const int* __restrict__ ulvl, double mx,
-                                          double* __restrict__ nodes, int pk, double p,
-                                          int qmax, double* __restrict__ norms,
-                                          double* __restrict__ scales) {
+__device__ __forceinline__ double seg_mx(const unsigned long long* gmax, int s, int pk) {
+  return pk == PK_0 ? (double)gmax[s] : __longlong_as_double((long long)gmax[s]);
+}
+
+// One CTA per layer: the additions above the work items (level by level),
+// then M_p and the quantizer scale (quant.py:94-104, :153-170).
+__global__ void __launch_bounds__(kThreads)
+k_l1_upper(const DevSeg* __restrict__ segs, const int4* __restrict__ uops,
+           const int* __restrict__ ulvl, const unsigned long long* __restrict__ gmax,
+           double* __restrict__ nodes, int pk, double p, int qmax,
+           double* __restrict__ norms, double* __restrict__ scales) {
+  const int s = blockIdx.x;
+  const DevSeg S = segs[s];
+  const double mx = seg_mx(gmax, s, pk);
+  double root = 0.0;
   if (mx != 0.0 && pk != PK_INF) {
     for (int lv = 0; lv < S.nlvl; ++lv) {
       const int b = ulvl[S.lvl_begin + lv], e = ulvl[S.lvl_begin + lv + 1];
       for (int o = b + threadIdx.x; o < e; o += blockDim.x) {
         const int4 op = uops[S.op_begin + o];
-        __stcg(nodes + op.x, __dadd_rn(__ldcg(nodes + op.y), __ldcg(nodes + op.z)));
+        nodes[op.x] = __dadd_rn(nodes[op.y], nodes[op.z]);
       }
       __syncthreads();
     }
+    root = nodes[S.root];
   }
   if (threadIdx.x == 0) {
     double M = 0.0;
@@ -426,10 +601,10 @@ __device__ __forceinline__ void seg_upper(const DevSeg& S, int s, const int4* __
       if (pk == PK_INF) {
         M = mx;                                                  // max|y|
       } else if (pk == PK_0) {
-        M = exp(__ddiv_rn(__ldcg(nodes + S.root), mx));          // exp(mean(log nz))
+        M = exp(__ddiv_rn(root, mx));                            // exp(mean(log nz))
       } else {
-        const double mean = __ddiv_rn(__ldcg(nodes + S.root), (double)S.n);  // np.mean
-        double r = mean;                                                     // mean ** (1/p)
+        const double mean = __ddiv_rn(root, (double)S.n);        // np.mean
+        double r = mean;                                         // mean ** (1/p)
         if (pk == PK_2) r = __dsqrt_rn(mean);
         else if (pk == PK_HALF) r = __dmul_rn(mean, mean);
         else if (pk == PK_GEN) r = pow(mean, __ddiv_rn(1.0, p));
@@ -441,20 +616,6 @@ __device__ __forceinline__ void seg_upper(const DevSeg& S, int s, const int4* __
                 : pk == PK_INF ? __ddiv_rn((double)qmax, M)
                                : __ddiv_rn((double)qmax, __dmul_rn(2.0, M));
   }
-}
-
-__device__ __forceinline__ double seg_mx(const unsigned long long* gmax, int s, int pk) {
-  return pk == PK_0 ? (double)gmax[s] : __longlong_as_double((long long)gmax[s]);
-}
-
-// One CTA per layer: additions above the work items, then M_p and the scale.
-__global__ void __launch_bounds__(kThreads)
-k_l1_upper(const DevSeg* __restrict__ segs, const int4* __restrict__ uops,
-           const int* __restrict__ ulvl, const unsigned long long* __restrict__ gmax,
-           double* __restrict__ nodes, int pk, double p, int qmax,
-           double* __restrict__ norms, double* __restrict__ scales) {
-  const int s = blockIdx.x;
-  seg_upper(segs[s], s, uops, ulvl, seg_mx(gmax, s, pk), nodes, pk, p, qmax, norms, scales);
 }
 
 int norm_kind(double p) {
@@ -491,6 +652,10 @@ int lc_l1_plan_destroy(lc_l1_plan_t p) {
   cudaFree(p->d_ulvl);
   cudaFree(p->d_wi_off);
   cudaFree(p->d_wi_meta);
+  cudaFree(p->d_wi_leaf0);
+  cudaFree(p->d_lf_start);
+  cudaFree(p->d_lf_meta);
+  cudaFree(p->d_lf_sum);
   cudaFree(p->d_nodes);
   cudaFree(p->d_max);
   delete p;
@@ -592,6 +757,23 @@ int lc_l1_plan_create(lc_l1_plan_t* out, const int64_t* seg_start, int32_t nseg)
     p->max_slots = std::max(p->max_slots, t.nslots);
     dt.push_back(d);
   }
+  // global leaf list in item order (each item's leaves contiguous)
+  std::vector<int> wi_leaf0;
+  std::vector<int64_t> lf_start;
+  std::vector<uint32_t> lf_meta;
+  for (size_t it = 0; it < wi_off.size(); ++it) {
+    const Tmpl& t = tmpls[wi_meta[3 * it + 1]];
+    wi_leaf0.push_back((int)lf_start.size());
+    for (size_t l = 0; l < t.leaf_rel.size(); ++l) {
+      lf_start.push_back(wi_off[it] + t.leaf_rel[l]);
+      lf_meta.push_back((uint32_t)t.leaf_size[l] | ((uint32_t)wi_meta[3 * it] << 8));
+    }
+  }
+  if (nseg >= (1 << 24)) {
+    delete p;
+    return lc::set_err(LC_E_ARG, "lc_l1_plan_create: at most 2^24 segments");
+  }
+  p->n_leaves = (int64_t)lf_start.size();
   p->n_items = (int)wi_off.size();
   p->n_nodes = node_ctr;
   int rc = LC_OK;
@@ -600,12 +782,15 @@ int lc_l1_plan_create(lc_l1_plan_t* out, const int64_t* seg_start, int32_t nseg)
       (rc = upload(&p->d_leaf_rel, leaf_rel)) || (rc = upload(&p->d_leaf_size, leaf_size)) ||
       (rc = upload(&p->d_tops, tops)) || (rc = upload(&p->d_tlvl, tlvl)) ||
       (rc = upload(&p->d_uops, uops)) || (rc = upload(&p->d_ulvl, ulvl)) ||
-      (rc = upload(&p->d_wi_off, wi_off)) || (rc = upload(&p->d_wi_meta, wi_meta))) {
+      (rc = upload(&p->d_wi_off, wi_off)) || (rc = upload(&p->d_wi_meta, wi_meta)) ||
+      (rc = upload(&p->d_wi_leaf0, wi_leaf0)) || (rc = upload(&p->d_lf_start, lf_start)) ||
+      (rc = upload(&p->d_lf_meta, lf_meta))) {
     lc_l1_plan_destroy(p);
     return rc;
   }
   if (cudaMalloc(&p->d_nodes, sizeof(double) * std::max(1, p->n_nodes)) != cudaSuccess ||
-      cudaMalloc(&p->d_max, sizeof(unsigned long long) * nseg) != cudaSuccess) {
+      cudaMalloc(&p->d_max, sizeof(unsigned long long) * nseg) != cudaSuccess ||
+      cudaMalloc(&p->d_lf_sum, sizeof(double) * std::max<int64_t>(1, p->n_leaves)) != cudaSuccess) {
     lc_l1_plan_destroy(p);
     return lc::set_err(LC_E_CUDA, "lc_l1_plan_create: cudaMalloc failed");
   }
@@ -616,6 +801,13 @@ int lc_l1_plan_create(lc_l1_plan_t* out, const int64_t* seg_start, int32_t nseg)
 }  // extern "C"
 
 namespace {
+
+// LIONCUB_L1_ITEMS=1: the per-item CTA kernel (leaves + tree in one CTA)
+// instead of the leaf-parallel pass + warp trees (A/B and cross-check).
+const bool g_l1_items_legacy = [] {
+  const char* e = std::getenv("LIONCUB_L1_ITEMS");
+  return e && e[0] == '1';
+}();
 
 template <bool LOG, bool COUNT>
 void launch_max(lc_l1_plan_t p, const float* g, const float* m, const uint8_t* mask, Hyp h,
@@ -642,9 +834,38 @@ int launch_items(lc_l1_plan_t p, const float* g, const float* m, const uint8_t* 
   return LC_OK;
 }
 
+template <bool MASK, int PK, bool LOG>
+int launch_leaves(lc_l1_plan_t p, const float* g, const float* m, const uint8_t* mask, Hyp h,
+                  const double* logs, double pv, int pk, cudaStream_t st) {
+  if (p->n_leaves > 0) {
+    auto kern = k_l1_leaves<MASK, PK, LOG>;
+    const int64_t groups_per_cta = kThreads / 8;
+    int64_t grid = (p->n_leaves + groups_per_cta - 1) / groups_per_cta;
+    grid = std::min<int64_t>(grid, (int64_t)lc::sm_count() * LC_L1_LEAF_MINB * 8);
+    kern<<<(int)grid, kThreads, 0, st>>>(g, m, mask, h, p->d_max, logs, pv, p->n_leaves,
+                                         p->d_lf_start, p->d_lf_meta, p->d_lf_sum);
+    LC_LAUNCH_CHECK();
+  }
+  const size_t smem = sizeof(double) * std::max(1, p->max_slots) * kTreeWarps;
+  if (smem > 48 * 1024)
+    LC_CUDA_TRY(cudaFuncSetAttribute(k_l1_item_trees, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+  k_l1_item_trees<<<(p->n_items + kTreeWarps - 1) / kTreeWarps, kTreeWarps * 32, smem, st>>>(
+      p->n_items, p->d_max, pk, p->d_wi_meta, p->d_wi_leaf0, p->d_tmpl, p->d_tops, p->d_tlvl,
+      p->d_lf_sum, std::max(1, p->max_slots), p->d_nodes);
+  return LC_OK;
+}
+
 template <int PK>
 int items_pk(lc_l1_plan_t p, const float* g, const float* m, const uint8_t* mask, Hyp h,
              const double* logs, double pv, cudaStream_t st) {
+  if (!g_l1_items_legacy) {
+    if (mask)
+      return logs ? launch_leaves<true, PK, true>(p, g, m, mask, h, logs, pv, PK, st)
+                  : launch_leaves<true, PK, false>(p, g, m, mask, h, logs, pv, PK, st);
+    return logs ? launch_leaves<false, PK, true>(p, g, m, mask, h, logs, pv, PK, st)
+                : launch_leaves<false, PK, false>(p, g, m, mask, h, logs, pv, PK, st);
+  }
   if (mask)
     return logs ? launch_items<true, PK, true>(p, g, m, mask, h, logs, pv, st)
                 : launch_items<true, PK, false>(p, g, m, mask, h, logs, pv, st);
