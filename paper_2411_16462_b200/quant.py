@@ -29,7 +29,7 @@ def draw_seed(rng) -> int:
         return int(rng.integers(0, 1 << 63, dtype="int64"))
     import torch
     if isinstance(rng, torch.Generator):
-        return int(torch.randint(0, 1 << 62, (1,), generator=rng).item())
+        return int(torch.randint(0, 1 << 62, (1,), generator=rng, device=rng.device).item())
     raise ConfigError(f"unsupported rng {type(rng).__name__}")
 
 
@@ -159,6 +159,8 @@ def _plan(dev, n: int):
     with _plans_lock:
         p = _plans.get(key)
         if p is None:
+            if len(_plans) >= 64:      # bounded cache of device plans
+                _plans.clear()
             import torch
             from .optimizer import _L1Plan
 

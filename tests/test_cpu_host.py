@@ -83,6 +83,29 @@ def test_config_validation_mirrors_reference():
     assert lc.SignPolicy("exact-ternary", 3).kernel_fill() == 0
 
 
+def test_quant_spec_kernel_flags_and_seeds():
+    import numpy as np
+    import torch
+    from paper_2411_16462_b200.quant import LC_Q_NO_ZERO, LC_Q_STOCHASTIC, draw_seed
+    assert lc.QuantSpec().kernel_flags() == 0
+    assert lc.QuantSpec(rounding="stochastic", no_zero=True).kernel_flags() == \
+        LC_Q_STOCHASTIC | LC_Q_NO_ZERO
+    assert lc.QuantSpec(norm_p=lc.INF).draw_seed(None) == 0       # nearest: no rng needed
+    with pytest.raises(lc.ConfigError, match="rng"):
+        lc.QuantSpec(rounding="stochastic").draw_seed(None)
+    a = draw_seed(np.random.default_rng(7))
+    assert a == draw_seed(np.random.default_rng(7)) and 0 <= a < 1 << 63
+    r = np.random.default_rng(7)
+    assert draw_seed(r) != draw_seed(r)                            # the rng advances per call
+    assert draw_seed(torch.Generator().manual_seed(1)) == \
+        draw_seed(torch.Generator().manual_seed(1))
+    assert draw_seed(12345) == 12345
+    with pytest.raises(lc.ConfigError):
+        draw_seed("seed")
+    with pytest.raises(lc.ConfigError):
+        lc.QuantSpec(norm_p=-1.0)
+
+
 def test_lane_and_field_widths():
     assert lc.choose_lane_bits(8, 15) == 8
     assert lc.choose_lane_bits(125, 15) == 16
