@@ -87,6 +87,9 @@ WORKLOADS = {
                               "stochastic rounding (QuantSpec variant)"),
     "gpt2s_ps": (gpt2_small_layout, "ps", None, None,
                  "GPT-2-small-sized buffer, full-precision (ps) vote"),
+    "gpt2s_1bit_syncall": (gpt2_small_layout, "compressed1bit", None, (1, "all"),
+                           "GPT-2-small-sized buffer, 1-bit vote + all-layer momentum sync "
+                           "every step"),
     "flat7b_1bit_sync": (lambda: {"w": (7_000_000_000,)}, "compressed1bit", None,
                          (1, "all"), "7e9 flat buffer, 1-bit vote + all-layer sync (configs[4])"),
 }
@@ -162,6 +165,9 @@ def step_roofline(n: int, P: int, F: int, kind: str, sync_frac: float,
     t_n = nvl / (nvl_gbs * 1e9)
     return {"hbm_bytes": hbm, "nvlink_bytes": nvl, "t_hbm_ms": t_h * 1e3,
             "t_nvlink_ms": t_n * 1e3, "bound": "hbm" if t_h >= t_n else "nvlink"}
+
+
+NVL_GBS = 770.0   # NVLink 5 per direction, B200_PROFILING.md
 
 
 def measured_peaks() -> tuple[dict, str]:
@@ -550,6 +556,16 @@ def main():
                 "avg_launch_ms": kern[dominant]["avg_ms"],
                 "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs" if peak_src ==
                 "measured" else "fallback 6650 GB/s (B200_PROFILING.md)"}
+        if dominant == "lc_mean_pull_f32" and P > 1:
+            # the momentum sync is NVLink-bound: per direction each rank pulls
+            # (P-1)/P of the synced fp32 values in and stores as much out
+            # synced values over the timed steps / launches in them
+            per_launch = (P - 1) / P * 4.0 * sync_frac * n * args.steps / max(
+                1, kern[dominant]["launches"])
+            ach = per_launch / (kern[dominant]["avg_ms"] * 1e-3) / 1e9
+            roof.update({"bound": "nvlink", "achieved": ach, "peak": NVL_GBS, "frac": ach / NVL_GBS,
+                         "algorithmic_bytes_per_launch": per_launch,
+                         "peak_source": "B200_PROFILING.md NVLink per direction"})
     sr = step_roofline(n, P, F, kind, sync_frac, hbm_peak, nb=norm_bytes(bits))
     sr["frac"] = max(sr["t_hbm_ms"], sr["t_nvlink_ms"]) / ms
 

@@ -149,7 +149,7 @@ _GOLDEN = 0x9E3779B97F4A7C15
 def splitmix_uniforms(seed: int, index) -> np.ndarray:
     """The CUDA path's stochastic-rounding stream (csrc/common.cuh
     ``lc::uniform01``): element e draws u = (splitmix64(seed + (e+1)*golden)
-    >> 11) * 2**-53, a counter-based stream (no sequential state, so any
+    >> 12) * 2**-52, a counter-based stream (no sequential state, so any
     element range of any rank can be drawn independently).  The reference
     draws from numpy's PCG64 (quant.py:107-116); parity of stochastic
     rounding with the reference is statistical, with this stream exact."""
@@ -159,7 +159,7 @@ def splitmix_uniforms(seed: int, index) -> np.ndarray:
         z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
         z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
         z = z ^ (z >> np.uint64(31))
-    return (z >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+    return (z >> np.uint64(12)).astype(np.float64) * (2.0 ** -52)
 
 
 def sround(v, u) -> np.ndarray:

@@ -79,16 +79,17 @@ __device__ __forceinline__ float lion_theta(float th, double s, double lr,
 }
 
 // Stochastic-rounding stream: element e of a rank's flat buffer draws
-// u = (splitmix64(seed + (e+1) * golden) >> 11) * 2^-53 in [0, 1) -- a
+// u = (splitmix64(seed + (e+1) * golden) >> 12) * 2^-52 in [0, 1) -- a
 // counter-based generator (no per-thread state; any element range can be
-// drawn independently).  oracle/lioncub_oracle.py splitmix_uniforms
-// restates it.
+// drawn independently).  The 52 bits become the mantissa of a double in
+// [1, 2) minus 1 (exact; no int->double conversion).
+// oracle/lioncub_oracle.py splitmix_uniforms restates it.
 __device__ __forceinline__ double uniform01(uint64_t seed, int64_t e) {
   uint64_t z = seed + (uint64_t)(e + 1) * 0x9E3779B97F4A7C15ull;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
   z ^= z >> 31;
-  return (double)(z >> 11) * 0x1.0p-53;
+  return __longlong_as_double((long long)((z >> 12) | 0x3FF0000000000000ull)) - 1.0;
 }
 
 __device__ __forceinline__ float4 ld_stream(const float4* p) {

@@ -705,6 +705,9 @@ def _ternary_precheck(topo, gen, g, m, mflat, n, hyp, dev, s, kind):
 # GPT-2-small (0.424 vs 0.441 ms), the owner vote at P = 2 for 1.1B params
 # (3.71 vs 3.76 ms: K1's doubled NVLink stores) and at P = 4 for both.
 AG_MAX_P = int(os.environ.get("LIONCUB_AG_MAX_P", "2"))
+# LIONCUB_SYNC_NCCL=1: the momentum sync over NCCL (all-to-all, owner mean,
+# allgather) even when the step exchanges over peer memory (A/B knob)
+SYNC_NCCL = os.environ.get("LIONCUB_SYNC_NCCL", "0") == "1"
 AG_MAX_N = int(os.environ.get("LIONCUB_AG_MAX_N", str(1 << 28)))
 
 
@@ -896,7 +899,7 @@ def maybe_sync_momentum(state: WorkerState, policy: SyncPolicy,
             longest = max(b - a for a, b in runs)
             smax = -(-longest // P)
             st = topo.stream.cuda_stream
-            if tp.p2p:
+            if tp.p2p and not SYNC_NCCL:
                 # owner r pulls block r of every selected range from every
                 # rank's momentum over NVLink, averages (f64, rank order) and
                 # stores the mean into every rank's momentum -- one kernel per
