@@ -626,6 +626,15 @@ def main():
                                   else "L2 flushed (252 MB write) before every timed step; "
                                        "steps timed individually, flush excluded")},
                 "roofline": roof, "step_roofline": sr, "kernels": kern,
+                # the exchange is fused into the kernels (peer-memory stores /
+                # loads), so its rate is reported over the whole step: the
+                # algorithmic NVLink bytes each rank moves per direction per
+                # step / step time, against the per-direction link peak
+                "nvlink": None if world == 1 else {
+                    "bytes_per_rank_per_direction": sr["nvlink_bytes"],
+                    "achieved_gbs_over_step": sr["nvlink_bytes"] / (ms * 1e-3) / 1e9,
+                    "peak_gbs": NVL_GBS,
+                    "frac_of_peak": sr["nvlink_bytes"] / (ms * 1e-3) / 1e9 / NVL_GBS},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "host_enqueue_ms_per_step": host_ms,
                 "clocks": clocks}
