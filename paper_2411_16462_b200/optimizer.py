@@ -278,7 +278,7 @@ class _Workspace:
         # the full-precision arm moves 8 B/param: NCCL's all-to-all beats SM
         # stores into peer memory for that volume (measured), so it stays on
         # the collective path; the 1-bit / p-bit payloads use peer memory
-        self.p2p = p2p = P > 1 and tp.p2p and kind != "f64"
+        self.p2p = p2p = P > 1 and tp.p2p and (kind != "f64" or PS_P2P)
         z = lambda k, dt=torch.int32: torch.zeros(max(k, 1), dtype=dt, device=dev)  # noqa
         self.key = (layout.key, P, kind, F)
         self.ag = None
@@ -705,6 +705,9 @@ def _ternary_precheck(topo, gen, g, m, mflat, n, hyp, dev, s, kind):
 # GPT-2-small (0.424 vs 0.441 ms), the owner vote at P = 2 for 1.1B params
 # (3.71 vs 3.76 ms: K1's doubled NVLink stores) and at P = 4 for both.
 AG_MAX_P = int(os.environ.get("LIONCUB_AG_MAX_P", "2"))
+# LIONCUB_PS_P2P=1: the full-precision arm's float64 c also goes over peer
+# memory (K1 stores into the owners' slots) instead of NCCL's all-to-all
+PS_P2P = os.environ.get("LIONCUB_PS_P2P", "0") == "1"
 # LIONCUB_SYNC_NCCL=1: the momentum sync over NCCL (all-to-all, owner mean,
 # allgather) even when the step exchanges over peer memory (A/B knob)
 SYNC_NCCL = os.environ.get("LIONCUB_SYNC_NCCL", "0") == "1"
