@@ -404,19 +404,20 @@ k_l1_items(const float* __restrict__ g, const float* __restrict__ m,
 // one warp per work item combines its leaves with the item's template tree.
 // ---------------------------------------------------------------------------
 // (a/max)**p etc. of |y| = a; FAST divides by the reciprocal y = RN(1/max)
-// with one Markstein correction (RN(a/max) whenever the quotient is normal,
-// validated bitwise by lc_debug_div_check), else IEEE __ddiv_rn.  FAST
-// flags (bad) a nonzero a whose quotient could be subnormal (a < thr =
-// max * 2^-1021); the caller then redoes the leaf with IEEE division.
+// with one Markstein correction, which is RN(a/max) whenever the quotient
+// is normal (validated bitwise by lc_debug_div_check); else IEEE __ddiv_rn.
+// Why FAST needs no per-element guard: c = RN(RN(b1 m) + RN((1-b1) g)) of
+// fp32 m, g is a multiple of 2^-202 (each rounded product of an fp32 value
+// >= 2^-149 with a double has ulp >= 2^-202), so a nonzero a >= 2^-202 and
+// a/max is normal whenever max < 2^819 (k_l1_leaves checks the range; the
+// log map, whose a can be tiny, always takes IEEE division).
 template <int PK, bool FAST>
-__device__ __forceinline__ double term_div(double a, double b, double y, double thr, double p,
-                                           bool& bad) {
+__device__ __forceinline__ double term_div(double a, double b, double y, double p) {
   if (PK == PK_0) return a > 0.0 ? log(a) : 0.0;
   double t;
   if (FAST) {
     const double q = __dmul_rn(a, y);
     t = __fma_rn(__fma_rn(-q, b, a), y, q);
-    bad |= (a < thr) & (a > 0.0);
   } else {
     t = __ddiv_rn(a, b);
   }
@@ -431,11 +432,11 @@ template <bool MASK, int PK, bool LOG, bool FAST>
 __device__ __forceinline__ double leaf_sum(const float* __restrict__ g, const float* __restrict__ m,
                                            const uint8_t* __restrict__ mask, const Hyp& h,
                                            int64_t e0, int sz, int k, unsigned gm, double b,
-                                           double y, double thr, double sv, double p, bool& bad) {
+                                           double y, double sv, double p) {
   auto one = [&](int64_t e) {
     double c = lc::lion_c(m[e], g[e], h);
     if (MASK && !mask[e]) c = 0.0;
-    return term_div<PK, FAST>(abs_y<LOG>(c, sv), b, y, thr, p, bad);
+    return term_div<PK, FAST>(abs_y<LOG>(c, sv), b, y, p);
   };
   double res = 0.0;
   if (sz < 8) {  // only a whole tiny layer: sequential from 0
@@ -454,7 +455,7 @@ __device__ __forceinline__ double leaf_sum(const float* __restrict__ g, const fl
       const int64_t e = e0 + 8 * i + k;
       double c = lc::lion_c(__ldcs(m + e), __ldcs(g + e), h);
       if (MASK && !mask[e]) c = 0.0;
-      const double v = term_div<PK, FAST>(abs_y<LOG>(c, sv), b, y, thr, p, bad);
+      const double v = term_div<PK, FAST>(abs_y<LOG>(c, sv), b, y, p);
       r = i == 0 ? v : __dadd_rn(r, v);
     }
   }
@@ -467,17 +468,15 @@ __device__ __forceinline__ double leaf_sum(const float* __restrict__ g, const fl
   return res;
 }
 
-// The rare general case (log map, extreme max, possibly subnormal
-// quotients) out of line, so the IEEE division does not weigh on the fast
-// path's registers.
+// The rare general case (log map, extreme max) out of line, so the IEEE
+// division does not weigh on the fast path's registers.
 template <bool MASK, int PK, bool LOG>
 __device__ __noinline__ double leaf_sum_ieee(const float* __restrict__ g,
                                              const float* __restrict__ m,
                                              const uint8_t* __restrict__ mask, Hyp h, int64_t e0,
                                              int sz, int k, unsigned gm, double b, double sv,
                                              double p) {
-  bool unused = false;
-  return leaf_sum<MASK, PK, LOG, false>(g, m, mask, h, e0, sz, k, gm, b, 0.0, 0.0, sv, p, unused);
+  return leaf_sum<MASK, PK, LOG, false>(g, m, mask, h, e0, sz, k, gm, b, 0.0, sv, p);
 }
 
 #ifndef LC_L1_LEAF_MINB
@@ -506,17 +505,14 @@ k_l1_leaves(const float* __restrict__ g, const float* __restrict__ m,
       continue;
     }
     const double sv = LOG ? logs[seg] : 0.0;
-    // reciprocal division unless max is extreme or the log map is on; a
-    // leaf with a possibly subnormal quotient is redone with IEEE division
-    const bool fast = !LOG && mx >= 1e-300 && mx < 1e300;
+    // reciprocal division unless max is extreme or the log map is on
+    // (term_div); p = 0 divides nothing
+    const bool fast = PK == PK_0 || (!LOG && mx >= 0x1p-1000 && mx < 0x1p819);
     double res;
-    bool bad = !fast;
-    if (fast) {
-      const double y = __drcp_rn(mx);
-      res = leaf_sum<MASK, PK, LOG, true>(g, m, mask, h, e0, sz, k, gm, mx, y,
-                                          __dmul_rn(mx, 0x1.0p-1021), sv, p, bad);
-    }
-    if (__any_sync(gm, bad))
+    if (fast)
+      res = leaf_sum<MASK, PK, LOG, true>(g, m, mask, h, e0, sz, k, gm, mx,
+                                          PK == PK_0 ? 0.0 : __drcp_rn(mx), sv, p);
+    else
       res = leaf_sum_ieee<MASK, PK, LOG>(g, m, mask, h, e0, sz, k, gm, mx, sv, p);
     if (k == 0) lf_sum[lf] = res;
   }

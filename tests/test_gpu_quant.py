@@ -150,3 +150,23 @@ def test_quantize_large_matches_oracle():
                dict(bits=5, norm_p=2.0, log_transform=True)):
         q = lc.quantize(torch.from_numpy(x).cuda(), lc.QuantSpec(**kw)).cpu().numpy()
         assert np.array_equal(q, O.quantize(x.astype(np.float64), O.Spec(**kw))), kw
+
+
+@pytest.mark.parametrize("p", [1.0, 2.0, 0.5])
+def test_norm_extreme_magnitudes_bit_exact(p):
+    """fp32 denormals next to values near FLT_MAX in one layer: the
+    reciprocal division's no-guard argument (csrc/l1norm.cu term_div) must
+    hold -- every quotient normal, every term correctly rounded."""
+    rng = np.random.default_rng(11)
+    n = 70_001
+    x = rng.standard_normal(n).astype(np.float32)
+    x[::7] = np.float32(1.4e-45) * rng.integers(1, 100, size=x[::7].size).astype(np.float32)
+    x[::11] *= np.float32(1e30)
+    x[5] = np.float32(3.0e38)
+    x[9] = np.float32(-1.4e-45)
+    x64 = x.astype(np.float64)
+    xt = torch.from_numpy(x).cuda()
+    assert lc.lp_mean_norm(xt, p) == O.lp_mean_norm(x64, p)
+    spec = lc.QuantSpec(bits=8, norm_p=p)
+    assert np.array_equal(lc.quantize(xt, spec).cpu().numpy(),
+                          O.quantize(x64, O.Spec(bits=8, norm_p=p)))
