@@ -658,20 +658,28 @@ struct ApplyArgs {
   int64_t blk_words;    // words per owner block (cw)
 };
 
+#ifndef LC_VOTE_SHARE
+#define LC_VOTE_SHARE 8  // 1/LC_VOTE_SHARE of the grid votes + pushes the owner block
+#endif
+
 template <int NP, bool NZ>
 __global__ void __launch_bounds__(256)
 k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_valid, int fill,
              int sum_mode, VoteOut out, uint32_t* __restrict__ flags, SyncD sy, ApplyArgs a) {
   griddep_wait();
   sync_wait(sy);
-  // ---- vote (same as k_vote_bits) ----
-  {
-    const int T = P >> 1;
-    const uint32_t fillmask = fill > 0 ? ~0u : 0u;
+  const int T = P >> 1;
+  const uint32_t fillmask = fill > 0 ? ~0u : 0u;
+  // ---- vote (same as k_vote_bits) by the first nvote CTAs; the others go
+  // straight to the theta update of this rank's own block, voting each
+  // super-tile's words in the warp (no wait), while the voters push the
+  // block to the peers over NVLink ----
+  const int nvote = max(1, (int)gridDim.x / LC_VOTE_SHARE);
+  if ((int)blockIdx.x < nvote) {
     uint32_t flag = 0;
     const int64_t nq = cw >> 2;
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq;
-         q += (int64_t)gridDim.x * blockDim.x) {
+         q += (int64_t)nvote * blockDim.x) {
       uint32_t pl[4][NP];
 #pragma unroll
       for (int w = 0; w < 4; ++w)
@@ -718,6 +726,30 @@ k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_val
     zw_ = ~0u;
     if (sidx >= nsup) return;
     const int j = (int)((sidx * 32) / a.blk_words);  // owner of this super-tile
+    if (j == sy.rank) {  // own block: vote this word from the P received rows
+      const int64_t wl = sidx * 32 + lane - (int64_t)j * a.blk_words;  // word in my block
+      uint32_t pl[NP];
+#pragma unroll
+      for (int pp = 0; pp < NP; ++pp) pl[pp] = 0u;
+      if (wl < cw) {
+        for (int r = 0; r < P; ++r) {
+          uint32_t carry = __ldcs(recv + (int64_t)r * cw + wl);
+#pragma unroll
+          for (int pp = 0; pp < NP; ++pp) {
+            const uint32_t t = pl[pp] & carry;
+            pl[pp] ^= carry;
+            carry = t;
+          }
+        }
+      }
+      const int64_t rem = n_valid - wl * 32;
+      const uint32_t vm = rem >= 32 ? ~0u : (rem <= 0 ? 0u : ((1u << rem) - 1u));
+      uint32_t v, nz, tie, fl = 0;
+      vote_word<NP>(pl, P, T, fillmask, vm, fill, sum_mode, v, nz, tie, fl);
+      sw_ = v;
+      if (NZ) zw_ = nz;
+      return;
+    }
     if (!((ready >> j) & 1u)) {
       if (lane == 0) {
         const unsigned long long t0 = globaltimer();
@@ -741,11 +773,21 @@ k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_val
       if (NZ) zw_ = __ldcv(a.nzb + w);
     }
   };
+  // start at this rank's own block (voted locally, no wait) and wrap: by
+  // the time the warps reach a remote block its owner's votes have landed
+  int64_t rot = (int64_t)sy.rank * a.blk_words / 32;  // blk_words % 32 == 0
+  if (rot >= nsup) rot = 0;
+  auto at = [&](int64_t i) {
+    if (i >= nsup) return nsup;  // past the end: fetch() returns nothing
+    const int64_t s = i + rot;
+    return s >= nsup ? s - nsup : s;
+  };
   uint32_t nxw, nxz;
-  fetch(gw, nxw, nxz);
-  for (int64_t sidx = gw; sidx < nsup; sidx += nw) {
+  fetch(at(gw), nxw, nxz);
+  for (int64_t i = gw; i < nsup; i += nw) {
+    const int64_t sidx = at(i);
     const uint32_t myw = nxw, myz = nxz;
-    fetch(sidx + nw, nxw, nxz);
+    fetch(at(i + nw), nxw, nxz);
 #pragma unroll 1
     for (int k0 = 0; k0 < 8; k0 += KU) {
       float4 tv[KU];
