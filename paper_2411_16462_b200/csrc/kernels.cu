@@ -463,6 +463,13 @@ k_fused_local(float* __restrict__ theta, float* __restrict__ m,
       }
       float mn[4], tn[4];
       uint32_t sbit[4], nzb[4], tb[4];
+      // the lane's 4 elements usually share one layer: one segment lookup
+      double qscale = 0.0;
+      bool quad_in = false;
+      if constexpr (MODE == LC_LOCAL_QUANT) {
+        qscale = cur.get(sq, e0);
+        quad_in = e0 + 3 < cur.hi;
+      }
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         double c = lion_c(me[k], ge[k], h);
@@ -470,7 +477,11 @@ k_fused_local(float* __restrict__ theta, float* __restrict__ m,
         mn[k] = lion_m(me[k], ge[k], h);
         double agg;  // the single-rank aggregate the vote signs
         if constexpr (MODE == LC_LOCAL_QUANT) {
-          agg = valid[k] ? (double)quant_l1(c, cur.get(sq, e0 + k), sq.qmax) : 1.0;
+          // one rank's vote is sign(q): rint(v) != 0 iff |v| > 0.5 (half-even),
+          // and clipping keeps the sign, so only v = scale*c is needed (a NaN
+          // v gives -1 like clip(rint(NaN)) = -qmax)
+          const double v = __dmul_rn(quad_in ? qscale : cur.get(sq, e0 + k), c);
+          agg = valid[k] ? (v > 0.5 ? 1.0 : (v >= -0.5 ? 0.0 : -1.0)) : 1.0;
         } else if constexpr (MODE == kLocalQuantX) {
           agg = valid[k] ? (double)quant_x(c, sq, cur, e0 + k) : 1.0;
         } else {
