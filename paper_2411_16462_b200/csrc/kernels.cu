@@ -144,13 +144,21 @@ __device__ __forceinline__ void encode4(const float ge[4], const float me[4], co
                                         uint32_t zflag, const SegQ& sq, CUR& cur,
                                         int64_t e0, double c[4], float mn[4], uint32_t st[4],
                                         uint32_t& flag) {
+  // the 4 elements usually share one layer: one segment lookup
+  double qscale = 0.0;
+  bool quad_in = false;
+  if constexpr (ENC == LC_ENC_QUANT_FIELDS) {
+    qscale = cur.get(sq, e0);
+    quad_in = e0 + 3 < cur.hi;
+  }
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     c[q] = lion_c(me[q], ge[q], h);
     if (MASK && !keep[q]) c[q] = 0.0;  // np.where(mask, c, 0.0)
     mn[q] = lion_m(me[q], ge[q], h);
     if constexpr (ENC == LC_ENC_QUANT_FIELDS) {
-      st[q] = valid[q] ? (uint32_t)(quant_l1(c[q], cur.get(sq, e0 + q), sq.qmax) + sq.qmax) : 0u;
+      const double sc = quad_in ? qscale : cur.get(sq, e0 + q);
+      st[q] = valid[q] ? (uint32_t)(quant_l1(c[q], sc, sq.qmax) + sq.qmax) : 0u;
     } else if constexpr (ENC == kEncQuantX) {
       st[q] = valid[q] ? (uint32_t)(quant_x(c[q], sq, cur, e0 + q) + sq.qmax) : 0u;
     } else if constexpr (ENC != LC_ENC_F64) {
