@@ -693,7 +693,10 @@ k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_val
   // straight to the theta update of this rank's own block, voting each
   // super-tile's words in the warp (no wait), while the voters push the
   // block to the peers over NVLink ----
-  const int nvote = max(1, (int)gridDim.x / LC_VOTE_SHARE);
+  // (measured: at P = 2 the whole grid voting first is faster for 1.1B
+  // params -- the pushed half is too large for a fraction of the SMs)
+  const int share = P >= 4 ? LC_VOTE_SHARE : 1;
+  const int nvote = max(1, (int)gridDim.x / share);
   if ((int)blockIdx.x < nvote) {
     uint32_t flag = 0;
     const int64_t nq = cw >> 2;
@@ -745,7 +748,7 @@ k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_val
     zw_ = ~0u;
     if (sidx >= nsup) return;
     const int j = (int)((sidx * 32) / a.blk_words);  // owner of this super-tile
-    if (j == sy.rank) {  // own block: vote this word from the P received rows
+    if (j == sy.rank && share > 1) {  // own block: vote this word from the P rows
       const int64_t wl = sidx * 32 + lane - (int64_t)j * a.blk_words;  // word in my block
       uint32_t pl[NP];
 #pragma unroll

@@ -12,7 +12,7 @@ run() {  # workload N extra-args...
       --master-port=$((29500 + n)) bench.py --gpus $n --workload "$w" "$@" \
       > gpurun_out/meas_${w}_n$n.json 2> gpurun_out/meas_${w}_n$n.err
   fi
-  echo "$w n=$n rc=$? $(tail -c 200 gpurun_out/meas_${w}_n$n.json | grep -o '"ms_per_step": [0-9.]*')"
+  echo "$w n=$n rc=$?"
 }
 run gpt2s_sumsigns 1
 for n in 2 4; do run gpt2s_sumsigns $n --no-cpu-baseline; done
@@ -20,4 +20,11 @@ for n in 1 2 4; do run tinyllama_1bit_sync $n --no-cpu-baseline --no-e2e; done
 for n in 1 2 4; do run gpt2s_l1_5bit $n --no-cpu-baseline --no-e2e; done
 for n in 1 4; do run gpt2s_qinf_stoch_5bit $n --no-cpu-baseline --no-e2e; done
 run c1_1bit_1m 1 --no-cpu-baseline
+run gpt2s_1bit_syncall 4 --no-cpu-baseline --no-e2e
 for n in 2 4; do run gpt2s_ps $n --no-cpu-baseline --no-e2e; done
+# reference arm (CPU port) on the default workload
+timeout 600 python bench.py --impl reference > gpurun_out/meas_reference_n1.json 2> gpurun_out/meas_reference_n1.err
+# kernel launch list of the default bench and ncu of the norm pass
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/launches_default.csv 2>/dev/null
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum --clock-control none -k regex:k_l1 --csv python tests/profile_kernels.py --n 1048576 --reps 1 > gpurun_out/ncu_l1_final.csv 2>/dev/null
+echo done
