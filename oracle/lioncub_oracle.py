@@ -143,23 +143,27 @@ def lp_mean_norm(x, p: float) -> float:
     return float(m * np.mean((a / m) ** p) ** (1.0 / p))
 
 
-_GOLDEN = 0x9E3779B97F4A7C15
-
-
-def splitmix_uniforms(seed: int, index) -> np.ndarray:
+def stream_uniforms(seed: int, index) -> np.ndarray:
     """The CUDA path's stochastic-rounding stream (csrc/common.cuh
-    ``lc::uniform01``): element e draws u = (splitmix64(seed + (e+1)*golden)
-    >> 12) * 2**-52, a counter-based stream (no sequential state, so any
-    element range of any rank can be drawn independently).  The reference
-    draws from numpy's PCG64 (quant.py:107-116); parity of stochastic
-    rounding with the reference is statistical, with this stream exact."""
+    ``lc::uniform01``): element e draws u = x * 2**-32 with x =
+    lowbias32(lo32(e)*0x9E3779B9 + lo32(seed) ^ hi32(e)*0x85EBCA6B ^
+    hi32(seed)) in wrapping uint32 arithmetic, a counter-based stream (no
+    sequential state, so any element range of any rank can be drawn
+    independently).  The reference draws from numpy's PCG64
+    (quant.py:107-116); parity of stochastic rounding with the reference is
+    statistical, with this stream exact."""
     e = np.asarray(index, dtype=np.uint64)
+    s = int(seed) & 0xFFFFFFFFFFFFFFFF
+    u32 = np.uint32
     with np.errstate(over="ignore"):
-        z = np.uint64(seed & 0xFFFFFFFFFFFFFFFF) + (e + np.uint64(1)) * np.uint64(_GOLDEN)
-        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
-        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
-        z = z ^ (z >> np.uint64(31))
-    return (z >> np.uint64(12)).astype(np.float64) * (2.0 ** -52)
+        x = (e & np.uint64(0xFFFFFFFF)).astype(u32) * u32(0x9E3779B9) + u32(s & 0xFFFFFFFF)
+        x ^= (e >> np.uint64(32)).astype(u32) * u32(0x85EBCA6B) ^ u32(s >> 32)
+        x ^= x >> u32(16)
+        x *= u32(0x7FEB352D)
+        x ^= x >> u32(15)
+        x *= u32(0x846CA68B)
+        x ^= x >> u32(16)
+    return x.astype(np.float64) * (2.0 ** -32)
 
 
 def sround(v, u) -> np.ndarray:
@@ -479,7 +483,7 @@ def distributed_step(thetas: Sequence[Mapping[str, np.ndarray]],
         uni = None
         if seeds is not None:
             idx = offset + np.arange(flat[0].size)
-            uni = [splitmix_uniforms(seeds[r], idx) for r in range(p)]
+            uni = [stream_uniforms(seeds[r], idx) for r in range(p)]
         offset += flat[0].size
         sign, vote = _vote_layer(flat, spec, algo, zero_mode, t, uniforms=uni)
         sign = np.asarray(sign).reshape(cs[0].shape)

@@ -79,17 +79,25 @@ __device__ __forceinline__ float lion_theta(float th, double s, double lr,
 }
 
 // Stochastic-rounding stream: element e of a rank's flat buffer draws
-// u = (splitmix64(seed + (e+1) * golden) >> 12) * 2^-52 in [0, 1) -- a
-// counter-based generator (no per-thread state; any element range can be
-// drawn independently).  The 52 bits become the mantissa of a double in
-// [1, 2) minus 1 (exact; no int->double conversion).
-// oracle/lioncub_oracle.py splitmix_uniforms restates it.
+// u = x * 2^-32 in [0, 1), x = lowbias32(lo32(e) * 0x9E3779B9 + lo32(seed)
+// ^ hi32(e) * 0x85EBCA6B ^ hi32(seed)) -- a counter-based generator (no
+// per-thread state; any element range can be drawn independently) in 32-bit
+// integer ops only: the splitmix64 stream it replaces spent ~35 issue slots
+// per element on 64-bit multiplies and left the stochastic step issue-bound.
+// For a fixed seed and hi32(e) the map lo32(e) -> x is a bijection, so no
+// two of 2^32 consecutive elements share a draw; the 32-bit resolution
+// biases E[round] by < 2^-32.  u is built exactly as the mantissa of a
+// double in [1, 2) minus 1.  oracle/lioncub_oracle.py stream_uniforms
+// restates it.
 __device__ __forceinline__ double uniform01(uint64_t seed, int64_t e) {
-  uint64_t z = seed + (uint64_t)(e + 1) * 0x9E3779B97F4A7C15ull;
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-  z ^= z >> 31;
-  return __longlong_as_double((long long)((z >> 12) | 0x3FF0000000000000ull)) - 1.0;
+  uint32_t x = (uint32_t)e * 0x9E3779B9u + (uint32_t)seed;
+  x ^= (uint32_t)((uint64_t)e >> 32) * 0x85EBCA6Bu ^ (uint32_t)(seed >> 32);
+  x ^= x >> 16;
+  x *= 0x7FEB352Du;
+  x ^= x >> 15;
+  x *= 0x846CA68Bu;
+  x ^= x >> 16;
+  return __hiloint2double((int)(0x3FF00000u | (x >> 12)), (int)(x << 20)) - 1.0;
 }
 
 __device__ __forceinline__ float4 ld_stream(const float4* p) {

@@ -133,7 +133,7 @@ def test_stochastic_quantize_matches_oracle_stream(p):
     spec = lc.QuantSpec(bits=4, norm_p=p, rounding="stochastic")
     seed = lc.QuantSpec(rounding="stochastic").draw_seed(np.random.default_rng(17))
     q = lc.quantize(torch.from_numpy(x).cuda(), spec, rng=np.random.default_rng(17))
-    u = O.splitmix_uniforms(seed, np.arange(x.size))
+    u = O.stream_uniforms(seed, np.arange(x.size))
     ref = O.quantize(x.astype(np.float64), O.Spec(bits=4, norm_p=p, rounding="stochastic"), u)
     assert np.array_equal(q.cpu().numpy(), ref)
     with pytest.raises(lc.ConfigError, match="rng"):

@@ -206,13 +206,13 @@ def test_oracle_apply_sign_and_pack_match_reference():
             np.array([off], "<i4").tobytes()
 
 
-def test_splitmix_stream_is_uniform_and_sround_unbiased():
-    u = O.splitmix_uniforms(12345, np.arange(1 << 20))
+def test_counter_stream_is_uniform_and_sround_unbiased():
+    u = O.stream_uniforms(12345, np.arange(1 << 20))
     assert u.min() >= 0.0 and u.max() < 1.0
     assert abs(u.mean() - 0.5) < 2e-3 and abs(u.var() - 1 / 12) < 2e-3
     # different seeds / offsets give different streams
-    assert not np.array_equal(u[:100], O.splitmix_uniforms(12346, np.arange(100)))
-    assert np.array_equal(u[50:60], O.splitmix_uniforms(12345, np.arange(50, 60)))
+    assert not np.array_equal(u[:100], O.stream_uniforms(12346, np.arange(100)))
+    assert np.array_equal(u[50:60], O.stream_uniforms(12345, np.arange(50, 60)))
     v = np.full(u.size, 2.3)
     q = O.sround(v, u)
     assert set(np.unique(q)) == {2, 3}
