@@ -253,25 +253,40 @@ struct SegCursorX {
 // floor(v) + (u < v - floor(v)), clip to +-qmax, then no_zero: a zero q of
 // a nonzero c becomes sign(c).  e: element index of the rank's flat buffer
 // (the stochastic stream position).
-__device__ __forceinline__ int quant_x(double c, const SegQ& sq, SegCursorX& cur, int64_t e) {
-  cur.at(sq, e);
+__device__ __forceinline__ double round_x(double c, double scale, double logs, const SegQ& sq,
+                                          int64_t e) {
   double y = c;
-  if (cur.logs > 0.0) {
-    const double l = log1p(__ddiv_rn(fabs(c), cur.logs));
+  if (logs > 0.0) {
+    const double l = log1p(__ddiv_rn(fabs(c), logs));
     y = c > 0.0 ? l : (c < 0.0 ? -l : 0.0);
   }
-  const double v = __dmul_rn(cur.scale, y);
-  double r;
+  const double v = __dmul_rn(scale, y);
   if (sq.qflags & LC_Q_STOCHASTIC) {
     const double lo = floor(v);
-    r = lo + (uniform01(sq.seed, e) < __dsub_rn(v, lo) ? 1.0 : 0.0);
-  } else {
-    r = rint(v);
+    return lo + (uniform01(sq.seed, e) < __dsub_rn(v, lo) ? 1.0 : 0.0);
   }
+  return rint(v);
+}
+
+__device__ __forceinline__ int quant_x(double c, const SegQ& sq, SegCursorX& cur, int64_t e) {
+  cur.at(sq, e);
+  double r = round_x(c, cur.scale, cur.logs, sq, e);
   r = fmin(fmax(r, -(double)sq.qmax), (double)sq.qmax);
   int q = (int)r;
   if ((sq.qflags & LC_Q_NO_ZERO) && q == 0 && c != 0.0) q = c > 0.0 ? 1 : -1;
   return q;
+}
+
+// sign(quant_x(c)) as +-1.0 / 0.0 without the int round trip (a single
+// rank votes on sign(q)): the clip keeps the sign of r (qmax >= 1), rounds
+// -0.0 to zero, and fmin/fmax map a NaN r to +qmax.
+__device__ __forceinline__ double quant_x_sign(double c, double scale, double logs,
+                                               const SegQ& sq, int64_t e) {
+  const double r = round_x(c, scale, logs, sq, e);
+  if (r > 0.0 || r != r) return 1.0;
+  if (r < 0.0) return -1.0;
+  if ((sq.qflags & LC_Q_NO_ZERO) && c != 0.0) return c > 0.0 ? 1.0 : -1.0;
+  return 0.0;
 }
 
 }  // namespace lc

@@ -474,7 +474,7 @@ k_fused_local(float* __restrict__ theta, float* __restrict__ m,
       // the lane's 4 elements usually share one layer: one segment lookup
       double qscale = 0.0;
       bool quad_in = false;
-      if constexpr (MODE == LC_LOCAL_QUANT) {
+      if constexpr (MODE == LC_LOCAL_QUANT || MODE == kLocalQuantX) {
         qscale = cur.get(sq, e0);
         quad_in = e0 + 3 < cur.hi;
       }
@@ -491,7 +491,11 @@ k_fused_local(float* __restrict__ theta, float* __restrict__ m,
           const double v = __dmul_rn(quad_in ? qscale : cur.get(sq, e0 + k), c);
           agg = valid[k] ? (v > 0.5 ? 1.0 : (v >= -0.5 ? 0.0 : -1.0)) : 1.0;
         } else if constexpr (MODE == kLocalQuantX) {
-          agg = valid[k] ? (double)quant_x(c, sq, cur, e0 + k) : 1.0;
+          agg = 1.0;
+          if (valid[k]) {
+            if (!quad_in) cur.at(sq, e0 + k);
+            agg = quant_x_sign(c, cur.scale, cur.logs, sq, e0 + k);
+          }
         } else {
           agg = c;
         }
