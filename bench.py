@@ -8,12 +8,20 @@ is one ``distributed_lion_step`` (+ ``maybe_sync_momentum`` where the
 workload syncs) over the workload's full synthetic parameter buffer, inputs
 resident in HBM.  Rank 0 prints ONE JSON line.
 
-Default workload = BASELINE.json configs[1]: the GPT-2-small-sized buffer
-(124,439,808 params in its 148 tensors) with the p-bit sum-of-signs vote
-(algo="direct", QuantSpec(bits=1)).  Every array (498 MB each) is larger
-than the 126 MB L2, so no L2 flush is needed between steps.  Workloads whose
-12 B/param working set is under 2x L2 (c1_1bit_1m) flush L2 before every
-step and time each step alone with its own event pair.
+Default workload = BASELINE.json configs[4], the largest configuration that
+fits one B200: a 7e9-parameter flat buffer, Lion Cub full step (1-bit
+majority vote + all-layer momentum sync every step; the sync is a no-op at
+one rank).  theta/m/g are 28 GB each (84 GB resident).  ``--workload
+tinyllama_1bit_sync`` is the north-star line (configs[3]), ``gpt2s_sumsigns``
+configs[1].  Every array of those workloads is larger than the 126 MB L2, so
+no L2 flush is needed between steps; workloads whose 12 B/param working set
+is under 2x L2 (c1_1bit_1m) flush L2 before every step and time each step
+alone with its own event pair.
+
+Reference arm (``--impl reference``): the UNMODIFIED reference ``lioncomm``
+(installed once into baseline/_ref with pip) through its own
+``run_ranks(P, fn, transport=InprocTransport(P))`` on the host cores, on a
+bounded per-rank sample of the workload, extrapolated linearly in params.
 """
 
 from __future__ import annotations
@@ -164,10 +172,12 @@ def step_roofline(n: int, P: int, F: int, kind: str, sync_frac: float,
     t_h = hbm / (hbm_gbs * 1e9)
     t_n = nvl / (nvl_gbs * 1e9)
     return {"hbm_bytes": hbm, "nvlink_bytes": nvl, "t_hbm_ms": t_h * 1e3,
-            "t_nvlink_ms": t_n * 1e3, "bound": "hbm" if t_h >= t_n else "nvlink"}
+            "t_nvlink_ms": t_n * 1e3, "t_nvlink_ms_at_900": nvl / 900e9 * 1e3,
+            "bound": "hbm" if t_h >= t_n else "nvlink"}
 
 
-NVL_GBS = 770.0   # NVLink 5 per direction, B200_PROFILING.md
+NVL_GBS = 770.0   # NVLink 5 per direction, measured peak in B200_PROFILING.md
+NVL_NOMINAL_GBS = 900.0  # north_star: 900 GB/s per direction
 
 
 def measured_peaks() -> tuple[dict, str]:
@@ -307,29 +317,162 @@ class CpuReference:
                 "cores": self.cores, "kind": "port", "sample": self.describe()}
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def load_lioncomm():
+    """The unmodified reference package, pip-installed into baseline/_ref
+    (`pip install --no-index --target baseline/_ref`), or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "lioncomm")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import lioncomm
+    return lioncomm
+
+
+class LioncommReference:
+    """The reference's own CPU path, unmodified: ``lioncomm``'s
+    ``distributed_lion_step`` (+ ``maybe_sync_momentum`` where the workload
+    syncs) on P rank threads sharing one ``InprocTransport`` through
+    ``run_ranks`` (collectives.py:363-403), on a ``sample``-param flat buffer
+    per rank.  Inputs follow BASELINE.md §2: fp32-generated, upcast to f64,
+    correlated workers (shared Laplace base + Laplace noise, runner.py:289-297),
+    seeds SeedSequence([0, rank]).  A workload that syncs a subset of its
+    layers keeps that fraction as a second layer of the sample.  Step time =
+    max over ranks of each rank's wall time for that step."""
+
+    def __init__(self, world: int, algo: str, bits, sync, frac_synced: float, sample: int):
+        import numpy as np
+        lcm = load_lioncomm()
+        if lcm is None:
+            raise RuntimeError("baseline/_ref has no lioncomm install")
+        from lioncomm import collectives as CC
+        from lioncomm import optimizer as O
+        from lioncomm import quant as Q
+        from lioncomm import transport as T
+        self.O, self.CC, self.T = O, CC, T
+        self.world, self.algo, self.bits, self.sample = world, algo, bits, sample
+        self.cores = world  # one numpy rank thread each (elementwise numpy is single-threaded)
+        kw = quant_kwargs(bits)
+        self.spec = None if kw is None else Q.QuantSpec(**kw)
+        self.policy = None
+        names = {"w": sample}
+        if sync is not None:
+            period, layers = sync
+            if layers == "all":
+                self.policy = O.SyncPolicy(period=period, layers="all")
+            else:
+                ns = max(1, int(round(frac_synced * sample)))
+                names = {"a_synced": ns, "w": sample - ns}
+                self.policy = O.SyncPolicy(period=period, layers=frozenset({"a_synced"}))
+        g0 = np.random.default_rng(np.random.SeedSequence([0]))
+        theta = {k: g0.standard_normal(c, dtype=np.float32).astype(np.float64)
+                 for k, c in names.items()}
+        base = {k: g0.laplace(0.0, 1.0, c).astype(np.float32) for k, c in names.items()}
+        self.states, self.grads = [], []
+        for r in range(world):
+            gr = np.random.default_rng(np.random.SeedSequence([0, r]))
+            mom = {k: (0.1 * gr.standard_normal(c, dtype=np.float32)).astype(np.float64)
+                   for k, c in names.items()}
+            grad = {k: (base[k] + gr.laplace(0.0, 1.0, c).astype(np.float32)).astype(np.float64)
+                    for k, c in names.items()}
+            self.states.append(O.WorkerState(params={k: v.copy() for k, v in theta.items()},
+                                             momentum=mom, iteration=0))
+            self.grads.append(grad)
+        self.rngs = [np.random.default_rng(100 + r) for r in range(world)]
+
+    def run(self, steps: int) -> list:
+        """``steps`` reference steps on every rank thread; per-step time =
+        max over ranks (seconds)."""
+        O, CC, T = self.O, self.CC, self.T
+        per_rank = [None] * self.world
+
+        def fn(topo):
+            r = topo.rank
+            st, times = self.states[r], []
+            for _ in range(steps):
+                t0 = time.perf_counter()
+                st = O.distributed_lion_step(st, self.grads[r], self.h_ref(), self.spec, topo,
+                                             self.algo, rng=self.rngs[r])
+                if self.policy is not None:
+                    st = O.maybe_sync_momentum(st, self.policy, topo)
+                times.append(time.perf_counter() - t0)
+            self.states[r] = st
+            per_rank[r] = times
+            return None
+
+        CC.run_ranks(self.world, fn, transport=T.InprocTransport(self.world), timeout=600.0)
+        return [max(per_rank[r][i] for r in range(self.world)) for i in range(steps)]
+
+    def h_ref(self):
+        return self.O.LionHyper(beta1=0.9, beta2=0.99, lr=1e-4, weight_decay=0.0)
+
+    def describe(self) -> str:
+        b = "" if self.bits is None else f", bits={self.bits}"
+        sy = "" if self.policy is None else \
+            f" + maybe_sync_momentum(period={self.policy.period})"
+        return (f"unmodified lioncomm (baseline/_ref) distributed_lion_step({self.algo}{b}){sy} "
+                f"via run_ranks({self.world}, InprocTransport) on a {self.sample}-param flat "
+                f"sample per rank, float64 numpy, {self.world} rank thread(s)")
+
+    def timed(self, budget_s: float) -> dict:
+        self.run(1)
+        times = []
+        t_end = time.perf_counter() + budget_s
+        while not times or time.perf_counter() < t_end or len(times) < 3:
+            times += self.run(1)
+        t = min(times)  # best of the budget (BASELINE.md §2: best of 3)
+        return {"value": self.world * self.sample / t, "unit": "params/s",
+                "cores": self.cores, "kind": "reference", "sample": self.describe(),
+                "ms_per_step_sample": t * 1e3, "extrapolated": True,
+                "extrapolation": "linear in params: params/s of the sample applied to the "
+                                 "workload (the reference needs ~77 B/param/rank of host RAM)"}
+
+
+def sync_fraction(shapes: dict, sync) -> float:
+    """Fraction of the params a firing sync averages (per firing step)."""
+    if sync is None:
+        return 0.0
+    _, layers = sync
+    n = numel(shapes)
+    return 1.0 if layers == "all" else sum(math.prod(shapes[k]) for k in layers) / n
+
+
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     layout_fn, algo, bits, sync, desc = WORKLOADS[args.workload]
-    n = numel(layout_fn())
+    shapes = layout_fn()
+    n = numel(shapes)
     world = args.gpus
     sample = min(n, args.ref_sample)
-    ref = CpuReference(world, algo, bits, sample)
-    for _ in range(args.warmup):
-        ref.step()
-    timed = [ref.step() for _ in range(args.steps)]
+    cfg = {"workload": args.workload, "description": desc, "params": n, "algo": algo,
+           "bits": bits, "world": world, "sample_params_per_rank": sample,
+           "same_config": False,
+           "extrapolation": f"params/s measured on a {sample}-param per-rank sample, "
+                            "applied linearly to the workload's params"}
+    if load_lioncomm() is not None:
+        ref = LioncommReference(world, algo, bits, sync, sync_fraction(shapes, sync), sample)
+        ref.run(args.warmup)
+        timed = ref.run(args.steps)
+        kind, cores, descr = "reference", ref.cores, ref.describe()
+    else:  # no pip install in baseline/_ref: the oracle port (labelled)
+        ref = CpuReference(world, algo, bits, sample)
+        for _ in range(args.warmup):
+            ref.step()
+        timed = [ref.step() for _ in range(args.steps)]
+        kind, cores, descr = "port", ref.cores, ref.describe()
     t = sum(timed) / len(timed)
     value = world * sample / t
     line = {"metric": METRIC, "value": value, "unit": "params/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+            "ms_per_step_extrapolated": world * n / value * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": args.workload, "description": desc, "params": n,
-                       "algo": algo, "bits": bits, "world": world,
-                       "sample_params_per_rank": sample},
-            "cpu_baseline": {"value": value, "unit": "params/s", "cores": ref.cores,
-                             "kind": "port", "sample": ref.describe()},
+            "dtype": "f64", "data": "synthetic", "impl": "reference", "config": cfg,
+            "cpu_baseline": {"value": value, "unit": "params/s", "cores": cores,
+                             "kind": kind, "sample": descr},
             "e2e": {"value": value, "unit": "params/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -352,12 +495,14 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="gpt2s_sumsigns", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="flat7b_1bit_sync", choices=sorted(WORKLOADS))
     ap.add_argument("--ref-sample", type=int, default=1 << 22)
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-chunk", type=int, default=1 << 23)
+    ap.add_argument("--e2e-steps", type=int, default=0,
+                    help="timed e2e steps (0: --steps, capped at 5 above 1e9 params)")
     ap.add_argument("--graph", action="store_true",
                     help="replay the single-GPU step as a CUDA graph (launch-bound sizes)")
     args = ap.parse_args()
@@ -405,24 +550,35 @@ def main():
         period, layers = sync
         policy = lc.SyncPolicy(period=period, layers=layers if isinstance(layers, str)
                                else frozenset(layers))
-        sel = n if layers == "all" else sum(math.prod(shapes[k]) for k in layers)
-        sync_frac = sel / n / period
+        sync_frac = sync_fraction(shapes, sync) / period
     h = lc.LionHyper(beta1=0.9, beta2=0.99, lr=1e-4, weight_decay=0.0)
 
-    # synthetic state: theta shared (seed 0), m and g per rank; g = base + noise
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(0)
+    # synthetic state: theta shared (seed 0), m and g per rank; g = base +
+    # noise (Laplace-correlated workers, runner.py:289-297).  Generated in
+    # 2^27-element chunks so a 7e9 buffer never needs more than its own
+    # 3 x 28 GB plus one chunk of temporaries.
     layout = lc.Layout(shapes)
     theta = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
-    theta.normal_(generator=gen)
-    base = torch.empty_like(theta).exponential_(generator=gen)
-    base *= torch.where(torch.rand(theta.shape, generator=gen, device=dev) < 0.5, -1.0, 1.0)
-    gen.manual_seed(1000 + rank)
-    mom = torch.empty_like(theta).normal_(generator=gen).mul_(0.1)
-    noise = torch.empty_like(theta).exponential_(generator=gen)
-    noise *= torch.where(torch.rand(theta.shape, generator=gen, device=dev) < 0.5, -1.0, 1.0)
-    grad = base.add_(noise)
-    del noise
+    mom = torch.empty_like(theta)
+    grad = torch.empty_like(theta)
+    gen = torch.Generator(device=dev)
+    CH = 1 << 27
+
+    def laplace(out, g_):
+        out.exponential_(generator=g_)
+        out.mul_(torch.where(torch.rand(out.shape, generator=g_, device=dev) < 0.5, -1.0, 1.0))
+
+    for ci, a in enumerate(range(0, max(n, 1), CH)):
+        b = min(max(n, 1), a + CH)
+        gen.manual_seed(ci * 2 + 1)               # shared across ranks
+        theta[a:b].normal_(generator=gen)
+        laplace(grad[a:b], gen)                    # the shared base
+        gen.manual_seed(1_000_003 * (rank + 1) + ci * 2)
+        mom[a:b].normal_(generator=gen).mul_(0.1)
+        noise = torch.empty(b - a, dtype=torch.float32, device=dev)
+        laplace(noise, gen)
+        grad[a:b].add_(noise)
+        del noise
     st = lc.WorkerState(params=layout.views(theta), momentum=layout.views(mom), iteration=0)
     del mom  # the state owns it (a P2P sync may re-home it; do not pin the old buffer)
     g = layout.views(grad)
@@ -511,7 +667,7 @@ def main():
     w0 = time.perf_counter()
     ms, host_ms, launches, _ = timed_pass(False)
     w1 = time.perf_counter()
-    _, _, _, phases = timed_pass(True)
+    ms_kpass, _, _, phases = timed_pass(True)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -549,9 +705,13 @@ def main():
     if dominant:
         bpl = kernel_bytes(dominant, n, P, F, kind, norm_bytes(bits))
         ach = bpl / (kern[dominant]["avg_ms"] * 1e-3) / 1e9
-        tt = traffic_table().get(f"{args.workload}/P{P}/{dominant}")
+        ttab = traffic_table()
+        tt = ttab.get(f"{args.workload}/P{P}/{dominant}")
         roof = {"kernel": dominant, "bound": "hbm", "achieved": ach, "peak": hbm_peak,
                 "unit": "GB/s", "frac": ach / hbm_peak, "traffic": tt,
+                "traffic_source": None if tt is None else
+                ttab.get("_sources", {}).get(f"{args.workload}/P{P}/{dominant}",
+                                             "profiles/traffic.json"),
                 "algorithmic_bytes_per_launch": bpl,
                 "avg_launch_ms": kern[dominant]["avg_ms"],
                 "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs" if peak_src ==
@@ -564,6 +724,7 @@ def main():
                 1, kern[dominant]["launches"])
             ach = per_launch / (kern[dominant]["avg_ms"] * 1e-3) / 1e9
             roof.update({"bound": "nvlink", "achieved": ach, "peak": NVL_GBS, "frac": ach / NVL_GBS,
+                         "frac_of_nominal_900": ach / NVL_NOMINAL_GBS,
                          "algorithmic_bytes_per_launch": per_launch,
                          "peak_source": "B200_PROFILING.md NVLink per direction"})
     sr = step_roofline(n, P, F, kind, sync_frac, hbm_peak, nb=norm_bytes(bits))
@@ -575,8 +736,9 @@ def main():
     e2e = None
     if not args.no_e2e:
         host_g = torch.empty(n, dtype=torch.float32, pin_memory=True)
-        host_g.copy_(grad[:n].cpu())
+        host_g.copy_(grad[:n])
         host_t = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        e2e_steps = args.e2e_steps or (min(args.steps, 5) if n > 1_000_000_000 else args.steps)
 
         def step_host(state):
             state = lc.distributed_lion_step_host(state, host_g, h, spec, topo, algo,
@@ -592,23 +754,34 @@ def main():
         f0 = torch.cuda.Event(enable_timing=True)
         f1 = torch.cuda.Event(enable_timing=True)
         f0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(e2e_steps):
             st = step_host(st)
         f1.record(stream)
         barrier()
-        ems = f0.elapsed_time(f1) / args.steps
+        ems = f0.elapsed_time(f1) / e2e_steps
         if world > 1:
             t = torch.tensor([ems], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
         e2e = {"value": P * n / (ems * 1e-3), "unit": "params/s", "ms_per_step": ems,
                "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n,
+               "steps": e2e_steps,
                "path": "distributed_lion_step_host: pinned host grads -> step -> pinned "
-                       f"host params, {args.e2e_chunk}-element chunks pipelined"}
+                       f"host params, {args.e2e_chunk}-element chunks pipelined",
+               "host_state": "g in and theta out every step (8 B/param over PCIe); the "
+                             "momentum stays resident on the device like a torch.optim "
+                             "state -- the reference API passes the whole f64 state "
+                             "(theta, m in and out) through host memory"}
 
-    cpu = None
+    cpu = cpu_port = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = CpuReference(1, algo, bits, min(n, args.ref_sample)).timed(args.cpu_budget)
+        sample = min(n, args.ref_sample)
+        if load_lioncomm() is not None:
+            cpu = LioncommReference(1, algo, bits, sync, sync_fraction(shapes, sync),
+                                    sample).timed(args.cpu_budget)
+        cpu_port = CpuReference(1, algo, bits, sample).timed(args.cpu_budget)
+        if cpu is None:
+            cpu = cpu_port
 
     if rank == 0:
         line = {"metric": METRIC, "value": P * n / (ms * 1e-3), "unit": "params/s",
@@ -626,6 +799,7 @@ def main():
                                   else "L2 flushed (252 MB write) before every timed step; "
                                        "steps timed individually, flush excluded")},
                 "roofline": roof, "step_roofline": sr, "kernels": kern,
+                "ms_per_step_kernel_pass": ms_kpass,
                 # the exchange is fused into the kernels (peer-memory stores /
                 # loads), so its rate is reported over the whole step: the
                 # algorithmic NVLink bytes each rank moves per direction per
@@ -634,8 +808,11 @@ def main():
                     "bytes_per_rank_per_direction": sr["nvlink_bytes"],
                     "achieved_gbs_over_step": sr["nvlink_bytes"] / (ms * 1e-3) / 1e9,
                     "peak_gbs": NVL_GBS,
-                    "frac_of_peak": sr["nvlink_bytes"] / (ms * 1e-3) / 1e9 / NVL_GBS},
-                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                    "frac_of_peak": sr["nvlink_bytes"] / (ms * 1e-3) / 1e9 / NVL_GBS,
+                    "peak_gbs_nominal": NVL_NOMINAL_GBS,
+                    "frac_of_nominal": sr["nvlink_bytes"] / (ms * 1e-3) / 1e9 / NVL_NOMINAL_GBS},
+                "cpu_baseline": cpu, "cpu_baseline_port": cpu_port,
+                "e2e": e2e, "gpu_launches": launches,
                 "host_enqueue_ms_per_step": host_ms,
                 "clocks": clocks}
         print(json.dumps(line))

@@ -76,7 +76,11 @@ typedef struct lc_sync {
   void* peer_flags[32]; /* rank j's uint64[P] flag array, mapped here     */
   uint64_t* my_flags;   /* this rank's flag array                          */
   uint32_t* counter;    /* zeroed device word, one per arrive site         */
-  uint32_t* err;
+  uint32_t* err;        /* 2 device words: [0] LC_FLAG_* bits, [1] bitmask
+                           of the ranks a wait timed out on.  A kernel whose
+                           wait times out writes nothing (theta, m and the
+                           peers' buffers keep their values) and its arrival
+                           publishes no epoch, so every live rank fails.   */
   uint64_t wait_epoch;
   uint64_t arrive_epoch;
   int32_t P, rank;
@@ -110,6 +114,12 @@ typedef struct lc_segments {
 int lc_abi_version(void);
 const char* lc_last_error(void);
 int lc_device_sm_count(int device);
+/* Share the GPU among `divisor` ranks that launch concurrently from separate
+ * host threads onto one device (simulated ranks of the peer-memory exchange,
+ * transport.LocalTransport(fused=True)): every grid this host thread sizes
+ * from the SM count uses SMs/divisor, so all ranks' barrier-waiting kernels
+ * are co-resident.  Thread-local; 1 (the default) = the whole GPU. */
+int lc_set_grid_divisor(int divisor);
 
 /* Maximum entries of a destination / peer table (blocks of a packed vector). */
 #define LC_MAX_BLOCKS 64
@@ -370,8 +380,9 @@ int lc_sym_close(void* ptr);
 int lc_enable_peer_access(int32_t device, int32_t peer);
 /* Stream-ordered cross-GPU barrier: publish `epoch` into slot `rank` of every
  * peer's flag array (peer_flags[j] = rank j's uint64[P] array), then wait
- * until all P slots of my_flags reach it.  Sets LC_FLAG_BARRIER_TIMEOUT in
- * *err after timeout_s instead of hanging (-> CollectiveError). */
+ * until all P slots of my_flags reach it.  After timeout_s instead of hanging
+ * it sets LC_FLAG_BARRIER_TIMEOUT in err[0] and bit j of err[1] for every
+ * rank j that never arrived (-> CollectiveError naming it). */
 int lc_barrier(void* const* peer_flags, int32_t P, int32_t rank, uint64_t* my_flags,
                uint64_t epoch, double timeout_s, uint32_t* err, void* stream);
 /* Momentum sync over peer memory (collectives.py:319-344): push block j of a
@@ -385,9 +396,11 @@ int lc_mean_bcast_f32(const float* recv, int32_t P, int64_t cnt, int64_t s,
 /* Same mean without staging: the owner loads elements [off, off+cnt) of
  * every rank's momentum directly (src[j] = rank j's buffer, peer pointers)
  * and stores the fp32 mean to out (nout = -1: NVLS multicast base; else
- * nout per-rank base pointers).  Ranks' buffers must be final (barrier). */
+ * nout per-rank base pointers).  Ranks' buffers must be final (barrier).
+ * err (nullable): the barrier's error words -- after a timeout nothing is
+ * averaged or stored. */
 int lc_mean_pull_f32(void* const* src, int32_t P, int64_t off, int64_t cnt,
-                     void* const* out, int32_t nout, void* stream);
+                     void* const* out, int32_t nout, const uint32_t* err, void* stream);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -82,6 +82,7 @@ SIGNATURES = {
     "lc_abi_version": (INT, []),
     "lc_last_error": (C.c_char_p, []),
     "lc_device_sm_count": (INT, [INT]),
+    "lc_set_grid_divisor": (INT, [INT]),
     "lc_encode": (INT, [P, P, P, I64, P, INT, INT, INT, P, P, I32, I64, I64, P, P, P]),
     "lc_vote_bits": (INT, [P, I32, I64, I64, INT, INT, P, P, P, I32, P, P, P]),
     "lc_vote_apply": (INT, [P, I32, I64, I64, INT, INT, P, P, I32, P, P, P, I64, P, P, D, D, P]),
@@ -129,7 +130,7 @@ SIGNATURES = {
     "lc_barrier": (INT, [P, I32, I32, P, C.c_uint64, D, P, P]),
     "lc_push_blocks_f32": (INT, [P, I64, I64, P, I32, P]),
     "lc_mean_bcast_f32": (INT, [P, I32, I64, I64, P, I32, P]),
-    "lc_mean_pull_f32": (INT, [P, I32, I64, I64, P, I32, P]),
+    "lc_mean_pull_f32": (INT, [P, I32, I64, I64, P, I32, P, P]),
 }
 
 _lock = threading.Lock()

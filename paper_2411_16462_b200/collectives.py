@@ -353,7 +353,9 @@ def run_ranks(world_size: int, fn, transport: DeviceTransport | None = None,
         tp = transport_factory(rank) if transport_factory is not None else transport
         topo = Topology(world_size=world_size, rank=rank, transport=tp, timeout=timeout)
         try:
-            with torch.cuda.device(tp.device(rank)):
+            # the rank thread's current stream is its transport stream
+            # (per-rank streams of LocalTransport(fused=True))
+            with torch.cuda.device(tp.device(rank)), torch.cuda.stream(tp.stream(rank)):
                 results[rank] = fn(topo)
         except BaseException as exc:  # surfaced below
             errors.append((rank, exc))

@@ -176,28 +176,44 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-// Every CTA: wait until all P peers published s.wait_epoch (acquire).
-__device__ __forceinline__ void sync_wait(const SyncD& s) {
-  if (!s.wait_epoch) return;
-  const int j = threadIdx.x;
-  if (j < s.P) {
-    const unsigned long long t0 = globaltimer();
-    while (true) {
-      unsigned long long v;
-      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(s.mine + j) : "memory");
-      if (v >= s.wait_epoch) break;
-      if (globaltimer() - t0 > s.timeout_ns) {
-        atomicOr(s.err, (uint32_t)LC_FLAG_BARRIER_TIMEOUT);
-        break;
-      }
-      __nanosleep(32);
+// A barrier wait gave up on peer j: err[0] gets LC_FLAG_BARRIER_TIMEOUT and
+// err[1] bit j (the rank that never arrived, reported by CollectiveError).
+__device__ __forceinline__ void sync_fail(uint32_t* err, int j) {
+  atomicOr(err, (uint32_t)LC_FLAG_BARRIER_TIMEOUT);
+  atomicOr(err + 1, 1u << (j & 31));
+}
+
+// Spin (one thread) until peer j's flag slot reaches `epoch`; false on
+// timeout (recorded in the error words).
+__device__ __forceinline__ bool wait_slot(const SyncD& s, int j, unsigned long long epoch) {
+  const unsigned long long t0 = globaltimer();
+  while (true) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(s.mine + j) : "memory");
+    if (v >= epoch) return true;
+    if (globaltimer() - t0 > s.timeout_ns) {
+      sync_fail(s.err, j);
+      return false;
     }
+    __nanosleep(32);
   }
-  __syncthreads();
+}
+
+// Every CTA: wait until all P peers published s.wait_epoch (acquire).
+// Returns false in every thread of the CTA if a peer timed out: the kernel
+// then writes nothing (no stale words reach theta, m or a peer).
+__device__ __forceinline__ bool sync_wait(const SyncD& s) {
+  if (!s.wait_epoch) return true;
+  const int j = threadIdx.x;
+  int ok = 1;
+  if (j < s.P) ok = wait_slot(s, j, s.wait_epoch);
+  return __syncthreads_and(ok) != 0;
 }
 
 // End of a kernel: the last CTA to finish publishes s.arrive_epoch to every
 // peer (each CTA fences its stores -- local and peer -- before counting).
+// After a barrier timeout on this rank nothing is published, so the peers'
+// waits time out too and every live rank reports the failure.
 __device__ __forceinline__ void sync_arrive(const SyncD& s) {
   if (!s.arrive_epoch) return;
   __syncthreads();
@@ -207,6 +223,8 @@ __device__ __forceinline__ void sync_arrive(const SyncD& s) {
     if (prev == gridDim.x - 1) {
       *s.counter = 0u;  // ready for the next launch of this site
       __threadfence_system();
+      const uint32_t e = *reinterpret_cast<volatile uint32_t*>(s.err);
+      if (e & LC_FLAG_BARRIER_TIMEOUT) return;
       for (int j = 0; j < s.P; ++j) {
         uint64_t* slot = s.peer[j] + s.rank;
         asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(slot), "l"(s.arrive_epoch)

@@ -31,6 +31,8 @@ int set_err(int code, const char* fmt, ...) {
   return code;
 }
 
+thread_local int g_grid_div = 1;  // lc_set_grid_divisor
+
 int sm_count() {
   static int cache[64] = {0};
   int dev = 0;
@@ -41,7 +43,8 @@ int sm_count() {
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
     cache[dev] = v > 0 ? v : 148;
   }
-  return cache[dev];
+  const int v = cache[dev] / g_grid_div;
+  return v > 0 ? v : 1;
 }
 
 int resident_ctas_of(const void* kernel, int block) {
@@ -155,6 +158,7 @@ __device__ __forceinline__ void encode4(const float ge[4], const float me[4], co
   for (int q = 0; q < 4; ++q) {
     c[q] = lion_c(me[q], ge[q], h);
     if (MASK && !keep[q]) c[q] = 0.0;  // np.where(mask, c, 0.0)
+    if (c[q] != c[q] && valid[q]) flag |= LC_FLAG_NAN;  // NaN update: the step raises
     mn[q] = lion_m(me[q], ge[q], h);
     if constexpr (ENC == LC_ENC_QUANT_FIELDS) {
       const double sc = quad_in ? qscale : cur.get(sq, e0 + q);
@@ -335,7 +339,7 @@ k_apply_update(float* __restrict__ theta, int64_t n, Dst sb, Dst nzb, int64_t wp
                int64_t woff, double lr, double wd, SyncD sy) {
   constexpr int KU = 4;
   griddep_wait();
-  sync_wait(sy);
+  if (!sync_wait(sy)) return;  // a peer never voted: theta stays untouched
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -520,8 +524,8 @@ k_fused_local(float* __restrict__ theta, float* __restrict__ m,
           zero = MODE != LC_LOCAL_BINARY;
           if (MODE == LC_LOCAL_BINARY && ternary && valid[k]) flag |= LC_FLAG_ZERO_SIGN;
           s = fillv;
-        } else {
-          s = -1.0;
+        } else {  // NaN: theta' = NaN like numpy's float path; the step raises
+          s = __longlong_as_double(0x7ff8000000000000ll);
           if (valid[k]) flag |= LC_FLAG_NAN;
         }
         tn[k] = lion_theta(te[k], s, lr, wd);
@@ -634,7 +638,10 @@ __global__ void __launch_bounds__(256)
 k_vote_bits(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_valid,
             int fill, int sum_mode, VoteOut out, uint32_t* __restrict__ flags, SyncD sy) {
   griddep_wait();
-  sync_wait(sy);
+  if (!sync_wait(sy)) {  // a peer's words never arrived: vote nothing
+    sync_arrive(sy);
+    return;
+  }
   const int T = P >> 1;
   const uint32_t fillmask = fill > 0 ? ~0u : 0u;
   uint32_t flag = 0;
@@ -701,7 +708,10 @@ __global__ void __launch_bounds__(256)
 k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_valid, int fill,
              int sum_mode, VoteOut out, uint32_t* __restrict__ flags, SyncD sy, ApplyArgs a) {
   griddep_wait();
-  sync_wait(sy);
+  if (!sync_wait(sy)) {  // a peer's words never arrived: no vote, no theta update
+    sync_arrive(sy);
+    return;
+  }
   const int T = P >> 1;
   const uint32_t fillmask = fill > 0 ? ~0u : 0u;
   // ---- vote (same as k_vote_bits) by the first nvote CTAs; the others go
@@ -758,6 +768,7 @@ k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_val
   const int64_t nwords = (a.n + 31) >> 5;
   float4* th4 = reinterpret_cast<float4*>(a.theta);
   uint32_t ready = 0u;  // owners whose voted block this warp has seen land
+  uint32_t bad = 0u;    // owners whose barrier timed out
   auto fetch = [&](int64_t sidx, uint32_t& sw_, uint32_t& zw_) {
     sw_ = 0u;
     zw_ = ~0u;
@@ -787,22 +798,12 @@ k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_val
       if (NZ) zw_ = nz;
       return;
     }
-    if (!((ready >> j) & 1u)) {
-      if (lane == 0) {
-        const unsigned long long t0 = globaltimer();
-        while (true) {
-          unsigned long long v;
-          asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(sy.mine + j) : "memory");
-          if (v >= sy.arrive_epoch) break;
-          if (globaltimer() - t0 > sy.timeout_ns) {
-            atomicOr(sy.err, (uint32_t)LC_FLAG_BARRIER_TIMEOUT);
-            break;
-          }
-          __nanosleep(32);
-        }
-      }
-      __syncwarp();
-      ready |= 1u << j;
+    if (!(((ready | bad) >> j) & 1u)) {
+      int ok = 1;
+      if (lane == 0) ok = wait_slot(sy, j, sy.arrive_epoch);
+      ok = __shfl_sync(kFull, ok, 0);
+      if (ok) ready |= 1u << j;
+      else bad |= 1u << j;  // owner j never published: its block is not updated
     }
     const int64_t w = sidx * 32 + lane;
     if (w < nwords) {
@@ -825,6 +826,7 @@ k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_val
     const int64_t sidx = at(i);
     const uint32_t myw = nxw, myz = nxz;
     fetch(at(i + nw), nxw, nxz);
+    if ((bad >> (int)((sidx * 32) / a.blk_words)) & 1u) continue;  // stale words: skip
 #pragma unroll 1
     for (int k0 = 0; k0 < 8; k0 += KU) {
       float4 tv[KU];
@@ -876,7 +878,10 @@ k_fields_vote(const uint32_t* __restrict__ sums, int rows, int64_t row_stride, i
               int P, int offset, int binary, int fill, VoteOut out,
               int64_t* __restrict__ values, SyncD sy) {
   griddep_wait();
-  sync_wait(sy);
+  if (!sync_wait(sy)) {
+    sync_arrive(sy);
+    return;
+  }
   constexpr int E = 32 / F;
   constexpr uint32_t FM = (F == 32) ? 0xffffffffu : ((1u << F) - 1u);
   const int lane = threadIdx.x & 31;
@@ -933,7 +938,10 @@ __global__ void __launch_bounds__(256)
 k_fields_vote_words(const uint32_t* __restrict__ sums, int rows, int64_t row_stride, int64_t n,
                     int P, int offset, int binary, int fill, VoteOut out, SyncD sy) {
   griddep_wait();
-  sync_wait(sy);
+  if (!sync_wait(sy)) {
+    sync_arrive(sy);
+    return;
+  }
   constexpr int E = 32 / F;  // fields per input word
   constexpr uint32_t FM = (F == 32) ? 0xffffffffu : ((1u << F) - 1u);
   const int64_t nout = (n + 31) / 32;
@@ -983,7 +991,10 @@ __global__ void __launch_bounds__(256)
 k_f64_sum_vote(const double* __restrict__ recv, int P, int64_t len, int64_t stride, int tree,
                int fill, VoteOut out, double* __restrict__ values, SyncD sy) {
   griddep_wait();
-  sync_wait(sy);
+  if (!sync_wait(sy)) {
+    sync_arrive(sy);
+    return;
+  }
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1187,7 +1198,7 @@ k_vote_update(const uint32_t* __restrict__ rows, int64_t stride, int P, float* _
               uint32_t* __restrict__ flags, SyncD sy) {
   constexpr int KU = LC_VU_KU;  // theta sub-tiles in flight per batch
   griddep_wait();
-  sync_wait(sy);
+  if (!sync_wait(sy)) return;  // a peer's rows never arrived: theta untouched
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1362,6 +1373,12 @@ extern "C" {
 int lc_abi_version(void) { return LIONCUB_ABI_VERSION; }
 
 const char* lc_last_error(void) { return err_msg().c_str(); }
+
+int lc_set_grid_divisor(int divisor) {
+  if (divisor < 1 || divisor > 1024) return set_err(LC_E_ARG, "lc_set_grid_divisor: divisor in [1,1024]");
+  g_grid_div = divisor;
+  return LC_OK;
+}
 
 int lc_device_sm_count(int device) {
   int v = 0;

@@ -41,6 +41,7 @@ __global__ void k_barrier(Ptrs peer_flags, uint64_t* __restrict__ my_flags, int 
       if (v >= epoch) break;
       if (globaltimer_ns() - t0 > timeout_ns) {
         atomicOr(err, (uint32_t)LC_FLAG_BARRIER_TIMEOUT);
+        atomicOr(err + 1, 1u << (j & 31));  // the rank that never arrived
         break;
       }
       __nanosleep(64);
@@ -137,7 +138,11 @@ k_mean_bcast(const float* __restrict__ recv, int P, int64_t cnt, int64_t s, Ptrs
 // summed in float64 in rank order, divided once, rounded once to fp32, and
 // stored to every rank (NVLS multicast, or one store per rank).
 __global__ void __launch_bounds__(256)
-k_mean_pull(Ptrs src, int P, int64_t off, int64_t cnt, Ptrs out, int nout, int vec) {
+k_mean_pull(Ptrs src, int P, int64_t off, int64_t cnt, Ptrs out, int nout, int vec,
+            const uint32_t* __restrict__ err) {
+  // the barrier before this kernel timed out: a peer's momentum is not final,
+  // so nothing is averaged or stored (the step reports CollectiveError)
+  if (err && (*reinterpret_cast<const volatile uint32_t*>(err) & LC_FLAG_BARRIER_TIMEOUT)) return;
   const double dp = (double)P;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t done = 0;
@@ -301,7 +306,7 @@ int lc_mean_bcast_f32(const float* recv, int32_t P, int64_t cnt, int64_t s, void
 }
 
 int lc_mean_pull_f32(void* const* src, int32_t P, int64_t off, int64_t cnt, void* const* out,
-                     int32_t nout, void* stream) {
+                     int32_t nout, const uint32_t* err, void* stream) {
   Ptrs sp, o;
   const int nt = nout < 0 ? 1 : nout;
   if (cnt < 0 || off < 0 || P < 1 || nout == 0 || nout < -1 || !make_ptrs(sp, src, P) ||
@@ -312,7 +317,7 @@ int lc_mean_pull_f32(void* const* src, int32_t P, int64_t off, int64_t cnt, void
   for (int j = 0; j < P && vec; ++j) vec = aligned16(sp.p[j]);
   for (int k = 0; k < nt && vec; ++k) vec = aligned16(o.p[k]);
   k_mean_pull<<<grid_for(vec ? cnt / 4 : cnt), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      sp, P, off, cnt, o, nout, vec);
+      sp, P, off, cnt, o, nout, vec, err);
   LC_LAUNCH_CHECK();
   return LC_OK;
 }

@@ -237,11 +237,22 @@ class WorkerState:
 
 
 def hash_params(params: Mapping) -> str:
-    """Stable digest for cross-rank checks (optimizer.py:34-40); fp32 bytes."""
+    """Stable digest for cross-rank checks, identical to the reference's
+    (optimizer.py:34-40): sha256 over each layer's name and its values as
+    little-endian float64 bytes, in sorted-name order -- so a digest of the
+    GPU state equals the reference's digest of the same values.  Layers are
+    streamed to the host in 2^24-element chunks."""
+    import numpy as np
     h = hashlib.sha256()
+    chunk = 1 << 24
     for name in sorted(params):
         h.update(name.encode())
-        h.update(params[name].detach().to(torch.float32).contiguous().cpu().numpy().tobytes())
+        v = params[name]
+        flat = v.detach().reshape(-1) if isinstance(v, torch.Tensor) else \
+            torch.from_numpy(np.ascontiguousarray(v).reshape(-1))
+        for a in range(0, flat.numel(), chunk):
+            part = flat[a:a + chunk].to("cpu", torch.float64).numpy()
+            h.update(np.ascontiguousarray(part, dtype="<f8").tobytes())
     return h.hexdigest()
 
 
@@ -283,6 +294,7 @@ class _Workspace:
         self.key = (layout.key, P, kind, F)
         self.ag = None
         self.flags = z(1)
+        self.flags_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
         self.counters = z(4)   # arrive counters of the in-kernel barriers
         self.k5_sync = None
         self.syncs = None
@@ -302,11 +314,24 @@ class _Workspace:
         if p2p:
             key = (layout.key, P, kind, F)
             sym = lambda name, k, dt=torch.int32: tp.sym_buffer(r, key + (name,), k, dt)  # noqa
-            self.recv = sym("recv", rlen, rdt)
+            # receive slots in two halves used by alternate steps: with the
+            # in-kernel barriers, an owner may still be reading its slots of
+            # step t (the in-warp vote of its own block in k_vote_apply runs
+            # after it published e2) when a fast peer's K1 of step t+1
+            # already stores into this owner's slots -- it lands in the other
+            # half.  The half counter lives on the shared buffer, so every
+            # workspace mapping it alternates in the same global order.
+            self.recv = sym("recv", 2 * rlen, rdt)
+            if not hasattr(self.recv, "steps"):
+                self.recv.steps = 0
+            half = rlen * torch.empty((), dtype=rdt).element_size()
+            self.recv_half = [self.recv.local.data_ptr() + h * half for h in (0, 1)]
+            self.dst_half = [_lib.table([self.recv.peers[j] + h * half + r * blk_bytes
+                                         for j in range(P)]) for h in (0, 1)]
+            self.dst = self.dst_half[0]
             self.full = sym("full", P * cw)
             self.nz = sym("nz", P * cw) if ternary else None
             self.ties = sym("ties", P * cw) if metrics else None
-            self.dst = _lib.table([self.recv.peers[j] + r * blk_bytes for j in range(P)])
             used = [b for b in (self.full, self.nz, self.ties) if b is not None]
             if all(getattr(b, "mc", 0) for b in used):
                 # NVLS: the owner stores its voted block once to the multicast
@@ -356,7 +381,9 @@ class _Workspace:
 
 def _workspace(th: FlatParamSet, topo: Topology, kind: str, F: int, ternary: bool,
                metrics: bool) -> _Workspace:
-    key = (id(topo.transport), topo.world_size, topo.rank, kind, F, ternary, metrics)
+    # keyed by the transport's serial, not id(): a rebuilt transport never
+    # inherits a workspace whose peer tables point into freed mappings
+    key = (topo.transport.serial, topo.world_size, topo.rank, kind, F, ternary, metrics)
     ws = th.workspace.get(key)
     if ws is None:
         ws = _Workspace(th.layout, topo, kind, F, ternary, metrics)
@@ -420,6 +447,18 @@ def _flat_mask(mask, layout: Layout, dev):
     return flat
 
 
+class _Ptr:
+    """A raw device address where the kernels take ``tensor.data_ptr()``."""
+
+    __slots__ = ("p",)
+
+    def __init__(self, p: int):
+        self.p = p
+
+    def data_ptr(self) -> int:
+        return self.p
+
+
 def _off(t: torch.Tensor, elems: int) -> int:
     return t.data_ptr() + elems * t.element_size()
 
@@ -436,6 +475,20 @@ def _on_device(dev):
 def _on_stream(stream, dev):
     cur = torch.cuda.current_stream(dev)
     return _NULL if cur.cuda_stream == stream.cuda_stream else torch.cuda.stream(stream)
+
+
+def _raise_nan(ws):
+    """A NaN Lion update (c = NaN from a NaN gradient or momentum) is an
+    error: the reference's behaviour is undefined there (numpy casts NaN to
+    int64 -- PackRangeError, ConfigError or a garbage update depending on
+    the path).  The kernels flag it (LC_FLAG_NAN); the flag is read back
+    without a host sync, so a step that does not synchronise raises at the
+    next step.  The single-rank kernel leaves theta' = NaN at those elements."""
+    if int(ws.flags_host[0]) & _lib.LC_FLAG_NAN:
+        ws.flags.zero_()
+        ws.flags_host.zero_()
+        raise ConfigError("non-finite Lion update: c = beta1*m + (1-beta1)*g is NaN "
+                          "(NaN gradient or momentum)")
 
 
 def _raise_flags(bits: int, binary: bool):
@@ -574,6 +627,12 @@ def _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out,
     hyp = h.c_struct(t)
     eta, wd = hyp.lr, hyp.weight_decay
     sum_mode = 0
+    if algo in ("ps", "ps_efficient") and spec is not None and spec.bits == 1 and ternary:
+        # ps sums apply_sign's ternary signs exactly (optimizer.py:151-152,
+        # collectives.py:132-165); the binary sign path cannot carry zeros,
+        # so carry them as a 2-bit max-norm no_zero quantizer, which is
+        # exactly sign(c) in {-1, 0, +1} (quant.py:127-173)
+        spec = _TERNARY_SIGNS
     if algo == "compressed1bit":
         kind, binary, qmax = "1bit", True, 0
     elif spec is None:
@@ -587,16 +646,23 @@ def _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out,
     seed = spec.draw_seed(rng) if (kind == "fields" and not binary) else 0
     F = 1
     if kind == "fields":
-        # reference capacity rule first: CapacityError before any exchange
-        choose_lane_bits(P, qmax, binary_signs=binary)
+        if algo == "direct":
+            # reference capacity rule first: CapacityError before any exchange
+            choose_lane_bits(P, qmax, binary_signs=binary)
+        # (ps sums int64 on the reference; here the carry-free field must fit
+        # 32 bits, i.e. P * 2 * qmax < 2^32 -- CapacityError beyond that)
         F = field_bits(P, 1 if binary else 2 * qmax)
         if binary and P > 1 and topo.transport.p2p:
             # sum-of-signs over peer memory: ship 1-bit signs; the owner's
             # bit-sliced counter yields the same exact p-bit sums 2k-P
             kind, F, sum_mode = "1bit", 1, 1
-    if P > 1 and topo.transport.poll_error(topo.rank):
-        raise CollectiveError("a peer never reached the step barrier",
-                              generation=topo.generation)
+    tp = topo.transport
+    strict = P > 1 and tp.error_mode == "step"
+    if P > 1:
+        tp.check_usable(topo.rank)
+        if not strict and tp.poll_error(topo.rank):   # deferred: last step's timeout
+            tp.fail(topo.rank, "a peer never reached the previous step's barrier",
+                    tp.error_state(topo.rank)[1], topo.generation, "step")
     metrics = metrics_out is not None
     n = layout.n
     with _on_device(dev):
@@ -612,7 +678,12 @@ def _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out,
             mflat = _flat_mask(mask, layout, dev)
             ws = _workspace(th, topo, kind if P > 1 else "local", F,
                             ternary and (kind != "1bit" or sum_mode == 1), metrics)
+            _raise_nan(ws)  # a NaN update seen by an earlier (unsynced) step
             gen = topo.next_generation()
+            if strict:
+                _mark = getattr(tp, "mark_reached", None)
+                if _mark is not None:
+                    _mark(topo.rank, gen)
             if metrics:
                 c_local = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
                 _lib.call("lc_compute_c", g.flat.data_ptr(), m.flat.data_ptr(),
@@ -653,6 +724,9 @@ def _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out,
                                         n, g, m, mflat, hyp, segs, s,
                                         tree=algo == "ps_efficient", pipe=pipe,
                                         theta=th.flat)
+                if strict and not ws.p2p and hasattr(tp, "wait_collectives"):
+                    # NCCL exchange: no theta update unless every collective landed
+                    tp.wait_collectives(topo.rank, gen, "vote exchange")
                 if ws.applied:
                     pass
                 elif pipe is None:
@@ -666,6 +740,10 @@ def _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out,
                         pipe.emit_out(c, th.flat, stream)
             if pipe is not None:
                 pipe.finish(stream)
+            ws.flags_host.copy_(ws.flags, non_blocking=True)
+            if strict and P > 1 and ws.p2p:
+                tp.check_step(topo.rank, gen, "step")   # syncs the stream
+                _raise_nan(ws)
             if metrics:
                 _fill_metrics(metrics_out, layout, dev, ws, nz, c_local, s)
     return WorkerState(params=th, momentum=m, iteration=t)
@@ -695,7 +773,12 @@ def _ternary_precheck(topo, gen, g, m, mflat, n, hyp, dev, s, kind):
                   _lib.table([voted.data_ptr()]), None, None, 1, flags.data_ptr(), None, s)
     if topo.world_size > 1:
         topo.transport.allreduce_max_u32(topo.rank, gen, flags)
+        if topo.transport.error_mode == "step" and hasattr(topo.transport, "wait_collectives"):
+            topo.transport.wait_collectives(topo.rank, gen, "zero-sign precheck")
     _raise_flags(int(flags.item()), binary=kind == "1bit")
+
+
+_TERNARY_SIGNS = QuantSpec(bits=2, norm_p=float("inf"), no_zero=True)
 
 
 # When the 1-bit step allgathers the sign words (K1 stores its words into
@@ -773,6 +856,11 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
         ws.applied = True
         return None
     sy1 = sy2 = sy3 = None
+    recv_ptr = None
+    if ws.p2p:
+        h = ws.recv.steps & 1
+        ws.recv.steps += 1
+        ws.dst, recv_ptr = ws.dst_half[h], ws.recv_half[h]
     if fused:
         # the barriers live inside the kernels: K1's last CTA publishes e1,
         # the vote waits for e1 and publishes e2, K5 waits for e2
@@ -805,7 +893,7 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
     if ws.p2p:
         if not fused:
             tp.device_barrier(r, gen)      # every rank's blocks have landed
-        recv, rows = ws.recv.local, P
+        recv, rows = _Ptr(recv_ptr), P
     elif kind == "1bit":
         tp.alltoall(r, gen, ws.send, ws.recv, cw * 4)
         recv = ws.recv
@@ -871,7 +959,11 @@ def _symmetric_momentum(m: FlatParamSet, topo: Topology) -> FlatParamSet:
     if getattr(m, "sym", None) is not None:
         return m
     layout = m.layout
-    buf = topo.transport.sym_buffer(topo.rank, (layout.key, "momentum"), max(layout.n, 1),
+    # one mapped buffer per momentum state: two states with the same layout
+    # on one transport (two models, an A/B arm) must not share it.  The
+    # token is drawn in call order, which every rank shares (collective).
+    tok = topo.transport.next_token(topo.rank)
+    buf = topo.transport.sym_buffer(topo.rank, (layout.key, "momentum", tok), max(layout.n, 1),
                                     torch.float32)
     buf.local.copy_(m.flat)
     out = FlatParamSet(buf.local, layout)
@@ -920,8 +1012,11 @@ def maybe_sync_momentum(state: WorkerState, policy: SyncPolicy,
                     if a % 4 == 0:
                         sr = -(-sr // 4) * 4   # 16-byte aligned owner blocks
                     cnt = max(0, min(sr, ln - r * sr))
-                    _lib.call("lc_mean_pull_f32", src, P, a + r * sr, cnt, outs, nout, st)
+                    _lib.call("lc_mean_pull_f32", src, P, a + r * sr, cnt, outs, nout,
+                              tp.error_word(r), st)
                 tp.device_barrier(r, gen)
+                if tp.error_mode == "step":
+                    tp.check_step(r, gen, "momentum sync")
             else:
                 key = ("sync", P, smax)
                 scratch = m.workspace.get(key)
@@ -932,6 +1027,8 @@ def maybe_sync_momentum(state: WorkerState, policy: SyncPolicy,
                     gen = topo.next_generation()
                     seg = m.flat[a:b]
                     mean_into(topo, gen, seg, seg, scratch)
+                if tp.error_mode == "step" and hasattr(tp, "wait_collectives"):
+                    tp.wait_collectives(r, gen, "momentum sync")
     return replace(state, params=th, momentum=m)
 
 

@@ -31,6 +31,7 @@ rendezvous, since the ranks share one stream).
 from __future__ import annotations
 
 import ctypes as C
+import itertools
 import os
 import threading
 import time
@@ -75,15 +76,71 @@ def _wrap(ptr: int, numel: int, dtype, dev) -> torch.Tensor:
     return t.view(dtype)
 
 
+_SERIAL = itertools.count(1)
+
+
+def _error_mode() -> str:
+    m = os.environ.get("LIONCUB_ERRORS", "step")
+    if m not in ("step", "deferred"):
+        raise ConfigError('LIONCUB_ERRORS must be "step" or "deferred"')
+    return m
+
+
 class DeviceTransport:
     """Collectives over device buffers for ranks 0..world_size-1.
 
     Buffers are CUDA tensors; byte counts/displacements are host integers.
     Every call is stream-ordered on ``stream(rank)``.
+
+    Failure reporting (``error_mode``, env ``LIONCUB_ERRORS``):
+      "step" (default) -- like the reference (transport.py:66-70,150-156), a
+        step whose exchange timed out raises ``CollectiveError`` naming the
+        missing rank in the SAME call: the step waits for its kernels (one
+        host sync per multi-rank step) and reads the barrier error words;
+        on the NCCL exchange it polls ncclCommGetAsyncError against a host
+        deadline and aborts the communicator.  theta and the iteration are
+        unchanged (the update kernels skip every block whose votes did not
+        arrive); m holds m' (K1 updates it before the exchange).
+      "deferred" -- no host sync: the error words are copied back
+        asynchronously and the NEXT step raises.
+    After a failure the transport is unusable (``broken``): rebuild it.
     """
 
     world_size: int
     p2p: bool = False
+    error_mode: str = "step"
+    serial: int = 0
+
+    def _init_common(self):
+        self.serial = next(_SERIAL)
+        self.error_mode = _error_mode()
+        self.broken = {}   # rank -> why its exchanges are unusable
+
+    def next_token(self, rank: int) -> int:
+        """Per-rank counter for collective allocations that must not be
+        shared between objects (every rank draws in the same order)."""
+        toks = self.__dict__.setdefault("_tokens", {})
+        toks[rank] = toks.get(rank, 0) + 1
+        return toks[rank]
+
+    def check_usable(self, rank: int):
+        why = getattr(self, "broken", {}).get(rank)
+        if why:
+            raise CollectiveError(f"transport unusable after an earlier failure: {why}",
+                                  rank=rank)
+
+    def fail(self, rank: int, message: str, missing=None, generation=None, phase=None):
+        """Mark this rank's endpoint broken and raise CollectiveError naming
+        the lowest missing rank (or this rank when unknown)."""
+        who = missing[0] if missing else rank
+        self.__dict__.setdefault("broken", {})[rank] = \
+            f"{message} (rank {who}, generation {generation})"
+        raise CollectiveError(message + (f"; ranks never seen: {list(missing)}" if missing else ""),
+                              rank=who, generation=generation, phase=phase)
+
+    def check_step(self, rank: int, gen: int, phase: str):
+        """Strict mode, peer-memory exchange: wait for this rank's step and
+        raise if one of its in-kernel barriers timed out."""
 
     def sym_buffer(self, rank: int, key, numel: int, dtype) -> SymBuffer:
         """Collective: a zeroed buffer mapped on every rank (p2p mode)."""
@@ -159,36 +216,149 @@ class _Rendezvous:
                 self.cv.wait(left)
 
 
-class LocalTransport(DeviceTransport):
-    """P simulated ranks on one GPU, one host thread per rank."""
+class _PeerSync:
+    """Device-side barrier plumbing of the peer-memory exchange: a P-slot
+    epoch flag array per rank mapped on every rank (``sym_buffer``), a
+    device error word per rank (word 0: LC_FLAG_* bits, word 1: bitmask of
+    the ranks a barrier timed out waiting for), and the monotonically
+    increasing epochs the kernels publish (csrc/common.cuh sync_wait /
+    sync_arrive, csrc/p2p.cu k_barrier)."""
+
+    timeout: float = DEFAULT_TIMEOUT
+
+    def _flags(self, rank):
+        flags = self.sym_buffer(rank, ("__barrier__",), self.world_size, torch.int64)
+        if rank not in self._err:
+            dev = self.device(rank)
+            self._err[rank] = torch.zeros(2, dtype=torch.int32, device=dev)
+            self._err_host[rank] = torch.zeros(2, dtype=torch.int32, pin_memory=True)
+            self._epoch[rank] = 0
+        return flags
+
+    def error_word(self, rank) -> int:
+        """Device address of this rank's barrier error words (2 x uint32)."""
+        self._flags(rank)
+        return self._err[rank].data_ptr()
+
+    def take_epochs(self, rank, k):
+        self._flags(rank)
+        first = self._epoch[rank] + 1
+        self._epoch[rank] += k
+        return list(range(first, first + k))
+
+    def sync_struct(self, rank, counter, wait_epoch, arrive_epoch):
+        flags = self._flags(rank)
+        sy = _lib.Sync()
+        for j, p in enumerate(flags.peers):
+            sy.peer_flags[j] = p
+        sy.my_flags = flags.local.data_ptr()
+        sy.counter = counter.data_ptr()
+        sy.err = self._err[rank].data_ptr()
+        sy.wait_epoch, sy.arrive_epoch = wait_epoch, arrive_epoch
+        sy.P, sy.rank, sy.timeout_s = self.world_size, rank, self.timeout
+        return sy
+
+    def device_barrier_kernel(self, rank, gen):
+        flags = self._flags(rank)
+        (epoch,) = self.take_epochs(rank, 1)
+        st = self.stream(rank).cuda_stream
+        _lib.call("lc_barrier", _lib.table(flags.peers), self.world_size, rank,
+                  flags.local.data_ptr(), epoch, self.timeout,
+                  self._err[rank].data_ptr(), st)
+
+    def poll_error(self, rank):
+        """Non-blocking: the barrier error flag as of the last poll; schedules
+        the next device->host copy of it."""
+        if rank not in self._err:
+            return False
+        seen = bool(self._err_host[rank][0].item())
+        self._err_host[rank].copy_(self._err[rank], non_blocking=True)
+        return seen
+
+    def error_state(self, rank) -> tuple:
+        """(flag bits, ranks never seen) of this rank's error words; host
+        sync on the rank's stream (error paths and strict steps only)."""
+        if rank not in self._err:
+            return 0, []
+        self.stream(rank).synchronize()
+        w = self._err[rank].tolist()
+        miss = [j for j in range(self.world_size) if (w[1] >> j) & 1]
+        return w[0] & 0xFFFFFFFF, miss
+
+    def clear_error(self, rank):
+        if rank in self._err:
+            self._err[rank].zero_()
+            self._err_host[rank].zero_()
+
+    def check_step(self, rank, gen, phase):
+        if rank not in self._err:
+            return
+        bits, miss = self.error_state(rank)
+        if bits & _lib.LC_FLAG_BARRIER_TIMEOUT:
+            self.fail(rank, "a peer never reached the step barrier", miss, gen, phase)
+
+
+class LocalTransport(_PeerSync, DeviceTransport):
+    """P simulated ranks on one GPU, one host thread per rank.
+
+    Default: every rank enqueues on the device's default stream, so each
+    collective is a host rendezvous followed by stream-ordered copies from
+    the peers' buffers, and ``device_barrier`` is the rendezvous itself.
+
+    ``fused=True`` (peer-memory mode only) runs the PRODUCTION multi-GPU
+    path on one GPU: every simulated rank gets its own CUDA stream, the step
+    kernels order themselves with the in-kernel epoch barriers exactly as on
+    NVLink (K1 stores into the owners' receive slots and publishes e1,
+    k_vote_apply / k_vote_update wait on the peers' flags ...), and each rank
+    thread sizes its grids for 1/P of the SMs (lc_set_grid_divisor) so the
+    P ranks' barrier-waiting kernels are co-resident.  Host collectives then
+    order the rank streams with CUDA events."""
 
     def __init__(self, world_size: int, device=None, timeout: float = DEFAULT_TIMEOUT,
-                 p2p: bool = True):
+                 p2p: bool = True, fused: bool = False):
         if world_size < 1:
             raise ConfigError("world_size must be >= 1")
         if not torch.cuda.is_available():
             raise ConfigError("LocalTransport needs a CUDA device")
+        if fused and not p2p:
+            raise ConfigError("LocalTransport(fused=True) needs the peer-memory mode")
         self.world_size = world_size
         self.dev = (torch.device(device) if device is not None
                     else torch.device("cuda", torch.cuda.current_device()))
         self.timeout = timeout
         self.p2p = p2p
+        self.fused = fused and world_size > 1
         self._stream = torch.cuda.default_stream(self.dev)
+        self._streams = ([torch.cuda.Stream(self.dev) for _ in range(world_size)]
+                         if self.fused else None)
         self._posts = [None] * world_size
+        self._events = [None] * world_size
         self._rv = _Rendezvous(world_size)
         self._sym = {}
+        self._err, self._err_host, self._epoch = {}, {}, {}
+        self._tls = threading.local()
+        self._init_common()
+
+    @property
+    def fused_barriers(self):
+        return self.fused
 
     def sym_buffer(self, rank, key, numel, dtype):
         k = (rank, key)
         if k not in self._sym:
             t = torch.zeros(max(numel, 1), dtype=dtype, device=self.dev)
-            posts = self._exchange(rank, 0, "sym_buffer", t.data_ptr())
+            if self.fused:
+                torch.cuda.synchronize(self.dev)  # zeroed before a peer stream writes
+            posts = self._exchange(rank, 0, "sym_buffer", t.data_ptr(), order=False)
             peers = list(posts)
-            self._done(rank, 0, "sym_buffer")
+            self._done(rank, 0, "sym_buffer", order=False)
             self._sym[k] = SymBuffer(t, peers)
         return self._sym[k]
 
     def device_barrier(self, rank, gen):
+        if self.fused:
+            self.device_barrier_kernel(rank, gen)
+            return
         # all simulated ranks enqueue on the same stream: the host rendezvous
         # orders every rank's earlier kernels before every later one
         self._rv.wait(rank, gen, "barrier", self.timeout)
@@ -197,14 +367,41 @@ class LocalTransport(DeviceTransport):
         return self.dev
 
     def stream(self, rank):
-        return self._stream
+        if not self.fused:
+            return self._stream
+        if getattr(self._tls, "div", None) != self.world_size:
+            # this rank thread's launches get 1/P of the SMs
+            _lib.check(_lib.load().lc_set_grid_divisor(self.world_size), "lc_set_grid_divisor")
+            self._tls.div = self.world_size
+        return self._streams[rank]
 
-    def _exchange(self, rank, gen, phase, post):
+    def _exchange(self, rank, gen, phase, post, order=True):
         self._posts[rank] = post
+        if self.fused and order:
+            # the payload is ready once this rank's stream reaches here
+            ev = torch.cuda.Event()
+            ev.record(self._streams[rank])
+            self._events[rank] = ev
         self._rv.wait(rank, gen, phase + ":post", self.timeout)
+        if self.fused and order:
+            for j, ev in enumerate(list(self._events)):
+                if j != rank:
+                    self._streams[rank].wait_event(ev)
         return self._posts
 
-    def _done(self, rank, gen, phase):
+    def _done(self, rank, gen, phase, order=True):
+        if self.fused and order:
+            # nobody reuses a source buffer before every reader copied it
+            ev = torch.cuda.Event()
+            ev.record(self._streams[rank])
+            self._rv.wait(rank, gen, phase + ":read", self.timeout)
+            self._events[rank] = ev
+            self._rv.wait(rank, gen, phase + ":done", self.timeout)
+            for j, e in enumerate(list(self._events)):
+                if j != rank:
+                    self._streams[rank].wait_event(e)
+            self._rv.wait(rank, gen, phase + ":waited", self.timeout)
+            return
         self._rv.wait(rank, gen, phase + ":done", self.timeout)
 
     def alltoall(self, rank, gen, send, recv, nbytes_per_peer):
@@ -264,7 +461,7 @@ class LocalTransport(DeviceTransport):
         self._done(rank, gen, "allreduce_max")
 
 
-class NcclTransport(DeviceTransport):
+class NcclTransport(_PeerSync, DeviceTransport):
     """NCCL communicators over NVLink, one per GPU rank.
 
     ``comms`` maps rank -> lc_comm_t handle for the ranks this process
@@ -272,8 +469,12 @@ class NcclTransport(DeviceTransport):
     """
 
     def __init__(self, world_size: int, comms: dict, devices: dict, group=None,
-                 threaded: bool = False, p2p: bool | None = None):
+                 threaded: bool = False, p2p: bool | None = None,
+                 timeout: float = DEFAULT_TIMEOUT):
         self.world_size = world_size
+        self.timeout = timeout
+        self._init_common()
+        self._alive = {}    # threaded mode: generation -> ranks that reached it
         self._comms = comms
         self._devices = devices
         self._group = group
@@ -357,7 +558,7 @@ class NcclTransport(DeviceTransport):
             peers = list(self._posts)
             self._rv.wait(rank, 0, "sym_buffer:done", DEFAULT_TIMEOUT)
             buf = SymBuffer(t, peers)
-        elif self._nvls_ok and key[-1] in ("full", "nz", "ties", "momentum") \
+        elif self._nvls_ok and (key[-1] in ("full", "nz", "ties") or "momentum" in key) \
                 and self._try_torch_symm(rank, k, numel, dtype):
             return self._sym[k]
         else:
@@ -421,61 +622,65 @@ class NcclTransport(DeviceTransport):
             self._nvls_ok = False
             return False
 
-    def _flags(self, rank):
-        flags = self.sym_buffer(rank, ("__barrier__",), self.world_size, torch.int64)
-        if rank not in self._err:
-            dev = self._devices[rank]
-            self._err[rank] = torch.zeros(1, dtype=torch.int32, device=dev)
-            self._err_host[rank] = torch.zeros(1, dtype=torch.int32, pin_memory=True)
-            self._epoch[rank] = 0
-        return flags
-
-    def error_word(self, rank) -> int:
-        """Device address of this rank's barrier error word (uint32)."""
-        self._flags(rank)
-        return self._err[rank].data_ptr()
-
-    def take_epochs(self, rank, k):
-        self._flags(rank)
-        first = self._epoch[rank] + 1
-        self._epoch[rank] += k
-        return list(range(first, first + k))
-
     @property
     def fused_barriers(self):
         return self.p2p and self._fused_env
 
-    def sync_struct(self, rank, counter, wait_epoch, arrive_epoch):
-        flags = self._flags(rank)
-        sy = _lib.Sync()
-        for j, p in enumerate(flags.peers):
-            sy.peer_flags[j] = p
-        sy.my_flags = flags.local.data_ptr()
-        sy.counter = counter.data_ptr()
-        sy.err = self._err[rank].data_ptr()
-        sy.wait_epoch, sy.arrive_epoch = wait_epoch, arrive_epoch
-        sy.P, sy.rank, sy.timeout_s = self.world_size, rank, DEFAULT_TIMEOUT
-        return sy
-
     def device_barrier(self, rank, gen):
-        flags = self._flags(rank)
-        (epoch,) = self.take_epochs(rank, 1)
-        st = self.stream(rank).cuda_stream
-        _lib.call("lc_barrier", _lib.table(flags.peers), self.world_size, rank,
-                  flags.local.data_ptr(), epoch, DEFAULT_TIMEOUT,
-                  self._err[rank].data_ptr(), st)
-
-    def poll_error(self, rank):
-        """Non-blocking: the barrier error flag as of the last poll; schedules
-        the next device->host copy of it."""
-        if rank not in self._err:
-            return False
-        seen = bool(self._err_host[rank].item())
-        self._err_host[rank].copy_(self._err[rank], non_blocking=True)
-        return seen
+        self.device_barrier_kernel(rank, gen)
 
     def _c(self, rank):
-        return self._comms[rank]
+        c = self._comms[rank]
+        if c is None:
+            self.check_usable(rank)
+            raise CollectiveError("NCCL communicator closed", rank=rank)
+        return c
+
+    def mark_reached(self, rank, gen):
+        """Threaded mode: record that ``rank`` entered the exchange of ``gen``
+        (names the missing rank if the exchange later times out)."""
+        if self._threaded:
+            with self._rv.cv:
+                self._alive.setdefault(gen, set()).add(rank)
+                for g in [g for g in self._alive if g < gen - 8]:
+                    del self._alive[g]
+
+    def _missing_ranks(self, rank, gen) -> list:
+        if self._threaded:
+            with self._rv.cv:
+                seen = set(self._alive.get(gen, ()))
+            return [j for j in range(self.world_size) if j not in seen]
+        try:  # process per GPU: the live ranks check in on the rendezvous store
+            import torch.distributed as dist
+            store = dist.distributed_c10d._get_default_store()
+            store.set(f"lioncub/alive/{self.serial}/{gen}/{rank}", "1")
+            t_end = time.monotonic() + min(5.0, self.timeout)
+            keys = [f"lioncub/alive/{self.serial}/{gen}/{j}" for j in range(self.world_size)]
+            while time.monotonic() < t_end and not store.check(keys):
+                time.sleep(0.05)
+            return [j for j, k in enumerate(keys) if not store.check([k])]
+        except Exception:
+            return []
+
+    def wait_collectives(self, rank, gen, phase):
+        """Strict mode, NCCL exchange: wait until this rank's enqueued NCCL
+        work completes, polling ncclCommGetAsyncError against the host
+        deadline (reference transport.py:66-70); on error or timeout abort
+        the communicator (the stream's NCCL kernels exit) and raise
+        CollectiveError before any theta update is enqueued."""
+        ev = torch.cuda.Event()
+        ev.record(self.stream(rank))
+        deadline = time.monotonic() + self.timeout
+        lib = _lib.load()
+        while not ev.query():
+            rc = lib.lc_comm_check(self._comms[rank])
+            if rc != _lib.LC_OK or time.monotonic() > deadline:
+                why = _lib.last_error() if rc != _lib.LC_OK else "timed out"
+                missing = self._missing_ranks(rank, gen)
+                lib.lc_comm_abort(self._comms[rank])
+                self._comms[rank] = None
+                self.fail(rank, f"NCCL exchange failed ({why})", missing, gen, phase)
+            time.sleep(20e-6)
 
     def _st(self, rank):
         return self.stream(rank).cuda_stream

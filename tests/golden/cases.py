@@ -65,6 +65,13 @@ STEP_CASES = [
     _c("p4", "ps_efficient", 8, "laplace", iteration=1, seed=44),
     _c("p5", "ps", 4, "ties", zero_mode="exact-ternary", seed=45),
     _c("p6", "ps_efficient", 5, "ties", iteration=1, seed=46),
+    # ps / ps_efficient over a QuantSpec: the int64 sum of apply_sign or
+    # quantize outputs (optimizer.py:151-158), ternary zeros included
+    _c("ps1", "ps", 4, "ties", bits=1, zero_mode="exact-ternary", seed=71),
+    _c("ps2", "ps_efficient", 3, "zeros", bits=1, seed=72),
+    _c("ps3", "ps", 2, "laplace", iteration=1, bits=5, seed=73),
+    _c("ps4", "ps_efficient", 8, "outliers", bits=3, zero_mode="exact-ternary", seed=74),
+    _c("ps5", "ps", 1, "zeros", bits=1, zero_mode="exact-ternary", seed=75),
     # selective momentum sync (optimizer.py:244-258) after the step
     _c("s1", "compressed1bit", 4, "laplace", iteration=9, seed=51,
        sync=(10, ["a.weight", "d"])),

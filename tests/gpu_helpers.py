@@ -78,6 +78,21 @@ def run_step_case(case: dict, theta, ms, gs, mask=None, transport=None,
     return lc.run_ranks(world, fn, transport=transport)
 
 
+# Exchange modes of the simulated multi-rank tests (P ranks on one GPU):
+#   peer-memory -- kernels store into the peers' buffers, host rendezvous
+#                  between phases (one shared stream);
+#   collectives -- the NCCL-path structure (all-to-all / reduce-scatter /
+#                  allgather) as device copies;
+#   fused       -- the production NVLink path: per-rank streams, in-kernel
+#                  epoch barriers, k_vote_apply / k_vote_update / replicated
+#                  K1 (run without metrics_out, which selects the plain vote).
+EXCHANGES = ["peer-memory", "collectives", "fused"]
+
+
+def make_transport(world: int, mode: str):
+    return lc.LocalTransport(world, p2p=mode != "collectives", fused=mode == "fused")
+
+
 def assert_f32_equal(got, ref64, what=""):
     """The CUDA state is fp32; the reference keeps float64.  The step computes
     in float64 and rounds once, so it must equal float32(reference) exactly

@@ -65,14 +65,14 @@ def main():
     cnt = max(0, min(s, n - rank * s))
     local_out = _lib.table([vec.local.data_ptr()])
     timed("pull", lambda: _lib.call("lc_mean_pull_f32", _lib.table(vec.peers), world,
-                                    rank * s, cnt, _lib.table([stage.local.data_ptr()]), 1, st),
+                                    rank * s, cnt, _lib.table([stage.local.data_ptr()]), 1, None, st),
           (world - 1) * cnt * 4)
     if vec.mc:
         timed("mcast", lambda: _lib.call("lc_mean_pull_f32", local_out, 1, rank * s, cnt,
-                                         _lib.table([vec.mc]), -1, st), cnt * 4)
+                                         _lib.table([vec.mc]), -1, None, st), cnt * 4)
     peers_out = _lib.table(vec.peers)
     timed("store_all", lambda: _lib.call("lc_mean_pull_f32", local_out, 1, rank * s, cnt,
-                                         peers_out, world, st), (world - 1) * cnt * 4)
+                                         peers_out, world, None, st), (world - 1) * cnt * 4)
     if rank == 0:
         res["n"] = n
         res["world"] = world

@@ -9,7 +9,7 @@ import pytest
 import torch
 
 from tests import golden_io as G
-from tests.gpu_helpers import assert_f32_equal, grads_like, make_state
+from tests.gpu_helpers import EXCHANGES, assert_f32_equal, grads_like, make_state, make_transport
 
 pytestmark = pytest.mark.gpu
 
@@ -24,9 +24,9 @@ def _need_gpu():
     _lib.load()
 
 
-@pytest.mark.parametrize("p2p", [True, False], ids=["peer-memory", "collectives"])
+@pytest.mark.parametrize("xchg", EXCHANGES)
 @pytest.mark.parametrize("i", range(len(G.metrics_golden()[1]["signsgd"])))
-def test_signsgd_and_divergence_match_reference(i, p2p):
+def test_signsgd_and_divergence_match_reference(i, xchg):
     sizes = G.step_sizes()
     c = G.signsgd_case(i, sizes)
     h = lc.LionHyper(beta1=0.9, beta2=0.99, lr=1e-3, weight_decay=0.1)
@@ -44,7 +44,7 @@ def test_signsgd_and_divergence_match_reference(i, p2p):
         return ({k: v.cpu().numpy() for k, v in st2.params.items()},
                 {k: v.cpu().numpy() for k, v in st2.momentum.items()}, div, st2.iteration)
 
-    res = lc.run_ranks(c["world"], fn, transport=lc.LocalTransport(c["world"], p2p=p2p))
+    res = lc.run_ranks(c["world"], fn, transport=make_transport(c["world"], xchg))
     for r, (th, m, div, it) in enumerate(res):
         assert it == c["iteration"] + 1
         for k in sizes:

@@ -16,7 +16,8 @@ import torch
 from oracle import lioncub_oracle as O
 from tests import golden_io as G
 from tests.golden.cases import quant_kwargs
-from tests.gpu_helpers import assert_f32_equal, run_step_case, step_seeds
+from tests.gpu_helpers import (EXCHANGES, assert_f32_equal, make_transport, run_step_case,
+                               step_seeds)
 
 pytestmark = pytest.mark.gpu
 
@@ -34,20 +35,23 @@ def _need_gpu():
 STEP_NAMES = [c["name"] for c in G.step_cases()]
 
 
-@pytest.mark.parametrize("p2p", [True, False], ids=["peer-memory", "collectives"])
+@pytest.mark.parametrize("xchg", EXCHANGES)
 @pytest.mark.parametrize("name", STEP_NAMES)
-def test_step_matches_reference_golden(name, p2p):
+def test_step_matches_reference_golden(name, xchg):
     """Both exchange modes: kernels storing into peers' buffers (NVLink
     path) and the collective path (NCCL path), simulated ranks on one GPU."""
     gc = G.step_case(name)
     case = gc["case"]
     res = run_step_case(case, gc["theta"], gc["m"], gc["g"], mask=gc["mask"],
-                        transport=lc.LocalTransport(case["world"], p2p=p2p))
+                        transport=make_transport(case["world"], xchg),
+                        metrics=xchg != "fused")
     for r, (th, m, met, it) in enumerate(res):
         assert it == case["iteration"] + 1
         for k in gc["sizes"]:
             assert_f32_equal(th[k], gc["theta_out"][k], f"{name} theta {k} r{r}")
             assert_f32_equal(m[k], gc["m_out"][r][k], f"{name} m {k} r{r}")
+            if met is None:   # fused exchange: the production kernels, no metrics
+                continue
             assert np.array_equal(met["vote_sign"][k], gc["sign"][k]), (name, k)
             assert met["ties"][k] == gc["ties"][k], (name, k, met["ties"][k])
             if gc["c"][r][k] is not None:
@@ -198,7 +202,7 @@ def test_collective_matches_reference_golden(name):
 BIG = {"emb": (40_000,), "h0.w": (300_017,), "h1.w": (262_144,), "norm": (1_000,)}
 
 
-@pytest.mark.parametrize("p2p", [True, False], ids=["peer-memory", "collectives"])
+@pytest.mark.parametrize("xchg", EXCHANGES)
 @pytest.mark.parametrize("algo,bits,world,kind,zm", [
     ("compressed1bit", None, 4, "laplace", "alternating"),
     ("compressed1bit", None, 8, "ties", "alternating"),
@@ -211,7 +215,7 @@ BIG = {"emb": (40_000,), "h0.w": (300_017,), "h1.w": (262_144,), "norm": (1_000,
     ("compressed1bit", None, 1, "laplace", "alternating"),
     ("direct", 5, 1, "outliers", "alternating"),
 ])
-def test_step_matches_oracle_large(algo, bits, world, kind, zm, p2p):
+def test_step_matches_oracle_large(algo, bits, world, kind, zm, xchg):
     ranks = O.synth_rank_inputs(7, world, BIG, kind)
     h = O.Hyper(0.9, 0.99, 1e-4, 0.1)
     spec = None if bits is None else O.Spec(bits)
@@ -223,13 +227,15 @@ def test_step_matches_oracle_large(algo, bits, world, kind, zm, p2p):
                 zero_mode=zm)
     res = run_step_case(case, ranks[0]["theta"], [rk["m"] for rk in ranks],
                         [rk["g"] for rk in ranks],
-                        transport=lc.LocalTransport(world, p2p=p2p))
+                        transport=make_transport(world, xchg),
+                        metrics=xchg != "fused")
     for r, (th, m, met, _) in enumerate(res):
         for k in BIG:
             assert_f32_equal(th[k], nt[0][k], f"theta {k}")
             assert_f32_equal(m[k], nm[r][k], f"m {k}")
-            assert np.array_equal(met["vote_sign"][k], sign[k])
-            assert met["ties"][k] == ties[k]
+            if met is not None:
+                assert np.array_equal(met["vote_sign"][k], sign[k])
+                assert met["ties"][k] == ties[k]
 
 
 QVARIANTS = [
@@ -242,10 +248,10 @@ QVARIANTS = [
 ]
 
 
-@pytest.mark.parametrize("p2p", [True, False], ids=["peer-memory", "collectives"])
+@pytest.mark.parametrize("xchg", EXCHANGES)
 @pytest.mark.parametrize("world", [1, 4])
 @pytest.mark.parametrize("qi", range(len(QVARIANTS)))
-def test_quant_variants_match_oracle_large(qi, world, p2p):
+def test_quant_variants_match_oracle_large(qi, world, xchg):
     """Every exactly-reproducible quantizer variant at 600K params: max norm,
     p = 2 / 0.5, log map, no_zero, and stochastic rounding -- the latter
     bit-exact against the oracle fed the same counter-based stream (its
@@ -264,11 +270,13 @@ def test_quant_variants_match_oracle_large(qi, world, p2p):
                 rng_seed=500)
     res = run_step_case(case, ranks[0]["theta"], [rk["m"] for rk in ranks],
                         [rk["g"] for rk in ranks],
-                        transport=lc.LocalTransport(world, p2p=p2p))
+                        transport=make_transport(world, xchg),
+                        metrics=xchg != "fused")
     for r, (th, m, met, _) in enumerate(res):
         for k in BIG:
-            assert np.array_equal(met["vote_sign"][k], sign[k]), (k, r)
-            assert met["ties"][k] == ties[k]
+            if met is not None:
+                assert np.array_equal(met["vote_sign"][k], sign[k]), (k, r)
+                assert met["ties"][k] == ties[k]
             assert_f32_equal(th[k], nt[0][k], f"theta {k}")
             assert_f32_equal(m[k], nm[r][k], f"m {k}")
 
@@ -306,8 +314,8 @@ def test_stochastic_rounding_is_unbiased():
     assert abs(up[lo].mean() - scaled[lo].mean()) < 5e-3
 
 
-@pytest.mark.parametrize("p2p", [True, False], ids=["peer-memory", "collectives"])
-def test_momentum_sync_matches_oracle_large(p2p):
+@pytest.mark.parametrize("xchg", EXCHANGES)
+def test_momentum_sync_matches_oracle_large(xchg):
     world = 8
     ranks = O.synth_rank_inputs(3, world, BIG, "laplace")
     h = O.Hyper(0.9, 0.99, 1e-4, 0.0)
@@ -318,7 +326,7 @@ def test_momentum_sync_matches_oracle_large(p2p):
                 iteration=9, zero_mode="alternating", sync=(10, ["emb", "h1.w"]))
     res = run_step_case(case, ranks[0]["theta"], [rk["m"] for rk in ranks],
                         [rk["g"] for rk in ranks], metrics=False,
-                        transport=lc.LocalTransport(world, p2p=p2p))
+                        transport=make_transport(world, xchg))
     for r, (_, m, _, _) in enumerate(res):
         for k in BIG:
             assert_f32_equal(m[k], synced[r][k], f"m {k} r{r}")
@@ -334,7 +342,7 @@ EDGE_SIZES = [
 ]
 
 
-@pytest.mark.parametrize("p2p", [True, False], ids=["peer-memory", "collectives"])
+@pytest.mark.parametrize("xchg", EXCHANGES)
 @pytest.mark.parametrize("si", range(len(EDGE_SIZES)))
 @pytest.mark.parametrize("algo,bits,world,zm", [
     ("compressed1bit", None, 3, "alternating"),
@@ -344,7 +352,7 @@ EDGE_SIZES = [
     ("ps_efficient", None, 4, "alternating"),
     ("direct", 5, 1, "alternating"),
 ])
-def test_edge_sizes_match_oracle(algo, bits, world, zm, si, p2p):
+def test_edge_sizes_match_oracle(algo, bits, world, zm, si, xchg):
     """Vectors smaller than one owner block / one warp tile / one word, and
     layer boundaries off the 32- and 1024-element grids: most ranks own
     nothing and every tail path runs."""
@@ -357,23 +365,25 @@ def test_edge_sizes_match_oracle(algo, bits, world, zm, si, p2p):
         h, spec, algo, 4, zero_mode=zm)
     case = dict(world=world, lr=1e-3, wd=0.1, bits=bits, algo=algo, iteration=4, zero_mode=zm)
     res = run_step_case(case, ranks[0]["theta"], [rk["m"] for rk in ranks],
-                        [rk["g"] for rk in ranks], transport=lc.LocalTransport(world, p2p=p2p))
+                        [rk["g"] for rk in ranks], transport=make_transport(world, xchg),
+                        metrics=xchg != "fused")
     for r, (th, m, met, _) in enumerate(res):
         for k in sizes:
             assert_f32_equal(th[k], nt[0][k], f"theta {k}")
             assert_f32_equal(m[k], nm[r][k], f"m {k}")
-            assert np.array_equal(met["vote_sign"][k].reshape(-1), sign[k].reshape(-1))
-            assert met["ties"][k] == ties[k]
+            if met is not None:
+                assert np.array_equal(met["vote_sign"][k].reshape(-1), sign[k].reshape(-1))
+                assert met["ties"][k] == ties[k]
 
 
-@pytest.mark.parametrize("p2p", [True, False], ids=["peer-memory", "collectives"])
+@pytest.mark.parametrize("xchg", EXCHANGES)
 @pytest.mark.parametrize("algo,bits,world,zm,sync", [
     ("compressed1bit", None, 4, "alternating", (2, ["emb"])),
     ("direct", 1, 3, "alternating", None),
     ("direct", 5, 4, "exact-ternary", (3, "all")),
     ("ps", None, 2, "exact-ternary", None),
 ])
-def test_multi_step_trajectory_matches_oracle(algo, bits, world, zm, sync, p2p):
+def test_multi_step_trajectory_matches_oracle(algo, bits, world, zm, sync, xchg):
     """Six consecutive steps on the device-resident state (workspaces,
     epochs and symmetric buffers reused) against the oracle fed the fp32-
     rounded state each step -- the fp32-state contract of DESIGN.md."""
@@ -397,15 +407,17 @@ def test_multi_step_trajectory_matches_oracle(algo, bits, world, zm, sync, p2p):
     case = dict(world=world, lr=1e-3, wd=0.1, bits=bits, algo=algo, iteration=it0,
                 zero_mode=zm, sync=sync)
     res = run_step_case(case, ranks[0]["theta"], [rk["m"] for rk in ranks],
-                        [rk["g"] for rk in ranks], transport=lc.LocalTransport(world, p2p=p2p),
+                        [rk["g"] for rk in ranks], transport=make_transport(world, xchg),
+                        metrics=xchg != "fused",
                         steps=steps)
     for r, (th, m, met, it) in enumerate(res):
         assert it == it0 + steps
         for k in sizes:
             assert_f32_equal(th[k], thetas[r][k], f"theta {k} r{r}")
             assert_f32_equal(m[k], moms[r][k], f"m {k} r{r}")
-            assert np.array_equal(met["vote_sign"][k], sign[k])
-            assert met["ties"][k] == ties[k]
+            if met is not None:
+                assert np.array_equal(met["vote_sign"][k], sign[k])
+                assert met["ties"][k] == ties[k]
 
 
 # ---- reference error behaviour ---------------------------------------------
@@ -562,13 +574,13 @@ def test_l1_norms_bit_exact_large(sizes):
         _lib.load().lc_l1_plan_destroy(plan.value)
 
 
-@pytest.mark.parametrize("p2p", [True, False], ids=["peer-memory", "collectives"])
+@pytest.mark.parametrize("xchg", EXCHANGES)
 @pytest.mark.parametrize("algo,bits,world,chunk", [
     ("compressed1bit", None, 1, 65536), ("direct", 1, 1, 1 << 20), ("direct", 5, 1, 4096),
     ("compressed1bit", None, 3, 65536), ("direct", 1, 4, 3 * 1024), ("direct", 5, 2, 65536),
     ("ps", None, 2, 100_000),
 ])
-def test_host_buffer_step_matches_device_step(algo, bits, world, chunk, p2p):
+def test_host_buffer_step_matches_device_step(algo, bits, world, chunk, xchg):
     """distributed_lion_step_host (pipelined pinned-host grads in, theta out)
     == distributed_lion_step on device buffers, bit for bit."""
     sizes = {"a": (150_001,), "b": (7,), "c": (65_536,)}
@@ -577,7 +589,7 @@ def test_host_buffer_step_matches_device_step(algo, bits, world, chunk, p2p):
                 zero_mode="alternating")
     ref = run_step_case(case, ranks[0]["theta"], [r["m"] for r in ranks],
                         [r["g"] for r in ranks], metrics=False,
-                        transport=lc.LocalTransport(world, p2p=p2p))
+                        transport=make_transport(world, xchg))
     h = lc.LionHyper(0.9, 0.99, 1e-3, 0.1)
     spec = None if bits is None else lc.QuantSpec(bits=bits)
     names = sorted(sizes)
@@ -593,7 +605,7 @@ def test_host_buffer_step_matches_device_step(algo, bits, world, chunk, p2p):
         topo.stream.synchronize()
         return out.numpy().copy(), {k: v.cpu().numpy() for k, v in st.momentum.items()}
 
-    got = lc.run_ranks(world, fn, transport=lc.LocalTransport(world, p2p=p2p))
+    got = lc.run_ranks(world, fn, transport=make_transport(world, xchg))
     for r in range(world):
         th_flat, mom = got[r]
         exp_th = np.concatenate([ref[r][0][k] for k in names])
