@@ -166,7 +166,7 @@ def step_roofline(n: int, P: int, F: int, kind: str, sync_frac: float,
     else:
         hbm = 36.0 * n
         nvl = (P - 1) / P * n * 8.0 + (P - 1) / P * n / 8.0
-    if sync_frac:
+    if sync_frac and P > 1:   # one rank: the mean of one row is the row (no-op)
         hbm += 16.0 * sync_frac * n
         nvl += sync_frac * 2 * (P - 1) / P * 4.0 * n
     t_h = hbm / (hbm_gbs * 1e9)

@@ -1278,6 +1278,15 @@ k_vote_update(const uint32_t* __restrict__ rows, int64_t stride, int P, float* _
   if (flag) atomicOr(flags, flag);
 }
 
+// An empty launch that still takes part in the in-kernel barriers: a rank
+// whose share of a phase is empty (an owner block past the end of a short
+// vector) must publish its epoch all the same, or its peers time out.
+__global__ void k_sync_only(SyncD sy) {
+  griddep_wait();
+  sync_wait(sy);
+  sync_arrive(sy);
+}
+
 }  // namespace lc
 
 // ===========================================================================
@@ -1357,6 +1366,15 @@ int dispatch_fields(int F, const float* g, float* m, const uint8_t* mask, int64_
   }
 }
 
+// Nothing to compute, but the launch's barrier role stays (k_sync_only).
+int sync_only(const lc_sync* sync, void* stream) {
+  if (!sync || (!sync->wait_epoch && !sync->arrive_epoch)) return LC_OK;
+  LC_CUDA_TRY(launch_pdl(k_sync_only, 1, 32, 0, reinterpret_cast<cudaStream_t>(stream),
+                         to_syncd(sync)));
+  LC_LAUNCH_CHECK();
+  return LC_OK;
+}
+
 // Build a Dst table from a host array of nd pointers (nd <= LC_MAX_BLOCKS).
 bool make_dst(Dst& d, void* const* ptrs, int nd) {
   if (nd < 1 || nd > LC_MAX_BLOCKS || !ptrs) return false;
@@ -1392,7 +1410,7 @@ int lc_encode(const float* g, float* m, const uint8_t* mask, int64_t n,
               const lc_segments* segs, void* const* dst, int32_t nblocks, int64_t L,
               int64_t eoff, uint32_t* flags, const lc_sync* sync, void* stream) {
   if (n < 0 || !hp || !flags) return set_err(LC_E_ARG, "lc_encode: bad arguments");
-  if (n == 0) return LC_OK;
+  if (n == 0) return sync_only(sync, stream);
   if (!g || !m) return set_err(LC_E_ARG, "lc_encode: null pointer");
   if (!aligned16(g) || !aligned16(m)) return set_err(LC_E_ARG, "lc_encode: g/m must be 16-byte aligned");
   const bool rep = (enc & LC_ENC_REPLICATE) != 0;
@@ -1433,7 +1451,7 @@ int lc_apply_update(float* theta, int64_t n, void* const* sign_bits, void* const
                     int32_t nsrc, int64_t wpb, int64_t woff, double lr, double wd,
                     const lc_sync* sync, void* stream) {
   if (n < 0) return set_err(LC_E_ARG, "lc_apply_update: n < 0");
-  if (n == 0) return LC_OK;
+  if (n == 0) return sync_only(sync, stream);
   Dst sb, zb;
   if (!theta || !make_dst(sb, sign_bits, nsrc) || (nz_bits && !make_dst(zb, nz_bits, nsrc)))
     return set_err(LC_E_ARG, "lc_apply_update: bad pointers / source table");
@@ -1522,7 +1540,7 @@ int lc_vote_bits(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid, i
                  int32_t nout, uint32_t* flags, const lc_sync* sync, void* stream) {
   if (P < 1 || P > 255 || cw < 0 || (cw % 4) != 0 || !flags)
     return set_err(LC_E_ARG, "lc_vote_bits: P must be in [1,255], cw a multiple of 4");
-  if (cw == 0) return LC_OK;
+  if (cw == 0) return sync_only(sync, stream);
   VoteOut o;
   if (!recv || !make_out(o, voted, nz, tie_bits, nout))
     return set_err(LC_E_ARG, "lc_vote_bits: bad pointers / output table");
@@ -1582,7 +1600,7 @@ int lc_vote_update(const uint32_t* rows, int64_t row_stride, int32_t P, float* t
                    int fill, int sum_mode, double lr, double wd, uint32_t* flags,
                    const lc_sync* sync, void* stream) {
   if (n < 0 || P < 1 || P > 255 || !flags) return set_err(LC_E_ARG, "lc_vote_update: bad arguments");
-  if (n == 0) return LC_OK;
+  if (n == 0) return sync_only(sync, stream);
   if (!rows || !theta || row_stride < (n + 31) / 32)
     return set_err(LC_E_ARG, "lc_vote_update: null pointer / rows shorter than ceil(n/32)");
   if (!aligned16(theta)) return set_err(LC_E_ARG, "lc_vote_update: theta must be 16-byte aligned");
@@ -1616,7 +1634,7 @@ int lc_fields_vote(const uint32_t* sums, int32_t rows, int64_t row_stride, int64
                    void* const* voted, void* const* nz, void* const* tie_bits, int32_t nout,
                    int64_t* values, const lc_sync* sync, void* stream) {
   if (n < 0 || P < 1 || rows < 1) return set_err(LC_E_ARG, "lc_fields_vote: bad arguments");
-  if (n == 0) return LC_OK;
+  if (n == 0) return sync_only(sync, stream);
   VoteOut o;
   if (!sums || !make_out(o, voted, nz, tie_bits, nout))
     return set_err(LC_E_ARG, "lc_fields_vote: bad pointers / output table");
@@ -1660,7 +1678,7 @@ int lc_f64_sum_vote(const double* recv, int32_t P, int64_t len, int64_t stride, 
                     double* values, const lc_sync* sync, void* stream) {
   if (len < 0 || P < 1 || (tree && P > 64) || nout > 32)
     return set_err(LC_E_ARG, "lc_f64_sum_vote: bad arguments");
-  if (len == 0) return LC_OK;
+  if (len == 0) return sync_only(sync, stream);
   VoteOut o;
   if (!recv || !make_out(o, voted, nz, tie_bits, nout))
     return set_err(LC_E_ARG, "lc_f64_sum_vote: bad pointers / output table");

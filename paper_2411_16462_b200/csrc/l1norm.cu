@@ -20,6 +20,9 @@
 #include <map>
 #include <vector>
 
+#include <map>
+#include <mutex>
+
 #include "common.cuh"
 
 namespace {
@@ -623,12 +626,44 @@ int norm_kind(double p) {
   return PK_GEN;
 }
 
+// Plan tables live in stream-ordered allocations on a private non-blocking
+// stream: creating or destroying a plan never synchronises the device (a
+// cudaFree would wait for every stream -- including kernels of other ranks
+// spinning on an in-kernel barrier for this thread's next launch).
+cudaStream_t plan_stream() {
+  static std::mutex mu;
+  static std::map<int, cudaStream_t> streams;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = streams.find(dev);
+  if (it != streams.end()) return it->second;
+  cudaStream_t s = nullptr;
+  cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  streams.emplace(dev, s);
+  return s;
+}
+
+template <typename T>
+int dev_alloc(T** dst, size_t bytes) {
+  LC_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(dst), bytes, plan_stream()));
+  return LC_OK;
+}
+
 template <typename T>
 int upload(T** dst, const std::vector<T>& v) {
   size_t bytes = std::max<size_t>(1, v.size()) * sizeof(T);
-  LC_CUDA_TRY(cudaMalloc(dst, bytes));
-  if (!v.empty()) LC_CUDA_TRY(cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  LC_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(dst), bytes, plan_stream()));
+  if (!v.empty())
+    LC_CUDA_TRY(cudaMemcpyAsync(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice,
+                                plan_stream()));
+  // pageable source: wait for this copy only (the plan stream), not the device
+  LC_CUDA_TRY(cudaStreamSynchronize(plan_stream()));
   return LC_OK;
+}
+
+void dev_free(void* p) {
+  if (p) cudaFreeAsync(p, plan_stream());
 }
 
 }  // namespace
@@ -637,23 +672,23 @@ extern "C" {
 
 int lc_l1_plan_destroy(lc_l1_plan_t p) {
   if (!p) return LC_OK;
-  cudaFree(p->d_seg_start);
-  cudaFree(p->d_seg);
-  cudaFree(p->d_tmpl);
-  cudaFree(p->d_leaf_rel);
-  cudaFree(p->d_leaf_size);
-  cudaFree(p->d_tops);
-  cudaFree(p->d_tlvl);
-  cudaFree(p->d_uops);
-  cudaFree(p->d_ulvl);
-  cudaFree(p->d_wi_off);
-  cudaFree(p->d_wi_meta);
-  cudaFree(p->d_wi_leaf0);
-  cudaFree(p->d_lf_start);
-  cudaFree(p->d_lf_meta);
-  cudaFree(p->d_lf_sum);
-  cudaFree(p->d_nodes);
-  cudaFree(p->d_max);
+  dev_free(p->d_seg_start);
+  dev_free(p->d_seg);
+  dev_free(p->d_tmpl);
+  dev_free(p->d_leaf_rel);
+  dev_free(p->d_leaf_size);
+  dev_free(p->d_tops);
+  dev_free(p->d_tlvl);
+  dev_free(p->d_uops);
+  dev_free(p->d_ulvl);
+  dev_free(p->d_wi_off);
+  dev_free(p->d_wi_meta);
+  dev_free(p->d_wi_leaf0);
+  dev_free(p->d_lf_start);
+  dev_free(p->d_lf_meta);
+  dev_free(p->d_lf_sum);
+  dev_free(p->d_nodes);
+  dev_free(p->d_max);
   delete p;
   return LC_OK;
 }
@@ -784,11 +819,12 @@ int lc_l1_plan_create(lc_l1_plan_t* out, const int64_t* seg_start, int32_t nseg)
     lc_l1_plan_destroy(p);
     return rc;
   }
-  if (cudaMalloc(&p->d_nodes, sizeof(double) * std::max(1, p->n_nodes)) != cudaSuccess ||
-      cudaMalloc(&p->d_max, sizeof(unsigned long long) * nseg) != cudaSuccess ||
-      cudaMalloc(&p->d_lf_sum, sizeof(double) * std::max<int64_t>(1, p->n_leaves)) != cudaSuccess) {
+  if (dev_alloc(&p->d_nodes, sizeof(double) * std::max(1, p->n_nodes)) != LC_OK ||
+      dev_alloc(&p->d_max, sizeof(unsigned long long) * nseg) != LC_OK ||
+      dev_alloc(&p->d_lf_sum, sizeof(double) * std::max<int64_t>(1, p->n_leaves)) != LC_OK ||
+      cudaStreamSynchronize(plan_stream()) != cudaSuccess) {
     lc_l1_plan_destroy(p);
-    return lc::set_err(LC_E_CUDA, "lc_l1_plan_create: cudaMalloc failed");
+    return lc::set_err(LC_E_CUDA, "lc_l1_plan_create: cudaMallocAsync failed");
   }
   *out = p;
   return LC_OK;

@@ -227,13 +227,15 @@ class _PeerSync:
     timeout: float = DEFAULT_TIMEOUT
 
     def _flags(self, rank):
-        flags = self.sym_buffer(rank, ("__barrier__",), self.world_size, torch.int64)
         if rank not in self._err:
+            # allocate before the rendezvous: once any rank is past it, its
+            # kernels may spin on this rank, and a pinned (cudaHostAlloc)
+            # allocation may wait for the device
             dev = self.device(rank)
             self._err[rank] = torch.zeros(2, dtype=torch.int32, device=dev)
             self._err_host[rank] = torch.zeros(2, dtype=torch.int32, pin_memory=True)
             self._epoch[rank] = 0
-        return flags
+        return self.sym_buffer(rank, ("__barrier__",), self.world_size, torch.int64)
 
     def error_word(self, rank) -> int:
         """Device address of this rank's barrier error words (2 x uint32)."""
@@ -295,6 +297,12 @@ class _PeerSync:
             return
         bits, miss = self.error_state(rank)
         if bits & _lib.LC_FLAG_BARRIER_TIMEOUT:
+            if os.environ.get("LIONCUB_DEBUG_BARRIER"):
+                import sys
+                fl = self._flags(rank)
+                print(f"[lioncub] rank {rank} phase {phase} epoch {self._epoch[rank]} "
+                      f"flags {fl.local.tolist()} err {self._err[rank].tolist()}",
+                      file=sys.stderr)
             self.fail(rank, "a peer never reached the step barrier", miss, gen, phase)
 
 
@@ -348,7 +356,11 @@ class LocalTransport(_PeerSync, DeviceTransport):
         if k not in self._sym:
             t = torch.zeros(max(numel, 1), dtype=dtype, device=self.dev)
             if self.fused:
-                torch.cuda.synchronize(self.dev)  # zeroed before a peer stream writes
+                # zeroed before a peer stream may write into it: wait for THIS
+                # rank's stream only (a device-wide synchronize would also wait
+                # for peers' kernels spinning on a barrier this rank has yet to
+                # join)
+                torch.cuda.current_stream(self.dev).synchronize()
             posts = self._exchange(rank, 0, "sym_buffer", t.data_ptr(), order=False)
             peers = list(posts)
             self._done(rank, 0, "sym_buffer", order=False)
@@ -369,10 +381,13 @@ class LocalTransport(_PeerSync, DeviceTransport):
     def stream(self, rank):
         if not self.fused:
             return self._stream
-        if getattr(self._tls, "div", None) != self.world_size:
-            # this rank thread's launches get 1/P of the SMs
-            _lib.check(_lib.load().lc_set_grid_divisor(self.world_size), "lc_set_grid_divisor")
-            self._tls.div = self.world_size
+        div = 2 * self.world_size
+        if getattr(self._tls, "div", None) != div:
+            # this rank thread's launches get 1/(2P) of the SMs: the P ranks'
+            # barrier-waiting grids plus a late rank's running kernel always
+            # fit on the GPU together, whatever the CTA placement
+            _lib.check(_lib.load().lc_set_grid_divisor(div), "lc_set_grid_divisor")
+            self._tls.div = div
         return self._streams[rank]
 
     def _exchange(self, rank, gen, phase, post, order=True):

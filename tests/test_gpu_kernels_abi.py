@@ -135,14 +135,20 @@ def test_vote_apply_abi_matches_oracle(P, n, algo, bits, zm, kind):
     finally:
         _lib.check(lib.lc_set_grid_divisor(1))
     torch.cuda.synchronize()
-    words = O.pack_signs(np.where(sign_ref == 0, 1, sign_ref))
+    # sign bit = voted +1 (a zero aggregate has bit 0 and nz 0 in ternary)
+    words = O.pack_words((sign_ref > 0).astype(np.int64), 1)
     nzw = O.pack_words((sign_ref != 0).astype(np.int64), 1)
+    # bits past n in the last word are wire padding (voted +1): compare valid bits
+    valid = np.full(words.size, 0xFFFFFFFF, np.uint32)
+    if n % 32:
+        valid[-1] = (1 << (n % 32)) - 1
     for k in range(P):
         assert R.err[k].tolist() == [0, 0], f"rank {k} barrier error {R.err[k].tolist()}"
         got = R.full[k].cpu().numpy().view(np.uint32)[:words.size]
-        assert np.array_equal(got, words), f"gather buffer of rank {k}"
+        assert np.array_equal(got & valid, words & valid), f"gather buffer of rank {k}"
         if nzmode:
-            assert np.array_equal(R.nz[k].cpu().numpy().view(np.uint32)[:nzw.size], nzw)
+            gz = R.nz[k].cpu().numpy().view(np.uint32)[:nzw.size]
+            assert np.array_equal(gz & valid, nzw & valid)
         assert_f32_equal(R.theta[k].cpu().numpy(), th_ref, f"theta r{k}")
         assert_f32_equal(R.m[k].cpu().numpy(), m_ref[k], f"m r{k}")
         assert int(R.kflags[k][0]) == 0
@@ -172,7 +178,10 @@ def test_replicate_encode_and_vote_update_abi_match_oracle(P, n, algo, bits, zm,
         for r in range(P):
             s = O.apply_sign(cs[r], "alternating" if fill else "exact-ternary", it + 1)
             ref = O.pack_signs(np.where(s == 0, 1, s))
-            assert np.array_equal(got[r, :ref.size], ref), f"row {r} on rank {k}"
+            valid = np.full(ref.size, 0xFFFFFFFF, np.uint32)
+            if n % 32:
+                valid[-1] = (1 << (n % 32)) - 1
+            assert np.array_equal(got[r, :ref.size] & valid, ref & valid), f"row {r} on rank {k}"
     th_ref, m_ref, _ = R.oracle(algo, None if bits is None else O.Spec(bits), it, zm)
     for r in range(P):
         _lib.call("lc_vote_update", rows[r].data_ptr(), row, P, R.theta[r].data_ptr(), n, fill,
