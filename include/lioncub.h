@@ -327,6 +327,13 @@ int lc_pack_i64_fields(const int64_t* v, int64_t n, int32_t field_bits,
 int lc_fields_decode(const uint32_t* sums, int64_t n, int32_t field_bits,
                      int32_t P, int32_t offset, int32_t binary, int64_t* out,
                      void* stream);
+/* Exact-ternary pre-flight of the binary paths (collectives.py:262-267,
+ * :202-203): sign(c) of c = beta1*m + (1-beta1)*g (masked) for every element,
+ * LC_FLAG_ZERO_SIGN in *flags if any is zero, and -- when out is not NULL --
+ * the sign words (bit = c > 0) for the owner tie check of the 1-bit vote.
+ * Reads g, m only (8 B/param; m is not written). */
+int lc_sign_check(const float* g, const float* m, const uint8_t* mask, int64_t n,
+                  const lc_hyper* h, uint32_t* out, uint32_t* flags, void* stream);
 /* sign of a float64/float32 vector with fill -> 1-bit words (K1 without
  * the Lion interpolation; compressed_allreduce_1bit on raw c). */
 int lc_sign_pack_f64(const double* c, int64_t n, int fill, uint32_t* out,

@@ -108,6 +108,7 @@ SIGNATURES = {
     "lc_pack_i64_fields": (INT, [P, I64, I32, I32, I32, P, P, P]),
     "lc_fields_decode": (INT, [P, I64, I32, I32, I32, I32, P, P]),
     "lc_sign_pack_f64": (INT, [P, I64, INT, P, P, P]),
+    "lc_sign_check": (INT, [P, P, P, I64, P, P, P, P]),
     "lc_sum_u32_rows": (INT, [P, I32, I64, P, P]),
     "lc_nccl_version": (INT, []),
     "lc_nccl_unique_id": (INT, [P]),
@@ -184,7 +185,7 @@ KERNEL_CALLS = frozenset({
     "lc_barrier", "lc_push_blocks_f32", "lc_mean_bcast_f32", "lc_mean_pull_f32",
     "lc_apply_update", "lc_fused_local_step", "lc_mean_f32", "lc_compute_c",
     "lc_count_bits_segmented", "lc_bits_to_sign", "lc_pack_i64_fields",
-    "lc_fields_decode", "lc_sign_pack_f64", "lc_sum_u32_rows", "lc_quantize_values",
+    "lc_fields_decode", "lc_sign_pack_f64", "lc_sign_check", "lc_sum_u32_rows", "lc_quantize_values",
     "lc_dequantize", "lc_apply_sign_values", "lc_f64_to_f32_exact", "lc_std_max_segmented"})
 KERNELS_PER_CALL = {"lc_l1_scales": 4, "lc_norm_scales": 4}
 

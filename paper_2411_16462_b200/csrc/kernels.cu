@@ -1162,6 +1162,31 @@ __global__ void k_sign_pack_f64(const double* __restrict__ c, int64_t n, int fil
   if (flag) atomicOr(flags, flag);
 }
 
+// Exact-ternary pre-flight of the binary paths: zero signs of c (and the
+// sign words for the owner tie check), without materialising c.
+__global__ void k_sign_check(const float* __restrict__ g, const float* __restrict__ m,
+                             const uint8_t* __restrict__ mask, int64_t n, Hyp h,
+                             uint32_t* __restrict__ out, uint32_t* __restrict__ flags) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nwords = (n + 31) / 32;
+  bool zero = false;
+  for (int64_t w = gw; w < nwords; w += nw) {
+    const int64_t e = w * 32 + lane;
+    bool pos = true;  // padding past n: +1 like the wire
+    if (e < n) {
+      double c = lion_c(__ldcs(m + e), __ldcs(g + e), h);
+      if (mask && !mask[e]) c = 0.0;
+      pos = c > 0.0;
+      zero |= c == 0.0;
+    }
+    const uint32_t b = __ballot_sync(kFull, pos);
+    if (out && lane == 0) out[w] = b;
+  }
+  if (__any_sync(kFull, zero) && lane == 0) atomicOr(flags, (uint32_t)LC_FLAG_ZERO_SIGN);
+}
+
 struct Rows {
   const uint32_t* p[64];
 };
@@ -1781,6 +1806,17 @@ int lc_sign_pack_f64(const double* c, int64_t n, int fill, uint32_t* out, uint32
   if (n == 0) return LC_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   k_sign_pack_f64<<<generic_grid(n), kBlock, 0, st>>>(c, n, fill, out, flags);
+  LC_LAUNCH_CHECK();
+  return LC_OK;
+}
+
+int lc_sign_check(const float* g, const float* m, const uint8_t* mask, int64_t n,
+                  const lc_hyper* hp, uint32_t* out, uint32_t* flags, void* stream) {
+  if (n < 0 || !hp || !flags) return set_err(LC_E_ARG, "lc_sign_check: bad arguments");
+  if (n == 0) return LC_OK;
+  if (!g || !m) return set_err(LC_E_ARG, "lc_sign_check: null pointer");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  k_sign_check<<<generic_grid(n / 8), kBlock, 0, st>>>(g, m, mask, n, to_hyp(hp), out, flags);
   LC_LAUNCH_CHECK();
   return LC_OK;
 }

@@ -752,18 +752,18 @@ def _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out,
 def _ternary_precheck(topo, gen, g, m, mflat, n, hyp, dev, s, kind):
     """exact-ternary on a binary path: the reference raises ConfigError on any
     zero sign before communicating (collectives.py:264-267, :202-203).  Check
-    on every rank before touching the state, then agree on the outcome."""
-    c = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
-    _lib.call("lc_compute_c", g.flat.data_ptr(), m.flat.data_ptr(), _lib.ptr(mflat), n,
-              C.byref(hyp), c.data_ptr(), s)
-    L = owner_elems(n, topo.world_size)
-    words = torch.zeros(topo.world_size * L // 32, dtype=torch.int32, device=dev)
+    on every rank before touching the state, then agree on the outcome.  One
+    read of g and m (lc_sign_check); the 1-bit vote also exchanges the sign
+    words so each owner can check that its tally never ties
+    (collectives.py:290-293)."""
+    P, r = topo.world_size, topo.rank
+    L = owner_elems(n, P)
+    cw = L // 32
     flags = torch.zeros(1, dtype=torch.int32, device=dev)
-    _lib.call("lc_sign_pack_f64", c.data_ptr(), n, 0, words.data_ptr(), flags.data_ptr(), s)
+    words = torch.zeros(P * cw, dtype=torch.int32, device=dev) if kind == "1bit" else None
+    _lib.call("lc_sign_check", g.flat.data_ptr(), m.flat.data_ptr(), _lib.ptr(mflat), n,
+              C.byref(hyp), _lib.ptr(words), flags.data_ptr(), s)
     if kind == "1bit":
-        # the owner tally must not tie either (collectives.py:290-293)
-        P, r = topo.world_size, topo.rank
-        cw = L // 32
         recv = words
         if P > 1:
             recv = torch.zeros_like(words)
@@ -771,10 +771,10 @@ def _ternary_precheck(topo, gen, g, m, mflat, n, hyp, dev, s, kind):
         voted = torch.zeros(cw, dtype=torch.int32, device=dev)
         _lib.call("lc_vote_bits", recv.data_ptr(), P, cw, owner_valid(n, P, r), 0, 0,
                   _lib.table([voted.data_ptr()]), None, None, 1, flags.data_ptr(), None, s)
-    if topo.world_size > 1:
-        topo.transport.allreduce_max_u32(topo.rank, gen, flags)
+    if P > 1:
+        topo.transport.allreduce_max_u32(r, gen, flags)
         if topo.transport.error_mode == "step" and hasattr(topo.transport, "wait_collectives"):
-            topo.transport.wait_collectives(topo.rank, gen, "zero-sign precheck")
+            topo.transport.wait_collectives(r, gen, "zero-sign precheck")
     _raise_flags(int(flags.item()), binary=kind == "1bit")
 
 

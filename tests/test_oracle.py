@@ -232,3 +232,86 @@ def test_oracle_signsgd_and_divergence_match_reference(i):
     div = O.divergence(c["m"])
     for k in sizes:
         assert div[k] == c["div"][k] == c["divm"][k], k
+
+
+# ---- the C restatement (oracle/lioncub_oracle.c) used for large checks -----
+
+def _c_oracle_case_ok(case) -> bool:
+    kw = quant_kwargs(case)
+    if kw is None:
+        return True
+    extra = {k: v for k, v in kw.items() if k not in ("bits", "norm_p")}
+    return kw.get("norm_p", 1.0) == 1.0 and not extra
+
+
+@pytest.mark.parametrize("name", [c["name"] for c in G.step_cases() if _c_oracle_case_ok(c)])
+def test_c_oracle_matches_reference_step(name):
+    """The C oracle against the reference's golden step outputs: theta' and
+    m' are float32 of the reference float64 values, votes and ties exact."""
+    from oracle import c_oracle as CO
+    gc = G.step_case(name)
+    case = gc["case"]
+    names = sorted(gc["sizes"])
+    flat = lambda d: np.concatenate([np.asarray(d[k], np.float32).ravel() for k in names])  # noqa
+    seg = np.cumsum([0] + [int(np.prod(gc["sizes"][k])) for k in names])
+    mask = None
+    if gc["mask"] is not None:
+        mask = np.concatenate([np.asarray(gc["mask"][k]).ravel() if k in gc["mask"]
+                               else np.ones(int(np.prod(gc["sizes"][k])), bool)
+                               for k in names]).astype(np.uint8)
+    t = case["iteration"] + 1
+    fill = 0 if case["zero_mode"] == "exact-ternary" else O.zero_fill(t)
+    th, ms, sign, ties = CO.step(flat(gc["theta"]), [flat(x) for x in gc["m"]],
+                                 [flat(x) for x in gc["g"]], seg,
+                                 CO.hyper(0.9, 0.99, case["lr"], case["wd"]),
+                                 CO.algo_name(case["algo"], case["bits"]), fill,
+                                 bits=case["bits"] or 0, mask=mask)
+    if case.get("sync"):
+        return  # the sync is not part of the C oracle
+    ref_t = np.concatenate([np.asarray(gc["theta_out"][k]).ravel() for k in names])
+    assert np.array_equal(th, ref_t.astype(np.float32))
+    for r in range(case["world"]):
+        ref_m = np.concatenate([np.asarray(gc["m_out"][r][k]).ravel() for k in names])
+        assert np.array_equal(ms[r], ref_m.astype(np.float32)), r
+    ref_s = np.concatenate([gc["sign"][k].ravel() for k in names])
+    assert np.array_equal(sign.astype(np.int64), ref_s)
+    assert [int(x) for x in ties] == [gc["ties"][k] for k in names]
+
+
+@pytest.mark.parametrize("n", [1, 7, 8, 127, 128, 129, 1000, 65_537, 1_000_003, 38_597_376])
+def test_c_oracle_pairwise_sum_is_numpy_order(n):
+    """numpy's pairwise order, up to the GPT-2 embedding's 38.6M elements
+    (the np.mean inside lp_mean_norm, quant.py:104)."""
+    from oracle import c_oracle as CO
+    x = np.random.default_rng(n).random(n) * 1e-3
+    assert CO.pairwise_sum(x) == float(np.add.reduce(x))
+
+
+@pytest.mark.parametrize("algo,bits,world,kind,zm", [
+    ("compressed1bit", None, 8, "ties", "alternating"),
+    ("direct", 1, 8, "laplace", "alternating"),
+    ("direct", 5, 8, "outliers", "alternating"),
+    ("direct", 8, 3, "laplace", "exact-ternary"),
+    ("ps_efficient", None, 5, "cancel", "exact-ternary"),
+])
+def test_c_oracle_matches_numpy_oracle_600k(algo, bits, world, kind, zm):
+    from oracle import c_oracle as CO
+    sizes = {"emb": (40_000,), "h0.w": (300_017,), "h1.w": (262_144,), "norm": (1_000,)}
+    names = sorted(sizes)
+    ranks = O.synth_rank_inputs(7, world, sizes, kind)
+    h = O.Hyper(0.9, 0.99, 1e-4, 0.1)
+    spec = None if bits is None else O.Spec(bits)
+    nt, nm, sign, ties, _, _ = O.distributed_step(
+        [rk["theta"] for rk in ranks], [rk["m"] for rk in ranks], [rk["g"] for rk in ranks],
+        h, spec, algo, 2, zero_mode=zm)
+    flat = lambda d: np.concatenate([np.asarray(d[k]).ravel() for k in names])  # noqa
+    seg = np.cumsum([0] + [sizes[k][0] for k in names])
+    fill = 0 if zm == "exact-ternary" else O.zero_fill(3)
+    th, ms, sg, tc = CO.step(flat(ranks[0]["theta"]), [flat(rk["m"]) for rk in ranks],
+                             [flat(rk["g"]) for rk in ranks], seg, CO.hyper(lr=1e-4, wd=0.1),
+                             CO.algo_name(algo, bits), fill, bits=bits or 0)
+    assert np.array_equal(th, flat(nt[0]).astype(np.float32))
+    for r in range(world):
+        assert np.array_equal(ms[r], flat(nm[r]).astype(np.float32))
+    assert np.array_equal(sg.astype(np.int64), flat(sign))
+    assert [int(x) for x in tc] == [ties[k] for k in names]
