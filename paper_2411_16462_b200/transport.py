@@ -79,6 +79,20 @@ def _wrap(ptr: int, numel: int, dtype, dev) -> torch.Tensor:
 _SERIAL = itertools.count(1)
 
 
+def host_wait(stream=None):
+    """Block the calling host thread until ``stream`` (default: the current
+    stream) has drained -- through a CUDA event.  torch's Stream.synchronize
+    stalls every OTHER host thread's kernel launches on the device while it
+    waits (measured on B200: one launch in 1 s), which deadlocks simulated
+    ranks that still have to launch the kernels the waited-on stream spins
+    for; an event wait does not."""
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    ev = torch.cuda.Event()
+    ev.record(stream)
+    ev.synchronize()
+
+
 def _error_mode() -> str:
     m = os.environ.get("LIONCUB_ERRORS", "step")
     if m not in ("step", "deferred"):
@@ -282,7 +296,7 @@ class _PeerSync:
         sync on the rank's stream (error paths and strict steps only)."""
         if rank not in self._err:
             return 0, []
-        self.stream(rank).synchronize()
+        host_wait(self.stream(rank))
         w = self._err[rank].tolist()
         miss = [j for j in range(self.world_size) if (w[1] >> j) & 1]
         return w[0] & 0xFFFFFFFF, miss
@@ -360,7 +374,7 @@ class LocalTransport(_PeerSync, DeviceTransport):
                 # rank's stream only (a device-wide synchronize would also wait
                 # for peers' kernels spinning on a barrier this rank has yet to
                 # join)
-                torch.cuda.current_stream(self.dev).synchronize()
+                host_wait(torch.cuda.current_stream(self.dev))
             posts = self._exchange(rank, 0, "sym_buffer", t.data_ptr(), order=False)
             peers = list(posts)
             self._done(rank, 0, "sym_buffer", order=False)
@@ -567,7 +581,7 @@ class NcclTransport(_PeerSync, DeviceTransport):
         dev = self._devices[rank]
         if self._threaded:
             t = torch.zeros(max(numel, 1), dtype=dtype, device=dev)
-            torch.cuda.synchronize(dev)  # zeroed before any peer may write into it
+            host_wait(torch.cuda.current_stream(dev))  # zeroed before any peer writes into it
             self._posts[rank] = t.data_ptr()
             self._rv.wait(rank, 0, "sym_buffer:post", DEFAULT_TIMEOUT)
             peers = list(self._posts)

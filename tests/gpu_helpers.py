@@ -4,6 +4,7 @@ from __future__ import annotations
 
 import numpy as np
 import torch
+from paper_2411_16462_b200.transport import host_wait
 
 import paper_2411_16462_b200 as lc
 from paper_2411_16462_b200.optimizer import FlatParamSet
@@ -63,7 +64,7 @@ def run_step_case(case: dict, theta, ms, gs, mask=None, transport=None,
                                            rng=rng)
             if sync is not None:
                 st2 = lc.maybe_sync_momentum(st2, sync, topo)
-        torch.cuda.synchronize()
+        host_wait()
         out_t = {k: v.detach().cpu().numpy().copy() for k, v in st2.params.items()}
         out_m = {k: v.detach().cpu().numpy().copy() for k, v in st2.momentum.items()}
         out_met = None

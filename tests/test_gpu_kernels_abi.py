@@ -22,6 +22,7 @@ pytestmark = pytest.mark.gpu
 
 lc = pytest.importorskip("paper_2411_16462_b200")
 from paper_2411_16462_b200 import _lib  # noqa: E402
+from paper_2411_16462_b200.transport import host_wait  # noqa: E402
 from paper_2411_16462_b200.collectives import owner_elems, owner_valid  # noqa: E402
 
 
@@ -220,7 +221,7 @@ def test_vote_apply_large_offsets_and_double_buffered_slots():
         for _ in range(2):
             st = lc.distributed_lion_step(st, g, lc.LionHyper(lr=1e-3), None, topo,
                                           "compressed1bit")
-        torch.cuda.synchronize()
+        host_wait()
         return {k: v.cpu().numpy() for k, v in st.params.items()}
 
     res = lc.run_ranks(P, fn, transport=lc.LocalTransport(P, fused=True))
@@ -289,13 +290,13 @@ def test_step_raises_collective_error_naming_missing_rank(algo):
         g = st.new_grad_buffer()
         g["w"].copy_(torch.from_numpy(r["g"]["w"]))
         st = lc.distributed_lion_step(st, g, lc.LionHyper(lr=1e-3), spec, topo, algo)
-        torch.cuda.synchronize()
+        host_wait()
         if topo.rank == 1:
             return None                      # rank 1 dies after step 1
         before = st.params["w"].clone()
         with pytest.raises(lc.CollectiveError) as ei:
             lc.distributed_lion_step(st, g, lc.LionHyper(lr=1e-3), spec, topo, algo)
-        torch.cuda.synchronize()
+        host_wait()
         out[topo.rank] = (ei.value.rank, torch.equal(st.params["w"], before), st.iteration)
         with pytest.raises(lc.CollectiveError, match="unusable"):
             lc.distributed_lion_step(st, g, lc.LionHyper(lr=1e-3), spec, topo, algo)

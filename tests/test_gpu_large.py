@@ -35,6 +35,7 @@ pytestmark = pytest.mark.gpu
 
 lc = pytest.importorskip("paper_2411_16462_b200")
 from paper_2411_16462_b200 import _lib  # noqa: E402
+from paper_2411_16462_b200.transport import host_wait  # noqa: E402
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -138,7 +139,7 @@ def run_simulated(world, layout, theta, ms, gs, h, spec, algo, zero_mode="altern
                                       zero_mode=zero_mode)
         if sync is not None:
             st = lc.maybe_sync_momentum(st, sync, topo)
-        torch.cuda.synchronize()
+        host_wait()
         return st
 
     out = lc.run_ranks(world, fn, transport=tp)

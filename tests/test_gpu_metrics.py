@@ -15,6 +15,7 @@ pytestmark = pytest.mark.gpu
 
 lc = pytest.importorskip("paper_2411_16462_b200")
 from paper_2411_16462_b200 import _lib  # noqa: E402
+from paper_2411_16462_b200.transport import host_wait  # noqa: E402
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -39,7 +40,7 @@ def test_signsgd_and_divergence_match_reference(i, xchg):
         st2 = lc.signsgd_majority_step(st, g, h, topo, algo=c["algo"],
                                        zero_mode=c["zero_mode"])
         div = lc.momentum_divergence(st2, topo)
-        torch.cuda.synchronize()
+        host_wait()
         assert torch.equal(g.flat.view(torch.int32), g0.view(torch.int32))  # grads untouched
         return ({k: v.cpu().numpy() for k, v in st2.params.items()},
                 {k: v.cpu().numpy() for k, v in st2.momentum.items()}, div, st2.iteration)

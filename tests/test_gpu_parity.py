@@ -23,6 +23,7 @@ pytestmark = pytest.mark.gpu
 
 lc = pytest.importorskip("paper_2411_16462_b200")
 from paper_2411_16462_b200 import _lib  # noqa: E402
+from paper_2411_16462_b200.transport import host_wait  # noqa: E402
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -602,7 +603,7 @@ def test_host_buffer_step_matches_device_step(algo, bits, world, chunk, xchg):
         out = torch.empty(host_g.numel(), dtype=torch.float32).pin_memory()
         st = lc.distributed_lion_step_host(st, host_g, h, spec, topo, algo,
                                            params_out=out, chunk=chunk)
-        topo.stream.synchronize()
+        host_wait()
         return out.numpy().copy(), {k: v.cpu().numpy() for k, v in st.momentum.items()}
 
     got = lc.run_ranks(world, fn, transport=make_transport(world, xchg))
