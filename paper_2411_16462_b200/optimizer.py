@@ -966,23 +966,14 @@ def _symmetric_momentum(m: FlatParamSet, topo: Topology) -> FlatParamSet:
     buf = topo.transport.sym_buffer(topo.rank, (layout.key, "momentum", tok), max(layout.n, 1),
                                     torch.float32)
     buf.local.copy_(m.flat)
+    # one-time re-homing: let the copy land before this rank takes part in
+    # the sync's in-kernel barriers
+    from .transport import host_wait
+    host_wait(topo.stream)
     out = FlatParamSet(buf.local, layout)
     out.sym = buf
     out.workspace = m.workspace
     return out
-
-
-_DBG_T0 = None
-if os.environ.get("LIONCUB_DEBUG_BARRIER"):
-    import time as _time
-    _DBG_T0 = _time.monotonic()
-
-
-def _dbg(rank, what):
-    import sys
-    import time as _time
-    print(f"[lioncub] t={_time.monotonic() - _DBG_T0:9.4f} rank {rank}: {what}", file=sys.stderr,
-          flush=True)
 
 
 def maybe_sync_momentum(state: WorkerState, policy: SyncPolicy,
@@ -1012,17 +1003,10 @@ def maybe_sync_momentum(state: WorkerState, policy: SyncPolicy,
                 # rank's momentum over NVLink, averages (f64, rank order) and
                 # stores the mean into every rank's momentum -- one kernel per
                 # range, one barrier before (all m' final) and one after
-                dbg = _DBG_T0 is not None
-                if dbg:
-                    _dbg(r, "sync: enter")
                 m = _symmetric_momentum(m, topo)
-                if dbg:
-                    _dbg(r, "sync: momentum re-homed")
                 mc = getattr(m.sym, "mc", 0)
                 gen = topo.next_generation()
                 tp.device_barrier(r, gen)
-                if dbg:
-                    _dbg(r, "sync: barrier 1 launched")
                 src = _lib.table(m.sym.peers)
                 outs, nout = ((_lib.table([mc]), -1) if mc else
                               (_lib.table(m.sym.peers), P))
@@ -1035,8 +1019,6 @@ def maybe_sync_momentum(state: WorkerState, policy: SyncPolicy,
                     _lib.call("lc_mean_pull_f32", src, P, a + r * sr, cnt, outs, nout,
                               tp.error_word(r), st)
                 tp.device_barrier(r, gen)
-                if dbg:
-                    _dbg(r, "sync: barrier 2 launched")
                 if tp.error_mode == "step":
                     tp.check_step(r, gen, "momentum sync")
             else:

@@ -344,6 +344,22 @@ class LocalTransport(_PeerSync, DeviceTransport):
             raise ConfigError("LocalTransport needs a CUDA device")
         if fused and not p2p:
             raise ConfigError("LocalTransport(fused=True) needs the peer-memory mode")
+        if fused and world_size > 1:
+            # every rank stream needs its own hardware queue: streams that
+            # alias onto one queue serialise, and a kernel spinning on an
+            # in-kernel barrier then blocks the peer kernel queued behind it
+            conns = int(os.environ.get("CUDA_DEVICE_MAX_CONNECTIONS", "8"))
+            if conns < world_size + 2:
+                raise ConfigError(
+                    f"LocalTransport(fused=True) with {world_size} ranks needs "
+                    f"CUDA_DEVICE_MAX_CONNECTIONS >= {world_size + 2} (got {conns}), set "
+                    "before CUDA initialises")
+            # lazy module loading: the first launch of a kernel waits for the
+            # running kernels -- a rank spinning on a barrier for a peer whose
+            # launch is queued behind that load never finishes
+            if os.environ.get("CUDA_MODULE_LOADING", "LAZY").upper() != "EAGER":
+                raise ConfigError("LocalTransport(fused=True) needs CUDA_MODULE_LOADING=EAGER, "
+                                  "set before CUDA initialises")
         self.world_size = world_size
         self.dev = (torch.device(device) if device is not None
                     else torch.device("cuda", torch.cuda.current_device()))
