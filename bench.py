@@ -136,6 +136,10 @@ def kernel_bytes(name: str, n: int, P: int, F: int, kind: str, nb: float = 16.0)
         if kind == "f64":
             return 12.0 * n + 8.0 * n
         return 12.0 * n + n * F / 8.0
+    if name == "lc_encode_sync":   # g, m in; signs + m' out (m' to the owners' staging)
+        return 12.0 * n + n / 8.0
+    if name == "lc_vote_apply_sync":  # theta r/w, staging rows in, words; means land in m
+        return 8.0 * n + 4.0 * n + n / 8.0
     if name == "lc_apply_update":
         return 8.0 * n + n / 8.0
     if name == "lc_vote_bits":
@@ -592,10 +596,9 @@ def main():
     def step(state):
         if graph is not None:
             return graph.step()
-        state = lc.distributed_lion_step(state, g, h, spec, topo, algo, rng=rng)
-        if policy is not None:
-            state = lc.maybe_sync_momentum(state, policy, topo)
-        return state
+        # sync=policy: distributed_lion_step + maybe_sync_momentum, with the
+        # sync fused into the step's kernels where it can be (layers="all")
+        return lc.distributed_lion_step(state, g, h, spec, topo, algo, rng=rng, sync=policy)
 
     def barrier():
         torch.cuda.synchronize()
@@ -716,11 +719,21 @@ def main():
                 "avg_launch_ms": kern[dominant]["avg_ms"],
                 "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs" if peak_src ==
                 "measured" else "fallback 6650 GB/s (B200_PROFILING.md)"}
+        if dominant in ("lc_encode_sync", "lc_vote_apply_sync") and P > 1:
+            # NVLink-bound halves of the fused momentum sync: (P-1)/P of the
+            # m' rows leave in K1, (P-1)/P of the means leave in the vote kernel
+            per_launch = (P - 1) / P * (4.0 + 1.0 / 8.0) * n
+            ach = per_launch / (kern[dominant]["avg_ms"] * 1e-3) / 1e9
+            roof.update({"bound": "nvlink", "achieved": ach, "peak": NVL_GBS, "frac": ach / NVL_GBS,
+                         "frac_of_nominal_900": ach / NVL_NOMINAL_GBS,
+                         "algorithmic_bytes_per_launch": per_launch,
+                         "peak_source": "B200_PROFILING.md NVLink per direction (measured)"})
         if dominant == "lc_mean_pull_f32" and P > 1:
-            # the momentum sync is NVLink-bound: per direction each rank pulls
-            # (P-1)/P of the synced fp32 values in and stores as much out
-            # synced values over the timed steps / launches in them
-            per_launch = (P - 1) / P * 4.0 * sync_frac * n * args.steps / max(
+            # the momentum sync is NVLink-bound (synced values over the timed
+            # steps / launches in them)
+            # per direction: the other owners pull this rank's blocks AND this
+            # owner stores its mean into every other rank: 2 (P-1)/P x 4 B
+            per_launch = 2 * (P - 1) / P * 4.0 * sync_frac * n * args.steps / max(
                 1, kern[dominant]["launches"])
             ach = per_launch / (kern[dominant]["avg_ms"] * 1e-3) / 1e9
             roof.update({"bound": "nvlink", "achieved": ach, "peak": NVL_GBS, "frac": ach / NVL_GBS,
@@ -734,7 +747,22 @@ def main():
     # gradients in, updated parameters out (distributed_lion_step_host
     # pipelines both copies with the kernels chunk by chunk)
     e2e = None
-    if not args.no_e2e:
+    # pinned host g and theta (8 B/param) per rank must fit the host's RAM
+    # with every local rank doing the same (7e9 params x 8 ranks would need
+    # 448 GB): otherwise the e2e leg is skipped and says why
+    e2e_skip = None
+    try:
+        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+    except (ValueError, OSError):
+        avail = 0
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    if avail and 8 * n * local_world > 0.7 * avail:
+        e2e_skip = (f"host RAM: {local_world} ranks x 8 B/param x {n} params = "
+                    f"{8 * n * local_world / 1e9:.0f} GB pinned > 70% of the "
+                    f"{avail / 1e9:.0f} GB available")
+        e2e = {"value": None, "unit": "params/s", "h2d_bytes_per_step": 4 * n,
+               "d2h_bytes_per_step": 4 * n, "skipped": e2e_skip}
+    if not args.no_e2e and e2e_skip is None:
         host_g = torch.empty(n, dtype=torch.float32, pin_memory=True)
         host_g.copy_(grad[:n])
         host_t = torch.empty(n, dtype=torch.float32, pin_memory=True)

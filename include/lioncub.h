@@ -178,6 +178,29 @@ int lc_vote_apply(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid,
                   int64_t n, const uint32_t* full, const uint32_t* nz_full, double lr,
                   double weight_decay, void* stream);
 
+/* ---- The momentum sync fused into the step (SyncPolicy(layers="all")
+ * firing at this step; maybe_sync_momentum, optimizer.py:244-258, with
+ * allreduce_mean_f32, collectives.py:319-344) ----
+ * lc_encode_sync: the 1-bit encode (as lc_encode, LC_ENC_SIGN1, eoff 0) that
+ *   stores m' of block j into mstage[j] -- owner j's staging row for this
+ *   rank (L floats, 16-byte aligned) -- instead of the local m.
+ * lc_vote_apply_sync: lc_vote_apply plus the owner mean: this owner's P
+ *   staged rows (mean_stage + r*mean_L, r in rank order) summed in float64,
+ *   divided once, rounded once to fp32 and stored into every rank's momentum
+ *   block (mean_out[k], k < P); mean_cnt valid elements; mean_work: a device
+ *   word the call zeroes (CTAs take 8192-element chunks from it).  The mean
+ *   needs only sync->wait_epoch (every rank's lc_encode_sync finished).  The
+ *   caller orders the next step after every owner's mean (a barrier). */
+int lc_encode_sync(const float* g, float* m, const uint8_t* mask, int64_t n,
+                   const lc_hyper* h, int fill, void* const* dst, int32_t nblocks, int64_t L,
+                   uint32_t* flags, const lc_sync* sync, void* const* mstage, void* stream);
+int lc_vote_apply_sync(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid,
+                       int fill, int sum_mode, void* const* voted, void* const* nz,
+                       int32_t nout, uint32_t* flags, const lc_sync* sync, float* theta,
+                       int64_t n, const uint32_t* full, const uint32_t* nz_full, double lr,
+                       double weight_decay, const float* mean_stage, void* const* mean_out,
+                       int64_t mean_L, int64_t mean_cnt, uint32_t* mean_work, void* stream);
+
 /* ---- K5v: vote + theta update over allgathered sign words ----
  * rows: P rows (stride row_stride >= ceil(n/32) words) of every rank's
  * 1-bit sign words for the whole vector (lc_encode with LC_ENC_REPLICATE

@@ -202,11 +202,17 @@ __device__ __forceinline__ void stage_subtile(uint32_t* sw, int lane, const uint
 #define LC_ENC_MINB 2
 #endif
 
-template <int ENC, int F, bool MASK>
+// MPUSH (the momentum sync fused into the step, SyncPolicy layers="all"):
+// m' of block j is stored into owner j's staging row for this rank
+// (mst.p[j], L floats per row) instead of the local m -- the owner averages
+// the P rows and stores the mean into every rank's m in k_vote_apply, so the
+// all-to-all half of the sync overlaps K1's HBM stream.
+template <int ENC, int F, bool MASK, bool MPUSH = false>
 __global__ void __launch_bounds__(256, LC_ENC_MINB)
 k_encode(const float* __restrict__ g, float* __restrict__ m,
          const uint8_t* __restrict__ mask, int64_t n, Hyp h, int fill, SegQ sq,
-         Dst dst, int64_t L, int64_t eoff, int nrep, uint32_t* __restrict__ flags, SyncD sy) {
+         Dst dst, int64_t L, int64_t eoff, int nrep, uint32_t* __restrict__ flags, SyncD sy,
+         Dst mst) {
   griddep_wait();
   constexpr int WPS = (ENC == LC_ENC_F64) ? 1 : 32 * F;  // words per super-tile
   constexpr int KU = LC_ENC_KU;  // sub-tiles whose loads are in flight together
@@ -256,7 +262,12 @@ k_encode(const float* __restrict__ g, float* __restrict__ m,
           uint32_t st[4];
           encode4<ENC, MASK>(ge, me, keep, valid_all, h, fillbit, zflag, sq, cur,
                              ebase + k * 128 + lane * 4, c, mn, st, flag);
-          st_stream(mp + k * 32, make_float4(mn[0], mn[1], mn[2], mn[3]));
+          if constexpr (MPUSH) {
+            float4* sp = reinterpret_cast<float4*>(reinterpret_cast<float*>(mst.p[j]) + boff) + lane;
+            st_stream(sp + k * 32, make_float4(mn[0], mn[1], mn[2], mn[3]));
+          } else {
+            st_stream(mp + k * 32, make_float4(mn[0], mn[1], mn[2], mn[3]));
+          }
           if constexpr (ENC == LC_ENC_F64) {
             double* o = reinterpret_cast<double*>(dst.p[j]) + boff + k * 128 + lane * 4;
             *reinterpret_cast<double2*>(o) = make_double2(c[0], c[1]);
@@ -289,9 +300,11 @@ k_encode(const float* __restrict__ g, float* __restrict__ m,
         float mn[4];
         uint32_t st[4];
         encode4<ENC, MASK>(ge, me, keep, valid, h, fillbit, zflag, sq, cur, e0, c, mn, st, flag);
+        float* mdst = m + e0;
+        if constexpr (MPUSH) mdst = reinterpret_cast<float*>(mst.p[j]) + boff + k * 128 + lane * 4;
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          if (valid[q]) m[e0 + q] = mn[q];
+          if (valid[q]) mdst[q] = mn[q];
         if constexpr (ENC == LC_ENC_F64) {
           double* o = reinterpret_cast<double*>(dst.p[j]) + boff + k * 128 + lane * 4;
 #pragma unroll
@@ -703,10 +716,67 @@ struct ApplyArgs {
 #define LC_VOTE_SHARE 8  // 1/LC_VOTE_SHARE of the grid votes + pushes the owner block
 #endif
 
+// The momentum sync fused into the step (the owner half of
+// allreduce_mean_f32, collectives.py:319-344): this owner's P staged rows of
+// m' (stage + r*L, written by every rank's K1 in MPUSH mode) are summed in
+// float64 in rank order, divided once, rounded once to fp32 and stored into
+// every rank's momentum block (out.p[k]).  Chunks are taken from a work
+// counter by every CTA once its vote / theta role is done.
+struct MeanArgs {
+  const float* stage;  // null: no sync this step
+  Dst out;             // out.p[k]: rank k's momentum + owner offset
+  int64_t L;           // staging row stride (floats)
+  int64_t cnt;         // valid elements of this owner's block
+  unsigned int* work;  // zeroed chunk counter
+};
+
+constexpr int kMeanChunk = 8192;  // elements per work item (256 threads x 8 float4)
+
+__device__ __forceinline__ void mean_quad(const MeanArgs& ma, int P, int64_t i, double dp) {
+  double acc[4];
+  float4 x = __ldcs(reinterpret_cast<const float4*>(ma.stage + i));
+  acc[0] = x.x; acc[1] = x.y; acc[2] = x.z; acc[3] = x.w;
+  for (int r = 1; r < P; ++r) {
+    x = __ldcs(reinterpret_cast<const float4*>(ma.stage + (int64_t)r * ma.L + i));
+    acc[0] = __dadd_rn(acc[0], (double)x.x);
+    acc[1] = __dadd_rn(acc[1], (double)x.y);
+    acc[2] = __dadd_rn(acc[2], (double)x.z);
+    acc[3] = __dadd_rn(acc[3], (double)x.w);
+  }
+  const float4 v = make_float4(__double2float_rn(__ddiv_rn(acc[0], dp)),
+                               __double2float_rn(__ddiv_rn(acc[1], dp)),
+                               __double2float_rn(__ddiv_rn(acc[2], dp)),
+                               __double2float_rn(__ddiv_rn(acc[3], dp)));
+  for (int k = 0; k < P; ++k) *reinterpret_cast<float4*>(reinterpret_cast<float*>(ma.out.p[k]) + i) = v;
+}
+
+__device__ void mean_role(const MeanArgs& ma, int P) {
+  __shared__ long long chunk;
+  const double dp = (double)P;
+  while (true) {
+    __syncthreads();
+    if (threadIdx.x == 0) chunk = (long long)atomicAdd(ma.work, 1u);
+    __syncthreads();
+    const int64_t c0 = (int64_t)chunk * kMeanChunk;
+    if (c0 >= ma.cnt) break;
+    const int64_t c1 = c0 + kMeanChunk < ma.cnt ? c0 + kMeanChunk : ma.cnt;
+    const int64_t q1 = c0 + ((c1 - c0) & ~(int64_t)3);
+    for (int64_t i = c0 + 4 * (int64_t)threadIdx.x; i < q1; i += 4 * (int64_t)blockDim.x)
+      mean_quad(ma, P, i, dp);
+    for (int64_t i = q1 + threadIdx.x; i < c1; i += blockDim.x) {  // ragged tail
+      double acc = (double)ma.stage[i];
+      for (int r = 1; r < P; ++r) acc = __dadd_rn(acc, (double)ma.stage[(int64_t)r * ma.L + i]);
+      const float v = __double2float_rn(__ddiv_rn(acc, dp));
+      for (int k = 0; k < P; ++k) reinterpret_cast<float*>(ma.out.p[k])[i] = v;
+    }
+  }
+}
+
 template <int NP, bool NZ>
 __global__ void __launch_bounds__(256)
 k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_valid, int fill,
-             int sum_mode, VoteOut out, uint32_t* __restrict__ flags, SyncD sy, ApplyArgs a) {
+             int sum_mode, VoteOut out, uint32_t* __restrict__ flags, SyncD sy, ApplyArgs a,
+             MeanArgs ma) {
   griddep_wait();
   if (!sync_wait(sy)) {  // a peer's words never arrived: no vote, no theta update
     sync_arrive(sy);
@@ -864,6 +934,9 @@ k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_val
       }
     }
   }
+  // every CTA whose theta share is done joins the fused momentum mean
+  // (needs only e1: the staged rows are complete even if an owner's vote timed out)
+  if (ma.stage) mean_role(ma, P);
 }
 
 // ---------------------------------------------------------------------------
@@ -1354,16 +1427,28 @@ int generic_grid(int64_t n) {
 thread_local SyncD g_sync{};     // sync of the encode launch being dispatched
 thread_local int64_t g_eoff = 0;  // element offset of the encode launch
 thread_local int g_nrep = 0;      // replicate-mode destinations (0: owner blocks)
+thread_local bool g_mpush = false;  // m' -> owners' staging rows (g_mst)
+thread_local Dst g_mst{};
 
 template <int ENC, int F, bool MASK>
 int launch_encode(const float* g, float* m, const uint8_t* mask, int64_t n, Hyp h,
                   int fill, SegQ sq, const Dst& dst, int64_t L, uint32_t* flags,
                   cudaStream_t st) {
-  auto kern = k_encode<ENC, F, MASK>;
   int64_t nsup = (n + 1023) >> 10;
+  if constexpr (ENC == LC_ENC_SIGN1) {
+    if (g_mpush) {
+      auto kern = k_encode<ENC, F, MASK, true>;
+      int grid = stream_grid(kern, kBlock, nsup, kBlock / 32);
+      LC_CUDA_TRY(launch_pdl(kern, grid, kBlock, 0, st, g, m, mask, n, h, fill, sq, dst, L,
+                             g_eoff, g_nrep, flags, g_sync, g_mst));
+      LC_LAUNCH_CHECK();
+      return LC_OK;
+    }
+  }
+  auto kern = k_encode<ENC, F, MASK, false>;
   int grid = stream_grid(kern, kBlock, nsup, kBlock / 32);
   LC_CUDA_TRY(launch_pdl(kern, grid, kBlock, 0, st, g, m, mask, n, h, fill, sq, dst, L, g_eoff,
-                         g_nrep, flags, g_sync));
+                         g_nrep, flags, g_sync, g_mst));
   LC_LAUNCH_CHECK();
   return LC_OK;
 }
@@ -1448,6 +1533,7 @@ int lc_encode(const float* g, float* m, const uint8_t* mask, int64_t n,
   Dst d;
   if (!make_dst(d, dst, nblocks)) return set_err(LC_E_ARG, "lc_encode: bad destination table");
   g_nrep = rep ? nblocks : 0;
+  g_mpush = false;
   Hyp h = to_hyp(hp);
   SegQ sq = to_segq(segs);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -1470,6 +1556,35 @@ int lc_encode(const float* g, float* m, const uint8_t* mask, int64_t n,
     default:
       return set_err(LC_E_ARG, "lc_encode: unknown encoding %d", enc);
   }
+}
+
+int lc_encode_sync(const float* g, float* m, const uint8_t* mask, int64_t n,
+                   const lc_hyper* hp, int fill, void* const* dst, int32_t nblocks, int64_t L,
+                   uint32_t* flags, const lc_sync* sync, void* const* mstage, void* stream) {
+  Dst ms;
+  if (!mstage || !make_dst(ms, mstage, nblocks) || !dst || nblocks < 1)
+    return set_err(LC_E_ARG, "lc_encode_sync: one staging row per owner block required");
+  for (int j = 0; j < nblocks; ++j)
+    if ((reinterpret_cast<uintptr_t>(ms.p[j]) & 15u) != 0)
+      return set_err(LC_E_ARG, "lc_encode_sync: staging rows must be 16-byte aligned");
+  // the plain 1-bit encode, with m' routed to the owners' staging rows
+  if (n < 0 || !hp || !flags) return set_err(LC_E_ARG, "lc_encode_sync: bad arguments");
+  if (n == 0) return sync_only(sync, stream);
+  if (!g || !m || !aligned16(g) || !aligned16(m))
+    return set_err(LC_E_ARG, "lc_encode_sync: g/m must be 16-byte aligned");
+  if (L <= 0 || (L % 1024) != 0 || (int64_t)nblocks * L < n)
+    return set_err(LC_E_ARG, "lc_encode_sync: blocks (multiple of 1024) must cover n");
+  Dst d;
+  if (!make_dst(d, dst, nblocks)) return set_err(LC_E_ARG, "lc_encode_sync: bad destination table");
+  g_nrep = 0;
+  g_eoff = 0;
+  g_sync = to_syncd(sync);
+  g_mst = ms;
+  g_mpush = true;
+  const int rc = dispatch_mask<LC_ENC_SIGN1, 1>(g, m, mask, n, to_hyp(hp), fill, to_segq(nullptr), d,
+                                                 L, flags, reinterpret_cast<cudaStream_t>(stream));
+  g_mpush = false;
+  return rc;
 }
 
 int lc_apply_update(float* theta, int64_t n, void* const* sign_bits, void* const* nz_bits,
@@ -1586,6 +1701,37 @@ int lc_vote_bits(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid, i
   return LC_OK;
 }
 
+namespace {
+thread_local MeanArgs g_mean{};  // set by lc_vote_apply_sync for its launch
+}
+
+int lc_vote_apply_sync(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid, int fill,
+                       int sum_mode, void* const* voted, void* const* nz, int32_t nout,
+                       uint32_t* flags, const lc_sync* sync, float* theta, int64_t n,
+                       const uint32_t* full, const uint32_t* nz_full, double lr, double wd,
+                       const float* mean_stage, void* const* mean_out, int64_t mean_L,
+                       int64_t mean_cnt, uint32_t* mean_work, void* stream) {
+  MeanArgs ma{};
+  if (!mean_stage || !mean_out || !mean_work || mean_L <= 0 || (mean_L % 4) != 0 ||
+      mean_cnt < 0 || mean_cnt > mean_L || !make_dst(ma.out, mean_out, P))
+    return set_err(LC_E_ARG, "lc_vote_apply_sync: bad momentum-mean arguments");
+  if ((reinterpret_cast<uintptr_t>(mean_stage) & 15u) != 0)
+    return set_err(LC_E_ARG, "lc_vote_apply_sync: staging must be 16-byte aligned");
+  for (int k = 0; k < P; ++k)
+    if ((reinterpret_cast<uintptr_t>(ma.out.p[k]) & 15u) != 0)
+      return set_err(LC_E_ARG, "lc_vote_apply_sync: momentum blocks must be 16-byte aligned");
+  ma.stage = mean_cnt > 0 ? mean_stage : nullptr;
+  ma.L = mean_L;
+  ma.cnt = mean_cnt;
+  ma.work = mean_work;
+  LC_CUDA_TRY(cudaMemsetAsync(mean_work, 0, sizeof(uint32_t), reinterpret_cast<cudaStream_t>(stream)));
+  g_mean = ma;
+  const int rc = lc_vote_apply(recv, P, cw, n_valid, fill, sum_mode, voted, nz, nout, flags, sync,
+                               theta, n, full, nz_full, lr, wd, stream);
+  g_mean = MeanArgs{};
+  return rc;
+}
+
 int lc_vote_apply(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid, int fill,
                   int sum_mode, void* const* voted, void* const* nz, int32_t nout,
                   uint32_t* flags, const lc_sync* sync, float* theta, int64_t n,
@@ -1606,7 +1752,7 @@ int lc_vote_apply(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid, 
     auto kern = k_vote_apply<NP, NZ>;                                                      \
     int grid = stream_grid(kern, kBlock, (n + 1023) >> 10, kBlock / 32);                   \
     LC_CUDA_TRY(launch_pdl(kern, grid, kBlock, 0, st, recv, P, cw, n_valid, fill, sum_mode, \
-                           o, flags, sy, a));                                              \
+                           o, flags, sy, a, g_mean));                                      \
   } while (0)
 #define LC_VA_NZ(NP) do { if (nz) LC_VA(NP, true); else LC_VA(NP, false); } while (0)
   if (P <= 1) LC_VA_NZ(1);

@@ -529,17 +529,30 @@ def _validate(spec, algo):
 def distributed_lion_step(state: WorkerState, grad_i, h: LionHyper,
                           spec: QuantSpec | None, topo: Topology, algo: str,
                           mask: Mapping | None = None, zero_mode: str = "alternating",
-                          rng=None, metrics_out: dict | None = None) -> WorkerState:
+                          rng=None, metrics_out: dict | None = None,
+                          sync: SyncPolicy | None = None) -> WorkerState:
     """One distributed Lion Cub step (optimizer.py:172-210) on this rank.
 
     Every rank must call it in the same order with the same layout; the
     input state is donated (updated in place).  ``metrics_out`` receives the
     reference's per-layer "ties", "vote_sign" and "c_local" (costly: a host
-    sync and an f64 copy of c)."""
+    sync and an f64 copy of c).
+
+    ``sync`` (an addition to the reference signature): the step is followed
+    by ``maybe_sync_momentum(state', sync, topo)`` -- with identical results
+    -- and when the policy fires with ``layers="all"`` on the peer-memory
+    1-bit / sum-of-signs path the sync is FUSED into the step: K1 stores m'
+    into the owners' staging rows over NVLink while it streams g and m, and
+    each owner averages its rows and stores the mean into every rank's
+    momentum inside the vote/update kernel.  A later maybe_sync_momentum call
+    for the same iteration is then a no-op."""
     _validate(spec, algo)
     _check_shapes(state.params, grad_i)
-    return _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out,
-                      rng=rng)
+    out = _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out,
+                     rng=rng, sync=sync)
+    if sync is not None and getattr(out, "_lc_synced", None) != out.iteration:
+        out = maybe_sync_momentum(out, sync, topo)
+    return out
 
 
 class _HostPipe:
@@ -615,8 +628,20 @@ def distributed_lion_step_host(state: WorkerState, grad_host: torch.Tensor, h: L
                       rng=rng)
 
 
+def _fused_sync_ok(sync, layout, topo, t, kind, metrics, pipe, n) -> bool:
+    """The momentum sync can ride inside this step (see distributed_lion_step)."""
+    if sync is None or not sync.fires(t) or topo.world_size < 2 or kind != "1bit":
+        return False
+    tp = topo.transport
+    if not (tp.p2p and tp.fused_barriers) or metrics or pipe is not None or SYNC_NCCL:
+        return False
+    if n > AG_MAX_N or topo.world_size > AG_MAX_P:   # the owner-vote exchange
+        return layout.runs(sync.selects) == [(0, n)]
+    return False
+
+
 def _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out, pipe=None,
-               rng=None):
+               rng=None, sync=None):
     layout, th, m = state.flat()
     dev = th.flat.device
     P = topo.world_size
@@ -694,6 +719,7 @@ def _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out,
             segs = None
             if kind == "fields" and not binary:
                 segs = _quant_scales(ws, layout, dev, g.flat, m.flat, mflat, hyp, spec, s, seed)
+            msync = None
             if P == 1:
                 mode = (_lib.LC_LOCAL_BINARY if binary else
                         _lib.LC_LOCAL_QUANT if kind == "fields" else _lib.LC_LOCAL_PS)
@@ -720,10 +746,14 @@ def _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out,
                             pipe.emit_out(c, th.flat, stream)
                 nz = _loc(ws.nz) if metrics else None
             else:
+                if _fused_sync_ok(sync, layout, topo, t, kind, metrics, pipe, n) and \
+                        not (ternary and binary):
+                    m = _symmetric_momentum(m, topo)
+                    msync = m
                 nz = _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill,
                                         n, g, m, mflat, hyp, segs, s,
                                         tree=algo == "ps_efficient", pipe=pipe,
-                                        theta=th.flat)
+                                        theta=th.flat, msync=msync)
                 if strict and not ws.p2p and hasattr(tp, "wait_collectives"):
                     # NCCL exchange: no theta update unless every collective landed
                     tp.wait_collectives(topo.rank, gen, "vote exchange")
@@ -741,12 +771,19 @@ def _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out,
             if pipe is not None:
                 pipe.finish(stream)
             ws.flags_host.copy_(ws.flags, non_blocking=True)
+            if msync is not None:
+                # every owner's mean has landed everywhere (and every owner
+                # finished reading its staging rows) before the next step
+                tp.device_barrier(topo.rank, gen)
             if strict and P > 1 and ws.p2p:
                 tp.check_step(topo.rank, gen, "step")   # syncs the stream
                 _raise_nan(ws)
             if metrics:
                 _fill_metrics(metrics_out, layout, dev, ws, nz, c_local, s)
-    return WorkerState(params=th, momentum=m, iteration=t)
+    out = WorkerState(params=th, momentum=m, iteration=t)
+    if msync is not None:
+        out._lc_synced = t
+    return out
 
 
 def _ternary_precheck(topo, gen, g, m, mflat, n, hyp, dev, s, kind):
@@ -816,7 +853,7 @@ class _Allgather:
 
 
 def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, g, m, mflat,
-                       hyp, segs, s, tree=False, pipe=None, theta=None):
+                       hyp, segs, s, tree=False, pipe=None, theta=None, msync=None):
     """K1 encode -> exchange -> owner vote into the gather buffer (+nz, ties).
     With ``theta`` on the fused peer-memory path the theta update runs in
     the vote's grid (``ws.applied`` is set)."""
@@ -834,7 +871,7 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
         enc, fb = _lib.LC_ENC_F64, 64
     fused = ws.p2p and tp.fused_barriers
     if kind == "1bit" and fused and ws.tout is None and pipe is None and theta is not None \
-            and P <= AG_MAX_P and n <= AG_MAX_N:
+            and P <= AG_MAX_P and n <= AG_MAX_N and msync is None:
         # allgather exchange: K1 stores its sign words into every rank, the
         # last CTA publishes e1; K5v waits for e1 and votes + updates locally
         if ws.ag is None:
@@ -883,6 +920,12 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
             _lib.call("lc_encode", _off(g.flat, a), _off(m.flat, a), None, b - a,
                       C.byref(hyp), fill, enc, fb, None, ws.dst, P, L, a,
                       ws.flags.data_ptr(), sy1 if c == last else None, s)
+    elif msync is not None:
+        # K1 with m' routed to the owners' staging rows (the sync's all-to-all)
+        stage = tp.sym_buffer(r, ws.key + ("mstage",), P * L, torch.float32)
+        _lib.call("lc_encode_sync", gp, mp, mk, n, C.byref(hyp), fill, ws.dst, P, L,
+                  ws.flags.data_ptr(), sy1,
+                  _lib.table([stage.peers[j] + r * L * 4 for j in range(P)]), s)
     else:
         if pipe is not None:
             pipe.wait_all_in(torch.cuda.ExternalStream(s))
@@ -907,9 +950,19 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
             and theta is not None:
         # vote + theta update in one grid: each warp waits only for the owner
         # of the block it updates (the allgather and K5 overlap the skew)
-        _lib.call("lc_vote_apply", recv.data_ptr(), P, cw, nvalid, fill, sum_mode, ws.vout,
-                  ws.nzout, ws.nout, ws.flags.data_ptr(), sy2, theta.data_ptr(), n,
-                  _loc(ws.full).data_ptr(), _lib.ptr(_loc(ws.nz)), hyp.lr, hyp.weight_decay, s)
+        if msync is None:
+            _lib.call("lc_vote_apply", recv.data_ptr(), P, cw, nvalid, fill, sum_mode, ws.vout,
+                      ws.nzout, ws.nout, ws.flags.data_ptr(), sy2, theta.data_ptr(), n,
+                      _loc(ws.full).data_ptr(), _lib.ptr(_loc(ws.nz)), hyp.lr,
+                      hyp.weight_decay, s)
+        else:
+            stage = tp.sym_buffer(r, ws.key + ("mstage",), P * L, torch.float32)
+            outs = _lib.table([msync.sym.peers[k] + r * L * 4 for k in range(P)])
+            _lib.call("lc_vote_apply_sync", recv.data_ptr(), P, cw, nvalid, fill, sum_mode,
+                      ws.vout, ws.nzout, ws.nout, ws.flags.data_ptr(), sy2, theta.data_ptr(), n,
+                      _loc(ws.full).data_ptr(), _lib.ptr(_loc(ws.nz)), hyp.lr,
+                      hyp.weight_decay, stage.local.data_ptr(), outs, L, nvalid,
+                      ws.counters[3:4].data_ptr(), s)
         ws.applied = True
         return _loc(ws.nz)
     if kind == "1bit":
@@ -986,8 +1039,9 @@ def maybe_sync_momentum(state: WorkerState, policy: SyncPolicy,
     owner j's staging slot, the owner averages its P rows in float64 rank
     order and stores the fp32 mean into every rank's momentum (two barriers).
     NCCL exchange: all-to-all, owner mean, allgather (collectives.mean_into)."""
-    if not policy.fires(state.iteration):
-        return state
+    if not policy.fires(state.iteration) or \
+            getattr(state, "_lc_synced", None) == state.iteration:
+        return state   # not firing, or already synced inside the step
     layout, th, m = state.flat()
     dev = m.flat.device
     P, r = topo.world_size, topo.rank

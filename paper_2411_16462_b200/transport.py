@@ -296,8 +296,13 @@ class _PeerSync:
         sync on the rank's stream (error paths and strict steps only)."""
         if rank not in self._err:
             return 0, []
-        host_wait(self.stream(rank))
-        w = self._err[rank].tolist()
+        # one stream-ordered copy into pinned memory and one event wait
+        host = self._err_host[rank]
+        st = self.stream(rank)
+        with torch.cuda.stream(st):
+            host.copy_(self._err[rank], non_blocking=True)
+        host_wait(st)
+        w = host.tolist()
         miss = [j for j in range(self.world_size) if (w[1] >> j) & 1]
         return w[0] & 0xFFFFFFFF, miss
 

@@ -47,6 +47,7 @@ def run_step_case(case: dict, theta, ms, gs, mask=None, transport=None,
         period, layers = case["sync"]
         sync = lc.SyncPolicy(period=period,
                              layers=layers if isinstance(layers, str) else frozenset(layers))
+    fused_sync = bool(getattr(transport, "fused", False))
     cmask = None
     if mask is not None:
         cmask = {k: torch.from_numpy(np.asarray(v)).cuda() for k, v in mask.items()}
@@ -59,9 +60,16 @@ def run_step_case(case: dict, theta, ms, gs, mask=None, transport=None,
         for _ in range(steps):
             met = {} if metrics else None
             rng = None if rng_seed is None else np.random.default_rng(rng_seed + r)
-            st2 = lc.distributed_lion_step(st2, g, h, spec, topo, case["algo"], mask=cmask,
-                                           zero_mode=case["zero_mode"], metrics_out=met,
-                                           rng=rng)
+            if fused_sync:
+                # the production path: the sync rides inside the step when it
+                # can (layers="all" on the owner-vote exchange)
+                st2 = lc.distributed_lion_step(st2, g, h, spec, topo, case["algo"], mask=cmask,
+                                               zero_mode=case["zero_mode"], metrics_out=met,
+                                               rng=rng, sync=sync)
+            else:
+                st2 = lc.distributed_lion_step(st2, g, h, spec, topo, case["algo"], mask=cmask,
+                                               zero_mode=case["zero_mode"], metrics_out=met,
+                                               rng=rng)
             if sync is not None:
                 st2 = lc.maybe_sync_momentum(st2, sync, topo)
         host_wait()

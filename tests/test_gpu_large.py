@@ -290,3 +290,47 @@ def test_flat_buffer_past_2_32_elements(world, n):
         assert torch.equal(out[0].params.flat[:n].view(torch.int32),
                            out[1].params.flat[:n].view(torch.int32))
     assert math.isfinite(float(out[0].params.flat[n - 1]))
+
+
+def test_flat_600m_p4_fused_momentum_sync():
+    """The momentum sync fused into the step (SyncPolicy(1, "all") passed to
+    distributed_lion_step on the production exchange) at 600M params, P = 4:
+    windows of theta' / m' against the C oracle + the f64 rank-ordered mean,
+    and every rank's full momentum identical afterwards."""
+    P, n = 4, 600_000_037
+    layout = lc.Layout({"w": (n,)})
+    theta, ms, gs = synth(n, P, "laplace", seed=41)
+    w = 4096
+    starts = _windows(layout, n, P, extra=(n // 3, n // 2))
+    th_w, m_w, g_w = _gather_windows(starts, w, theta, ms, gs)
+    it, lr = 6, 1e-3
+    seg = np.arange(len(starts) + 1, dtype=np.int64) * w
+    ref_t, ref_m, _, _ = CO.step(th_w, m_w, g_w, seg, CO.hyper(lr=lr), "compressed1bit",
+                                 O.zero_fill(it + 1))
+    mean = O.mean_f32(ref_m)
+    tp = lc.LocalTransport(P, fused=True)
+    thetas = [theta.clone() for _ in range(P - 1)] + [theta]
+    policy = lc.SyncPolicy(period=1, layers="all")
+
+    def fn(topo):
+        r = topo.rank
+        st = lc.WorkerState(params=layout.views(thetas[r]), momentum=layout.views(ms[r]),
+                            iteration=it)
+        st = lc.distributed_lion_step(st, layout.views(gs[r]), lc.LionHyper(lr=lr), None, topo,
+                                      "compressed1bit", sync=policy)
+        assert getattr(st, "_lc_synced", None) == it + 1   # fused, not a separate pass
+        st = lc.maybe_sync_momentum(st, policy, topo)      # no-op for this iteration
+        host_wait()
+        return st
+
+    out = lc.run_ranks(P, fn, transport=tp)
+    m0 = out[0].momentum.flat
+    for r, st in enumerate(out):
+        got_t = np.concatenate([_host(st.params.flat[a:a + w]) for a in starts])
+        got_m = np.concatenate([_host(st.momentum.flat[a:a + w]) for a in starts])
+        assert np.array_equal(got_t.view(np.int32), ref_t.view(np.int32)), f"theta r{r}"
+        assert np.array_equal(got_m.view(np.int32), mean.view(np.int32)), f"m r{r}"
+        if r:
+            assert torch.equal(st.momentum.flat[:n].view(torch.int32), m0[:n].view(torch.int32))
+            assert torch.equal(st.params.flat[:n].view(torch.int32),
+                               out[0].params.flat[:n].view(torch.int32))

@@ -316,21 +316,30 @@ def test_stochastic_rounding_is_unbiased():
 
 
 @pytest.mark.parametrize("xchg", EXCHANGES)
-def test_momentum_sync_matches_oracle_large(xchg):
-    world = 8
+@pytest.mark.parametrize("world,layers,algo,bits", [
+    (8, ("emb", "h1.w"), "compressed1bit", None),
+    (8, "all", "compressed1bit", None),        # fused into the step (fused exchange)
+    (4, "all", "direct", 1),                   # sum-of-signs + fused sync
+    (3, "all", "compressed1bit", None),
+])
+def test_momentum_sync_matches_oracle_large(xchg, world, layers, algo, bits):
     ranks = O.synth_rank_inputs(3, world, BIG, "laplace")
     h = O.Hyper(0.9, 0.99, 1e-4, 0.0)
-    _, nm, *_ = O.distributed_step([rk["theta"] for rk in ranks], [rk["m"] for rk in ranks],
-                                   [rk["g"] for rk in ranks], h, None, "compressed1bit", 9)
-    synced = O.sync_momentum(nm, 10, frozenset({"emb", "h1.w"}), 10)
-    case = dict(world=world, lr=1e-4, wd=0.0, bits=None, algo="compressed1bit",
-                iteration=9, zero_mode="alternating", sync=(10, ["emb", "h1.w"]))
+    nt, nm, *_ = O.distributed_step([rk["theta"] for rk in ranks], [rk["m"] for rk in ranks],
+                                    [rk["g"] for rk in ranks], h,
+                                    None if bits is None else O.Spec(bits), algo, 9)
+    sel = "all" if layers == "all" else frozenset(layers)
+    synced = O.sync_momentum(nm, 10, sel, 10)
+    case = dict(world=world, lr=1e-4, wd=0.0, bits=bits, algo=algo,
+                iteration=9, zero_mode="alternating",
+                sync=(10, "all" if layers == "all" else list(layers)))
     res = run_step_case(case, ranks[0]["theta"], [rk["m"] for rk in ranks],
                         [rk["g"] for rk in ranks], metrics=False,
                         transport=make_transport(world, xchg))
-    for r, (_, m, _, _) in enumerate(res):
+    for r, (th, m, _, _) in enumerate(res):
         for k in BIG:
             assert_f32_equal(m[k], synced[r][k], f"m {k} r{r}")
+            assert_f32_equal(th[k], nt[0][k], f"theta {k} r{r}")
 
 
 # ---- edge sizes and multi-step trajectories --------------------------------
@@ -380,6 +389,8 @@ def test_edge_sizes_match_oracle(algo, bits, world, zm, si, xchg):
 @pytest.mark.parametrize("xchg", EXCHANGES)
 @pytest.mark.parametrize("algo,bits,world,zm,sync", [
     ("compressed1bit", None, 4, "alternating", (2, ["emb"])),
+    ("compressed1bit", None, 4, "alternating", (2, "all")),   # fused sync every other step
+    ("direct", 1, 3, "alternating", (1, "all")),              # fused sync every step
     ("direct", 1, 3, "alternating", None),
     ("direct", 5, 4, "exact-ternary", (3, "all")),
     ("ps", None, 2, "exact-ternary", None),
