@@ -731,23 +731,52 @@ struct MeanArgs {
 };
 
 constexpr int kMeanChunk = 8192;  // elements per work item (256 threads x 8 float4)
+constexpr int kMeanILP = 4;       // float4 quads per thread whose row loads are in flight together
 
-__device__ __forceinline__ void mean_quad(const MeanArgs& ma, int P, int64_t i, double dp) {
-  double acc[4];
-  float4 x = __ldcs(reinterpret_cast<const float4*>(ma.stage + i));
-  acc[0] = x.x; acc[1] = x.y; acc[2] = x.z; acc[3] = x.w;
-  for (int r = 1; r < P; ++r) {
-    x = __ldcs(reinterpret_cast<const float4*>(ma.stage + (int64_t)r * ma.L + i));
-    acc[0] = __dadd_rn(acc[0], (double)x.x);
-    acc[1] = __dadd_rn(acc[1], (double)x.y);
-    acc[2] = __dadd_rn(acc[2], (double)x.z);
-    acc[3] = __dadd_rn(acc[3], (double)x.w);
+__device__ __forceinline__ float4 mean_of(const double acc[4], double dp) {
+  return make_float4(__double2float_rn(__ddiv_rn(acc[0], dp)), __double2float_rn(__ddiv_rn(acc[1], dp)),
+                     __double2float_rn(__ddiv_rn(acc[2], dp)), __double2float_rn(__ddiv_rn(acc[3], dp)));
+}
+
+// Owner mean of one chunk: each thread holds kMeanILP quads; for every rank
+// row their loads are issued together (the row order of the float64 sum is
+// kept), then the fp32 means go to every rank's momentum.
+__device__ __forceinline__ void mean_chunk(const MeanArgs& ma, int P, int64_t c0, int64_t q1,
+                                           double dp) {
+  const int64_t step = 4 * (int64_t)blockDim.x;
+  for (int64_t base = c0 + 4 * (int64_t)threadIdx.x; base < q1; base += step * kMeanILP) {
+    double acc[kMeanILP][4];
+    bool on[kMeanILP];
+#pragma unroll
+    for (int u = 0; u < kMeanILP; ++u) on[u] = base + u * step < q1;
+    for (int r = 0; r < P; ++r) {
+      const float* row = ma.stage + (int64_t)r * ma.L;
+      float4 x[kMeanILP];
+#pragma unroll
+      for (int u = 0; u < kMeanILP; ++u)
+        if (on[u]) x[u] = __ldcs(reinterpret_cast<const float4*>(row + base + u * step));
+#pragma unroll
+      for (int u = 0; u < kMeanILP; ++u) {
+        if (!on[u]) continue;
+        if (r == 0) {
+          acc[u][0] = x[u].x; acc[u][1] = x[u].y; acc[u][2] = x[u].z; acc[u][3] = x[u].w;
+        } else {
+          acc[u][0] = __dadd_rn(acc[u][0], (double)x[u].x);
+          acc[u][1] = __dadd_rn(acc[u][1], (double)x[u].y);
+          acc[u][2] = __dadd_rn(acc[u][2], (double)x[u].z);
+          acc[u][3] = __dadd_rn(acc[u][3], (double)x[u].w);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kMeanILP; ++u) {
+      if (!on[u]) continue;
+      const float4 v = mean_of(acc[u], dp);
+      const int64_t i = base + u * step;
+      for (int k = 0; k < P; ++k)
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(ma.out.p[k]) + i) = v;
+    }
   }
-  const float4 v = make_float4(__double2float_rn(__ddiv_rn(acc[0], dp)),
-                               __double2float_rn(__ddiv_rn(acc[1], dp)),
-                               __double2float_rn(__ddiv_rn(acc[2], dp)),
-                               __double2float_rn(__ddiv_rn(acc[3], dp)));
-  for (int k = 0; k < P; ++k) *reinterpret_cast<float4*>(reinterpret_cast<float*>(ma.out.p[k]) + i) = v;
 }
 
 __device__ void mean_role(const MeanArgs& ma, int P) {
@@ -761,8 +790,7 @@ __device__ void mean_role(const MeanArgs& ma, int P) {
     if (c0 >= ma.cnt) break;
     const int64_t c1 = c0 + kMeanChunk < ma.cnt ? c0 + kMeanChunk : ma.cnt;
     const int64_t q1 = c0 + ((c1 - c0) & ~(int64_t)3);
-    for (int64_t i = c0 + 4 * (int64_t)threadIdx.x; i < q1; i += 4 * (int64_t)blockDim.x)
-      mean_quad(ma, P, i, dp);
+    mean_chunk(ma, P, c0, q1, dp);
     for (int64_t i = q1 + threadIdx.x; i < c1; i += blockDim.x) {  // ragged tail
       double acc = (double)ma.stage[i];
       for (int r = 1; r < P; ++r) acc = __dadd_rn(acc, (double)ma.stage[(int64_t)r * ma.L + i]);
@@ -772,7 +800,7 @@ __device__ void mean_role(const MeanArgs& ma, int P) {
   }
 }
 
-template <int NP, bool NZ>
+template <int NP, bool NZ, bool MEAN>
 __global__ void __launch_bounds__(256)
 k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_valid, int fill,
              int sum_mode, VoteOut out, uint32_t* __restrict__ flags, SyncD sy, ApplyArgs a,
@@ -936,7 +964,9 @@ k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_val
   }
   // every CTA whose theta share is done joins the fused momentum mean
   // (needs only e1: the staged rows are complete even if an owner's vote timed out)
-  if (ma.stage) mean_role(ma, P);
+  if constexpr (MEAN) {
+    if (ma.stage) mean_role(ma, P);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1749,7 +1779,7 @@ int lc_vote_apply(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid, 
   ApplyArgs a{theta, n, full, nz_full, lr, wd, cw};
 #define LC_VA(NP, NZ)                                                                      \
   do {                                                                                     \
-    auto kern = k_vote_apply<NP, NZ>;                                                      \
+    auto kern = g_mean.stage ? k_vote_apply<NP, NZ, true> : k_vote_apply<NP, NZ, false>;   \
     int grid = stream_grid(kern, kBlock, (n + 1023) >> 10, kBlock / 32);                   \
     LC_CUDA_TRY(launch_pdl(kern, grid, kBlock, 0, st, recv, P, cw, n_valid, fill, sum_mode, \
                            o, flags, sy, a, g_mean));                                      \

@@ -39,6 +39,9 @@ CONFIGS = [  # (algo, QuantSpec kwargs or None, input kind, zero mode, sync)
     ("ps_efficient", None, "laplace", "alternating", None),
     ("compressed1bit", None, "laplace", "alternating", (10, frozenset({"emb", "h1.w"}))),
     ("direct", dict(bits=1), "zeros", "alternating", (10, "all")),
+    # sync of every layer every other step: fused into the step on NVLink
+    ("compressed1bit", None, "laplace", "alternating", (2, "all")),
+    ("direct", dict(bits=1), "laplace", "alternating", (1, "all")),
     # quantizer variants (stochastic: the oracle is fed the same stream)
     ("direct", dict(bits=5, norm_p=INF), "outliers", "alternating", None),
     ("direct", dict(bits=4, rounding="stochastic"), "laplace", "alternating", None),
@@ -146,13 +149,12 @@ def main():
         g = st.new_grad_buffer()
         for k, v in mine["g"].items():
             g[k].copy_(torch.from_numpy(v))
+        policy = None if sync is None else lc.SyncPolicy(period=sync[0], layers=sync[1])
         for i in range(3):
+            # sync=policy: the sync rides inside the step when it can
             st = lc.distributed_lion_step(st, g, lc.LionHyper(0.9, 0.99, 1e-4, 0.1),
                                           None if qkw is None else lc.QuantSpec(**qkw),
-                                          topo, algo, zero_mode=zm)
-            if sync is not None:
-                st = lc.maybe_sync_momentum(st, lc.SyncPolicy(period=sync[0], layers=sync[1]),
-                                            topo)
+                                          topo, algo, zero_mode=zm, sync=policy)
         torch.cuda.synchronize()
         for k in SIZES:
             checked += 1
