@@ -190,7 +190,10 @@ int lc_vote_apply(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid,
  *   block (mean_out[k], k < P); mean_cnt valid elements; mean_work: a device
  *   word the call zeroes (CTAs take 8192-element chunks from it).  The mean
  *   needs only sync->wait_epoch (every rank's lc_encode_sync finished).  The
- *   caller orders the next step after every owner's mean (a barrier). */
+ *   caller orders the next step after every owner's mean (a barrier).
+ *   side_stream: run the mean as its own kernel on that stream, concurrently
+ *   with the vote/update grid (capped to leave it SMs), joined back into
+ *   `stream`; NULL: every vote/update CTA joins the mean after its share. */
 int lc_encode_sync(const float* g, float* m, const uint8_t* mask, int64_t n,
                    const lc_hyper* h, int fill, void* const* dst, int32_t nblocks, int64_t L,
                    uint32_t* flags, const lc_sync* sync, void* const* mstage, void* stream);
@@ -199,7 +202,8 @@ int lc_vote_apply_sync(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_va
                        int32_t nout, uint32_t* flags, const lc_sync* sync, float* theta,
                        int64_t n, const uint32_t* full, const uint32_t* nz_full, double lr,
                        double weight_decay, const float* mean_stage, void* const* mean_out,
-                       int64_t mean_L, int64_t mean_cnt, uint32_t* mean_work, void* stream);
+                       int64_t mean_L, int64_t mean_cnt, uint32_t* mean_work,
+                       void* side_stream, void* stream);
 
 /* ---- K5v: vote + theta update over allgathered sign words ----
  * rows: P rows (stride row_stride >= ceil(n/32) words) of every rank's

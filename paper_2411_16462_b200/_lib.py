@@ -88,7 +88,7 @@ SIGNATURES = {
     "lc_vote_apply": (INT, [P, I32, I64, I64, INT, INT, P, P, I32, P, P, P, I64, P, P, D, D, P]),
     "lc_encode_sync": (INT, [P, P, P, I64, P, INT, P, I32, I64, P, P, P, P]),
     "lc_vote_apply_sync": (INT, [P, I32, I64, I64, INT, INT, P, P, I32, P, P, P, I64, P, P, D, D,
-                                 P, P, I64, I64, P, P]),
+                                 P, P, I64, I64, P, P, P]),
     "lc_vote_update": (INT, [P, I64, I32, P, I64, INT, INT, D, D, P, P, P]),
     "lc_fields_vote": (INT, [P, I32, I64, I64, I32, I32, I32, I32, INT, P, P, P, I32, P, P, P]),
     "lc_f64_sum_vote": (INT, [P, I32, I64, I64, INT, INT, P, P, P, I32, P, P, P]),

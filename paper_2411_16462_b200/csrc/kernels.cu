@@ -731,7 +731,6 @@ struct MeanArgs {
 };
 
 constexpr int kMeanChunk = 8192;  // elements per work item (256 threads x 8 float4)
-constexpr int kMeanILP = 4;       // float4 quads per thread whose row loads are in flight together
 
 __device__ __forceinline__ float4 mean_of(const double acc[4], double dp) {
   return make_float4(__double2float_rn(__ddiv_rn(acc[0], dp)), __double2float_rn(__ddiv_rn(acc[1], dp)),
@@ -741,6 +740,7 @@ __device__ __forceinline__ float4 mean_of(const double acc[4], double dp) {
 // Owner mean of one chunk: each thread holds kMeanILP quads; for every rank
 // row their loads are issued together (the row order of the float64 sum is
 // kept), then the fp32 means go to every rank's momentum.
+template <int kMeanILP>  // float4 quads per thread whose row loads are in flight together
 __device__ __forceinline__ void mean_chunk(const MeanArgs& ma, int P, int64_t c0, int64_t q1,
                                            double dp) {
   const int64_t step = 4 * (int64_t)blockDim.x;
@@ -779,6 +779,7 @@ __device__ __forceinline__ void mean_chunk(const MeanArgs& ma, int P, int64_t c0
   }
 }
 
+template <int ILP>
 __device__ void mean_role(const MeanArgs& ma, int P) {
   __shared__ long long chunk;
   const double dp = (double)P;
@@ -790,7 +791,7 @@ __device__ void mean_role(const MeanArgs& ma, int P) {
     if (c0 >= ma.cnt) break;
     const int64_t c1 = c0 + kMeanChunk < ma.cnt ? c0 + kMeanChunk : ma.cnt;
     const int64_t q1 = c0 + ((c1 - c0) & ~(int64_t)3);
-    mean_chunk(ma, P, c0, q1, dp);
+    mean_chunk<ILP>(ma, P, c0, q1, dp);
     for (int64_t i = q1 + threadIdx.x; i < c1; i += blockDim.x) {  // ragged tail
       double acc = (double)ma.stage[i];
       for (int r = 1; r < P; ++r) acc = __dadd_rn(acc, (double)ma.stage[(int64_t)r * ma.L + i]);
@@ -798,6 +799,17 @@ __device__ void mean_role(const MeanArgs& ma, int P) {
       for (int k = 0; k < P; ++k) reinterpret_cast<float*>(ma.out.p[k])[i] = v;
     }
   }
+}
+
+// The fused sync's owner mean as its own lean kernel, run on a side stream
+// CONCURRENTLY with k_vote_apply (whose grid is capped so both are
+// resident): the NVLink-store-bound mean overlaps the HBM-bound theta update.
+// It needs only every rank's K1 (sy.wait_epoch = e1).
+__global__ void __launch_bounds__(256, 4)
+k_sync_mean(SyncD sy, MeanArgs ma, int P) {
+  griddep_wait();
+  if (!sync_wait(sy)) return;  // a peer's staged rows never arrived: no mean
+  mean_role<2>(ma, P);
 }
 
 template <int NP, bool NZ, bool MEAN>
@@ -965,7 +977,7 @@ k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_val
   // every CTA whose theta share is done joins the fused momentum mean
   // (needs only e1: the staged rows are complete even if an owner's vote timed out)
   if constexpr (MEAN) {
-    if (ma.stage) mean_role(ma, P);
+    if (ma.stage) mean_role<4>(ma, P);
   }
 }
 
@@ -1732,15 +1744,42 @@ int lc_vote_bits(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid, i
 }
 
 namespace {
-thread_local MeanArgs g_mean{};  // set by lc_vote_apply_sync for its launch
+thread_local MeanArgs g_mean{};  // set by lc_vote_apply_sync for its launch (inline mode)
+thread_local int g_va_cap = 0;   // > 0: k_vote_apply grid capped at this many CTAs per SM
+
+// fork/join events of the side-stream mean, one pair per host thread
+struct ForkEvents {
+  cudaEvent_t fork = nullptr, join = nullptr;
+  int dev = -1;
+};
+thread_local ForkEvents g_fork;
+
+int fork_events(cudaEvent_t& fork, cudaEvent_t& join) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (g_fork.dev != dev) {
+    if (g_fork.fork) cudaEventDestroy(g_fork.fork);
+    if (g_fork.join) cudaEventDestroy(g_fork.join);
+    LC_CUDA_TRY(cudaEventCreateWithFlags(&g_fork.fork, cudaEventDisableTiming));
+    LC_CUDA_TRY(cudaEventCreateWithFlags(&g_fork.join, cudaEventDisableTiming));
+    g_fork.dev = dev;
+  }
+  fork = g_fork.fork;
+  join = g_fork.join;
+  return LC_OK;
 }
+}  // namespace
+
+#ifndef LC_SYNC_VA_CTAS
+#define LC_SYNC_VA_CTAS 1  // vote/update CTAs per SM while the side-stream mean runs
+#endif
 
 int lc_vote_apply_sync(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid, int fill,
                        int sum_mode, void* const* voted, void* const* nz, int32_t nout,
                        uint32_t* flags, const lc_sync* sync, float* theta, int64_t n,
                        const uint32_t* full, const uint32_t* nz_full, double lr, double wd,
                        const float* mean_stage, void* const* mean_out, int64_t mean_L,
-                       int64_t mean_cnt, uint32_t* mean_work, void* stream) {
+                       int64_t mean_cnt, uint32_t* mean_work, void* side_stream, void* stream) {
   MeanArgs ma{};
   if (!mean_stage || !mean_out || !mean_work || mean_L <= 0 || (mean_L % 4) != 0 ||
       mean_cnt < 0 || mean_cnt > mean_L || !make_dst(ma.out, mean_out, P))
@@ -1754,12 +1793,37 @@ int lc_vote_apply_sync(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_va
   ma.L = mean_L;
   ma.cnt = mean_cnt;
   ma.work = mean_work;
-  LC_CUDA_TRY(cudaMemsetAsync(mean_work, 0, sizeof(uint32_t), reinterpret_cast<cudaStream_t>(stream)));
-  g_mean = ma;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  LC_CUDA_TRY(cudaMemsetAsync(mean_work, 0, sizeof(uint32_t), st));
+  if (!side_stream) {  // inline: every CTA joins the mean after its theta share
+    g_mean = ma;
+    const int rc = lc_vote_apply(recv, P, cw, n_valid, fill, sum_mode, voted, nz, nout, flags,
+                                 sync, theta, n, full, nz_full, lr, wd, stream);
+    g_mean = MeanArgs{};
+    return rc;
+  }
+  // side stream: fork after K1 (and the work-counter reset), the lean mean
+  // kernel fills the SMs the capped vote/update grid leaves free, join
+  cudaStream_t side = reinterpret_cast<cudaStream_t>(side_stream);
+  cudaEvent_t fork, join;
+  if (int rc = fork_events(fork, join)) return rc;
+  LC_CUDA_TRY(cudaEventRecord(fork, st));
+  LC_CUDA_TRY(cudaStreamWaitEvent(side, fork, 0));
+  g_va_cap = LC_SYNC_VA_CTAS;
   const int rc = lc_vote_apply(recv, P, cw, n_valid, fill, sum_mode, voted, nz, nout, flags, sync,
                                theta, n, full, nz_full, lr, wd, stream);
-  g_mean = MeanArgs{};
-  return rc;
+  g_va_cap = 0;
+  if (rc) return rc;
+  if (ma.stage) {
+    SyncD wait = to_syncd(sync);
+    wait.arrive_epoch = 0;  // the mean publishes nothing (the caller's barrier follows)
+    const int grid = stream_grid(k_sync_mean, kBlock, (mean_cnt + kMeanChunk - 1) / kMeanChunk, 1);
+    LC_CUDA_TRY(launch_pdl(k_sync_mean, grid, kBlock, 0, side, wait, ma, (int)P));
+    LC_LAUNCH_CHECK();
+  }
+  LC_CUDA_TRY(cudaEventRecord(join, side));
+  LC_CUDA_TRY(cudaStreamWaitEvent(st, join, 0));
+  return LC_OK;
 }
 
 int lc_vote_apply(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid, int fill,
@@ -1781,6 +1845,7 @@ int lc_vote_apply(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid, 
   do {                                                                                     \
     auto kern = g_mean.stage ? k_vote_apply<NP, NZ, true> : k_vote_apply<NP, NZ, false>;   \
     int grid = stream_grid(kern, kBlock, (n + 1023) >> 10, kBlock / 32);                   \
+    if (g_va_cap > 0 && grid > sm_count() * g_va_cap) grid = sm_count() * g_va_cap;       \
     LC_CUDA_TRY(launch_pdl(kern, grid, kBlock, 0, st, recv, P, cw, n_valid, fill, sum_mode, \
                            o, flags, sy, a, g_mean));                                      \
   } while (0)

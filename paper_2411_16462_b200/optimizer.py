@@ -852,6 +852,20 @@ class _Allgather:
         self.L = row * 32              # one "block" covering the whole vector
 
 
+# LIONCUB_SYNC_MEAN=inline: the fused sync's owner mean runs inside the
+# vote/update grid (every CTA joins after its theta share) instead of as a
+# concurrent kernel on a side stream (A/B knob)
+SYNC_MEAN_INLINE = os.environ.get("LIONCUB_SYNC_MEAN", "side") == "inline"
+
+
+def _sync_side_stream(ws, topo):
+    if SYNC_MEAN_INLINE:
+        return None
+    if getattr(ws, "side", None) is None:
+        ws.side = torch.cuda.Stream(topo.device)
+    return ws.side.cuda_stream
+
+
 def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, g, m, mflat,
                        hyp, segs, s, tree=False, pipe=None, theta=None, msync=None):
     """K1 encode -> exchange -> owner vote into the gather buffer (+nz, ties).
@@ -962,7 +976,7 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
                       ws.vout, ws.nzout, ws.nout, ws.flags.data_ptr(), sy2, theta.data_ptr(), n,
                       _loc(ws.full).data_ptr(), _lib.ptr(_loc(ws.nz)), hyp.lr,
                       hyp.weight_decay, stage.local.data_ptr(), outs, L, nvalid,
-                      ws.counters[3:4].data_ptr(), s)
+                      ws.counters[3:4].data_ptr(), _sync_side_stream(ws, topo), s)
         ws.applied = True
         return _loc(ws.nz)
     if kind == "1bit":
