@@ -100,6 +100,8 @@ WORKLOADS = {
                            "every step"),
     "flat7b_1bit_sync": (lambda: {"w": (7_000_000_000,)}, "compressed1bit", None,
                          (1, "all"), "7e9 flat buffer, 1-bit vote + all-layer sync (configs[4])"),
+    "flat7b_1bit": (lambda: {"w": (7_000_000_000,)}, "compressed1bit", None, None,
+                    "7e9 flat buffer, 1-bit vote, no momentum sync (the non-firing C5 step)"),
 }
 
 

@@ -194,6 +194,11 @@ int lc_vote_apply(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid,
  *   side_stream: run the mean as its own kernel on that stream, concurrently
  *   with the vote/update grid (capped to leave it SMs), joined back into
  *   `stream`; NULL: every vote/update CTA joins the mean after its share. */
+/* The owner mean of the fused sync on its own (as lc_vote_apply_sync's side
+ * kernel; stand-alone for tuning and the NVLink microbenchmark): wait
+ * (nullable) -> wait_epoch only; ctas_per_sm > 0 caps the grid. */
+int lc_sync_mean(const lc_sync* wait, const float* stage, void* const* out, int32_t P, int64_t L,
+                 int64_t cnt, uint32_t* work, int32_t ctas_per_sm, void* stream);
 int lc_encode_sync(const float* g, float* m, const uint8_t* mask, int64_t n,
                    const lc_hyper* h, int fill, void* const* dst, int32_t nblocks, int64_t L,
                    uint32_t* flags, const lc_sync* sync, void* const* mstage, void* stream);

@@ -87,6 +87,7 @@ SIGNATURES = {
     "lc_vote_bits": (INT, [P, I32, I64, I64, INT, INT, P, P, P, I32, P, P, P]),
     "lc_vote_apply": (INT, [P, I32, I64, I64, INT, INT, P, P, I32, P, P, P, I64, P, P, D, D, P]),
     "lc_encode_sync": (INT, [P, P, P, I64, P, INT, P, I32, I64, P, P, P, P]),
+    "lc_sync_mean": (INT, [P, P, P, I32, I64, I64, P, I32, P]),
     "lc_vote_apply_sync": (INT, [P, I32, I64, I64, INT, INT, P, P, I32, P, P, P, I64, P, P, D, D,
                                  P, P, I64, I64, P, P, P]),
     "lc_vote_update": (INT, [P, I64, I32, P, I64, INT, INT, D, D, P, P, P]),
@@ -185,7 +186,7 @@ def check(rc: int, what: str = "", rank=None, generation=None):
 # Entry points that enqueue one of OUR kernels (for launch accounting).
 KERNEL_CALLS = frozenset({
     "lc_encode", "lc_vote_bits", "lc_vote_apply", "lc_vote_update", "lc_encode_sync",
-    "lc_vote_apply_sync", "lc_fields_vote", "lc_f64_sum_vote",
+    "lc_vote_apply_sync", "lc_sync_mean", "lc_fields_vote", "lc_f64_sum_vote",
     "lc_barrier", "lc_push_blocks_f32", "lc_mean_bcast_f32", "lc_mean_pull_f32",
     "lc_apply_update", "lc_fused_local_step", "lc_mean_f32", "lc_compute_c",
     "lc_count_bits_segmented", "lc_bits_to_sign", "lc_pack_i64_fields",

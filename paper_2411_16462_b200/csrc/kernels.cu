@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(256, LC_ENC_MINB)
 k_encode(const float* __restrict__ g, float* __restrict__ m,
          const uint8_t* __restrict__ mask, int64_t n, Hyp h, int fill, SegQ sq,
          Dst dst, int64_t L, int64_t eoff, int nrep, uint32_t* __restrict__ flags, SyncD sy,
-         Dst mst) {
+         Dst mst, int64_t rot) {
   griddep_wait();
   constexpr int WPS = (ENC == LC_ENC_F64) ? 1 : 32 * F;  // words per super-tile
   constexpr int KU = LC_ENC_KU;  // sub-tiles whose loads are in flight together
@@ -229,7 +229,12 @@ k_encode(const float* __restrict__ g, float* __restrict__ m,
   std::conditional_t<ENC == kEncQuantX, SegCursorX, SegCursor> cur;
   const bool valid_all[4] = {true, true, true, true};
 
-  for (int64_t sidx = gw; sidx < nsup; sidx += nw) {
+  // rot: the rank's starting owner block (rank + 1), so that at any moment
+  // the P ranks store into P different owners -- no incast on one owner's
+  // links while the others idle (the all-to-all stays balanced)
+  for (int64_t it = gw; it < nsup; it += nw) {
+    int64_t sidx = it + rot;
+    if (sidx >= nsup) sidx -= nsup;
     const int64_t ebase = sidx << 10;
     const int64_t gbase = eoff + ebase;            // element index in the full vector
     const int j = (int)(gbase / L);
@@ -1471,6 +1476,15 @@ thread_local int64_t g_eoff = 0;  // element offset of the encode launch
 thread_local int g_nrep = 0;      // replicate-mode destinations (0: owner blocks)
 thread_local bool g_mpush = false;  // m' -> owners' staging rows (g_mst)
 thread_local Dst g_mst{};
+thread_local int64_t g_rot = 0;     // starting super-tile of the encode launch
+
+// Owner-block exchanges start each rank at owner (rank + 1) % P.
+int64_t encode_rotation(const lc_sync* sync, int64_t n, int64_t L, int64_t eoff, bool rep) {
+  if (!sync || sync->P < 2 || rep || eoff != 0) return 0;
+  const int64_t nsup = (n + 1023) >> 10;
+  if (nsup < 1) return 0;
+  return ((int64_t)((sync->rank + 1) % sync->P) * (L >> 10)) % nsup;
+}
 
 template <int ENC, int F, bool MASK>
 int launch_encode(const float* g, float* m, const uint8_t* mask, int64_t n, Hyp h,
@@ -1482,7 +1496,7 @@ int launch_encode(const float* g, float* m, const uint8_t* mask, int64_t n, Hyp 
       auto kern = k_encode<ENC, F, MASK, true>;
       int grid = stream_grid(kern, kBlock, nsup, kBlock / 32);
       LC_CUDA_TRY(launch_pdl(kern, grid, kBlock, 0, st, g, m, mask, n, h, fill, sq, dst, L,
-                             g_eoff, g_nrep, flags, g_sync, g_mst));
+                             g_eoff, g_nrep, flags, g_sync, g_mst, g_rot));
       LC_LAUNCH_CHECK();
       return LC_OK;
     }
@@ -1490,7 +1504,7 @@ int launch_encode(const float* g, float* m, const uint8_t* mask, int64_t n, Hyp 
   auto kern = k_encode<ENC, F, MASK, false>;
   int grid = stream_grid(kern, kBlock, nsup, kBlock / 32);
   LC_CUDA_TRY(launch_pdl(kern, grid, kBlock, 0, st, g, m, mask, n, h, fill, sq, dst, L, g_eoff,
-                         g_nrep, flags, g_sync, g_mst));
+                         g_nrep, flags, g_sync, g_mst, g_rot));
   LC_LAUNCH_CHECK();
   return LC_OK;
 }
@@ -1576,6 +1590,7 @@ int lc_encode(const float* g, float* m, const uint8_t* mask, int64_t n,
   if (!make_dst(d, dst, nblocks)) return set_err(LC_E_ARG, "lc_encode: bad destination table");
   g_nrep = rep ? nblocks : 0;
   g_mpush = false;
+  g_rot = encode_rotation(sync, n, L, eoff, rep);
   Hyp h = to_hyp(hp);
   SegQ sq = to_segq(segs);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -1623,6 +1638,7 @@ int lc_encode_sync(const float* g, float* m, const uint8_t* mask, int64_t n,
   g_sync = to_syncd(sync);
   g_mst = ms;
   g_mpush = true;
+  g_rot = encode_rotation(sync, n, L, 0, false);
   const int rc = dispatch_mask<LC_ENC_SIGN1, 1>(g, m, mask, n, to_hyp(hp), fill, to_segq(nullptr), d,
                                                  L, flags, reinterpret_cast<cudaStream_t>(stream));
   g_mpush = false;
@@ -1823,6 +1839,31 @@ int lc_vote_apply_sync(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_va
   }
   LC_CUDA_TRY(cudaEventRecord(join, side));
   LC_CUDA_TRY(cudaStreamWaitEvent(st, join, 0));
+  return LC_OK;
+}
+
+int lc_sync_mean(const lc_sync* wait, const float* stage, void* const* out, int32_t P, int64_t L,
+                 int64_t cnt, uint32_t* work, int32_t ctas_per_sm, void* stream) {
+  MeanArgs ma{};
+  if (P < 1 || P > LC_MAX_BLOCKS || !stage || !work || L <= 0 || (L % 4) != 0 || cnt < 0 ||
+      cnt > L || !make_dst(ma.out, out, P) || (reinterpret_cast<uintptr_t>(stage) & 15u))
+    return set_err(LC_E_ARG, "lc_sync_mean: bad arguments");
+  for (int k = 0; k < P; ++k)
+    if ((reinterpret_cast<uintptr_t>(ma.out.p[k]) & 15u) != 0)
+      return set_err(LC_E_ARG, "lc_sync_mean: outputs must be 16-byte aligned");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  LC_CUDA_TRY(cudaMemsetAsync(work, 0, sizeof(uint32_t), st));
+  if (cnt == 0) return LC_OK;
+  ma.stage = stage;
+  ma.L = L;
+  ma.cnt = cnt;
+  ma.work = work;
+  SyncD w = to_syncd(wait);
+  w.arrive_epoch = 0;
+  int grid = stream_grid(k_sync_mean, kBlock, (cnt + kMeanChunk - 1) / kMeanChunk, 1);
+  if (ctas_per_sm > 0 && grid > sm_count() * ctas_per_sm) grid = sm_count() * ctas_per_sm;
+  LC_CUDA_TRY(launch_pdl(k_sync_mean, grid, kBlock, 0, st, w, ma, (int)P));
+  LC_LAUNCH_CHECK();
   return LC_OK;
 }
 

@@ -852,14 +852,15 @@ class _Allgather:
         self.L = row * 32              # one "block" covering the whole vector
 
 
-# LIONCUB_SYNC_MEAN=inline: the fused sync's owner mean runs inside the
-# vote/update grid (every CTA joins after its theta share) instead of as a
-# concurrent kernel on a side stream (A/B knob)
-SYNC_MEAN_INLINE = os.environ.get("LIONCUB_SYNC_MEAN", "side") == "inline"
+# LIONCUB_SYNC_MEAN: where the fused sync's owner mean runs -- "serial": its
+# own kernel after the vote/update kernel; "side": concurrently with it on a
+# side stream (vote/update grid capped); "inline": inside the vote/update grid
+# (every CTA joins after its theta share)
+SYNC_MEAN = os.environ.get("LIONCUB_SYNC_MEAN", "serial")   # serial | side | inline
 
 
 def _sync_side_stream(ws, topo):
-    if SYNC_MEAN_INLINE:
+    if SYNC_MEAN == "inline":
         return None
     if getattr(ws, "side", None) is None:
         ws.side = torch.cuda.Stream(topo.device)
@@ -969,6 +970,17 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
                       ws.nzout, ws.nout, ws.flags.data_ptr(), sy2, theta.data_ptr(), n,
                       _loc(ws.full).data_ptr(), _lib.ptr(_loc(ws.nz)), hyp.lr,
                       hyp.weight_decay, s)
+        elif SYNC_MEAN == "serial":
+            # vote/update, then the owner mean as its own full-occupancy kernel
+            # (stream order: the vote kernel already waited for every K1)
+            stage = tp.sym_buffer(r, ws.key + ("mstage",), P * L, torch.float32)
+            outs = _lib.table([msync.sym.peers[k] + r * L * 4 for k in range(P)])
+            _lib.call("lc_vote_apply", recv.data_ptr(), P, cw, nvalid, fill, sum_mode, ws.vout,
+                      ws.nzout, ws.nout, ws.flags.data_ptr(), sy2, theta.data_ptr(), n,
+                      _loc(ws.full).data_ptr(), _lib.ptr(_loc(ws.nz)), hyp.lr,
+                      hyp.weight_decay, s)
+            _lib.call("lc_sync_mean", None, stage.local.data_ptr(), outs, P, L, nvalid,
+                      ws.counters[3:4].data_ptr(), 0, s)
         else:
             stage = tp.sym_buffer(r, ws.key + ("mstage",), P * L, torch.float32)
             outs = _lib.table([msync.sym.peers[k] + r * L * 4 for k in range(P)])

@@ -70,6 +70,15 @@ def main():
     if vec.mc:
         timed("mcast", lambda: _lib.call("lc_mean_pull_f32", local_out, 1, rank * s, cnt,
                                          _lib.table([vec.mc]), -1, None, st), cnt * 4)
+    # the fused sync's owner mean: P local staged rows -> fp32 mean stored into
+    # every rank (k_sync_mean), at several grid sizes (CTAs per SM)
+    work = torch.zeros(1, dtype=torch.int32, device=dev)
+    mean_out = _lib.table([p + rank * s * 4 for p in vec.peers])
+    cnt_m = max(0, min(s, n - rank * s))
+    for cps in (1, 2, 4, 8):
+        timed(f"sync_mean_cps{cps}", lambda c=cps: _lib.call(
+            "lc_sync_mean", None, stage.local.data_ptr(), mean_out, world, s, cnt_m,
+            work.data_ptr(), c, st), (world - 1) * cnt_m * 4)
     peers_out = _lib.table(vec.peers)
     timed("store_all", lambda: _lib.call("lc_mean_pull_f32", local_out, 1, rank * s, cnt,
                                          peers_out, world, None, st), (world - 1) * cnt * 4)
