@@ -7,6 +7,8 @@
 // Math that decides a sign (c, the p-bit scale, the update) runs in float64
 // with every product/sum rounded separately (no FMA contraction) so results
 // equal the float64 numpy reference bit-for-bit; fp32 state is rounded once.
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -1786,9 +1788,29 @@ int fork_events(cudaEvent_t& fork, cudaEvent_t& join) {
 }
 }  // namespace
 
-#ifndef LC_SYNC_VA_CTAS
-#define LC_SYNC_VA_CTAS 1  // vote/update CTAs per SM while the side-stream mean runs
-#endif
+// CTAs per SM of the vote/update grid and of the side-stream mean while they
+// run together (LIONCUB_SYNC_SIDE_CTAS="va,mean").  Default 2,1: the mean
+// needs few SMs to saturate NVLink stores, the theta update wants HBM
+// bandwidth.  Measured, 7e9 params, 4 x B200, whole sync step: 3,1 69.7 ms;
+// 2,1 67.8; 2,2 69.5; 4,1 73.7; 1,2 78.4 (serial kernels: 75.0, the mean
+// inside the vote grid: 75.8).
+struct SideCtas {
+  int va = 2, mean = 1;
+};
+const SideCtas& side_ctas() {
+  static const SideCtas c = [] {
+    SideCtas v;
+    if (const char* e = std::getenv("LIONCUB_SYNC_SIDE_CTAS")) {
+      int a = 0, b = 0;
+      if (std::sscanf(e, "%d,%d", &a, &b) == 2 && a > 0 && b > 0) {
+        v.va = a;
+        v.mean = b;
+      }
+    }
+    return v;
+  }();
+  return c;
+}
 
 int lc_vote_apply_sync(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid, int fill,
                        int sum_mode, void* const* voted, void* const* nz, int32_t nout,
@@ -1825,7 +1847,7 @@ int lc_vote_apply_sync(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_va
   if (int rc = fork_events(fork, join)) return rc;
   LC_CUDA_TRY(cudaEventRecord(fork, st));
   LC_CUDA_TRY(cudaStreamWaitEvent(side, fork, 0));
-  g_va_cap = LC_SYNC_VA_CTAS;
+  g_va_cap = side_ctas().va;
   const int rc = lc_vote_apply(recv, P, cw, n_valid, fill, sum_mode, voted, nz, nout, flags, sync,
                                theta, n, full, nz_full, lr, wd, stream);
   g_va_cap = 0;
@@ -1833,7 +1855,8 @@ int lc_vote_apply_sync(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_va
   if (ma.stage) {
     SyncD wait = to_syncd(sync);
     wait.arrive_epoch = 0;  // the mean publishes nothing (the caller's barrier follows)
-    const int grid = stream_grid(k_sync_mean, kBlock, (mean_cnt + kMeanChunk - 1) / kMeanChunk, 1);
+    int grid = stream_grid(k_sync_mean, kBlock, (mean_cnt + kMeanChunk - 1) / kMeanChunk, 1);
+    if (grid > sm_count() * side_ctas().mean) grid = sm_count() * side_ctas().mean;
     LC_CUDA_TRY(launch_pdl(k_sync_mean, grid, kBlock, 0, side, wait, ma, (int)P));
     LC_LAUNCH_CHECK();
   }

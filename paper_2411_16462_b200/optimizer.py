@@ -856,7 +856,7 @@ class _Allgather:
 # own kernel after the vote/update kernel; "side": concurrently with it on a
 # side stream (vote/update grid capped); "inline": inside the vote/update grid
 # (every CTA joins after its theta share)
-SYNC_MEAN = os.environ.get("LIONCUB_SYNC_MEAN", "serial")   # serial | side | inline
+SYNC_MEAN = os.environ.get("LIONCUB_SYNC_MEAN", "side")   # side | serial | inline
 
 
 def _sync_side_stream(ws, topo):
