@@ -341,6 +341,11 @@ int lc_f64_to_f32_exact(const double* x, int64_t n, float* out, uint32_t* flags,
 int lc_std_max_segmented(const float* rows, int32_t P, int64_t n, int64_t stride,
                          const int64_t* seg_start, int32_t nseg, double* out_max,
                          void* stream);
+/* Vote sign vs the sign of the full-precision aggregate (runner.py:171-177):
+ * counts[0] = #(vote == sign(ref) and vote != 0), counts[1] = #(vote ==
+ * -sign(ref), both nonzero); ref = allreduce_mean_f32(c_local). */
+int lc_sign_agreement(const int8_t* vote, const float* ref, int64_t n, int64_t* counts,
+                      void* stream);
 /* c as float64 (metrics_out["c_local"], optimizer.py:209). */
 int lc_compute_c(const float* g, const float* m, const uint8_t* mask,
                  int64_t n, const lc_hyper* h, double* c, void* stream);

@@ -17,7 +17,7 @@ from .optimizer import (VOTE_ALGOS, FlatParamSet, Layout, LionHyper,  # noqa: F4
                         distributed_lion_step_host, divergence_from_momenta,
                         momentum_divergence, signsgd_majority_step,
                         hash_params, lion_step, load_checkpoint,
-                        maybe_sync_momentum, save_checkpoint)
+                        maybe_sync_momentum, save_checkpoint, vote_agreement)
 from .quant import (INF, PackedBits, QuantSpec, SignPolicy, apply_sign,  # noqa: F401
                     dequantize, lp_mean_norm, pack, quantize, unpack)
 from .torch_optim import LionCub, lioncub_comm_hook  # noqa: F401

@@ -107,6 +107,7 @@ SIGNATURES = {
     "lc_f64_to_f32_exact": (INT, [P, I64, P, P, P]),
     "lc_std_max_segmented": (INT, [P, I32, I64, I64, P, I32, P, P]),
     "lc_compute_c": (INT, [P, P, P, I64, P, P, P]),
+    "lc_sign_agreement": (INT, [P, P, I64, P, P]),
     "lc_count_bits_segmented": (INT, [P, P, I32, P, P]),
     "lc_bits_to_sign": (INT, [P, P, I64, P, P]),
     "lc_pack_i64_fields": (INT, [P, I64, I32, I32, I32, P, P, P]),
@@ -189,6 +190,7 @@ KERNEL_CALLS = frozenset({
     "lc_vote_apply_sync", "lc_sync_mean", "lc_fields_vote", "lc_f64_sum_vote",
     "lc_barrier", "lc_push_blocks_f32", "lc_mean_bcast_f32", "lc_mean_pull_f32",
     "lc_apply_update", "lc_fused_local_step", "lc_mean_f32", "lc_compute_c",
+    "lc_sign_agreement",
     "lc_count_bits_segmented", "lc_bits_to_sign", "lc_pack_i64_fields",
     "lc_fields_decode", "lc_sign_pack_f64", "lc_sign_check", "lc_sum_u32_rows", "lc_quantize_values",
     "lc_dequantize", "lc_apply_sign_values", "lc_f64_to_f32_exact", "lc_std_max_segmented"})

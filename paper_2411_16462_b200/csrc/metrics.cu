@@ -62,9 +62,51 @@ k_std_max(const float* __restrict__ rows, int P, int64_t n, int64_t stride,
       if (tab[i]) atomicMax(&out[s_first + i], tab[i]);
 }
 
+// runner.py:171-177: the vote sign against the sign of the full-precision
+// aggregate ref = allreduce_mean_f32(c_local): match where equal and the vote
+// is nonzero, flip where strictly opposite (both nonzero).  np.sign of a NaN
+// mean is NaN, which matches nothing.
+__global__ void __launch_bounds__(kBlock)
+k_sign_agreement(const int8_t* __restrict__ vote, const float* __restrict__ ref, int64_t n,
+                 unsigned long long* __restrict__ out) {
+  unsigned long long match = 0, flip = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int v = vote[i];
+    const float r = ref[i];
+    const int s = r > 0.f ? 1 : (r < 0.f ? -1 : 0);
+    const bool nan = r != r;
+    match += (!nan && v != 0 && v == s);
+    flip += (!nan && v != 0 && s != 0 && v == -s);
+  }
+  for (int o = 16; o; o >>= 1) {
+    match += __shfl_xor_sync(0xffffffffu, match, o);
+    flip += __shfl_xor_sync(0xffffffffu, flip, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(out, match);
+    atomicAdd(out + 1, flip);
+  }
+}
+
 }  // namespace
 
 extern "C" {
+
+int lc_sign_agreement(const int8_t* vote, const float* ref, int64_t n, int64_t* counts,
+                      void* stream) {
+  if (n < 0 || !counts) return lc::set_err(LC_E_ARG, "lc_sign_agreement: bad arguments");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  LC_CUDA_TRY(cudaMemsetAsync(counts, 0, 2 * sizeof(int64_t), st));
+  if (n == 0) return LC_OK;
+  if (!vote || !ref) return lc::set_err(LC_E_ARG, "lc_sign_agreement: null pointer");
+  int64_t grid = (n + kBlock - 1) / kBlock;
+  grid = std::min<int64_t>(grid, (int64_t)lc::sm_count() * 8);
+  k_sign_agreement<<<(int)grid, kBlock, 0, st>>>(vote, ref, n,
+                                                 reinterpret_cast<unsigned long long*>(counts));
+  LC_LAUNCH_CHECK();
+  return LC_OK;
+}
 
 int lc_std_max_segmented(const float* rows, int32_t P, int64_t n, int64_t stride,
                          const int64_t* seg_start, int32_t nseg, double* out_max,

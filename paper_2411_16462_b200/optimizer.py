@@ -716,6 +716,10 @@ def _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out,
             if ternary and binary:
                 _ternary_precheck(topo, gen, g, m, mflat, n, hyp, dev, s,
                                   "1bit" if algo == "compressed1bit" else "fields")
+            timer = None
+            if metrics:   # metrics_out["t_quant"/"t_comm"] (optimizer.py:141-168)
+                timer = {"start": torch.cuda.Event(enable_timing=True)}
+                timer["start"].record(stream)
             segs = None
             if kind == "fields" and not binary:
                 segs = _quant_scales(ws, layout, dev, g.flat, m.flat, mflat, hyp, spec, s, seed)
@@ -744,6 +748,9 @@ def _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out,
                     if pipe is not None:
                         for c in range(len(pipe.ranges)):
                             pipe.emit_out(c, th.flat, stream)
+                if timer is not None:   # one fused pass: quantize + the one-rank vote
+                    _mark(timer, "enc", stream)
+                    _mark(timer, "vote", stream)
                 nz = _loc(ws.nz) if metrics else None
             else:
                 if _fused_sync_ok(sync, layout, topo, t, kind, metrics, pipe, n) and \
@@ -753,7 +760,7 @@ def _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out,
                 nz = _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill,
                                         n, g, m, mflat, hyp, segs, s,
                                         tree=algo == "ps_efficient", pipe=pipe,
-                                        theta=th.flat, msync=msync)
+                                        theta=th.flat, msync=msync, timer=timer)
                 if strict and not ws.p2p and hasattr(tp, "wait_collectives"):
                     # NCCL exchange: no theta update unless every collective landed
                     tp.wait_collectives(topo.rank, gen, "vote exchange")
@@ -780,6 +787,19 @@ def _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out,
                 _raise_nan(ws)
             if metrics:
                 _fill_metrics(metrics_out, layout, dev, ws, nz, c_local, s)
+                # device time of the phases the reference times with
+                # perf_counter in _vote: the quantize/pack pass (norms + K1)
+                # and the collective (exchange + vote); 1-bit: all t_comm
+                t0, t1, t2 = timer["start"], timer["enc"], timer["vote"]
+                t2.synchronize()
+                if algo == "compressed1bit":
+                    metrics_out["t_comm"] = metrics_out.get("t_comm", 0.0) + \
+                        t0.elapsed_time(t2) * 1e-3
+                else:
+                    metrics_out["t_quant"] = metrics_out.get("t_quant", 0.0) + \
+                        t0.elapsed_time(t1) * 1e-3
+                    metrics_out["t_comm"] = metrics_out.get("t_comm", 0.0) + \
+                        t1.elapsed_time(t2) * 1e-3
     out = WorkerState(params=th, momentum=m, iteration=t)
     if msync is not None:
         out._lc_synced = t
@@ -867,8 +887,15 @@ def _sync_side_stream(ws, topo):
     return ws.side.cuda_stream
 
 
+def _mark(timer, name, stream):
+    if timer is not None:
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        timer[name] = ev
+
+
 def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, g, m, mflat,
-                       hyp, segs, s, tree=False, pipe=None, theta=None, msync=None):
+                       hyp, segs, s, tree=False, pipe=None, theta=None, msync=None, timer=None):
     """K1 encode -> exchange -> owner vote into the gather buffer (+nz, ties).
     With ``theta`` on the fused peer-memory path the theta update runs in
     the vote's grid (``ws.applied`` is set)."""
@@ -947,6 +974,7 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
         _lib.call("lc_encode", gp, mp, mk, n, C.byref(hyp), fill, enc, fb,
                   C.byref(segs) if segs is not None else None, ws.dst, P, L, 0,
                   ws.flags.data_ptr(), sy1, s)
+    _mark(timer, "enc", torch.cuda.ExternalStream(s) if timer is not None else None)
     rows = 1
     if ws.p2p:
         if not fused:
@@ -1011,6 +1039,7 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
             tp.allgather(r, gen, ws.nz[r * cw:], ws.nz, cw * 4)
         if ws.ties is not None:
             tp.allgather(r, gen, ws.ties[r * cw:], ws.ties, cw * 4)
+    _mark(timer, "vote", torch.cuda.ExternalStream(s) if timer is not None else None)
     return _loc(ws.nz)
 
 
@@ -1023,6 +1052,7 @@ def _fill_metrics(out: dict, layout: Layout, dev, ws, nz, c_local, s):
     signs = torch.empty(max(n, 1), dtype=torch.int8, device=dev)
     _lib.call("lc_bits_to_sign", _loc(ws.full).data_ptr(), _lib.ptr(nz), n,
               signs.data_ptr(), s)
+    out["_flat"] = {"c_local": c_local[:n], "vote_sign": signs[:n]}   # for vote_agreement
     signs = signs.long()
     cl = counts.tolist()
     for i, k in enumerate(layout.names):
@@ -1030,6 +1060,31 @@ def _fill_metrics(out: dict, layout: Layout, dev, ws, nz, c_local, s):
         out.setdefault("ties", {})[k] = int(cl[i])
         out.setdefault("vote_sign", {})[k] = signs[o:o + c].view(layout.shapes[k])
         out.setdefault("c_local", {})[k] = c_local[o:o + c].view(layout.shapes[k])
+
+
+def vote_agreement(metrics_out: dict, topo: Topology) -> dict:
+    """The runner's per-step vote metrics (runner.py:171-182) from a step's
+    ``metrics_out``, on the device: ``tie_rate`` = all layers' ties / n;
+    ``sign_match`` / ``flip_rate`` = the vote sign against the sign of the
+    full-precision aggregate ``allreduce_mean_f32(c_local)`` (bit-identical
+    to the reference's mean), counted in one kernel.  Collective: every rank
+    calls it after the same step."""
+    from .collectives import allreduce_mean_f32
+    flat = metrics_out.get("_flat")
+    if flat is None:
+        raise ConfigError("vote_agreement needs the metrics_out of a distributed_lion_step")
+    c_local, vote = flat["c_local"], flat["vote_sign"]
+    n = vote.numel()
+    dev = vote.device
+    with _on_device(dev), _on_stream(topo.stream, dev):
+        ref = allreduce_mean_f32(c_local, topo)
+        counts = torch.zeros(2, dtype=torch.int64, device=dev)
+        _lib.call("lc_sign_agreement", vote.data_ptr(), ref.data_ptr(), n, counts.data_ptr(),
+                  topo.stream.cuda_stream)
+        match, flip = counts.tolist()
+    ties = sum(metrics_out["ties"].values())
+    return {"tie_rate": ties / n if n else 0.0, "sign_match": match / n if n else 0.0,
+            "flip_rate": flip / n if n else 0.0}
 
 
 def _symmetric_momentum(m: FlatParamSet, topo: Topology) -> FlatParamSet:

@@ -80,11 +80,24 @@ def run_step_case(case: dict, out: dict):
         st2 = distributed_lion_step(st, grads, h, spec, topo, case["algo"],
                                     mask=mask, zero_mode=case["zero_mode"],
                                     metrics_out=metrics)
+        # the runner's vote metrics of this step (runner.py:171-182), before
+        # the sync (the runner computes them from the step's metrics_out)
+        match = flip = counted = 0
+        for layer in sorted(SIZES):
+            ref = np.sign(allreduce_mean_f32(metrics["c_local"][layer], topo))
+            vs = metrics["vote_sign"][layer]
+            match += int(np.count_nonzero((vs == ref) & (vs != 0)))
+            flip += int(np.count_nonzero((vs == -ref) & (vs != 0) & (ref != 0)))
+            counted += vs.size
+        metrics["agree"] = (match, flip, counted)
         if sync is not None:
             st2 = maybe_sync_momentum(st2, sync, topo)
         return st2, metrics
 
     res = run_ranks(world, fn, transport=InprocTransport(world))
+    out[f"{name}/out/agree"] = np.asarray(res[0][1]["agree"], dtype=np.int64)
+    out[f"{name}/out/timing_keys"] = np.asarray(
+        [int("t_quant" in res[0][1]), int("t_comm" in res[0][1])], dtype=np.int64)
     p = f"{name}/"
     for layer in SIZES:
         out[p + f"in/theta/{layer}"] = ranks[0]["theta"][layer]

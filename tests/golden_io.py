@@ -51,6 +51,7 @@ def step_case(name: str) -> dict:
                norm=[{k: data.get(p + f"out/norm/{r}/{k}") for k in sizes}
                      for r in range(world)],
                c=[{k: data.get(p + f"out/c/{r}/{k}") for k in sizes} for r in range(world)],
+               agree=data.get(p + "out/agree"), timing_keys=data.get(p + "out/timing_keys"),
                mask={k: data[p + f"in/mask/{k}"] for k in sizes
                      if (p + f"in/mask/{k}") in data} or None)
     return out

@@ -114,3 +114,43 @@ def test_divergence_and_allgather_known_answers():
     for out in lc.run_ranks(3, fn):                  # test_collectives.py:226-235
         assert len(out) == 3 and all(np.array_equal(out[i], vecs[i]) for i in range(3))
         assert out[0].dtype == np.float64
+
+
+@pytest.mark.parametrize("xchg", ["peer-memory", "collectives"])
+@pytest.mark.parametrize("name", [c["name"] for c in G.step_cases()])
+def test_vote_agreement_and_phase_timing_match_reference(name, xchg):
+    """The runner's per-step vote metrics (runner.py:171-182) through
+    vote_agreement -- the vote sign against sign(allreduce_mean_f32(c_local))
+    -- equal the reference's counts exactly; metrics_out carries the
+    reference's phase-timing keys (t_quant only off the 1-bit path,
+    optimizer.py:141-168) as positive device times."""
+    gc = G.step_case(name)
+    case = gc["case"]
+    world = case["world"]
+    from tests.golden.cases import quant_kwargs
+    kw = quant_kwargs(case)
+    h = lc.LionHyper(beta1=0.9, beta2=0.99, lr=case["lr"], weight_decay=case["wd"])
+    cmask = None
+    if gc["mask"] is not None:
+        cmask = {k: torch.from_numpy(np.asarray(v)).cuda() for k, v in gc["mask"].items()}
+
+    def fn(topo):
+        r = topo.rank
+        st = make_state(gc["theta"], gc["m"][r], case["iteration"])
+        g = grads_like(st, gc["g"][r])
+        met = {}
+        lc.distributed_lion_step(st, g, h, None if kw is None else lc.QuantSpec(**kw), topo,
+                                 case["algo"], mask=cmask, zero_mode=case["zero_mode"],
+                                 metrics_out=met)
+        agree = lc.vote_agreement(met, topo)
+        return agree, {k: met[k] for k in ("t_quant", "t_comm") if k in met}
+
+    res = lc.run_ranks(world, fn, transport=make_transport(world, xchg))
+    match, flip, counted = (int(x) for x in gc["agree"])
+    has_q, has_c = (bool(x) for x in gc["timing_keys"])
+    for agree, times in res:
+        assert round(agree["sign_match"] * counted) == match, (agree, match)
+        assert round(agree["flip_rate"] * counted) == flip, (agree, flip)
+        assert round(agree["tie_rate"] * counted) == sum(gc["ties"].values())
+        assert ("t_quant" in times) == has_q and ("t_comm" in times) == has_c
+        assert all(v > 0 for v in times.values())
