@@ -732,3 +732,51 @@ def test_checkpoint_resume_equals_continuous(tmp_path):
     assert a.iteration == b.iteration == 6
     assert torch.equal(a.params.flat[:a.params.layout.n], b.params.flat[:b.params.layout.n])
     assert torch.equal(a.momentum.flat[:a.params.layout.n], b.momentum.flat[:b.params.layout.n])
+
+
+@pytest.mark.parametrize("world,algo,bits,xchg", [
+    (1, "compressed1bit", None, "peer-memory"),
+    (1, "direct", 1, "peer-memory"),
+    (1, "ps", None, "peer-memory"),
+    (2, "compressed1bit", None, "fused"),      # allgather exchange
+    (3, "direct", 1, "fused"),                # owner vote, sum-of-signs
+    (4, "compressed1bit", None, "fused"),
+])
+def test_lioncub_overlap_backward_equals_plain(world, algo, bits, xchg, monkeypatch):
+    """LionCub(overlap_backward=True) encodes 1024-aligned chunks of the flat
+    buffer from post-accumulate-grad hooks while backward runs; six training
+    steps give the bit-identical state of the ordinary step."""
+    from paper_2411_16462_b200 import overlap
+    monkeypatch.setattr(overlap, "CHUNK", 1 << 14)
+    torch.manual_seed(1)
+
+    def make():
+        return torch.nn.Sequential(torch.nn.Linear(64, 512), torch.nn.Tanh(),
+                                   torch.nn.Linear(512, 256), torch.nn.Tanh(),
+                                   torch.nn.Linear(256, 1)).cuda()
+
+    init = {k: v.clone() for k, v in make().state_dict().items()}
+    xs = [torch.randn(128, 64, device="cuda") for _ in range(world)]
+    ys = [x.sum(dim=1, keepdim=True).sin() for x in xs]
+
+    def run(overlap_on):
+        def fn(topo):
+            model = make()
+            model.load_state_dict(init)
+            opt = lc.LionCub(model.named_parameters(), topo, lr=1e-3,
+                             spec=None if bits is None else lc.QuantSpec(bits=bits), algo=algo,
+                             overlap_backward=overlap_on)
+            if overlap_on:
+                assert opt._early is not None, "configuration should overlap"
+            for _ in range(6):
+                opt.zero_grad()
+                torch.nn.functional.mse_loss(model(xs[topo.rank]), ys[topo.rank]).backward()
+                opt.step()
+            host_wait()
+            return opt.lion_state.params.flat.cpu().numpy(), opt.lion_state.momentum.flat.cpu().numpy()
+        return lc.run_ranks(world, fn, transport=make_transport(world, xchg))
+
+    plain, over = run(False), run(True)
+    for (tp_, mp_), (to_, mo_) in zip(plain, over):
+        assert np.array_equal(tp_.view(np.int32), to_.view(np.int32))
+        assert np.array_equal(mp_.view(np.int32), mo_.view(np.int32))
