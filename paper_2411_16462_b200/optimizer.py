@@ -706,9 +706,9 @@ def _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out,
             _raise_nan(ws)  # a NaN update seen by an earlier (unsynced) step
             gen = topo.next_generation()
             if strict:
-                _mark = getattr(tp, "mark_reached", None)
-                if _mark is not None:
-                    _mark(topo.rank, gen)
+                reached = getattr(tp, "mark_reached", None)
+                if reached is not None:
+                    reached(topo.rank, gen)
             if metrics:
                 c_local = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
                 _lib.call("lc_compute_c", g.flat.data_ptr(), m.flat.data_ptr(),
