@@ -98,7 +98,7 @@ enum {
 /* Per-layer segment table of a flat buffer (layers in sorted-name order).
  * The quantizer (quant.py:127-173) is q = clip(round(scale[s] * y), +-qmax)
  * with y = c, or y = sign(c) log1p(|c| / log_scale[s]) when log_scale is
- * given and log_scale[s] > 0 (log_transform, quant.py:146-150). */
+ * given and log_scale[s] > 0 (log_transform, quant.py:143-146). */
 typedef struct lc_segments {
   const int64_t* start; /* device, nseg+1 offsets (elements)               */
   const double* scale;  /* device, nseg scales: qmax/(2 M_p), or qmax/M_inf
@@ -125,12 +125,12 @@ int lc_set_grid_divisor(int divisor);
 #define LC_MAX_BLOCKS 64
 
 /* ---- K1: fused Lion interpolate + sign/quantize + pack + momentum EMA ----
- * Replaces optimizer.py:199-201 (c, mask), :205 (m'), quant.py:273-279
- * (apply_sign), quant.py:330-356 (pack width 1 / F-bit fields),
- * quant.py:236-243 (finite-p quantize given the per-layer scale), and the
+ * Replaces optimizer.py:199-201 (c, mask), :205 (m'), quant.py:198-204
+ * (apply_sign), quant.py:255-281 (pack width 1 / F-bit fields),
+ * quant.py:161-168 (finite-p quantize given the per-layer scale), and the
  * offsetting of collectives.py:201-210.  Computes c and m' in float64 from
  * fp32 g,m (no FMA contraction) and writes m' (fp32) in place.
- *   fill: +1 / -1 = alternating zero fill (quant.py:151-153), 0 = ternary.
+ *   fill: +1 / -1 = alternating zero fill (quant.py:76-78), 0 = ternary.
  *   field_bits: 1 for SIGN1, F in {1,2,4,8,16,32} for *_FIELDS, 64 for F64.
  *   dst[j], j < nblocks: where block j (elements [j*L, (j+1)*L)) of the
  *     packed vector goes -- uint32 words (L*F/32 per block) or doubles.
@@ -277,11 +277,11 @@ int lc_fused_local_step(float* theta, float* m, const float* g,
 int lc_mean_f32(const float* recv, int32_t P, int64_t len, int64_t stride,
                 float* out, void* stream);
 
-/* ---- L1 norm per segment, numpy-exact (quant.py:156-179, p=1):
+/* ---- L1 norm per segment, numpy-exact (quant.py:81-104, p=1):
  * M1 = max|c| * (pairwise_sum(|c|/max) / n) with numpy's pairwise
  * summation order reproduced exactly; c recomputed from g,m,mask.
  * Writes per-segment norms and scale = qmax/(2 M1) (0 if M1 == 0),
- * quant.py:236.  The plan holds the summation-tree schedule (device). */
+ * quant.py:161.  The plan holds the summation-tree schedule (device). */
 typedef struct lc_l1_plan_s* lc_l1_plan_t;
 int lc_l1_plan_create(lc_l1_plan_t* plan, const int64_t* seg_start_host,
                       int32_t nseg);
@@ -356,7 +356,7 @@ int lc_count_bits_segmented(const uint32_t* bits, const int64_t* seg_start,
 int lc_bits_to_sign(const uint32_t* sign_bits, const uint32_t* nz_bits,
                     int64_t n, int8_t* out, void* stream);
 /* int64 values -> F-bit fields of v+offset (binary: (v+1)>>1), range check
- * into flags (collectives.py:201-210, quant.py:330-356). */
+ * into flags (collectives.py:201-210, quant.py:255-281). */
 int lc_pack_i64_fields(const int64_t* v, int64_t n, int32_t field_bits,
                        int32_t offset, int32_t binary, uint32_t* out,
                        uint32_t* flags, void* stream);

@@ -42,12 +42,12 @@ class OracleCapacityError(OracleConfigError):
 # ---------------------------------------------------------------------------
 
 def zero_fill(iteration: int) -> int:
-    """``SignPolicy.zero_fill`` (quant.py:151-153): +1 on odd t, -1 on even."""
+    """``SignPolicy.zero_fill`` (quant.py:76-78): +1 on odd t, -1 on even."""
     return 1 if iteration % 2 == 1 else -1
 
 
 def apply_sign(x, mode: str, iteration: int) -> np.ndarray:
-    """``apply_sign`` (quant.py:273-279).  -0.0 == 0 so it takes the fill."""
+    """``apply_sign`` (quant.py:198-204).  -0.0 == 0 so it takes the fill."""
     x = np.asarray(x)
     s = np.sign(x).astype(np.int64)
     if mode == "alternating":
@@ -57,7 +57,7 @@ def apply_sign(x, mode: str, iteration: int) -> np.ndarray:
 
 def pairwise_sum(a: np.ndarray) -> float:
     """numpy's float64 pairwise summation order (the order ``np.mean`` uses
-    inside ``lp_mean_norm``, quant.py:179).  Blocks of <=128 elements use 8
+    inside ``lp_mean_norm``, quant.py:104).  Blocks of <=128 elements use 8
     strided accumulators combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7));
     larger blocks split at n/2 rounded down to a multiple of 8.  Kept here
     as executable documentation of the order the CUDA norm kernel mirrors;
@@ -90,7 +90,7 @@ def pairwise_sum(a: np.ndarray) -> float:
 
 
 def lp_mean_norm_l1(x) -> float:
-    """``lp_mean_norm(x, 1)`` (quant.py:156-179, finite-p branch):
+    """``lp_mean_norm(x, 1)`` (quant.py:81-104, finite-p branch):
     M1 = max|x| * mean(|x|/max|x|)."""
     x = np.asarray(x, dtype=np.float64)
     if x.size == 0:
@@ -104,7 +104,7 @@ def lp_mean_norm_l1(x) -> float:
 
 def quantize_l1(x, bits: int) -> np.ndarray:
     """``quantize`` with ``QuantSpec(bits, norm_p=1, rounding="nearest")``
-    (quant.py:202-248): q = clip(round_half_even(qmax/(2 M1) * x), +-qmax)."""
+    (quant.py:127-173): q = clip(round_half_even(qmax/(2 M1) * x), +-qmax)."""
     x = np.asarray(x, dtype=np.float64)
     if x.size == 0:
         raise OracleConfigError("quantize of an empty vector")
@@ -210,7 +210,7 @@ def quantize(x, spec: "Spec", uniforms=None) -> np.ndarray:
 
 def quant_scale(x, spec: "Spec") -> tuple:
     """(scale, log_scale) the quantizer multiplies by: the per-layer scalars
-    the CUDA norm kernels produce (quant.py:146-170)."""
+    the CUDA norm kernels produce (quant.py:143-161)."""
     x = np.asarray(x, dtype=np.float64)
     y, s = x, None
     if spec.log_transform:
@@ -238,7 +238,7 @@ def dequantize(q, spec: "Spec", norm: float, log_scale: float | None = None) -> 
 
 
 def pack_words(stored, width: int) -> np.ndarray:
-    """``pack(values, width)`` payload (quant.py:330-356) viewed as
+    """``pack(values, width)`` payload (quant.py:255-281) viewed as
     little-endian uint32 words: element i sits at bits
     ``width*(i % (32//width))`` of word ``i // (32//width)``.  Widths 16/32
     extend the same layout (the B200 wire uses them for wide p-bit sums)."""
@@ -253,13 +253,13 @@ def pack_words(stored, width: int) -> np.ndarray:
 
 
 def pack_signs(s) -> np.ndarray:
-    """``pack(s, 1, 1)`` (quant.py:336-341): {-1,+1} -> {0,1}, 1 bit each."""
+    """``pack(s, 1, 1)`` (quant.py:261-266): {-1,+1} -> {0,1}, 1 bit each."""
     s = np.asarray(s, dtype=np.int64)
     return pack_words((s + 1) >> 1, 1)
 
 
 def unpack_words(words, width: int, count: int) -> np.ndarray:
-    """Inverse of ``pack_words`` (``unpack``, quant.py:359-375)."""
+    """Inverse of ``pack_words`` (``unpack``, quant.py:284-300)."""
     words = np.asarray(words, dtype=np.uint32).astype(np.uint64)
     per = 32 // width
     shifts = np.arange(per, dtype=np.uint64) * np.uint64(width)

@@ -2,7 +2,7 @@
 //
 // All kernels stream fp32 state with 128-bit loads: one warp covers a tile of
 // 128 consecutive elements (lane l owns elements 4l..4l+3), so the 1-bit words
-// of a tile (bit b of word w = element 32w+b, quant.py:330-356 layout) are
+// of a tile (bit b of word w = element 32w+b, quant.py:255-281 layout) are
 // assembled with three shuffle-ORs across the 8 lanes that share a word.
 // Math that decides a sign (c, the p-bit scale, the update) runs in float64
 // with every product/sum rounded separately (no FMA contraction) so results
@@ -91,7 +91,7 @@ struct SegCursor {
   }
 };
 
-// q = clip(round_half_even(scale*c), +-qmax)   (quant.py:236-243)
+// q = clip(round_half_even(scale*c), +-qmax)   (quant.py:161-168)
 __device__ __forceinline__ int quant_l1(double c, double scale, int qmax) {
   double r = rint(__dmul_rn(scale, c));
   r = fmin(fmax(r, -(double)qmax), (double)qmax);

@@ -1,6 +1,6 @@
 // numpy-exact per-layer L1 mean norm for the p-bit Lion Cub path.
 //
-// quant.py:156-179 computes M1 = max|c| * mean(|c|/max|c|).  np.mean sums
+// quant.py:81-104 computes M1 = max|c| * mean(|c|/max|c|).  np.mean sums
 // float64 with numpy's pairwise algorithm: blocks of <= 128 elements use 8
 // strided accumulators combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus a
 // sequential tail; larger blocks split at n/2 rounded down to a multiple of 8
@@ -143,7 +143,7 @@ using lc::Hyp;
 enum { PK_1 = 0, PK_2 = 1, PK_HALF = 2, PK_GEN = 3, PK_0 = 4, PK_INF = 5 };
 
 // |y| for y = c, or the log map y = sign(c) log1p(|c|/s) when s > 0
-// (quant.py:119-120, :146-150): |y| = log1p(|c|/s).
+// (quant.py:119-120, :143-146): |y| = log1p(|c|/s).
 template <bool LOG>
 __device__ __forceinline__ double abs_y(double c, double s) {
   double a = fabs(c);
@@ -331,7 +331,7 @@ k_l1_items(const float* __restrict__ g, const float* __restrict__ m,
   const DevTmpl T = tmpl[ti];
   // max|y| (or, for p = 0, the nonzero count: only its being 0 matters here)
   const double mx = PK == PK_0 ? (double)gmax[seg] : __longlong_as_double((long long)gmax[seg]);
-  if (mx == 0.0) {  // lp_mean_norm returns 0 before summing (quant.py:96-102)
+  if (mx == 0.0) {  // lp_mean_norm returns 0 before summing (quant.py:101-103)
     if (threadIdx.x == 0) nodes[node] = 0.0;
     return;
   }
@@ -573,7 +573,7 @@ __device__ __forceinline__ double seg_mx(const unsigned long long* gmax, int s, 
 }
 
 // One CTA per layer: the additions above the work items (level by level),
-// then M_p and the quantizer scale (quant.py:94-104, :153-170).
+// then M_p and the quantizer scale (quant.py:94-104, :148-161).
 __global__ void __launch_bounds__(kThreads)
 k_l1_upper(const DevSeg* __restrict__ segs, const int4* __restrict__ uops,
            const int* __restrict__ ulvl, const unsigned long long* __restrict__ gmax,

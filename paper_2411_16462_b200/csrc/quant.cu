@@ -26,7 +26,7 @@ __global__ void k_quantize_values(const float* __restrict__ x, int64_t n, lc::Se
     q[e] = lc::quant_x((double)x[e], sq, cur, e);
 }
 
-// y = q * mult; log map undone as sign(y) * s * expm1(|y|) (quant.py:186-195,
+// y = q * mult; log map undone as sign(y) * s * expm1(|y|) (quant.py:183-195,
 // :123-124), numpy's left-to-right order.
 __global__ void k_dequantize(const int64_t* __restrict__ q, int64_t n, double mult,
                              double s, int log, double* __restrict__ out) {

@@ -411,7 +411,7 @@ class _L1Plan:
 
 def _quant_scales(ws: _Workspace, layout: Layout, dev, g, m, mask, hyp, spec: QuantSpec,
                   stream, seed: int = 0):
-    """Per-layer quantizer scalars on the device (quant.py:127-170): the
+    """Per-layer quantizer scalars on the device (quant.py:143-161): the
     log-map scale M1(c) when ``log_transform``, then M_p of y and the scale
     qmax/(2 M_p) (qmax/M_inf for p = inf).  Returns the segment table K1
     quantizes with."""

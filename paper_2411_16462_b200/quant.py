@@ -1,7 +1,7 @@
 """Quantizer / sign-policy configuration of the drop-in API.
 
 ``QuantSpec`` and ``SignPolicy`` take the reference's constructor arguments
-and validation (lioncomm/quant.py:102-153).  On the CUDA path the quantizer
+and validation (lioncomm/quant.py:27-78).  On the CUDA path the quantizer
 itself runs inside the fused interpolate kernel (csrc/kernels.cu, K1) and the
 per-layer mean p-norm in csrc/l1norm.cu.  Every variant of the reference is
 implemented: norm_p 1 (the paper's Lion Cub p-bit scheme), any finite p,
@@ -175,7 +175,7 @@ def _plan(dev, n: int):
 
 def scale_tables(plan_handle: int, g, m, mask, hyp, spec: QuantSpec, norms, scales,
                  logs, stream) -> None:
-    """Per-segment quantizer scalars (quant.py:146-170) into device arrays:
+    """Per-segment quantizer scalars (quant.py:143-161) into device arrays:
     ``logs`` (2*nseg doubles; first half M1(c)) when log_transform, then the
     norm M_p of y in ``norms`` and the scale in ``scales``."""
     args = (plan_handle, g.data_ptr(), m.data_ptr(), _lib.ptr(mask), _C.byref(hyp))

@@ -56,7 +56,7 @@ def test_error_codes_map_to_reference_exceptions():
 
 
 def test_config_validation_mirrors_reference():
-    # optimizer.py:50-60, :86-93; quant.py:119-125, :145-149
+    # optimizer.py:50-60, :86-93; quant.py:44-50, :70-74
     with pytest.raises(lc.ConfigError):
         lc.LionHyper(beta1=1.0)
     with pytest.raises(lc.ConfigError):

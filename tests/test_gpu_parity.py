@@ -67,7 +67,7 @@ def _hyper(lr=1e-3, wd=0.0):
 @pytest.mark.parametrize("name", [c["name"] for c in G.step_cases()
                                   if c["algo"] == "compressed1bit"])
 def test_packed_sign_words_bit_exact(name):
-    """K1's 1-bit words == pack(apply_sign(c), 1, 1).payload (quant.py:330-356)."""
+    """K1's 1-bit words == pack(apply_sign(c), 1, 1).payload (quant.py:255-281)."""
     gc = G.step_case(name)
     case = gc["case"]
     fill = 0 if case["zero_mode"] == "exact-ternary" else O.zero_fill(case["iteration"] + 1)
