@@ -388,6 +388,15 @@ int lc_nccl_unique_id(uint8_t out[128]);
 int lc_comm_init_rank(lc_comm_t* comm, const uint8_t id[128], int32_t nranks,
                       int32_t rank);
 int lc_comm_init_all(lc_comm_t* comms, int32_t ndev, const int32_t* devices);
+/* `count` communicators initialised together (ncclGroupStart/End around the
+ * ncclCommInitRank calls): ids[128*i], nranks[i], ranks[i].  Used for the
+ * per-direction pair communicators of the frame transport. */
+int lc_comm_init_group(lc_comm_t* comms, const uint8_t* ids, const int32_t* nranks,
+                       const int32_t* ranks, int32_t count);
+/* Point-to-point bytes (ncclSend / ncclRecv) on `stream`: the frames of
+ * Transport.send/recv (transport.py:32-45) over NVLink. */
+int lc_send_bytes(lc_comm_t comm, const void* buf, int64_t bytes, int32_t peer, void* stream);
+int lc_recv_bytes(lc_comm_t comm, void* buf, int64_t bytes, int32_t peer, void* stream);
 int lc_comm_destroy(lc_comm_t comm);
 int lc_comm_abort(lc_comm_t comm);
 /* LC_OK, or LC_E_COLLECTIVE if the communicator hit an asynchronous error. */

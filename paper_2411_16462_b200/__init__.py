@@ -21,6 +21,7 @@ from .optimizer import (VOTE_ALGOS, FlatParamSet, Layout, LionHyper,  # noqa: F4
 from .quant import (INF, PackedBits, QuantSpec, SignPolicy, apply_sign,  # noqa: F401
                     dequantize, lp_mean_norm, pack, quantize, unpack)
 from .torch_optim import LionCub, lioncub_comm_hook  # noqa: F401
+from .frames import NcclFrameTransport  # noqa: F401
 from .transport import (DeviceTransport, LocalTransport,  # noqa: F401
                         NcclTransport)
 

@@ -67,6 +67,55 @@ int lc_comm_init_rank(lc_comm_t* out, const uint8_t id[128], int32_t nranks, int
   return LC_OK;
 }
 
+int lc_comm_init_group(lc_comm_t* out, const uint8_t* ids, const int32_t* nranks,
+                       const int32_t* ranks, int32_t count) {
+  if (!out || !ids || !nranks || !ranks || count < 1)
+    return lc::set_err(LC_E_ARG, "lc_comm_init_group: bad arguments");
+  int dev = 0;
+  LC_CUDA_TRY(cudaGetDevice(&dev));
+  std::vector<lc_comm_s*> cs(count, nullptr);
+  LC_NCCL_TRY(ncclGroupStart());
+  for (int i = 0; i < count; ++i) {
+    ncclUniqueId uid;
+    memcpy(&uid, ids + 128 * (size_t)i, sizeof(uid));
+    cs[i] = new lc_comm_s();
+    cs[i]->nranks = nranks[i];
+    cs[i]->rank = ranks[i];
+    cs[i]->device = dev;
+    ncclResult_t r = ncclCommInitRank(&cs[i]->comm, nranks[i], uid, ranks[i]);
+    if (r != ncclSuccess) {
+      ncclGroupEnd();
+      for (auto* c : cs) delete c;
+      return nccl_err(r, "ncclCommInitRank (group)");
+    }
+  }
+  ncclResult_t r = ncclGroupEnd();
+  if (r != ncclSuccess) {
+    for (auto* c : cs) delete c;
+    return nccl_err(r, "ncclGroupEnd (comm init)");
+  }
+  for (int i = 0; i < count; ++i) out[i] = cs[i];
+  return LC_OK;
+}
+
+int lc_send_bytes(lc_comm_t c, const void* buf, int64_t bytes, int32_t peer, void* stream) {
+  if (!c || bytes < 0 || peer < 0 || peer >= c->nranks)
+    return lc::set_err(LC_E_ARG, "lc_send_bytes: bad arguments");
+  if (bytes == 0) return LC_OK;
+  LC_NCCL_TRY(ncclSend(buf, (size_t)bytes, ncclUint8, peer, c->comm,
+                       reinterpret_cast<cudaStream_t>(stream)));
+  return LC_OK;
+}
+
+int lc_recv_bytes(lc_comm_t c, void* buf, int64_t bytes, int32_t peer, void* stream) {
+  if (!c || bytes < 0 || peer < 0 || peer >= c->nranks)
+    return lc::set_err(LC_E_ARG, "lc_recv_bytes: bad arguments");
+  if (bytes == 0) return LC_OK;
+  LC_NCCL_TRY(ncclRecv(buf, (size_t)bytes, ncclUint8, peer, c->comm,
+                       reinterpret_cast<cudaStream_t>(stream)));
+  return LC_OK;
+}
+
 int lc_comm_init_all(lc_comm_t* comms, int32_t ndev, const int32_t* devices) {
   if (!comms || ndev < 1 || !devices) return lc::set_err(LC_E_ARG, "lc_comm_init_all: bad arguments");
   std::vector<ncclComm_t> raw(ndev);

@@ -99,3 +99,87 @@ def test_thread_per_gpu_run_ranks(p2p):
                 assert_f32_equal(m[k], nm[r][k], f"m {k}")
     finally:
         tp.close()
+
+
+def _lioncomm():
+    """The unmodified reference, pip-installed in baseline/_ref (travels with
+    the repo snapshot; /root/reference does not exist on the GPU box)."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "lioncomm")):
+        pytest.skip("baseline/_ref has no lioncomm install")
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import lioncomm.collectives as RC
+    import lioncomm.quant as RQ
+    import lioncomm.transport as RT
+    return RC, RQ, RT
+
+
+def test_reference_collectives_over_nccl_frame_transport():
+    """The reference's own Python collectives (compressed_allreduce_1bit,
+    direct_allreduce, allreduce_mean_f32, ps_gather_broadcast) run unchanged
+    over NcclFrameTransport -- the Transport interface of transport.py:32-45
+    with frames crossing NVLink -- and give the results they give over the
+    reference's InprocTransport."""
+    n = _ngpu()
+    if n < 2:
+        pytest.skip("needs 2 GPUs")
+    import paper_2411_16462_b200 as lc
+    RC, RQ, RT = _lioncomm()
+    P = min(n, 4)
+    rng = np.random.default_rng(5)
+    cs = [rng.normal(size=10_007).astype(np.float32).astype(np.float64) for _ in range(P)]
+    qs = [rng.integers(-7, 8, size=10_007) for _ in range(P)]
+
+    def fn(topo):
+        r = topo.rank
+        a = RC.compressed_allreduce_1bit(cs[r], topo, RQ.SignPolicy("alternating", 3))
+        b = RC.direct_allreduce(qs[r], topo, q_max=7)
+        c = RC.allreduce_mean_f32(cs[r], topo)
+        d = RC.ps_gather_broadcast(cs[r], topo, efficient=True)
+        return a.values, a.ties, b.values, b.ties, c, d.values
+
+    eps = lc.NcclFrameTransport.init_all(list(range(P)))
+    got = RC.run_ranks(P, fn, transport_factory=lambda r: eps[r])
+    ref = RC.run_ranks(P, fn, transport=RT.InprocTransport(P))
+    for g, e in zip(got, ref):
+        for x, y in zip(g, e):
+            assert np.array_equal(np.asarray(x), np.asarray(y))
+
+
+@pytest.mark.parametrize("p2p", [True, False], ids=["nvlink-in-kernel-barriers", "nccl"])
+def test_dead_rank_raises_collective_error_naming_it(p2p):
+    """Thread-per-GPU, real NVLink: rank 1 stops after step 1.  Rank 0's
+    step 2 raises CollectiveError(rank=1) in the same call -- from the
+    kernels' barrier timeout (peer memory) or from the host deadline that
+    polls ncclCommGetAsyncError and aborts the communicator (NCCL) -- and
+    theta is unchanged."""
+    n = _ngpu()
+    if n < 2:
+        pytest.skip("needs 2 GPUs")
+    import paper_2411_16462_b200 as lc
+    import torch
+    tp = lc.NcclTransport.init_all([0, 1])
+    tp.p2p = p2p
+    tp.timeout = 3.0
+    out = {}
+
+    def fn(topo):
+        dev = topo.device
+        st = lc.WorkerState.initial({"w": torch.randn(300_000, device=dev,
+                                                      generator=torch.Generator(dev).manual_seed(0))})
+        g = st.new_grad_buffer()
+        g["w"].copy_(torch.randn(300_000, device=dev))
+        st = lc.distributed_lion_step(st, g, lc.LionHyper(lr=1e-3), None, topo, "compressed1bit")
+        torch.cuda.synchronize(dev)
+        if topo.rank == 1:
+            return
+        before = st.params["w"].clone()
+        with pytest.raises(lc.CollectiveError) as ei:
+            lc.distributed_lion_step(st, g, lc.LionHyper(lr=1e-3), None, topo, "compressed1bit")
+        torch.cuda.synchronize(dev)
+        out["who"] = ei.value.rank
+        out["same"] = bool(torch.equal(st.params["w"], before))
+
+    lc.run_ranks(2, fn, transport=tp)
+    assert out == {"who": 1, "same": True}
