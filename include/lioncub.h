@@ -395,6 +395,13 @@ int lc_comm_init_group(lc_comm_t* comms, const uint8_t* ids, const int32_t* nran
                        const int32_t* ranks, int32_t count);
 /* Point-to-point bytes (ncclSend / ncclRecv) on `stream`: the frames of
  * Transport.send/recv (transport.py:32-45) over NVLink. */
+/* Establish the NCCL p2p connections of 2-rank pair communicators in one
+ * group (a 1-byte send / receive on each, on its own device and stream):
+ * the first p2p call on a communicator connects it and blocks until the
+ * peer joins, so connecting lazily from threads that each send first would
+ * deadlock. */
+int lc_pair_connect(const lc_comm_t* comms, const int32_t* is_send, void* const* scratch,
+                    void* const* streams, int32_t count);
 int lc_send_bytes(lc_comm_t comm, const void* buf, int64_t bytes, int32_t peer, void* stream);
 int lc_recv_bytes(lc_comm_t comm, void* buf, int64_t bytes, int32_t peer, void* stream);
 int lc_comm_destroy(lc_comm_t comm);

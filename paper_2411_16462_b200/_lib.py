@@ -120,6 +120,7 @@ SIGNATURES = {
     "lc_comm_init_rank": (INT, [P, P, I32, I32]),
     "lc_comm_init_all": (INT, [P, I32, P]),
     "lc_comm_init_group": (INT, [P, P, P, P, I32]),
+    "lc_pair_connect": (INT, [P, P, P, P, I32]),
     "lc_send_bytes": (INT, [P, P, I64, I32, P]),
     "lc_recv_bytes": (INT, [P, P, I64, I32, P]),
     "lc_comm_destroy": (INT, [P]),

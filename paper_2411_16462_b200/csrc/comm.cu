@@ -116,6 +116,35 @@ int lc_recv_bytes(lc_comm_t c, void* buf, int64_t bytes, int32_t peer, void* str
   return LC_OK;
 }
 
+int lc_pair_connect(const lc_comm_t* comms, const int32_t* is_send, void* const* scratch,
+                    void* const* streams, int32_t count) {
+  if (!comms || !is_send || !scratch || !streams || count < 0)
+    return lc::set_err(LC_E_ARG, "lc_pair_connect: bad arguments");
+  int cur = 0;
+  LC_CUDA_TRY(cudaGetDevice(&cur));
+  LC_NCCL_TRY(ncclGroupStart());
+  for (int i = 0; i < count; ++i) {
+    const lc_comm_s* c = comms[i];
+    cudaSetDevice(c->device);
+    ncclResult_t r = is_send[i]
+        ? ncclSend(scratch[i], 1, ncclUint8, 1 - c->rank, c->comm, (cudaStream_t)streams[i])
+        : ncclRecv(scratch[i], 1, ncclUint8, 1 - c->rank, c->comm, (cudaStream_t)streams[i]);
+    if (r != ncclSuccess) {
+      ncclGroupEnd();
+      cudaSetDevice(cur);
+      return nccl_err(r, "lc_pair_connect");
+    }
+  }
+  ncclResult_t r = ncclGroupEnd();
+  for (int i = 0; i < count; ++i) {
+    cudaSetDevice(comms[i]->device);
+    cudaStreamSynchronize((cudaStream_t)streams[i]);
+  }
+  cudaSetDevice(cur);
+  if (r != ncclSuccess) return nccl_err(r, "lc_pair_connect: ncclGroupEnd");
+  return LC_OK;
+}
+
 int lc_comm_init_all(lc_comm_t* comms, int32_t ndev, const int32_t* devices) {
   if (!comms || ndev < 1 || !devices) return lc::set_err(LC_E_ARG, "lc_comm_init_all: bad arguments");
   std::vector<ncclComm_t> raw(ndev);

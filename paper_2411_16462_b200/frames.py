@@ -52,6 +52,20 @@ class _Chan:
         self.inflight = []             # (event, buffers) of sends not yet known done
 
 
+def _connect(outs: list, ins: list):
+    """Connect every pair communicator before any frame (lc_pair_connect)."""
+    chans = outs + ins
+    if not chans:
+        return
+    scratch = [torch.zeros(1, dtype=torch.uint8, device=ch.stream.device) for ch in chans]
+    n = len(chans)
+    _lib.check(_lib.load().lc_pair_connect(
+        (C.c_void_p * n)(*[ch.comm for ch in chans]),
+        (C.c_int32 * n)(*([1] * len(outs) + [0] * len(ins))),
+        (C.c_void_p * n)(*[t.data_ptr() for t in scratch]),
+        (C.c_void_p * n)(*[ch.stream.cuda_stream for ch in chans]), n), "pair connect")
+
+
 class NcclFrameTransport:
     """``Transport`` (transport.py:32-45) endpoint of ONE rank over NCCL."""
 
@@ -99,6 +113,7 @@ class NcclFrameTransport:
                     outc[d] = _Chan(handles[i], 1, dev)
                 else:
                     inc[s] = _Chan(handles[i], 0, dev)
+        _connect([*outc.values()], [*inc.values()])
         return cls(world_size, rank, dev, outc, inc, timeout)
 
     @classmethod
@@ -121,6 +136,7 @@ class NcclFrameTransport:
                            "pair communicator")
                 outs[s][d] = _Chan(hs[0], 1, torch.device("cuda", devices[s]))
                 ins[d][s] = _Chan(hs[1], 0, torch.device("cuda", devices[d]))
+        _connect([c for o in outs for c in o.values()], [c for i in ins for c in i.values()])
         return [cls(P, r, torch.device("cuda", devices[r]), outs[r], ins[r], timeout)
                 for r in range(P)]
 
