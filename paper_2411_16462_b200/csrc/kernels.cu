@@ -1789,27 +1789,27 @@ int fork_events(cudaEvent_t& fork, cudaEvent_t& join) {
 }  // namespace
 
 // CTAs per SM of the vote/update grid and of the side-stream mean while they
-// run together (LIONCUB_SYNC_SIDE_CTAS="va,mean").  Default 2,1: the mean
-// needs few SMs to saturate NVLink stores, the theta update wants HBM
-// bandwidth.  Measured, 7e9 params, 4 x B200, whole sync step: 3,1 69.7 ms;
-// 2,1 67.8; 2,2 69.5; 4,1 73.7; 1,2 78.4 (serial kernels: 75.0, the mean
-// inside the vote grid: 75.8).
+// run together (LIONCUB_SYNC_SIDE_CTAS="va,mean" overrides).  The mean needs
+// few SMs to saturate NVLink stores, the theta update wants HBM bandwidth;
+// at P = 2 half of each mean element stays local, so the mean needs more.
+// Measured, 7e9 params, whole sync step:
+//   4 x B200: 3,1 69.7 ms; 2,1 67.8; 2,2 69.5; 4,1 73.7; 1,2 78.4
+//             (serial kernels 75.0, the mean inside the vote grid 75.8)
+//   2 x B200: 2,1 60.5 ms; 1,2 50.9; 2,2 50.2; 2,4 50.2; 1,6 57.9
 struct SideCtas {
-  int va = 2, mean = 1;
+  int va, mean;
 };
-const SideCtas& side_ctas() {
-  static const SideCtas c = [] {
-    SideCtas v;
+SideCtas side_ctas(int P) {
+  static const SideCtas env = [] {
+    SideCtas v{0, 0};
     if (const char* e = std::getenv("LIONCUB_SYNC_SIDE_CTAS")) {
       int a = 0, b = 0;
-      if (std::sscanf(e, "%d,%d", &a, &b) == 2 && a > 0 && b > 0) {
-        v.va = a;
-        v.mean = b;
-      }
+      if (std::sscanf(e, "%d,%d", &a, &b) == 2 && a > 0 && b > 0) v = SideCtas{a, b};
     }
     return v;
   }();
-  return c;
+  if (env.va > 0) return env;
+  return P <= 2 ? SideCtas{2, 2} : SideCtas{2, 1};
 }
 
 int lc_vote_apply_sync(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid, int fill,
@@ -1847,7 +1847,7 @@ int lc_vote_apply_sync(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_va
   if (int rc = fork_events(fork, join)) return rc;
   LC_CUDA_TRY(cudaEventRecord(fork, st));
   LC_CUDA_TRY(cudaStreamWaitEvent(side, fork, 0));
-  g_va_cap = side_ctas().va;
+  g_va_cap = side_ctas(P).va;
   const int rc = lc_vote_apply(recv, P, cw, n_valid, fill, sum_mode, voted, nz, nout, flags, sync,
                                theta, n, full, nz_full, lr, wd, stream);
   g_va_cap = 0;
@@ -1856,7 +1856,7 @@ int lc_vote_apply_sync(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_va
     SyncD wait = to_syncd(sync);
     wait.arrive_epoch = 0;  // the mean publishes nothing (the caller's barrier follows)
     int grid = stream_grid(k_sync_mean, kBlock, (mean_cnt + kMeanChunk - 1) / kMeanChunk, 1);
-    if (grid > sm_count() * side_ctas().mean) grid = sm_count() * side_ctas().mean;
+    if (grid > sm_count() * side_ctas(P).mean) grid = sm_count() * side_ctas(P).mean;
     LC_CUDA_TRY(launch_pdl(k_sync_mean, grid, kBlock, 0, side, wait, ma, (int)P));
     LC_LAUNCH_CHECK();
   }
