@@ -25,7 +25,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define LIONCUB_ABI_VERSION 2
+#define LIONCUB_ABI_VERSION 3
 
 enum {
   LC_OK = 0,

@@ -722,6 +722,9 @@ struct ApplyArgs {
 #ifndef LC_VOTE_SHARE
 #define LC_VOTE_SHARE 8  // 1/LC_VOTE_SHARE of the grid votes + pushes the owner block
 #endif
+#ifndef LC_VA_KU
+#define LC_VA_KU 4       // theta sub-tiles in flight per warp in the update phase
+#endif
 
 // The momentum sync fused into the step (the owner half of
 // allreduce_mean_f32, collectives.py:319-344): this owner's P staged rows of
@@ -877,7 +880,7 @@ k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_val
   }
   sync_arrive(sy);  // last CTA: every peer learns this owner's block is out
   // ---- theta update, waiting per owner block ----
-  constexpr int KU = 4;
+  constexpr int KU = LC_VA_KU;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
