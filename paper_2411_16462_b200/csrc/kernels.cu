@@ -219,6 +219,10 @@ k_encode(const float* __restrict__ g, float* __restrict__ m,
   constexpr int WPS = (ENC == LC_ENC_F64) ? 1 : 32 * F;  // words per super-tile
   constexpr int KU = LC_ENC_KU;  // sub-tiles whose loads are in flight together
   __shared__ __align__(16) uint32_t stage[8][WPS];
+  // f64 c of one 128-element sub-tile per warp, re-laid out so every store
+  // instruction writes 512 contiguous bytes (whole sectors: a peer's slot
+  // over NVLink takes no partial-sector writes)
+  __shared__ __align__(16) double cstage[ENC == LC_ENC_F64 ? 8 : 1][ENC == LC_ENC_F64 ? 128 : 2];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -276,9 +280,15 @@ k_encode(const float* __restrict__ g, float* __restrict__ m,
             st_stream(mp + k * 32, make_float4(mn[0], mn[1], mn[2], mn[3]));
           }
           if constexpr (ENC == LC_ENC_F64) {
-            double* o = reinterpret_cast<double*>(dst.p[j]) + boff + k * 128 + lane * 4;
-            *reinterpret_cast<double2*>(o) = make_double2(c[0], c[1]);
-            *reinterpret_cast<double2*>(o + 2) = make_double2(c[2], c[3]);
+            double* cs = cstage[wib];
+            *reinterpret_cast<double2*>(cs + lane * 4) = make_double2(c[0], c[1]);
+            *reinterpret_cast<double2*>(cs + lane * 4 + 2) = make_double2(c[2], c[3]);
+            __syncwarp();
+            double2* o = reinterpret_cast<double2*>(reinterpret_cast<double*>(dst.p[j]) + boff +
+                                                    k * 128);
+            o[lane] = reinterpret_cast<const double2*>(cs)[lane];
+            o[32 + lane] = reinterpret_cast<const double2*>(cs)[32 + lane];
+            __syncwarp();
           } else {
             stage_subtile<F>(&stage[wib][k * 4 * F], lane, st);
           }
