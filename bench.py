@@ -721,6 +721,15 @@ def main():
                 "avg_launch_ms": kern[dominant]["avg_ms"],
                 "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs" if peak_src ==
                 "measured" else "fallback 6650 GB/s (B200_PROFILING.md)"}
+        if dominant == "lc_encode" and kind == "f64" and P > 1 and transport.p2p:
+            # full-precision arm over peer memory: K1 is bound by its (P-1)/P x
+            # 8 B/param of remote f64 stores
+            per_launch = (P - 1) / P * 8.0 * n
+            ach = per_launch / (kern[dominant]["avg_ms"] * 1e-3) / 1e9
+            roof.update({"bound": "nvlink", "achieved": ach, "peak": NVL_GBS, "frac": ach / NVL_GBS,
+                         "frac_of_nominal_900": ach / NVL_NOMINAL_GBS,
+                         "algorithmic_bytes_per_launch": per_launch,
+                         "peak_source": "B200_PROFILING.md NVLink per direction (measured)"})
         if dominant in ("lc_encode_sync", "lc_vote_apply_sync") and P > 1:
             # NVLink-bound halves of the fused momentum sync: (P-1)/P of the
             # m' rows leave in K1, (P-1)/P of the means leave in the vote kernel
