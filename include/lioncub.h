@@ -194,6 +194,11 @@ int lc_vote_apply(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid,
  *   side_stream: run the mean as its own kernel on that stream, concurrently
  *   with the vote/update grid (capped to leave it SMs), joined back into
  *   `stream`; NULL: every vote/update CTA joins the mean after its share. */
+/* Cap the grid of this host thread's next lc_vote_apply launches at
+ * ctas_per_sm CTAs per SM (0 = occupancy-sized), leaving SMs to a kernel
+ * the caller runs concurrently on another stream (the selective momentum
+ * sync's pull, fused into the step).  Thread-local. */
+int lc_set_vote_cap(int32_t ctas_per_sm);
 /* The owner mean of the fused sync on its own (as lc_vote_apply_sync's side
  * kernel; stand-alone for tuning and the NVLink microbenchmark): wait
  * (nullable) -> wait_epoch only; ctas_per_sm > 0 caps the grid. */

@@ -88,6 +88,7 @@ SIGNATURES = {
     "lc_vote_apply": (INT, [P, I32, I64, I64, INT, INT, P, P, I32, P, P, P, I64, P, P, D, D, P]),
     "lc_encode_sync": (INT, [P, P, P, I64, P, INT, P, I32, I64, P, P, P, P]),
     "lc_sync_mean": (INT, [P, P, P, I32, I64, I64, P, I32, P]),
+    "lc_set_vote_cap": (INT, [I32]),
     "lc_vote_apply_sync": (INT, [P, I32, I64, I64, INT, INT, P, P, I32, P, P, P, I64, P, P, D, D,
                                  P, P, I64, I64, P, P, P]),
     "lc_vote_update": (INT, [P, I64, I32, P, I64, INT, INT, D, D, P, P, P]),

@@ -1878,6 +1878,12 @@ int lc_vote_apply_sync(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_va
   return LC_OK;
 }
 
+int lc_set_vote_cap(int32_t ctas_per_sm) {
+  if (ctas_per_sm < 0) return set_err(LC_E_ARG, "lc_set_vote_cap: ctas_per_sm >= 0");
+  g_va_cap = ctas_per_sm;
+  return LC_OK;
+}
+
 int lc_sync_mean(const lc_sync* wait, const float* stage, void* const* out, int32_t P, int64_t L,
                  int64_t cnt, uint32_t* work, int32_t ctas_per_sm, void* stream) {
   MeanArgs ma{};

@@ -627,16 +627,23 @@ def distributed_lion_step_host(state: WorkerState, grad_host: torch.Tensor, h: L
                       rng=rng)
 
 
-def _fused_sync_ok(sync, layout, topo, t, kind, metrics, pipe, n) -> bool:
-    """The momentum sync can ride inside this step (see distributed_lion_step)."""
+def _fused_sync_mode(sync, layout, topo, t, kind, metrics, pipe, n):
+    """How the momentum sync rides inside this step (see
+    distributed_lion_step): "stage" -- every layer, m' routed to the owners
+    in K1 and averaged beside the theta update; "pull" -- selected layers,
+    each owner pulling its share from every rank beside the theta update;
+    None -- a separate maybe_sync_momentum after the step."""
     if sync is None or not sync.fires(t) or topo.world_size < 2 or kind != "1bit":
-        return False
+        return None
     tp = topo.transport
     if not (tp.p2p and tp.fused_barriers) or metrics or pipe is not None or SYNC_NCCL:
-        return False
-    if n > AG_MAX_N or topo.world_size > AG_MAX_P:   # the owner-vote exchange
-        return layout.runs(sync.selects) == [(0, n)]
-    return False
+        return None
+    if n <= AG_MAX_N and topo.world_size <= AG_MAX_P:   # allgather exchange
+        return None
+    runs = layout.runs(sync.selects)
+    if not runs:
+        return None
+    return "stage" if runs == [(0, n)] else "pull"
 
 
 def _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out, pipe=None,
@@ -752,14 +759,18 @@ def _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out,
                     _mark(timer, "vote", stream)
                 nz = _loc(ws.nz) if metrics else None
             else:
-                if _fused_sync_ok(sync, layout, topo, t, kind, metrics, pipe, n) and \
-                        not (ternary and binary):
+                mode = _fused_sync_mode(sync, layout, topo, t, kind, metrics, pipe, n)
+                sync_runs = None
+                if mode is not None and not (ternary and binary):
                     m = _symmetric_momentum(m, topo)
                     msync = m
+                    if mode == "pull":
+                        sync_runs = layout.runs(sync.selects)
                 nz = _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill,
                                         n, g, m, mflat, hyp, segs, s,
                                         tree=algo == "ps_efficient", pipe=pipe,
-                                        theta=th.flat, msync=msync, timer=timer)
+                                        theta=th.flat, msync=msync, timer=timer,
+                                        sync_runs=sync_runs)
                 if strict and not ws.p2p and hasattr(tp, "wait_collectives"):
                     # NCCL exchange: no theta update unless every collective landed
                     tp.wait_collectives(topo.rank, gen, "vote exchange")
@@ -878,6 +889,8 @@ class _Allgather:
 # side stream (vote/update grid capped); "inline": inside the vote/update grid
 # (every CTA joins after its theta share)
 SYNC_MEAN = os.environ.get("LIONCUB_SYNC_MEAN", "side")   # side | serial | inline
+# vote/update CTAs per SM while the selective sync's pull runs beside it
+SYNC_PULL_VOTE_CAP = int(os.environ.get("LIONCUB_SYNC_PULL_VOTE_CAP", "2"))
 
 
 def _sync_side_stream(ws, topo):
@@ -896,7 +909,8 @@ def _mark(timer, name, stream):
 
 
 def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, g, m, mflat,
-                       hyp, segs, s, tree=False, pipe=None, theta=None, msync=None, timer=None):
+                       hyp, segs, s, tree=False, pipe=None, theta=None, msync=None, timer=None,
+                       sync_runs=None):
     """K1 encode -> exchange -> owner vote into the gather buffer (+nz, ties).
     With ``theta`` on the fused peer-memory path the theta update runs in
     the vote's grid (``ws.applied`` is set)."""
@@ -963,7 +977,7 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
             _lib.call("lc_encode", _off(g.flat, a), _off(m.flat, a), None, b - a,
                       C.byref(hyp), fill, enc, fb, None, ws.dst, P, L, a,
                       ws.flags.data_ptr(), sy1 if c == last else None, s)
-    elif msync is not None:
+    elif msync is not None and sync_runs is None:
         # K1 with m' routed to the owners' staging rows (the sync's all-to-all)
         stage = tp.sym_buffer(r, ws.key + ("mstage",), P * L, torch.float32)
         _lib.call("lc_encode_sync", gp, mp, mk, n, C.byref(hyp), fill, ws.dst, P, L,
@@ -999,6 +1013,42 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
                       ws.nzout, ws.nout, ws.flags.data_ptr(), sy2, theta.data_ptr(), n,
                       _loc(ws.full).data_ptr(), _lib.ptr(_loc(ws.nz)), hyp.lr,
                       hyp.weight_decay, s)
+        elif sync_runs is not None:
+            # selected layers: on a side stream, once every K1 has published
+            # e1 (all m' final), each owner pulls its share of every selected
+            # range from every rank, averages in float64 rank order and
+            # stores the mean into every rank's m -- concurrently with the
+            # vote/update grid, capped to leave it SMs; the caller's barrier
+            # ends the step
+            side = torch.cuda.Stream(topo.device) if getattr(ws, "side_t", None) is None \
+                else ws.side_t
+            ws.side_t = side
+            main = torch.cuda.ExternalStream(s)
+            side.wait_stream(main)
+            if getattr(ws, "wait_e1", None) is None:
+                ws.wait_e1 = tp.sync_struct(r, ws.counters[3:4], 0, 0)
+            ws.wait_e1.wait_epoch, ws.wait_e1.arrive_epoch = e1, 0
+            ss = side.cuda_stream
+            _lib.call("lc_encode", gp, mp, None, 0, C.byref(hyp), fill, _lib.LC_ENC_SIGN1, 1,
+                      None, ws.dst, P, L, 0, ws.flags.data_ptr(), C.byref(ws.wait_e1), ss)
+            src = _lib.table(msync.sym.peers)
+            for a, b in sync_runs:
+                ln = b - a
+                sr = -(-ln // P)
+                if a % 4 == 0:
+                    sr = -(-sr // 4) * 4   # 16-byte aligned owner shares
+                cnt = max(0, min(sr, ln - r * sr))
+                _lib.call("lc_mean_pull_f32", src, P, a + r * sr, cnt, src, P,
+                          tp.error_word(r), ss)
+            _lib.check(_lib.load().lc_set_vote_cap(SYNC_PULL_VOTE_CAP), "lc_set_vote_cap")
+            try:
+                _lib.call("lc_vote_apply", recv.data_ptr(), P, cw, nvalid, fill, sum_mode,
+                          ws.vout, ws.nzout, ws.nout, ws.flags.data_ptr(), sy2, theta.data_ptr(),
+                          n, _loc(ws.full).data_ptr(), _lib.ptr(_loc(ws.nz)), hyp.lr,
+                          hyp.weight_decay, s)
+            finally:
+                _lib.load().lc_set_vote_cap(0)
+            main.wait_stream(side)
         elif SYNC_MEAN == "serial":
             # vote/update, then the owner mean as its own full-occupancy kernel
             # (stream order: the vote kernel already waited for every K1)

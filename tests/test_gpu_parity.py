@@ -780,3 +780,36 @@ def test_lioncub_overlap_backward_equals_plain(world, algo, bits, xchg, monkeypa
     for (tp_, mp_), (to_, mo_) in zip(plain, over):
         assert np.array_equal(tp_.view(np.int32), to_.view(np.int32))
         assert np.array_equal(mp_.view(np.int32), mo_.view(np.int32))
+
+
+@pytest.mark.parametrize("world,algo,bits", [(4, "compressed1bit", None), (3, "direct", 1),
+                                             (8, "compressed1bit", None)])
+def test_selective_sync_fused_into_step_matches_oracle(world, algo, bits):
+    """sync=SyncPolicy(period, {layers}) passed to the step on the production
+    exchange: each owner's pull of the selected layers runs beside the theta
+    update inside the step (mode "pull"); three steps (the sync firing on the
+    second) equal the oracle's step + maybe_sync_momentum."""
+    sizes = {"emb": (40_000,), "h0.w": (300_017,), "h1.w": (262_144,), "norm": (1_000,)}
+    sel = ["emb", "h1.w"]
+    ranks = O.synth_rank_inputs(13, world, sizes, "laplace")
+    h = O.Hyper(0.9, 0.99, 1e-4, 0.1)
+    spec = None if bits is None else O.Spec(bits)
+    f32 = lambda d: {k: np.asarray(v, np.float32).astype(np.float64) for k, v in d.items()}  # noqa
+    thetas = [f32(ranks[0]["theta"])] * world
+    moms = [f32(rk["m"]) for rk in ranks]
+    it0 = 0
+    for i in range(3):
+        nt, nm, *_ = O.distributed_step(thetas, moms, [rk["g"] for rk in ranks], h, spec, algo,
+                                        it0 + i)
+        nm = O.sync_momentum([f32(x) for x in nm], 2, frozenset(sel), it0 + i + 1)
+        thetas, moms = [f32(x) for x in nt], [f32(x) for x in nm]
+    case = dict(world=world, lr=1e-4, wd=0.1, bits=bits, algo=algo, iteration=it0,
+                zero_mode="alternating", sync=(2, sel))
+    res = run_step_case(case, ranks[0]["theta"], [rk["m"] for rk in ranks],
+                        [rk["g"] for rk in ranks], metrics=False,
+                        transport=make_transport(world, "fused"), steps=3)
+    for r, (th, m, _, it) in enumerate(res):
+        assert it == it0 + 3
+        for k in sizes:
+            assert_f32_equal(th[k], thetas[r][k], f"theta {k} r{r}")
+            assert_f32_equal(m[k], moms[r][k], f"m {k} r{r}")
