@@ -633,7 +633,8 @@ def _fused_sync_mode(sync, layout, topo, t, kind, metrics, pipe, n):
     in K1 and averaged beside the theta update; "pull" -- selected layers,
     each owner pulling its share from every rank beside the theta update;
     None -- a separate maybe_sync_momentum after the step."""
-    if sync is None or not sync.fires(t) or topo.world_size < 2 or kind != "1bit":
+    if sync is None or not sync.fires(t) or topo.world_size < 2 or kind != "1bit" or \
+            SYNC_FUSE == "0":
         return None
     tp = topo.transport
     if not (tp.p2p and tp.fused_barriers) or metrics or pipe is not None or SYNC_NCCL:
@@ -643,7 +644,9 @@ def _fused_sync_mode(sync, layout, topo, t, kind, metrics, pipe, n):
     runs = layout.runs(sync.selects)
     if not runs:
         return None
-    return "stage" if runs == [(0, n)] else "pull"
+    if runs == [(0, n)]:
+        return "stage"
+    return "pull" if SYNC_FUSE == "1" else None
 
 
 def _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out, pipe=None,
@@ -889,6 +892,9 @@ class _Allgather:
 # side stream (vote/update grid capped); "inline": inside the vote/update grid
 # (every CTA joins after its theta share)
 SYNC_MEAN = os.environ.get("LIONCUB_SYNC_MEAN", "side")   # side | serial | inline
+# LIONCUB_SYNC_FUSE: 1 (default) fuse every sync the step can carry; "all":
+# only the all-layer sync; 0: never (maybe_sync_momentum after the step)
+SYNC_FUSE = os.environ.get("LIONCUB_SYNC_FUSE", "1")
 # vote/update CTAs per SM while the selective sync's pull runs beside it
 SYNC_PULL_VOTE_CAP = int(os.environ.get("LIONCUB_SYNC_PULL_VOTE_CAP", "2"))
 
