@@ -896,7 +896,7 @@ SYNC_MEAN = os.environ.get("LIONCUB_SYNC_MEAN", "side")   # side | serial | inli
 # only the all-layer sync; 0: never (maybe_sync_momentum after the step)
 SYNC_FUSE = os.environ.get("LIONCUB_SYNC_FUSE", "1")
 # vote/update CTAs per SM while the selective sync's pull runs beside it
-SYNC_PULL_VOTE_CAP = int(os.environ.get("LIONCUB_SYNC_PULL_VOTE_CAP", "2"))
+SYNC_PULL_VOTE_CAP = int(os.environ.get("LIONCUB_SYNC_PULL_VOTE_CAP", "0"))
 
 
 def _sync_side_stream(ws, topo):
