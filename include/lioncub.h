@@ -25,7 +25,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define LIONCUB_ABI_VERSION 3
+#define LIONCUB_ABI_VERSION 4
 
 enum {
   LC_OK = 0,
@@ -72,10 +72,14 @@ typedef struct lc_hyper {
  * publishes it into every peer's flag slot `rank` after its last CTA
  * finished (per-CTA fence + atomic counter, st.release.sys).  This replaces
  * a separate barrier launch between K1 -> vote -> K5.  NULL = no sync. */
+#define LC_SYNC_COUNTER_WORDS 4
 typedef struct lc_sync {
   void* peer_flags[32]; /* rank j's uint64[P] flag array, mapped here     */
   uint64_t* my_flags;   /* this rank's flag array                          */
-  uint32_t* counter;    /* zeroed device word, one per arrive site         */
+  uint32_t* counter;    /* LC_SYNC_COUNTER_WORDS zeroed device words per
+                           arrive site: [0] arrivals, [1..2] the work
+                           counter of lc_vote_apply's update phase; every
+                           kernel leaves them zero when it finishes        */
   uint32_t* err;        /* 2 device words: [0] LC_FLAG_* bits, [1] bitmask
                            of the ranks a wait timed out on.  A kernel whose
                            wait times out writes nothing (theta, m and the

@@ -7,6 +7,7 @@
 // Math that decides a sign (c, the p-bit scale, the update) runs in float64
 // with every product/sum rounded separately (no FMA contraction) so results
 // equal the float64 numpy reference bit-for-bit; fp32 state is rounded once.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -727,6 +728,7 @@ struct ApplyArgs {
   const uint32_t* nzb;  // nullable
   double lr, wd;
   int64_t blk_words;    // words per owner block (cw)
+  int64_t chunk;        // super-tiles per work item of the update phase
 };
 
 #ifndef LC_VOTE_SHARE
@@ -832,14 +834,40 @@ k_sync_mean(SyncD sy, MeanArgs ma, int P) {
   mean_role<2>(ma, P);
 }
 
+#ifndef LC_VA_CHUNK
+#define LC_VA_CHUNK 8    // max super-tiles per work item of the update phase
+#endif
+#ifndef LC_VA_ITEMS
+#define LC_VA_ITEMS 131072  // work items per launch the chunk size aims for
+#endif
+
+// The update phase's work counter (sy.counter[1]) is reset by the last CTA
+// to finish its update (sy.counter[2] counts them), so the next launch on
+// the same sync site -- ordered after this grid -- starts from zero.
+__device__ __forceinline__ void va_retire(const SyncD& sy) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (atomicAdd(sy.counter + 2, 1u) == gridDim.x - 1) {
+      sy.counter[1] = 0u;
+      sy.counter[2] = 0u;
+      __threadfence();
+    }
+  }
+}
+
+#ifndef LC_VA_MINB
+#define LC_VA_MINB 4     // __launch_bounds__ min CTAs per SM of k_vote_apply (64 regs)
+#endif
+
 template <int NP, bool NZ, bool MEAN>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, LC_VA_MINB)
 k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_valid, int fill,
              int sum_mode, VoteOut out, uint32_t* __restrict__ flags, SyncD sy, ApplyArgs a,
              MeanArgs ma) {
   griddep_wait();
   if (!sync_wait(sy)) {  // a peer's words never arrived: no vote, no theta update
     sync_arrive(sy);
+    va_retire(sy);
     return;
   }
   const int T = P >> 1;
@@ -889,11 +917,13 @@ k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_val
     if (flag) atomicOr(flags, flag);
   }
   sync_arrive(sy);  // last CTA: every peer learns this owner's block is out
-  // ---- theta update, waiting per owner block ----
+  // ---- theta update, waiting per owner block.  Warps take work items of
+  // LC_VA_CHUNK super-tiles from a counter (sy.counter[1]) in rotated order
+  // -- this rank's own block first -- so the voter CTAs, which start late,
+  // simply take fewer items (a static split leaves their share as a tail) ----
   constexpr int KU = LC_VA_KU;
+  const int64_t CH = a.chunk;
   const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t nsup = (a.n + 1023) >> 10;
   const int64_t nwords = (a.n + 31) >> 5;
   float4* th4 = reinterpret_cast<float4*>(a.theta);
@@ -941,8 +971,8 @@ k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_val
       if (NZ) zw_ = __ldcv(a.nzb + w);
     }
   };
-  // start at this rank's own block (voted locally, no wait) and wrap: by
-  // the time the warps reach a remote block its owner's votes have landed
+  // rotated order: this rank's own block (voted locally, no wait) first, by
+  // the time the items reach a remote block its owner's votes have landed
   int64_t rot = (int64_t)sy.rank * a.blk_words / 32;  // blk_words % 32 == 0
   if (rot >= nsup) rot = 0;
   auto at = [&](int64_t i) {
@@ -950,13 +980,7 @@ k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_val
     const int64_t s = i + rot;
     return s >= nsup ? s - nsup : s;
   };
-  uint32_t nxw, nxz;
-  fetch(at(gw), nxw, nxz);
-  for (int64_t i = gw; i < nsup; i += nw) {
-    const int64_t sidx = at(i);
-    const uint32_t myw = nxw, myz = nxz;
-    fetch(at(i + nw), nxw, nxz);
-    if ((bad >> (int)((sidx * 32) / a.blk_words)) & 1u) continue;  // stale words: skip
+  auto update = [&](int64_t sidx, uint32_t myw, uint32_t myz) {
 #pragma unroll 1
     for (int k0 = 0; k0 < 8; k0 += KU) {
       float4 tv[KU];
@@ -993,7 +1017,36 @@ k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_val
         }
       }
     }
+  };
+  // positions (item, c) in the order the counter hands items out; the voted
+  // words of the next position are fetched one super-tile ahead and the next
+  // item's index is requested one item ahead, so neither latency is exposed
+  unsigned int* work = sy.counter + 1;
+  const int64_t nitems = (nsup + CH - 1) / CH;
+  unsigned int cur = 0u, ahead = 0u;
+  if (lane == 0) cur = atomicAdd(work, 1u);
+  cur = __shfl_sync(kFull, cur, 0);
+  if (lane == 0) ahead = atomicAdd(work, 1u);
+  int64_t c = 0;
+  uint32_t nxw, nxz;
+  fetch((int64_t)cur < nitems ? at((int64_t)cur * CH) : nsup, nxw, nxz);
+  while ((int64_t)cur < nitems) {
+    const int64_t sidx = at((int64_t)cur * CH + c);
+    const uint32_t myw = nxw, myz = nxz;
+    unsigned int ncur = cur;
+    int64_t nc = c + 1;
+    if (nc == CH) {
+      ncur = __shfl_sync(kFull, ahead, 0);
+      nc = 0;
+      if (lane == 0) ahead = atomicAdd(work, 1u);
+    }
+    fetch((int64_t)ncur < nitems ? at((int64_t)ncur * CH + nc) : nsup, nxw, nxz);
+    if (sidx < nsup && !((bad >> (int)((sidx * 32) / a.blk_words)) & 1u))  // bad: stale words
+      update(sidx, myw, myz);
+    cur = ncur;
+    c = nc;
   }
+  va_retire(sy);
   // every CTA whose theta share is done joins the fused momentum mean
   // (needs only e1: the staged rows are complete even if an owner's vote timed out)
   if constexpr (MEAN) {
@@ -1923,7 +1976,12 @@ int lc_vote_apply(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid, 
   if ((int64_t)P * cw * 32 < n) return set_err(LC_E_ARG, "lc_vote_apply: blocks do not cover n");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const SyncD sy = to_syncd(sync);
-  ApplyArgs a{theta, n, full, nz_full, lr, wd, cw};
+  // work items of up to LC_VA_CHUNK super-tiles: large vectors keep the
+  // counter's atomics few (one address: ~2.5 ns each), small ones keep the
+  // items short (the last item is the tail)
+  const int64_t nsup = (n + 1023) >> 10;
+  const int64_t chunk = std::min<int64_t>(LC_VA_CHUNK, std::max<int64_t>(1, (nsup + LC_VA_ITEMS - 1) / LC_VA_ITEMS));
+  ApplyArgs a{theta, n, full, nz_full, lr, wd, cw, chunk};
 #define LC_VA(NP, NZ)                                                                      \
   do {                                                                                     \
     auto kern = g_mean.stage ? k_vote_apply<NP, NZ, true> : k_vote_apply<NP, NZ, false>;   \

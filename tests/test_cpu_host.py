@@ -31,7 +31,7 @@ def test_library_exports_every_header_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert declared == set(_lib.SIGNATURES), declared ^ set(_lib.SIGNATURES)
-    assert lib.lc_abi_version() == 3
+    assert lib.lc_abi_version() == 4
     assert lib.lc_nccl_version() >= 22800
 
 
