@@ -77,9 +77,10 @@ typedef struct lc_sync {
   void* peer_flags[32]; /* rank j's uint64[P] flag array, mapped here     */
   uint64_t* my_flags;   /* this rank's flag array                          */
   uint32_t* counter;    /* LC_SYNC_COUNTER_WORDS zeroed device words per
-                           arrive site: [0] arrivals, [1..2] the work
-                           counter of lc_vote_apply's update phase; every
-                           kernel leaves them zero when it finishes        */
+                           arrive site: [0] arrivals (lc_vote_apply: vote
+                           units done), [1..3] lc_vote_apply's work
+                           counters (update items, retired CTAs, vote
+                           units claimed); every kernel leaves them zero  */
   uint32_t* err;        /* 2 device words: [0] LC_FLAG_* bits, [1] bitmask
                            of the ranks a wait timed out on.  A kernel whose
                            wait times out writes nothing (theta, m and the
@@ -89,7 +90,20 @@ typedef struct lc_sync {
   uint64_t arrive_epoch;
   int32_t P, rank;
   double timeout_s;
+  uint64_t* verdict;    /* nullable: a pinned host word.  lc_vote_apply and
+                           lc_vote_update store (epoch << 8) | status into it
+                           as soon as every wait of the step has resolved --
+                           epoch = arrive_epoch (wait_epoch if that is 0),
+                           status = the LC_FLAG_* bits of *flags (the NaN
+                           flag of K1 ...) | LC_FLAG_BARRIER_TIMEOUT -- so
+                           the host can check the step (lc_wait_verdict)
+                           while the theta update is still running         */
 } lc_sync;
+
+/* Spin (GIL-free, from ctypes) until *word carries an epoch >= epoch; its
+ * status byte goes to *status.  LC_E_COLLECTIVE if timeout_s passes first
+ * (the kernels' own bounded waits normally answer long before). */
+int lc_wait_verdict(const uint64_t* word, uint64_t epoch, double timeout_s, uint32_t* status);
 
 /* Quantizer variant flags (QuantSpec, quant.py:28-55). */
 enum {

@@ -68,7 +68,8 @@ class Sync(C.Structure):
     _fields_ = [("peer_flags", C.c_void_p * 32), ("my_flags", C.c_void_p),
                 ("counter", C.c_void_p), ("err", C.c_void_p),
                 ("wait_epoch", C.c_uint64), ("arrive_epoch", C.c_uint64),
-                ("P", C.c_int32), ("rank", C.c_int32), ("timeout_s", C.c_double)]
+                ("P", C.c_int32), ("rank", C.c_int32), ("timeout_s", C.c_double),
+                ("verdict", C.c_void_p)]
 
 
 P = C.c_void_p
@@ -80,6 +81,7 @@ INT = C.c_int
 # name -> (restype, argtypes).  Every exported symbol of include/lioncub.h.
 SIGNATURES = {
     "lc_abi_version": (INT, []),
+    "lc_wait_verdict": (INT, [P, C.c_uint64, D, P]),
     "lc_last_error": (C.c_char_p, []),
     "lc_device_sm_count": (INT, [INT]),
     "lc_set_grid_divisor": (INT, [INT]),

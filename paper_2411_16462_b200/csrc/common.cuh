@@ -1,6 +1,7 @@
 // Shared helpers for the Lion Cub sm_100a kernels.
 #pragma once
 
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -137,11 +138,16 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
+  // LIONCUB_PDL=0: plain stream order (A/B and diagnosis)
+  static const bool pdl = [] {
+    const char* e = getenv("LIONCUB_PDL");
+    return !(e && e[0] == '0');
+  }();
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
@@ -153,6 +159,7 @@ struct SyncD {
   uint32_t* err;
   unsigned long long wait_epoch, arrive_epoch, timeout_ns;
   int P, rank;
+  uint64_t* verdict;  // nullable pinned host word (lc_sync.verdict)
 };
 
 inline SyncD to_syncd(const lc_sync* s) {
@@ -167,6 +174,7 @@ inline SyncD to_syncd(const lc_sync* s) {
   d.timeout_ns = (unsigned long long)(s->timeout_s * 1e9);
   d.P = s->P;
   d.rank = s->rank;
+  d.verdict = s->verdict;
   return d;
 }
 
@@ -208,6 +216,18 @@ __device__ __forceinline__ bool sync_wait(const SyncD& s) {
   int ok = 1;
   if (j < s.P) ok = wait_slot(s, j, s.wait_epoch);
   return __syncthreads_and(ok) != 0;
+}
+
+// The step's verdict for the host (lc_sync.verdict): every wait resolved,
+// K1's flags final.  One thread.
+__device__ __forceinline__ void publish_verdict(const SyncD& s, const uint32_t* flags,
+                                                unsigned long long epoch, bool ok) {
+  if (!s.verdict) return;
+  const uint32_t f = *reinterpret_cast<const volatile uint32_t*>(flags);
+  const unsigned long long v =
+      (epoch << 8) | (f & 0xFu) | (ok ? 0u : (unsigned)LC_FLAG_BARRIER_TIMEOUT);
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(s.verdict), "l"(v) : "memory");
 }
 
 // End of a kernel: the last CTA to finish publishes s.arrive_epoch to every

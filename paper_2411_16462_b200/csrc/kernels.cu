@@ -8,6 +8,8 @@
 // with every product/sum rounded separately (no FMA contraction) so results
 // equal the float64 numpy reference bit-for-bit; fp32 state is rounded once.
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -841,6 +843,14 @@ k_sync_mean(SyncD sy, MeanArgs ma, int P) {
 #define LC_VA_ITEMS 131072  // work items per launch the chunk size aims for
 #endif
 
+#ifndef LC_VA_VILP
+#define LC_VA_VILP 1     // quads per lane in flight in a vote unit (1 or 2)
+#endif
+#ifndef LC_VA_UNIT
+#define LC_VA_UNIT 256
+#endif
+constexpr int kVoteUnitQuads = LC_VA_UNIT;  // uint4 word quads per vote unit (32K elements)
+
 // The update phase's work counter (sy.counter[1]) is reset by the last CTA
 // to finish its update (sy.counter[2] counts them), so the next launch on
 // the same sync site -- ordered after this grid -- starts from zero.
@@ -850,9 +860,110 @@ __device__ __forceinline__ void va_retire(const SyncD& sy) {
     if (atomicAdd(sy.counter + 2, 1u) == gridDim.x - 1) {
       sy.counter[1] = 0u;
       sy.counter[2] = 0u;
+      sy.counter[3] = 0u;
       __threadfence();
     }
   }
+}
+
+// Vote units of k_vote_apply.  Claims warp-sized units (the next claim in
+// flight while a unit is voted) until none is left, then counts its units
+// done with one system fence; the warp whose count completes the block
+// publishes e2.  Returns false (units exhausted).
+template <int NP>
+__device__ __forceinline__ void va_vote_quad(const uint32_t* __restrict__ recv, int P, int T,
+                                             int64_t cw, int64_t n_valid, int fill,
+                                             uint32_t fillmask, int sum_mode, const VoteOut& out,
+                                             int64_t q0, int64_t q1, uint32_t& flag) {
+  // two quads per lane with their P row loads in flight together
+  const bool on1 = q1 < (cw >> 2);
+  uint32_t pl[2][4][NP];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int w = 0; w < 4; ++w)
+#pragma unroll
+      for (int pp = 0; pp < NP; ++pp) pl[h][w][pp] = 0u;
+#pragma unroll 2
+  for (int j = 0; j < P; ++j) {
+    const uint4* row = reinterpret_cast<const uint4*>(recv + (int64_t)j * cw);
+    const uint4 x0 = __ldcs(row + q0);
+    const uint4 x1 = on1 ? __ldcs(row + q1) : make_uint4(0u, 0u, 0u, 0u);
+    const uint32_t xs[2][4] = {{x0.x, x0.y, x0.z, x0.w}, {x1.x, x1.y, x1.z, x1.w}};
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        uint32_t carry = xs[h][w];
+#pragma unroll
+        for (int pp = 0; pp < NP; ++pp) {
+          const uint32_t t = pl[h][w][pp] & carry;
+          pl[h][w][pp] ^= carry;
+          carry = t;
+        }
+      }
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if (h == 1 && !on1) break;
+    const int64_t q = h ? q1 : q0;
+    uint32_t v[4], nz[4], tie[4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const int64_t rem = n_valid - (4 * q + w) * 32;
+      const uint32_t vm = rem >= 32 ? ~0u : (rem <= 0 ? 0u : ((1u << rem) - 1u));
+      vote_word<NP>(pl[h][w], P, T, fillmask, vm, fill, sum_mode, v[w], nz[w], tie[w], flag);
+    }
+    vote_store(out, 4 * q, make_uint4(v[0], v[1], v[2], v[3]),
+               make_uint4(nz[0], nz[1], nz[2], nz[3]), make_uint4(tie[0], tie[1], tie[2], tie[3]));
+  }
+}
+
+template <int NP>
+__device__ __forceinline__ bool va_vote_units(const uint32_t* __restrict__ recv, int P, int T,
+                                              int64_t cw, int64_t n_valid, int fill,
+                                              uint32_t fillmask, int sum_mode, const VoteOut& out,
+                                              uint32_t* flags, const SyncD& sy, int64_t nunits,
+                                              int lane) {
+  const int64_t nq = cw >> 2;
+  unsigned int* vclaim = sy.counter + 3;
+  unsigned int* vdone = sy.counter;
+  unsigned int u = 0u, ahead = 0u, mine = 0u;
+  if (lane == 0) u = atomicAdd(vclaim, 1u);
+  u = __shfl_sync(kFull, u, 0);
+  if ((int64_t)u < nunits && lane == 0) ahead = atomicAdd(vclaim, 1u);
+  uint32_t flag = 0;
+  while ((int64_t)u < nunits) {
+    const int64_t qe = min(nq, ((int64_t)u + 1) * kVoteUnitQuads);
+#if LC_VA_VILP == 2
+    for (int64_t q = (int64_t)u * kVoteUnitQuads + lane; q < qe; q += 64)
+      va_vote_quad<NP>(recv, P, T, cw, n_valid, fill, fillmask, sum_mode, out, q,
+                       q + 32 < qe ? q + 32 : nq, flag);
+#else
+    for (int64_t q = (int64_t)u * kVoteUnitQuads + lane; q < qe; q += 32)
+      va_vote_quad<NP>(recv, P, T, cw, n_valid, fill, fillmask, sum_mode, out, q, nq, flag);
+#endif
+    ++mine;
+    u = __shfl_sync(kFull, ahead, 0);
+    if ((int64_t)u < nunits && lane == 0) ahead = atomicAdd(vclaim, 1u);
+  }
+  if (flag) atomicOr(flags, flag);
+  __syncwarp();
+  if (mine && lane == 0) {
+    __threadfence_system();  // this warp's stores (local and peers) first
+    if (atomicAdd(vdone, mine) + mine == (unsigned int)nunits) {
+      *vdone = 0u;  // ready for the next launch of this site
+      __threadfence_system();
+      const uint32_t e = *reinterpret_cast<volatile uint32_t*>(sy.err);
+      if (!(e & LC_FLAG_BARRIER_TIMEOUT)) {
+        for (int j = 0; j < sy.P; ++j)
+          asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(sy.peer[j] + sy.rank),
+                       "l"(sy.arrive_epoch) : "memory");
+      }
+    }
+  }
+  __syncwarp();
+  return false;
 }
 
 #ifndef LC_VA_MINB
@@ -862,68 +973,52 @@ __device__ __forceinline__ void va_retire(const SyncD& sy) {
 template <int NP, bool NZ, bool MEAN>
 __global__ void __launch_bounds__(256, LC_VA_MINB)
 k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_valid, int fill,
-             int sum_mode, VoteOut out, uint32_t* __restrict__ flags, SyncD sy, ApplyArgs a,
+             int sum_mode, const __grid_constant__ VoteOut out, uint32_t* __restrict__ flags,
+             const __grid_constant__ SyncD sy, ApplyArgs a,
              MeanArgs ma) {
   griddep_wait();
   if (!sync_wait(sy)) {  // a peer's words never arrived: no vote, no theta update
-    sync_arrive(sy);
+    if (blockIdx.x == 0 && threadIdx.x == 0) publish_verdict(sy, flags, sy.arrive_epoch, false);
     va_retire(sy);
     return;
   }
   const int T = P >> 1;
   const uint32_t fillmask = fill > 0 ? ~0u : 0u;
-  // ---- vote (same as k_vote_bits) by the first nvote CTAs; the others go
-  // straight to the theta update of this rank's own block, voting each
-  // super-tile's words in the warp (no wait), while the voters push the
-  // block to the peers over NVLink ----
+  const int lane = threadIdx.x & 31;
+  // ---- the owner vote (same as k_vote_bits) in warp-sized units taken from
+  // a counter (sy.counter[3]); the warp finishing the last unit publishes e2
+  // (sy.counter[0] counts finished units).  The voter CTAs take units first
+  // while the others start on the theta update of this rank's own block
+  // (voted in-warp); any warp about to wait for an owner's block finishes
+  // the remaining units first.  No wait in the kernel depends on a CTA
+  // being resident: e2 needs only the units, which resident warps drain.
   // (measured: at P = 2 the whole grid voting first is faster for 1.1B
-  // params -- the pushed half is too large for a fraction of the SMs)
+  // params -- the pushed half is too large for a fraction of the SMs) ----
   const int share = P >= 4 ? LC_VOTE_SHARE : 1;
   const int nvote = max(1, (int)gridDim.x / share);
-  if ((int)blockIdx.x < nvote) {
-    uint32_t flag = 0;
-    const int64_t nq = cw >> 2;
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq;
-         q += (int64_t)nvote * blockDim.x) {
-      uint32_t pl[4][NP];
-#pragma unroll
-      for (int w = 0; w < 4; ++w)
-#pragma unroll
-        for (int pp = 0; pp < NP; ++pp) pl[w][pp] = 0u;
-      for (int j = 0; j < P; ++j) {
-        uint4 x = __ldcs(reinterpret_cast<const uint4*>(recv + (int64_t)j * cw) + q);
-        uint32_t xs[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          uint32_t carry = xs[w];
-#pragma unroll
-          for (int pp = 0; pp < NP; ++pp) {
-            uint32_t t = pl[w][pp] & carry;
-            pl[w][pp] ^= carry;
-            carry = t;
-          }
-        }
-      }
-      uint32_t v[4], nz[4], tie[4];
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        int64_t rem = n_valid - (4 * q + w) * 32;
-        uint32_t vm = rem >= 32 ? ~0u : (rem <= 0 ? 0u : ((1u << rem) - 1u));
-        vote_word<NP>(pl[w], P, T, fillmask, vm, fill, sum_mode, v[w], nz[w], tie[w], flag);
-      }
-      vote_store(out, 4 * q, make_uint4(v[0], v[1], v[2], v[3]),
-                 make_uint4(nz[0], nz[1], nz[2], nz[3]), make_uint4(tie[0], tie[1], tie[2], tie[3]));
-    }
-    if (flag) atomicOr(flags, flag);
+  const int64_t nq = cw >> 2;
+  const int64_t nunits = (nq + kVoteUnitQuads - 1) / kVoteUnitQuads;
+  bool votes_left = true;  // this warp has not yet seen the units run out
+  auto vote_units = [&]() {
+    if (votes_left)
+      votes_left = va_vote_units<NP>(recv, P, T, cw, n_valid, fill, fillmask, sum_mode, out,
+                                     flags, sy, nunits, lane);
+  };
+  if ((int)blockIdx.x < nvote) vote_units();
+  if (sy.verdict && blockIdx.x == 0 && threadIdx.x == 0) {
+    // the host's verdict once every owner (this one included: its vote
+    // flags are final) has published its block -- the waits left in the
+    // update below then all succeed at once
+    bool ok = true;
+    for (int j = 0; j < P; ++j) ok = wait_slot(sy, j, sy.arrive_epoch) && ok;
+    publish_verdict(sy, flags, sy.arrive_epoch, ok);
   }
-  sync_arrive(sy);  // last CTA: every peer learns this owner's block is out
   // ---- theta update, waiting per owner block.  Warps take work items of
   // LC_VA_CHUNK super-tiles from a counter (sy.counter[1]) in rotated order
   // -- this rank's own block first -- so the voter CTAs, which start late,
   // simply take fewer items (a static split leaves their share as a tail) ----
   constexpr int KU = LC_VA_KU;
   const int64_t CH = a.chunk;
-  const int lane = threadIdx.x & 31;
   const int64_t nsup = (a.n + 1023) >> 10;
   const int64_t nwords = (a.n + 31) >> 5;
   float4* th4 = reinterpret_cast<float4*>(a.theta);
@@ -959,6 +1054,7 @@ k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_val
       return;
     }
     if (!(((ready | bad) >> j) & 1u)) {
+      vote_units();  // never wait while this owner's vote units remain
       int ok = 1;
       if (lane == 0) ok = wait_slot(sy, j, sy.arrive_epoch);
       ok = __shfl_sync(kFull, ok, 0);
@@ -1411,7 +1507,10 @@ k_vote_update(const uint32_t* __restrict__ rows, int64_t stride, int P, float* _
               uint32_t* __restrict__ flags, SyncD sy) {
   constexpr int KU = LC_VU_KU;  // theta sub-tiles in flight per batch
   griddep_wait();
-  if (!sync_wait(sy)) return;  // a peer's rows never arrived: theta untouched
+  const bool synced = sync_wait(sy);
+  // every wait of the step is behind us: the host may check it now
+  if (blockIdx.x == 0 && threadIdx.x == 0) publish_verdict(sy, flags, sy.wait_epoch, synced);
+  if (!synced) return;  // a peer's rows never arrived: theta untouched
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1623,6 +1722,26 @@ bool make_dst(Dst& d, void* const* ptrs, int nd) {
 extern "C" {
 
 int lc_abi_version(void) { return LIONCUB_ABI_VERSION; }
+
+int lc_wait_verdict(const uint64_t* word, uint64_t epoch, double timeout_s, uint32_t* status) {
+  if (!word || !status) return set_err(LC_E_ARG, "lc_wait_verdict: null pointer");
+  const auto t0 = std::chrono::steady_clock::now();
+  for (uint32_t spin = 0;; ++spin) {
+    const uint64_t v = __atomic_load_n(word, __ATOMIC_ACQUIRE);
+    if ((v >> 8) >= epoch) {
+      *status = (uint32_t)(v & 0xFFu);
+      return LC_OK;
+    }
+    if ((spin & 255u) == 255u) {
+      const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (dt > timeout_s) return set_err(LC_E_COLLECTIVE, "lc_wait_verdict: no verdict before the timeout");
+      if (dt > 1e-3) std::this_thread::yield();
+    }
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+  }
+}
 
 const char* lc_last_error(void) { return err_msg().c_str(); }
 

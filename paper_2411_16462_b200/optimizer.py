@@ -45,7 +45,7 @@ from .collectives import (Topology, choose_lane_bits, field_bits, mean_into,
                           owner_elems, owner_valid)
 from .errors import CollectiveError, ConfigError
 from .quant import QuantSpec, SignPolicy, scale_tables
-from .transport import DEFAULT_TIMEOUT
+from .transport import DEFAULT_TIMEOUT, host_wait
 
 LrSchedule = Union[float, Callable[[int], float]]
 VOTE_ALGOS = ("ps", "ps_efficient", "direct", "compressed1bit")
@@ -796,8 +796,17 @@ def _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out,
                 # finished reading its staging rows) before the next step
                 tp.device_barrier(topo.rank, gen)
             if strict and P > 1 and ws.p2p:
-                tp.check_step(topo.rank, gen, "step")   # syncs the stream
-                _raise_nan(ws)
+                ve = getattr(ws, "verdict_epoch", None) if msync is None else None
+                status = None if ve is None else tp.wait_verdict(topo.rank, ve)
+                if status is not None and not status & _lib.LC_FLAG_BARRIER_TIMEOUT:
+                    # every wait of the step succeeded; the theta update may
+                    # still be running (stream-ordered before any later work)
+                    if status & _lib.LC_FLAG_NAN:
+                        host_wait(stream)     # flags_host has landed
+                        _raise_nan(ws)
+                else:
+                    tp.check_step(topo.rank, gen, "step")   # syncs the stream
+                    _raise_nan(ws)
             if metrics:
                 _fill_metrics(metrics_out, layout, dev, ws, nz, c_local, s)
                 # device time of the phases the reference times with
@@ -896,6 +905,7 @@ SYNC_MEAN = os.environ.get("LIONCUB_SYNC_MEAN", "side")   # side | serial | inli
 # only the all-layer sync; 0: never (maybe_sync_momentum after the step)
 SYNC_FUSE = os.environ.get("LIONCUB_SYNC_FUSE", "1")
 # vote/update CTAs per SM while the selective sync's pull runs beside it
+SYNC_PULL_SIDE = os.environ.get("LIONCUB_SYNC_PULL_SIDE", "1") == "1"
 SYNC_PULL_VOTE_CAP = int(os.environ.get("LIONCUB_SYNC_PULL_VOTE_CAP", "0"))
 
 
@@ -905,6 +915,19 @@ def _sync_side_stream(ws, topo):
     if getattr(ws, "side", None) is None:
         ws.side = torch.cuda.Stream(topo.device)
     return ws.side.cuda_stream
+
+
+def _set_verdict(ws, tp, r, sy, epoch):
+    """Strict error mode: let the vote/update kernel publish the step's
+    verdict (every wait resolved, K1's flags) into the rank's pinned verdict
+    word at ``epoch``, so the step checks it without waiting for the theta
+    update to finish (lc_sync.verdict)."""
+    if epoch is not None and tp.error_mode == "step":
+        sy.verdict = tp.verdict_word(r)
+        ws.verdict_epoch = epoch
+    else:
+        sy.verdict = None
+        ws.verdict_epoch = None
 
 
 def _mark(timer, name, stream):
@@ -948,6 +971,7 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
         a, b = ws.syncs[0], ws.syncs[1]
         a.wait_epoch, a.arrive_epoch = 0, e1
         b.wait_epoch, b.arrive_epoch = e1, 0
+        _set_verdict(ws, tp, r, b, e1)
         _lib.call("lc_encode", gp, mp, mk, n, C.byref(hyp), fill,
                   _lib.LC_ENC_SIGN1 | _lib.LC_ENC_REPLICATE, 1, None, ag.dst[h], P, ag.L, 0,
                   ws.flags.data_ptr(), C.byref(a), s)
@@ -971,6 +995,11 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
         a.wait_epoch, a.arrive_epoch = 0, e1
         b.wait_epoch, b.arrive_epoch = e1, e2
         c.wait_epoch, c.arrive_epoch = e2, 0
+        # the early verdict only where the vote/update kernel is the step's
+        # last wait (no fused sync behind it)
+        _set_verdict(ws, tp, r, b, e2 if (msync is None and kind == "1bit" and pipe is None
+                                          and ws.tout is None and ws.nsrc == 1
+                                          and theta is not None) else None)
         sy1, sy2, sy3 = C.byref(a), C.byref(b), C.byref(c)
         ws.k5_sync = sy3
     if pipe is not None and segs is None and mflat is None:
@@ -1026,11 +1055,14 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
             # stores the mean into every rank's m -- concurrently with the
             # vote/update grid, capped to leave it SMs; the caller's barrier
             # ends the step
-            side = torch.cuda.Stream(topo.device) if getattr(ws, "side_t", None) is None \
-                else ws.side_t
-            ws.side_t = side
             main = torch.cuda.ExternalStream(s)
-            side.wait_stream(main)
+            if SYNC_PULL_SIDE:
+                side = torch.cuda.Stream(topo.device) if getattr(ws, "side_t", None) is None \
+                    else ws.side_t
+                ws.side_t = side
+                side.wait_stream(main)
+            else:
+                side = main
             if getattr(ws, "wait_e1", None) is None:
                 ws.wait_e1 = tp.sync_struct(r, ws.counters[12:16], 0, 0)
             ws.wait_e1.wait_epoch, ws.wait_e1.arrive_epoch = e1, 0
@@ -1054,7 +1086,8 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
                           hyp.weight_decay, s)
             finally:
                 _lib.load().lc_set_vote_cap(0)
-            main.wait_stream(side)
+            if side is not main:
+                main.wait_stream(side)
         elif SYNC_MEAN == "serial":
             # vote/update, then the owner mean as its own full-occupancy kernel
             # (stream order: the vote kernel already waited for every K1)

@@ -154,6 +154,7 @@ class EarlyStep:
         if P > 1:
             topo, tp, r, n, s = self.topo, self.topo.transport, self.topo.rank, self.n, self.s
             a_sy, b_sy, c_sy = ws.syncs
+            b_sy.verdict = None   # checked below through the error words
             hyp = self.hyp
             with _on_device(self.dev), _on_stream(self.stream, self.dev):
                 # every chunk is enqueued: publish the encode epoch e1

@@ -248,6 +248,11 @@ class _PeerSync:
             dev = self.device(rank)
             self._err[rank] = torch.zeros(2, dtype=torch.int32, device=dev)
             self._err_host[rank] = torch.zeros(2, dtype=torch.int32, pin_memory=True)
+            # the step verdict word the vote/update kernels store into
+            # (lc_sync.verdict): pinned, so the device writes it directly
+            if not hasattr(self, "_verdict"):
+                self._verdict = {}
+            self._verdict[rank] = torch.zeros(1, dtype=torch.int64, pin_memory=True)
             self._epoch[rank] = 0
         return self.sym_buffer(rank, ("__barrier__",), self.world_size, torch.int64)
 
@@ -281,6 +286,20 @@ class _PeerSync:
         _lib.call("lc_barrier", _lib.table(flags.peers), self.world_size, rank,
                   flags.local.data_ptr(), epoch, self.timeout,
                   self._err[rank].data_ptr(), st)
+
+    def verdict_word(self, rank) -> int:
+        """Host address of this rank's step-verdict word (lc_sync.verdict)."""
+        self._flags(rank)
+        return self._verdict[rank].data_ptr()
+
+    def wait_verdict(self, rank, epoch) -> int | None:
+        """Status byte of the step whose vote/update kernel publishes
+        ``epoch`` (LC_FLAG_* bits), or None if none arrived in time.  Spins
+        in C with the GIL released."""
+        st = C.c_uint32(0)
+        rc = _lib.load().lc_wait_verdict(self._verdict[rank].data_ptr(), epoch,
+                                         self.timeout + 10.0, C.byref(st))
+        return st.value if rc == _lib.LC_OK else None
 
     def poll_error(self, rank):
         """Non-blocking: the barrier error flag as of the last poll; schedules

@@ -61,6 +61,8 @@ class _Ranks:
         self.counter = [z(16) for _ in range(P)]
         self.err = [z(2) for _ in range(P)]
         self.kflags = [z(1) for _ in range(P)]
+        # pinned step-verdict words (lc_sync.verdict)
+        self.verdict = [torch.zeros(1, dtype=torch.int64, pin_memory=True) for _ in range(P)]
 
     def sync(self, r, wait, arrive, timeout=5.0, counter=0):
         sy = _lib.Sync()
@@ -71,6 +73,7 @@ class _Ranks:
         sy.err = self.err[r].data_ptr()
         sy.wait_epoch, sy.arrive_epoch = wait, arrive
         sy.P, sy.rank, sy.timeout_s = self.P, r, timeout
+        sy.verdict = self.verdict[r].data_ptr()
         return sy
 
     def oracle(self, algo, spec, it, zm):
@@ -154,6 +157,7 @@ def test_vote_apply_abi_matches_oracle(P, n, algo, bits, zm, kind):
         assert_f32_equal(R.m[k].cpu().numpy(), m_ref[k], f"m r{k}")
         assert int(R.kflags[k][0]) == 0
         assert R.flags[k].tolist() == [8] * P     # every owner published e2
+        assert int(R.verdict[k][0]) == 8 << 8     # the step verdict: e2, no flags
 
 
 @pytest.mark.parametrize("P,n,algo,bits,zm,kind", CASES)
@@ -192,6 +196,7 @@ def test_replicate_encode_and_vote_update_abi_match_oracle(P, n, algo, bits, zm,
         assert_f32_equal(R.theta[r].cpu().numpy(), th_ref, f"theta r{r}")
         assert_f32_equal(R.m[r].cpu().numpy(), m_ref[r], f"m r{r}")
         assert int(R.err[r][0]) == 0
+        assert int(R.verdict[r][0]) == 9 << 8     # verdict at the wait epoch e1
 
 
 def test_vote_apply_large_offsets_and_double_buffered_slots():
@@ -251,6 +256,7 @@ def test_kernels_time_out_on_a_missing_rank_and_write_nothing():
               R.full[0].data_ptr(), None, LR, WD, st)
     torch.cuda.synchronize()
     assert R.err[0].tolist() == [_lib.LC_FLAG_BARRIER_TIMEOUT, 1 << 1]
+    assert int(R.verdict[0][0]) == (51 << 8) | _lib.LC_FLAG_BARRIER_TIMEOUT
     assert torch.equal(R.theta[0], th0) and torch.equal(R.full[0], full0)
     assert int(R.flags[1][0]) == 100         # no epoch published to the peer
     row = 32 * -(-n // 1024)
@@ -263,6 +269,7 @@ def test_kernels_time_out_on_a_missing_rank_and_write_nothing():
               C.byref(R.sync(0, 50, 0, timeout=0.2)), st)
     torch.cuda.synchronize()
     assert R.err[0].tolist() == [_lib.LC_FLAG_BARRIER_TIMEOUT, 1 << 1]
+    assert int(R.verdict[0][0]) == (50 << 8) | _lib.LC_FLAG_BARRIER_TIMEOUT
     assert torch.equal(R.theta[0], th0)
     R.err[0].zero_()
     _lib.call("lc_barrier", _lib.table([f.data_ptr() for f in R.flags]), P, 0,
