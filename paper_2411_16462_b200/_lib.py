@@ -210,7 +210,7 @@ launches = 0  # kernels enqueued through call(); read by bench.py
 phase_events = None
 
 
-def call(name: str, *args, what: str | None = None):
+def call(name: str, *args, what: str | None = None, tag: str | None = None):
     global launches
     fn = getattr(load(), name)
     rec = phase_events
@@ -223,7 +223,7 @@ def call(name: str, *args, what: str | None = None):
         e0.record(stream)
         rc = fn(*args)
         e1.record(stream)
-        rec.setdefault(name, []).append((e0, e1))
+        rec.setdefault(tag or name, []).append((e0, e1))   # tag: a barrier-only launch
     else:
         rc = fn(*args)
     check(rc, what or name)

@@ -715,13 +715,15 @@ k_vote_bits(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_vali
 }
 
 // ---------------------------------------------------------------------------
-// K4+K5 fused (peer-memory path): the owner votes its block and pushes the
-// voted words into every rank's gather buffer, its last CTA publishes epoch
-// e2, and the same grid then updates theta super-tile by super-tile, each
-// warp waiting only for the owner of the block it is about to read (so the
-// update of already-voted blocks overlaps the slowest owner's vote).  All
-// CTAs of the grid are co-resident (occupancy-sized grid), so CTAs that wait
-// for their own rank's block never starve the CTAs still voting.
+// K4+K5 fused (peer-memory path): the grid votes the owner block in
+// warp-sized units and pushes the voted words into every rank's gather
+// buffer; the warp completing the last unit publishes epoch e2.  The same
+// grid then updates theta in work items handed out by a counter, this
+// rank's own block first, each warp waiting only for the owner of the block
+// it is about to read (so the update of already-voted blocks overlaps the
+// slowest owner's vote).  Both phases are work-counter driven, so nothing
+// waits on a CTA that is not resident (round 2: a static split deadlocked
+// when another stream's kernel held a few SM slots).
 // ---------------------------------------------------------------------------
 struct ApplyArgs {
   float* theta;
@@ -733,11 +735,8 @@ struct ApplyArgs {
   int64_t chunk;        // super-tiles per work item of the update phase
 };
 
-#ifndef LC_VOTE_SHARE
-#define LC_VOTE_SHARE 8  // 1/LC_VOTE_SHARE of the grid votes + pushes the owner block
-#endif
 #ifndef LC_VA_KU
-#define LC_VA_KU 4       // theta sub-tiles in flight per warp in the update phase
+#define LC_VA_KU 8       // theta sub-tiles in flight per warp in the update phase
 #endif
 
 // The momentum sync fused into the step (the owner half of
@@ -843,13 +842,10 @@ k_sync_mean(SyncD sy, MeanArgs ma, int P) {
 #define LC_VA_ITEMS 131072  // work items per launch the chunk size aims for
 #endif
 
-#ifndef LC_VA_VILP
-#define LC_VA_VILP 1     // quads per lane in flight in a vote unit (1 or 2)
-#endif
 #ifndef LC_VA_UNIT
 #define LC_VA_UNIT 256
 #endif
-constexpr int kVoteUnitQuads = LC_VA_UNIT;  // uint4 word quads per vote unit (32K elements)
+constexpr int kVoteUnitQuads = LC_VA_UNIT;  // max uint4 word quads per vote unit (32K elements)
 
 // The update phase's work counter (sy.counter[1]) is reset by the last CTA
 // to finish its update (sy.counter[2] counts them), so the next launch on
@@ -924,7 +920,7 @@ __device__ __forceinline__ bool va_vote_units(const uint32_t* __restrict__ recv,
                                               int64_t cw, int64_t n_valid, int fill,
                                               uint32_t fillmask, int sum_mode, const VoteOut& out,
                                               uint32_t* flags, const SyncD& sy, int64_t nunits,
-                                              int lane) {
+                                              int64_t unit, int lane) {
   const int64_t nq = cw >> 2;
   unsigned int* vclaim = sy.counter + 3;
   unsigned int* vdone = sy.counter;
@@ -934,15 +930,10 @@ __device__ __forceinline__ bool va_vote_units(const uint32_t* __restrict__ recv,
   if ((int64_t)u < nunits && lane == 0) ahead = atomicAdd(vclaim, 1u);
   uint32_t flag = 0;
   while ((int64_t)u < nunits) {
-    const int64_t qe = min(nq, ((int64_t)u + 1) * kVoteUnitQuads);
-#if LC_VA_VILP == 2
-    for (int64_t q = (int64_t)u * kVoteUnitQuads + lane; q < qe; q += 64)
+    const int64_t qe = min(nq, ((int64_t)u + 1) * unit);
+    for (int64_t q = (int64_t)u * unit + lane; q < qe; q += 64)
       va_vote_quad<NP>(recv, P, T, cw, n_valid, fill, fillmask, sum_mode, out, q,
                        q + 32 < qe ? q + 32 : nq, flag);
-#else
-    for (int64_t q = (int64_t)u * kVoteUnitQuads + lane; q < qe; q += 32)
-      va_vote_quad<NP>(recv, P, T, cw, n_valid, fill, fillmask, sum_mode, out, q, nq, flag);
-#endif
     ++mine;
     u = __shfl_sync(kFull, ahead, 0);
     if ((int64_t)u < nunits && lane == 0) ahead = atomicAdd(vclaim, 1u);
@@ -967,7 +958,7 @@ __device__ __forceinline__ bool va_vote_units(const uint32_t* __restrict__ recv,
 }
 
 #ifndef LC_VA_MINB
-#define LC_VA_MINB 4     // __launch_bounds__ min CTAs per SM of k_vote_apply (64 regs)
+#define LC_VA_MINB 3     // __launch_bounds__ min CTAs per SM of k_vote_apply (80 regs)
 #endif
 
 template <int NP, bool NZ, bool MEAN>
@@ -985,26 +976,19 @@ k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_val
   const int T = P >> 1;
   const uint32_t fillmask = fill > 0 ? ~0u : 0u;
   const int lane = threadIdx.x & 31;
-  // ---- the owner vote (same as k_vote_bits) in warp-sized units taken from
-  // a counter (sy.counter[3]); the warp finishing the last unit publishes e2
-  // (sy.counter[0] counts finished units).  The voter CTAs take units first
-  // while the others start on the theta update of this rank's own block
-  // (voted in-warp); any warp about to wait for an owner's block finishes
-  // the remaining units first.  No wait in the kernel depends on a CTA
-  // being resident: e2 needs only the units, which resident warps drain.
-  // (measured: at P = 2 the whole grid voting first is faster for 1.1B
-  // params -- the pushed half is too large for a fraction of the SMs) ----
-  const int share = P >= 4 ? LC_VOTE_SHARE : 1;
-  const int nvote = max(1, (int)gridDim.x / share);
+  // ---- 1. the owner vote (as k_vote_bits) in warp-sized units taken from a
+  // counter (sy.counter[3]); the warp whose finished units complete the
+  // block publishes e2 (sy.counter[0] counts them).  Every warp votes until
+  // the units run out, so e2 needs only the warps that are running: no wait
+  // in this kernel depends on a CTA being resident (another stream's kernel
+  // may hold some of the SMs) ----
   const int64_t nq = cw >> 2;
-  const int64_t nunits = (nq + kVoteUnitQuads - 1) / kVoteUnitQuads;
-  bool votes_left = true;  // this warp has not yet seen the units run out
-  auto vote_units = [&]() {
-    if (votes_left)
-      votes_left = va_vote_units<NP>(recv, P, T, cw, n_valid, fill, fillmask, sum_mode, out,
-                                     flags, sy, nunits, lane);
-  };
-  if ((int)blockIdx.x < nvote) vote_units();
+  // at most kVoteUnitQuads per unit, and ~4 units per warp so a small block's
+  // vote (the critical path to e2) spreads over the whole grid
+  int64_t unit = nq / ((int64_t)gridDim.x * (blockDim.x >> 5) * 4);
+  unit = unit < 32 ? 32 : (unit > kVoteUnitQuads ? kVoteUnitQuads : (unit & ~(int64_t)31));
+  va_vote_units<NP>(recv, P, T, cw, n_valid, fill, fillmask, sum_mode, out, flags, sy,
+                    (nq + unit - 1) / unit, unit, lane);
   if (sy.verdict && blockIdx.x == 0 && threadIdx.x == 0) {
     // the host's verdict once every owner (this one included: its vote
     // flags are final) has published its block -- the waits left in the
@@ -1013,10 +997,10 @@ k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_val
     for (int j = 0; j < P; ++j) ok = wait_slot(sy, j, sy.arrive_epoch) && ok;
     publish_verdict(sy, flags, sy.arrive_epoch, ok);
   }
-  // ---- theta update, waiting per owner block.  Warps take work items of
-  // LC_VA_CHUNK super-tiles from a counter (sy.counter[1]) in rotated order
-  // -- this rank's own block first -- so the voter CTAs, which start late,
-  // simply take fewer items (a static split leaves their share as a tail) ----
+  // ---- 2. theta update.  Warps take work items of up to LC_VA_CHUNK
+  // super-tiles from a counter (sy.counter[1]) in rotated order -- this
+  // rank's own block first, so the peers' blocks are usually out by the time
+  // the items reach them -- waiting per owner block for its e2 ----
   constexpr int KU = LC_VA_KU;
   const int64_t CH = a.chunk;
   const int64_t nsup = (a.n + 1023) >> 10;
@@ -1029,32 +1013,7 @@ k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_val
     zw_ = ~0u;
     if (sidx >= nsup) return;
     const int j = (int)((sidx * 32) / a.blk_words);  // owner of this super-tile
-    if (j == sy.rank && share > 1) {  // own block: vote this word from the P rows
-      const int64_t wl = sidx * 32 + lane - (int64_t)j * a.blk_words;  // word in my block
-      uint32_t pl[NP];
-#pragma unroll
-      for (int pp = 0; pp < NP; ++pp) pl[pp] = 0u;
-      if (wl < cw) {
-        for (int r = 0; r < P; ++r) {
-          uint32_t carry = __ldcs(recv + (int64_t)r * cw + wl);
-#pragma unroll
-          for (int pp = 0; pp < NP; ++pp) {
-            const uint32_t t = pl[pp] & carry;
-            pl[pp] ^= carry;
-            carry = t;
-          }
-        }
-      }
-      const int64_t rem = n_valid - wl * 32;
-      const uint32_t vm = rem >= 32 ? ~0u : (rem <= 0 ? 0u : ((1u << rem) - 1u));
-      uint32_t v, nz, tie, fl = 0;
-      vote_word<NP>(pl, P, T, fillmask, vm, fill, sum_mode, v, nz, tie, fl);
-      sw_ = v;
-      if (NZ) zw_ = nz;
-      return;
-    }
     if (!(((ready | bad) >> j) & 1u)) {
-      vote_units();  // never wait while this owner's vote units remain
       int ok = 1;
       if (lane == 0) ok = wait_slot(sy, j, sy.arrive_epoch);
       ok = __shfl_sync(kFull, ok, 0);
@@ -1067,8 +1026,6 @@ k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_val
       if (NZ) zw_ = __ldcv(a.nzb + w);
     }
   };
-  // rotated order: this rank's own block (voted locally, no wait) first, by
-  // the time the items reach a remote block its owner's votes have landed
   int64_t rot = (int64_t)sy.rank * a.blk_words / 32;  // blk_words % 32 == 0
   if (rot >= nsup) rot = 0;
   auto at = [&](int64_t i) {

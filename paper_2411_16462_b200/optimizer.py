@@ -901,11 +901,12 @@ class _Allgather:
 # side stream (vote/update grid capped); "inline": inside the vote/update grid
 # (every CTA joins after its theta share)
 SYNC_MEAN = os.environ.get("LIONCUB_SYNC_MEAN", "side")   # side | serial | inline
-# LIONCUB_SYNC_FUSE: 1 (default) fuse every sync the step can carry; "all":
-# only the all-layer sync; 0: never (maybe_sync_momentum after the step)
-SYNC_FUSE = os.environ.get("LIONCUB_SYNC_FUSE", "1")
+# LIONCUB_SYNC_FUSE: "all" (default) fuse the all-layer sync into the step;
+# 1: also the selective sync (the owner pull beside the theta update --
+# measured slower than the separate pull at 1.1B on 4 x B200: 3.93 vs 3.87
+# ms/step); 0: never (maybe_sync_momentum after the step)
+SYNC_FUSE = os.environ.get("LIONCUB_SYNC_FUSE", "all")
 # vote/update CTAs per SM while the selective sync's pull runs beside it
-SYNC_PULL_SIDE = os.environ.get("LIONCUB_SYNC_PULL_SIDE", "1") == "1"
 SYNC_PULL_VOTE_CAP = int(os.environ.get("LIONCUB_SYNC_PULL_VOTE_CAP", "0"))
 
 
@@ -1055,20 +1056,18 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
             # stores the mean into every rank's m -- concurrently with the
             # vote/update grid, capped to leave it SMs; the caller's barrier
             # ends the step
+            side = torch.cuda.Stream(topo.device) if getattr(ws, "side_t", None) is None \
+                else ws.side_t
+            ws.side_t = side
             main = torch.cuda.ExternalStream(s)
-            if SYNC_PULL_SIDE:
-                side = torch.cuda.Stream(topo.device) if getattr(ws, "side_t", None) is None \
-                    else ws.side_t
-                ws.side_t = side
-                side.wait_stream(main)
-            else:
-                side = main
+            side.wait_stream(main)
             if getattr(ws, "wait_e1", None) is None:
                 ws.wait_e1 = tp.sync_struct(r, ws.counters[12:16], 0, 0)
             ws.wait_e1.wait_epoch, ws.wait_e1.arrive_epoch = e1, 0
             ss = side.cuda_stream
             _lib.call("lc_encode", gp, mp, None, 0, C.byref(hyp), fill, _lib.LC_ENC_SIGN1, 1,
-                      None, ws.dst, P, L, 0, ws.flags.data_ptr(), C.byref(ws.wait_e1), ss)
+                      None, ws.dst, P, L, 0, ws.flags.data_ptr(), C.byref(ws.wait_e1), ss,
+                      tag="lc_wait_e1")
             src = _lib.table(msync.sym.peers)
             for a, b in sync_runs:
                 ln = b - a
@@ -1086,8 +1085,7 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
                           hyp.weight_decay, s)
             finally:
                 _lib.load().lc_set_vote_cap(0)
-            if side is not main:
-                main.wait_stream(side)
+            main.wait_stream(side)
         elif SYNC_MEAN == "serial":
             # vote/update, then the owner mean as its own full-occupancy kernel
             # (stream order: the vote kernel already waited for every K1)

@@ -784,11 +784,14 @@ def test_lioncub_overlap_backward_equals_plain(world, algo, bits, xchg, monkeypa
 
 @pytest.mark.parametrize("world,algo,bits", [(4, "compressed1bit", None), (3, "direct", 1),
                                              (8, "compressed1bit", None)])
-def test_selective_sync_fused_into_step_matches_oracle(world, algo, bits):
+def test_selective_sync_fused_into_step_matches_oracle(world, algo, bits, monkeypatch):
     """sync=SyncPolicy(period, {layers}) passed to the step on the production
-    exchange: each owner's pull of the selected layers runs beside the theta
-    update inside the step (mode "pull"); three steps (the sync firing on the
-    second) equal the oracle's step + maybe_sync_momentum."""
+    exchange with LIONCUB_SYNC_FUSE=1: each owner's pull of the selected
+    layers runs beside the theta update inside the step (mode "pull"); three
+    steps (the sync firing on the second) equal the oracle's step +
+    maybe_sync_momentum."""
+    import paper_2411_16462_b200.optimizer as opt
+    monkeypatch.setattr(opt, "SYNC_FUSE", "1")
     sizes = {"emb": (40_000,), "h0.w": (300_017,), "h1.w": (262_144,), "norm": (1_000,)}
     sel = ["emb", "h1.w"]
     ranks = O.synth_rank_inputs(13, world, sizes, "laplace")
