@@ -13,12 +13,15 @@ run() {  # tag workload N extra...
   fi
   echo "$w n=$n $tag rc=$? $(python -c "import json; d=json.loads(open('$out.json').read().strip().splitlines()[-1]); print('ms', round(d['ms_per_step'],3), 'frac', round(d['step_roofline']['frac'],3), {k: round(v['avg_ms'],3) for k,v in d['kernels'].items()})" 2>/dev/null)"
 }
+run default flat7b_1bit_sync 1 --steps 10
 for n in 2 4; do run "" flat7b_1bit_sync $n --steps 10 --no-cpu-baseline --no-e2e; done
+run default flat7b_1bit_sync 4 --steps 10 --no-cpu-baseline
 run "" flat7b_1bit 4 --steps 10 --no-cpu-baseline --no-e2e
 run "" c1_1bit_1m 1 --steps 50 --no-cpu-baseline --no-e2e
 run "" c1_1bit_1m 4 --steps 50 --no-cpu-baseline --no-e2e
 for n in 1 2 4; do run "" tinyllama_1bit_sync $n --steps 50 --no-cpu-baseline --no-e2e; done
 LIONCUB_ERRORS=deferred run deferred tinyllama_1bit_sync 4 --steps 50 --no-cpu-baseline --no-e2e
+for n in 2 4; do run "" tinyllama_1bit $n --steps 50 --no-cpu-baseline --no-e2e; done
 for n in 1 2 4; do run "" gpt2s_sumsigns $n --steps 50 --no-cpu-baseline --no-e2e; done
 LIONCUB_ERRORS=deferred run deferred gpt2s_sumsigns 4 --steps 50 --no-cpu-baseline --no-e2e
 for n in 1 4; do run "" gpt2s_l1_5bit $n --steps 50 --no-cpu-baseline --no-e2e; done
