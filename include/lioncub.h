@@ -72,15 +72,16 @@ typedef struct lc_hyper {
  * publishes it into every peer's flag slot `rank` after its last CTA
  * finished (per-CTA fence + atomic counter, st.release.sys).  This replaces
  * a separate barrier launch between K1 -> vote -> K5.  NULL = no sync. */
-#define LC_SYNC_COUNTER_WORDS 4
+#define LC_SYNC_COUNTER_WORDS 8
 typedef struct lc_sync {
   void* peer_flags[32]; /* rank j's uint64[P] flag array, mapped here     */
   uint64_t* my_flags;   /* this rank's flag array                          */
   uint32_t* counter;    /* LC_SYNC_COUNTER_WORDS zeroed device words per
                            arrive site: [0] arrivals (lc_vote_apply: vote
-                           units done), [1..3] lc_vote_apply's work
+                           units done), [1..4] lc_vote_apply's work
                            counters (update items, retired CTAs, vote
-                           units claimed); every kernel leaves them zero  */
+                           units claimed, CTA tickets); every kernel
+                           leaves them zero                                */
   uint32_t* err;        /* 2 device words: [0] LC_FLAG_* bits, [1] bitmask
                            of the ranks a wait timed out on.  A kernel whose
                            wait times out writes nothing (theta, m and the

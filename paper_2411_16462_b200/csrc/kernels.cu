@@ -735,8 +735,8 @@ struct ApplyArgs {
   int64_t chunk;        // super-tiles per work item of the update phase
 };
 
-#ifndef LC_VA_KU
-#define LC_VA_KU 8       // theta sub-tiles in flight per warp in the update phase
+#ifndef LC_VOTE_SHARE
+#define LC_VOTE_SHARE 8  // P >= 4: the first 1/LC_VOTE_SHARE of the CTAs to start vote
 #endif
 
 // The momentum sync fused into the step (the owner half of
@@ -857,6 +857,7 @@ __device__ __forceinline__ void va_retire(const SyncD& sy) {
       sy.counter[1] = 0u;
       sy.counter[2] = 0u;
       sy.counter[3] = 0u;
+      sy.counter[4] = 0u;
       __threadfence();
     }
   }
@@ -957,12 +958,15 @@ __device__ __forceinline__ bool va_vote_units(const uint32_t* __restrict__ recv,
   return false;
 }
 
-#ifndef LC_VA_MINB
-#define LC_VA_MINB 3     // __launch_bounds__ min CTAs per SM of k_vote_apply (80 regs)
-#endif
 
-template <int NP, bool NZ, bool MEAN>
-__global__ void __launch_bounds__(256, LC_VA_MINB)
+// WIDE: the grid has the GPU to itself -- 3 CTAs/SM (80 registers), 8 theta
+// sub-tiles in flight per warp.  Otherwise (capped beside the fused sync's
+// mean kernel, or running the mean itself) 4 CTAs/SM at 64 registers and 4
+// sub-tiles, so 2 vote CTAs + 2 mean CTAs fit an SM's register file.
+// Measured (4 x B200): 1.1B vote/update 1.52 ms WIDE vs 1.56; the 7e9 fused
+// sync step at P = 2 50.4 ms narrow vs 54.4 ms WIDE (mean CTAs starved).
+template <int NP, bool NZ, bool MEAN, bool WIDE>
+__global__ void __launch_bounds__(256, WIDE ? 3 : 4)
 k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_valid, int fill,
              int sum_mode, const __grid_constant__ VoteOut out, uint32_t* __restrict__ flags,
              const __grid_constant__ SyncD sy, ApplyArgs a,
@@ -978,17 +982,28 @@ k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_val
   const int lane = threadIdx.x & 31;
   // ---- 1. the owner vote (as k_vote_bits) in warp-sized units taken from a
   // counter (sy.counter[3]); the warp whose finished units complete the
-  // block publishes e2 (sy.counter[0] counts them).  Every warp votes until
-  // the units run out, so e2 needs only the warps that are running: no wait
-  // in this kernel depends on a CTA being resident (another stream's kernel
-  // may hold some of the SMs) ----
+  // block publishes e2 (sy.counter[0] counts them).  At P >= 4 the first
+  // 1/LC_VOTE_SHARE of the CTAs TO START (a ticket, sy.counter[4] -- not
+  // blockIdx) vote while the others begin the theta update of this rank's
+  // own block, voting those words in-warp, so the vote's NVLink pushes
+  // overlap the HBM-bound update.  Voters are CTAs that are running, and
+  // units are handed out dynamically, so e2 never waits for a CTA that is
+  // not resident (another stream's kernel may hold some of the SMs).  At
+  // P <= 3 every CTA votes first (measured faster for 1.1B at P = 2: the
+  // pushed half is too large for a fraction of the SMs) ----
+  __shared__ int s_voter;
+  const int share = P >= 4 ? LC_VOTE_SHARE : 1;
+  const unsigned int nvote = max(1u, gridDim.x / share);
+  if (threadIdx.x == 0) s_voter = atomicAdd(sy.counter + 4, 1u) < nvote;
+  __syncthreads();
   const int64_t nq = cw >> 2;
-  // at most kVoteUnitQuads per unit, and ~4 units per warp so a small block's
-  // vote (the critical path to e2) spreads over the whole grid
-  int64_t unit = nq / ((int64_t)gridDim.x * (blockDim.x >> 5) * 4);
+  // at most kVoteUnitQuads per unit, and ~4 units per voter warp so a small
+  // block's vote (the critical path to e2) spreads over every voter
+  int64_t unit = nq / ((int64_t)nvote * (blockDim.x >> 5) * 4);
   unit = unit < 32 ? 32 : (unit > kVoteUnitQuads ? kVoteUnitQuads : (unit & ~(int64_t)31));
-  va_vote_units<NP>(recv, P, T, cw, n_valid, fill, fillmask, sum_mode, out, flags, sy,
-                    (nq + unit - 1) / unit, unit, lane);
+  if (s_voter)
+    va_vote_units<NP>(recv, P, T, cw, n_valid, fill, fillmask, sum_mode, out, flags, sy,
+                      (nq + unit - 1) / unit, unit, lane);
   if (sy.verdict && blockIdx.x == 0 && threadIdx.x == 0) {
     // the host's verdict once every owner (this one included: its vote
     // flags are final) has published its block -- the waits left in the
@@ -999,9 +1014,10 @@ k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_val
   }
   // ---- 2. theta update.  Warps take work items of up to LC_VA_CHUNK
   // super-tiles from a counter (sy.counter[1]) in rotated order -- this
-  // rank's own block first, so the peers' blocks are usually out by the time
-  // the items reach them -- waiting per owner block for its e2 ----
-  constexpr int KU = LC_VA_KU;
+  // rank's own block first (voted in-warp at P >= 4: no wait), so the peers'
+  // blocks are usually out by the time the items reach them -- waiting per
+  // owner block for its e2 ----
+  constexpr int KU = WIDE ? 8 : 4;  // theta sub-tiles in flight per warp
   const int64_t CH = a.chunk;
   const int64_t nsup = (a.n + 1023) >> 10;
   const int64_t nwords = (a.n + 31) >> 5;
@@ -1013,6 +1029,30 @@ k_vote_apply(const uint32_t* __restrict__ recv, int P, int64_t cw, int64_t n_val
     zw_ = ~0u;
     if (sidx >= nsup) return;
     const int j = (int)((sidx * 32) / a.blk_words);  // owner of this super-tile
+    if (j == sy.rank && share > 1) {  // own block: vote this word from the P rows
+      const int64_t wl = sidx * 32 + lane - (int64_t)j * a.blk_words;  // word in my block
+      uint32_t pl[NP];
+#pragma unroll
+      for (int pp = 0; pp < NP; ++pp) pl[pp] = 0u;
+      if (wl < cw) {
+        for (int r = 0; r < P; ++r) {
+          uint32_t carry = __ldcs(recv + (int64_t)r * cw + wl);
+#pragma unroll
+          for (int pp = 0; pp < NP; ++pp) {
+            const uint32_t t = pl[pp] & carry;
+            pl[pp] ^= carry;
+            carry = t;
+          }
+        }
+      }
+      const int64_t rem = n_valid - wl * 32;
+      const uint32_t vm = rem >= 32 ? ~0u : (rem <= 0 ? 0u : ((1u << rem) - 1u));
+      uint32_t v, nz, tie, fl = 0;
+      vote_word<NP>(pl, P, T, fillmask, vm, fill, sum_mode, v, nz, tie, fl);
+      sw_ = v;
+      if (NZ) zw_ = nz;
+      return;
+    }
     if (!(((ready | bad) >> j) & 1u)) {
       int ok = 1;
       if (lane == 0) ok = wait_slot(sy, j, sy.arrive_epoch);
@@ -2060,7 +2100,9 @@ int lc_vote_apply(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid, 
   ApplyArgs a{theta, n, full, nz_full, lr, wd, cw, chunk};
 #define LC_VA(NP, NZ)                                                                      \
   do {                                                                                     \
-    auto kern = g_mean.stage ? k_vote_apply<NP, NZ, true> : k_vote_apply<NP, NZ, false>;   \
+    auto kern = g_mean.stage ? k_vote_apply<NP, NZ, true, false>                          \
+                : g_va_cap > 0 ? k_vote_apply<NP, NZ, false, false>                       \
+                               : k_vote_apply<NP, NZ, false, true>;                        \
     int grid = stream_grid(kern, kBlock, (n + 1023) >> 10, kBlock / 32);                   \
     if (g_va_cap > 0 && grid > sm_count() * g_va_cap) grid = sm_count() * g_va_cap;       \
     LC_CUDA_TRY(launch_pdl(kern, grid, kBlock, 0, st, recv, P, cw, n_valid, fill, sum_mode, \

@@ -104,12 +104,17 @@ struct DevTmpl {
 struct DevSeg {
   int64_t start, n;
   int op_begin, nlvl, lvl_begin, root;
+  int node_begin, node_count;  // the segment's tree nodes are contiguous
 };
+
+// k_l1_upper stages a segment's nodes in shared memory when they fit
+constexpr int kUpperSmemNodes = 24576;  // 192 KB of doubles
 
 }  // namespace
 
 struct lc_l1_plan_s {
   int nseg = 0;
+  int max_seg_nodes = 0;  // largest per-segment node count (k_l1_upper smem)
   int64_t n_total = 0;
   int n_items = 0, n_nodes = 0, max_slots = 0;
   std::vector<int64_t> seg_start;
@@ -579,20 +584,38 @@ k_l1_upper(const DevSeg* __restrict__ segs, const int4* __restrict__ uops,
            const int* __restrict__ ulvl, const unsigned long long* __restrict__ gmax,
            double* __restrict__ nodes, int pk, double p, int qmax,
            double* __restrict__ norms, double* __restrict__ scales) {
+  extern __shared__ double snode[];
   const int s = blockIdx.x;
   const DevSeg S = segs[s];
   const double mx = seg_mx(gmax, s, pk);
   double root = 0.0;
   if (mx != 0.0 && pk != PK_INF) {
-    for (int lv = 0; lv < S.nlvl; ++lv) {
-      const int b = ulvl[S.lvl_begin + lv], e = ulvl[S.lvl_begin + lv + 1];
-      for (int o = b + threadIdx.x; o < e; o += blockDim.x) {
-        const int4 op = uops[S.op_begin + o];
-        nodes[op.x] = __dadd_rn(nodes[op.y], nodes[op.z]);
-      }
+    if (S.node_count <= kUpperSmemNodes) {
+      // the levels run in shared memory: one load of the item nodes, then
+      // __syncthreads-separated levels without a global round trip each
+      const int nb = S.node_begin;
+      for (int i = threadIdx.x; i < S.node_count; i += blockDim.x) snode[i] = nodes[nb + i];
       __syncthreads();
+      for (int lv = 0; lv < S.nlvl; ++lv) {
+        const int b = ulvl[S.lvl_begin + lv], e = ulvl[S.lvl_begin + lv + 1];
+        for (int o = b + threadIdx.x; o < e; o += blockDim.x) {
+          const int4 op = uops[S.op_begin + o];
+          snode[op.x - nb] = __dadd_rn(snode[op.y - nb], snode[op.z - nb]);
+        }
+        __syncthreads();
+      }
+      root = snode[S.root - nb];
+    } else {
+      for (int lv = 0; lv < S.nlvl; ++lv) {
+        const int b = ulvl[S.lvl_begin + lv], e = ulvl[S.lvl_begin + lv + 1];
+        for (int o = b + threadIdx.x; o < e; o += blockDim.x) {
+          const int4 op = uops[S.op_begin + o];
+          nodes[op.x] = __dadd_rn(nodes[op.y], nodes[op.z]);
+        }
+        __syncthreads();
+      }
+      root = nodes[S.root];
     }
-    root = nodes[S.root];
   }
   if (threadIdx.x == 0) {
     double M = 0.0;
@@ -748,6 +771,7 @@ int lc_l1_plan_create(lc_l1_plan_t* out, const int64_t* seg_start, int32_t nseg)
       ops.push_back(Op{node, a.node, b.node, h});
       return R{node, h};
     };
+    const int node_first = node_ctr;
     R root = rec(0, n);
     std::stable_sort(ops.begin(), ops.end(), [](const Op& a, const Op& b) { return a.height < b.height; });
     DevSeg ds;
@@ -756,6 +780,8 @@ int lc_l1_plan_create(lc_l1_plan_t* out, const int64_t* seg_start, int32_t nseg)
     ds.op_begin = (int)uops.size();
     ds.lvl_begin = (int)ulvl.size();
     ds.root = root.node;
+    ds.node_begin = node_first;
+    ds.node_count = node_ctr - node_first;
     int h = 0;
     for (size_t i = 0; i < ops.size(); ++i)
       while (h < ops[i].height) {
@@ -807,6 +833,7 @@ int lc_l1_plan_create(lc_l1_plan_t* out, const int64_t* seg_start, int32_t nseg)
   p->n_leaves = (int64_t)lf_start.size();
   p->n_items = (int)wi_off.size();
   p->n_nodes = node_ctr;
+  for (const DevSeg& d : dsegs) p->max_seg_nodes = std::max(p->max_seg_nodes, d.node_count);
   int rc = LC_OK;
   if ((rc = upload(&p->d_seg_start, p->seg_start)) ||
       (rc = upload(&p->d_seg, dsegs)) || (rc = upload(&p->d_tmpl, dt)) ||
@@ -930,8 +957,19 @@ int norm_scales(lc_l1_plan_t p, const float* g, const float* m, const uint8_t* m
   }
   if (rc) return rc;
   LC_LAUNCH_CHECK();
-  k_l1_upper<<<p->nseg, kThreads, 0, st>>>(p->d_seg, p->d_uops, p->d_ulvl, p->d_max, p->d_nodes,
-                                           pk, pv, qmax, norms, scales);
+  const size_t smem = sizeof(double) * (size_t)std::min(p->max_seg_nodes, kUpperSmemNodes);
+  if (smem > 48 * 1024) {
+    static bool attr_set[64] = {};  // the attribute is per kernel and device
+    int dev = 0;
+    LC_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+      LC_CUDA_TRY(cudaFuncSetAttribute(k_l1_upper, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(sizeof(double) * kUpperSmemNodes)));
+      if (dev >= 0 && dev < 64) attr_set[dev] = true;
+    }
+  }
+  k_l1_upper<<<p->nseg, kThreads, smem, st>>>(p->d_seg, p->d_uops, p->d_ulvl, p->d_max,
+                                              p->d_nodes, pk, pv, qmax, norms, scales);
   LC_LAUNCH_CHECK();
   return LC_OK;
 }

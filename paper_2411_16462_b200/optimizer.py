@@ -294,7 +294,7 @@ class _Workspace:
         self.ag = None
         self.flags = z(1)
         self.flags_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
-        self.counters = z(16)  # 4 sync sites x LC_SYNC_COUNTER_WORDS (kernel counters)
+        self.counters = z(32)  # 4 sync sites x LC_SYNC_COUNTER_WORDS (kernel counters)
         self.k5_sync = None
         self.syncs = None
         self.applied = False
@@ -968,7 +968,7 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
         ag.buf.ag_steps += 1
         (e1,) = tp.take_epochs(r, 1)
         if ws.syncs is None:
-            ws.syncs = [tp.sync_struct(r, ws.counters[4 * i:4 * i + 4], 0, 0) for i in range(3)]
+            ws.syncs = [tp.sync_struct(r, ws.counters[8 * i:8 * i + 8], 0, 0) for i in range(3)]
         a, b = ws.syncs[0], ws.syncs[1]
         a.wait_epoch, a.arrive_epoch = 0, e1
         b.wait_epoch, b.arrive_epoch = e1, 0
@@ -991,7 +991,7 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
         # the vote waits for e1 and publishes e2, K5 waits for e2
         e1, e2 = tp.take_epochs(r, 2)
         if ws.syncs is None:   # built once per workspace; only epochs change
-            ws.syncs = [tp.sync_struct(r, ws.counters[4 * i:4 * i + 4], 0, 0) for i in range(3)]
+            ws.syncs = [tp.sync_struct(r, ws.counters[8 * i:8 * i + 8], 0, 0) for i in range(3)]
         a, b, c = ws.syncs
         a.wait_epoch, a.arrive_epoch = 0, e1
         b.wait_epoch, b.arrive_epoch = e1, e2
@@ -1062,7 +1062,7 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
             main = torch.cuda.ExternalStream(s)
             side.wait_stream(main)
             if getattr(ws, "wait_e1", None) is None:
-                ws.wait_e1 = tp.sync_struct(r, ws.counters[12:16], 0, 0)
+                ws.wait_e1 = tp.sync_struct(r, ws.counters[24:32], 0, 0)
             ws.wait_e1.wait_epoch, ws.wait_e1.arrive_epoch = e1, 0
             ss = side.cuda_stream
             _lib.call("lc_encode", gp, mp, None, 0, C.byref(hyp), fill, _lib.LC_ENC_SIGN1, 1,
@@ -1096,7 +1096,7 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
                       _loc(ws.full).data_ptr(), _lib.ptr(_loc(ws.nz)), hyp.lr,
                       hyp.weight_decay, s)
             _lib.call("lc_sync_mean", None, stage.local.data_ptr(), outs, P, L, nvalid,
-                      ws.counters[12:16].data_ptr(), 0, s)
+                      ws.counters[24:32].data_ptr(), 0, s)
         else:
             stage = tp.sym_buffer(r, ws.key + ("mstage",), P * L, torch.float32)
             outs = _lib.table([msync.sym.peers[k] + r * L * 4 for k in range(P)])
@@ -1104,7 +1104,7 @@ def _exchange_and_vote(topo, gen, ws, kind, binary, sum_mode, F, qmax, fill, n, 
                       ws.vout, ws.nzout, ws.nout, ws.flags.data_ptr(), sy2, theta.data_ptr(), n,
                       _loc(ws.full).data_ptr(), _lib.ptr(_loc(ws.nz)), hyp.lr,
                       hyp.weight_decay, stage.local.data_ptr(), outs, L, nvalid,
-                      ws.counters[12:16].data_ptr(), _sync_side_stream(ws, topo), s)
+                      ws.counters[24:32].data_ptr(), _sync_side_stream(ws, topo), s)
         ws.applied = True
         return _loc(ws.nz)
     if kind == "1bit":

@@ -94,7 +94,7 @@ class EarlyStep:
         self.gen = topo.next_generation()
         self.ws = ws = _workspace(th, topo, "1bit", 1, False, False)
         if ws.syncs is None:
-            ws.syncs = [tp.sync_struct(r, ws.counters[4 * i:4 * i + 4], 0, 0) for i in range(3)]
+            ws.syncs = [tp.sync_struct(r, ws.counters[8 * i:8 * i + 8], 0, 0) for i in range(3)]
         self.ag = P <= AG_MAX_P and n <= AG_MAX_N
         if self.ag:
             if ws.ag is None:

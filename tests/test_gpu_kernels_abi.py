@@ -58,7 +58,7 @@ class _Ranks:
         self.full = [z(P * self.cw) for _ in range(P)]      # every rank: gather buffer
         self.nz = [z(P * self.cw) for _ in range(P)]
         self.flags = [torch.full((P,), 100, dtype=torch.int64, device=dev) for _ in range(P)]
-        self.counter = [z(16) for _ in range(P)]
+        self.counter = [z(32) for _ in range(P)]
         self.err = [z(2) for _ in range(P)]
         self.kflags = [z(1) for _ in range(P)]
         # pinned step-verdict words (lc_sync.verdict)
@@ -69,7 +69,7 @@ class _Ranks:
         for j in range(self.P):
             sy.peer_flags[j] = self.flags[j].data_ptr()
         sy.my_flags = self.flags[r].data_ptr()
-        sy.counter = self.counter[r].data_ptr() + 16 * counter
+        sy.counter = self.counter[r].data_ptr() + 32 * counter
         sy.err = self.err[r].data_ptr()
         sy.wait_epoch, sy.arrive_epoch = wait, arrive
         sy.P, sy.rank, sy.timeout_s = self.P, r, timeout

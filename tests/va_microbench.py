@@ -53,7 +53,7 @@ def main():
     recv = torch.randint(-2**31, 2**31 - 1, (P * cw,), dtype=torch.int32, device=dev)
     full = torch.randint(-2**31, 2**31 - 1, (P * cw,), dtype=torch.int32, device=dev)
     flags = [torch.full((P,), 1 << 40, dtype=torch.int64, device=dev) for _ in range(P)]
-    counter = torch.zeros(16, dtype=torch.int32, device=dev)
+    counter = torch.zeros(32, dtype=torch.int32, device=dev)
     err = torch.zeros(2, dtype=torch.int32, device=dev)
     kflags = torch.zeros(1, dtype=torch.int32, device=dev)
     hyp = _lib.Hyper(0.9, 0.1, 0.99, 0.01, 1e-4, 0.1)
@@ -64,7 +64,7 @@ def main():
         for j in range(P):
             sy.peer_flags[j] = flags[j].data_ptr()
         sy.my_flags = flags[r].data_ptr()
-        sy.counter = counter.data_ptr() + 16 * ctr
+        sy.counter = counter.data_ptr() + 32 * ctr
         sy.err = err.data_ptr()
         sy.wait_epoch, sy.arrive_epoch = wait, arrive
         sy.P, sy.rank, sy.timeout_s = P, r, 5.0
