@@ -144,6 +144,10 @@ def kernel_bytes(name: str, n: int, P: int, F: int, kind: str, nb: float = 16.0)
         return 8.0 * n + 4.0 * n + n / 8.0
     if name == "lc_apply_update":
         return 8.0 * n + n / 8.0
+    if name == "lc_vote_apply":   # theta r/w, voted words, the owner's P slots
+        return 8.0 * n + n / 8.0 + P * L / 8.0
+    if name == "lc_vote_update":  # theta r/w, P replicated rows
+        return 8.0 * n + P * n / 8.0
     if name == "lc_vote_bits":
         return (P + 1) * L / 8.0
     if name == "lc_fields_vote":
