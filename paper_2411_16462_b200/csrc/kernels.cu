@@ -839,7 +839,7 @@ k_sync_mean(SyncD sy, MeanArgs ma, int P) {
 #define LC_VA_CHUNK 8    // max super-tiles per work item of the update phase
 #endif
 #ifndef LC_VA_ITEMS
-#define LC_VA_ITEMS 131072  // work items per launch the chunk size aims for
+#define LC_VA_ITEMS 32768   // work items per launch the chunk size aims for (GPT-2 size: 4 super-tiles)
 #endif
 
 #ifndef LC_VA_UNIT
