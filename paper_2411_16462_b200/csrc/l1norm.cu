@@ -488,7 +488,7 @@ __device__ __noinline__ double leaf_sum_ieee(const float* __restrict__ g,
 }
 
 #ifndef LC_L1_LEAF_MINB
-#define LC_L1_LEAF_MINB 4
+#define LC_L1_LEAF_MINB 5  // 48 registers: 5 CTAs/SM (measured 0.451 -> 0.433 ms at GPT-2 size)
 #endif
 template <bool MASK, int PK, bool LOG>
 __global__ void __launch_bounds__(kThreads, LC_L1_LEAF_MINB)
