@@ -775,6 +775,13 @@ def main():
         e2e_skip = (f"host RAM: {local_world} ranks x 8 B/param x {n} params = "
                     f"{8 * n * local_world / 1e9:.0f} GB pinned > 70% of the "
                     f"{avail / 1e9:.0f} GB available")
+    if world > 1 and not args.no_e2e:
+        # every rank takes the same branch (the e2e steps are collective)
+        ok = torch.tensor([0 if e2e_skip else 1], dtype=torch.int32, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if not int(ok.item()) and e2e_skip is None:
+            e2e_skip = "host RAM: another local rank could not pin its e2e buffers"
+    if e2e_skip is not None:
         e2e = {"value": None, "unit": "params/s", "h2d_bytes_per_step": 4 * n,
                "d2h_bytes_per_step": 4 * n, "skipped": e2e_skip}
     if not args.no_e2e and e2e_skip is None:
