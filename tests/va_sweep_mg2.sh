@@ -1,6 +1,6 @@
 # vote/update variants incl. the fused-sync 7e9 step (gpurun --gpus 4)
-VARIANTS=${VARIANTS:-"default m4k4"} bash tests/va_sweep3.sh
-for v in ${VARIANTS:-default m4k4}; do
+VARIANTS=${VARIANTS:-"default"} bash tests/va_sweep3.sh
+for v in ${VARIANTS:-default}; do
   if [ $v = default ]; then unset LIONCUB_LIB; else export LIONCUB_LIB=$PWD/paper_2411_16462_b200/_lib/liblioncub_$v.so; fi
   for wn in ${RUNS:-flat7b_1bit_sync:4:10 flat7b_1bit_sync:2:10 tinyllama_1bit:4:30 gpt2s_sumsigns:4:30}; do
     w=${wn%%:*}; rest=${wn#*:}; n=${rest%%:*}; st=${rest##*:}
