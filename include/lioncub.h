@@ -200,7 +200,8 @@ int lc_vote_apply(const uint32_t* recv, int32_t P, int64_t cw, int64_t n_valid,
 /* ---- The momentum sync fused into the step (SyncPolicy(layers="all")
  * firing at this step; maybe_sync_momentum, optimizer.py:244-258, with
  * allreduce_mean_f32, collectives.py:319-344) ----
- * lc_encode_sync: the 1-bit encode (as lc_encode, LC_ENC_SIGN1, eoff 0) that
+ * lc_encode_sync (sync required, sync->P == nblocks): the 1-bit encode (as
+ *   lc_encode, LC_ENC_SIGN1, eoff 0) that
  *   stores m' of block j into mstage[j] -- owner j's staging row for this
  *   rank (L floats, 16-byte aligned) -- instead of the local m.
  * lc_vote_apply_sync: lc_vote_apply plus the owner mean: this owner's P

@@ -240,10 +240,25 @@ k_encode(const float* __restrict__ g, float* __restrict__ m,
 
   // rot: the rank's starting owner block (rank + 1), so that at any moment
   // the P ranks store into P different owners -- no incast on one owner's
-  // links while the others idle (the all-to-all stays balanced)
-  for (int64_t it = gw; it < nsup; it += nw) {
-    int64_t sidx = it + rot;
-    if (sidx >= nsup) sidx -= nsup;
+  // links while the others idle (the all-to-all stays balanced).  MPUSH
+  // (m' to the owners' staging rows, 4 B/param over NVLink for the remote
+  // blocks) interleaves the owner blocks super-tile by super-tile instead,
+  // starting at owner rank + 1: every wave of warps keeps NVLink (remote
+  // blocks) and HBM (the own block) busy together, where the block-by-block
+  // order ran an NVLink-bound phase and then an HBM-bound one.
+  const int64_t nb = L >> 10;  // super-tiles per owner block (MPUSH: eoff == 0)
+  const int64_t span = MPUSH ? (int64_t)sy.P * nb : nsup;
+  for (int64_t it = gw; it < span; it += nw) {
+    int64_t sidx;
+    if constexpr (MPUSH) {
+      const int64_t q = it / sy.P;
+      const int b = (int)(it - q * sy.P);
+      sidx = (int64_t)((b + sy.rank + 1) % sy.P) * nb + q;
+      if (sidx >= nsup) continue;
+    } else {
+      sidx = it + rot;
+      if (sidx >= nsup) sidx -= nsup;
+    }
     const int64_t ebase = sidx << 10;
     const int64_t gbase = eoff + ebase;            // element index in the full vector
     const int j = (int)(gbase / L);
@@ -1817,6 +1832,8 @@ int lc_encode_sync(const float* g, float* m, const uint8_t* mask, int64_t n,
     return set_err(LC_E_ARG, "lc_encode_sync: blocks (multiple of 1024) must cover n");
   Dst d;
   if (!make_dst(d, dst, nblocks)) return set_err(LC_E_ARG, "lc_encode_sync: bad destination table");
+  if (!sync || sync->P != nblocks || sync->rank < 0 || sync->rank >= nblocks)
+    return set_err(LC_E_ARG, "lc_encode_sync: sync required, with P == nblocks (it orders the owner blocks)");
   g_nrep = 0;
   g_eoff = 0;
   g_sync = to_syncd(sync);
