@@ -1995,6 +1995,8 @@ int fork_events(cudaEvent_t& fork, cudaEvent_t& join) {
 //   4 x B200: 3,1 69.7 ms; 2,1 67.8; 2,2 69.5; 4,1 73.7; 1,2 78.4
 //             (serial kernels 75.0, the mean inside the vote grid 75.8)
 //   2 x B200: 2,1 60.5 ms; 1,2 50.9; 2,2 50.2; 2,4 50.2; 1,6 57.9
+//   after the vote/update redesign and the interleaved K1 (4 x B200):
+//             2,1 65.5 ms; 2,2 65.3; 3,1 66.6; 1,1 66.4 (tests/sweep_side3.sh)
 struct SideCtas {
   int va, mean;
 };
