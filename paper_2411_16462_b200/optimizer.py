@@ -543,8 +543,16 @@ def distributed_lion_step(state: WorkerState, grad_i, h: LionHyper,
     1-bit / sum-of-signs path the sync is FUSED into the step: K1 stores m'
     into the owners' staging rows over NVLink while it streams g and m, and
     each owner averages its rows and stores the mean into every rank's
-    momentum inside the vote/update kernel.  A later maybe_sync_momentum call
-    for the same iteration is then a no-op."""
+    momentum beside the vote/update kernel.  Selected layers run as the
+    separate owner pull after the step (``LIONCUB_SYNC_FUSE=1`` moves that
+    pull beside the theta update; measured slower at 1.1B).  A later
+    maybe_sync_momentum call for the same iteration is then a no-op.
+
+    Errors (``LIONCUB_ERRORS=step``, the default): a peer that never reaches
+    the exchange raises ``CollectiveError`` in this call; on the peer-memory
+    path the call returns as soon as the vote/update kernel has published
+    the step's verdict (every wait resolved), while the theta update may
+    still be running -- stream-ordered before any later work."""
     _validate(spec, algo)
     _check_shapes(state.params, grad_i)
     out = _step_impl(state, grad_i, h, spec, topo, algo, mask, zero_mode, metrics_out,
