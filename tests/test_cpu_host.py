@@ -261,3 +261,24 @@ def test_checkpoint_reference_format_roundtrip(tmp_path):
     assert open(out, "rb").read() == blob
     assert json.load(open(out + ".json")) == json.load(open(gold + ".json"))
     assert open(out + ".json").read() == open(gold + ".json").read()
+
+
+def test_bench_roofline_bytes_cover_every_step_kernel():
+    """bench.py's roofline divides algorithmic bytes by the dominant kernel's
+    time: every kernel a step can launch must have its bytes (a 0 would
+    report a 0 fraction), and the figures match DESIGN.md's table."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "bench_mod", os.path.join(os.path.dirname(os.path.dirname(__file__)), "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    n, P = 1 << 24, 4
+    for name in ("lc_fused_local_step", "lc_encode", "lc_encode_sync", "lc_vote_apply",
+                 "lc_vote_apply_sync", "lc_vote_update", "lc_apply_update", "lc_vote_bits",
+                 "lc_fields_vote", "lc_f64_sum_vote", "lc_l1_scales", "lc_norm_scales"):
+        assert bench.kernel_bytes(name, n, P, 1, "1bit") > 0, name
+    assert bench.kernel_bytes("lc_fused_local_step", n, 1, 1, "1bit") == 20.0 * n
+    assert bench.kernel_bytes("lc_encode", n, P, 1, "1bit") == 12.0 * n + n / 8.0
+    # theta r/w + voted words + the owner's P slots
+    assert bench.kernel_bytes("lc_vote_apply", n, P, 1, "1bit") == 8.0 * n + n / 8.0 + n / 8.0
